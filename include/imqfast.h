@@ -1,0 +1,180 @@
+/* imqfast.h -- C ABI of the B200-native fast inverse-multiquadric library.
+ *
+ * Drop-in for the reference interface /root/reference/proj/include/imqfast.h
+ * (arXiv 2205.04194 artifact).  Every function of that header is declared here
+ * with the same signature, argument meaning, return codes and ownership rules;
+ * the comment above each names the reference declaration it replaces.  The
+ * imq_ext_* functions at the end are additive B200 extensions (device
+ * pointers, streams, statistics) and do not alter any reference symbol.
+ *
+ * Conventions (reference imqfast.h:4-11):
+ *   - point sets are interleaved coordinate pairs x1,x2 (length 2n);
+ *   - functions returning int yield IMQ_OK or an error code; imq_last_error()
+ *     returns a thread-local message for the most recent failure;
+ *   - output buffers are caller-allocated unless documented otherwise.
+ * Device work runs on the CUDA device current at imq_operator_create (or at
+ * the call, for the stateless functions).  There is no CPU fallback: without
+ * a CUDA device the compute entry points fail with IMQ_ERR_INTERNAL.
+ */
+#ifndef IMQFAST_B200_H
+#define IMQFAST_B200_H
+
+#include <stddef.h>
+
+#if defined(__GNUC__)
+#define IMQ_API __attribute__((visibility("default")))
+#else
+#define IMQ_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* reference imqfast.h:20-26 */
+enum {
+  IMQ_OK = 0,
+  IMQ_ERR_INVALID_ARG = 1,
+  IMQ_ERR_SINGULAR = 2,
+  IMQ_ERR_IO = 3,
+  IMQ_ERR_INTERNAL = 4
+};
+
+/* reference imqfast.h:28 -- opaque handle (here: a device-resident operator) */
+typedef struct imq_operator imq_operator;
+
+/* reference imqfast.h:30 */
+IMQ_API const char* imq_last_error(void);
+
+/* reference imqfast.h:35-36 (levels <= 0: automatic, imqfast.h:32-34) */
+IMQ_API int imq_operator_create(const double* xy, size_t n, double t, int m, int levels,
+                        imq_operator** out);
+/* reference imqfast.h:37 (NULL is a no-op) */
+IMQ_API void imq_operator_destroy(imq_operator* op);
+/* reference imqfast.h:38-39 */
+IMQ_API int imq_operator_size(const imq_operator* op, size_t* out);
+IMQ_API int imq_operator_levels(const imq_operator* op, int* out);
+
+/* reference imqfast.h:41-42: b = A u, host buffers of length n */
+IMQ_API int imq_operator_apply(const imq_operator* op, const double* u, double* b_out);
+
+/* reference imqfast.h:44-45: exact O(n^2) product on the GPU */
+IMQ_API int imq_dense_matvec(const double* xy, size_t n, double t, const double* u, double* b_out);
+
+/* reference imqfast.h:47-53: pivoted LU + one refinement step, n <= 5000 */
+IMQ_API int imq_dense_solve(const double* xy, size_t n, double t, const double* f, double* c_out,
+                    double* residual_out);
+
+/* reference imqfast.h:55-59 */
+typedef struct {
+  int iterations;
+  double final_relative_residual;
+  int converged;
+} imq_solve_stats;
+
+/* reference imqfast.h:61-66: restarted GMRES, zero initial guess, device resident */
+IMQ_API int imq_iterative_solve(const imq_operator* op, const double* f, double tol, int max_iter,
+                        int restart, double* c_out, imq_solve_stats* stats_out);
+
+/* reference imqfast.h:68-70 */
+IMQ_API int imq_evaluate_interpolant(const double* centers_xy, const double* c, size_t n, double t,
+                             const double* x_xy, size_t nx, double* out);
+
+/* reference imqfast.h:72-78 */
+IMQ_API int imq_green_exact(const double* x3, const double* y3, double* out);
+IMQ_API int imq_green_truncated(const double* x3, const double* y3, int m, double* out);
+/* reference imqfast.h:80-81 */
+IMQ_API int imq_truncation_error_bound(double rho_major, double r, int m, double* out);
+
+/* reference imqfast.h:83-85 */
+IMQ_API int imq_auto_level(size_t n, int m, int* out);
+IMQ_API int imq_cost_upper_bound(size_t n, int m, int levels, double* out);
+
+/* reference imqfast.h:87-88 */
+IMQ_API int imq_halton2d(size_t n, double* xy_out);
+/* reference imqfast.h:90-91 */
+IMQ_API int imq_random_vector(size_t n, unsigned long long seed, double* out);
+
+/* reference imqfast.h:93-99 */
+IMQ_API int imq_read_points(const char* path, double** xy_out, size_t* n_out);
+IMQ_API int imq_write_points(const char* path, const double* xy, size_t n);
+IMQ_API void imq_free(void* p);
+
+/* reference imqfast.h:101-103: host worker threads (host-side utilities only) */
+IMQ_API int imq_set_threads(int n);
+
+/* reference imqfast.h:105-112 */
+typedef struct {
+  const double* xy;
+  size_t n;
+  double t;
+  int m;
+  int levels;
+  unsigned long long seed;
+} imq_verify_config;
+
+/* reference imqfast.h:114 */
+typedef void (*imq_verify_callback)(const char* name, int pass, double value, void* user_data);
+
+/* reference imqfast.h:116-123 */
+IMQ_API int imq_verify(const imq_verify_config* cfg, imq_verify_callback cb, void* user_data);
+
+/* ------------------------------------------------------------------------
+ * B200 extensions (additive; SURVEY §8(b) "Additive extensions").
+ * ---------------------------------------------------------------------- */
+
+/* b = A u on device buffers (original point order) enqueued on `stream`
+ * (a cudaStream_t, NULL = the operator's stream); no host synchronisation. */
+IMQ_API int imq_ext_operator_apply_device(const imq_operator* op, const double* d_u, double* d_b,
+                                  void* stream);
+/* Same on vectors already permuted into the operator's Morton order. */
+IMQ_API int imq_ext_operator_apply_sorted_device(const imq_operator* op, const double* d_us,
+                                         double* d_bs, void* stream);
+/* Waits for all work queued on the operator's stream. */
+IMQ_API int imq_ext_operator_synchronize(const imq_operator* op);
+/* perm_out[p] = original index of the p-th point in Morton order (length n). */
+IMQ_API int imq_ext_operator_permutation(const imq_operator* op, int* perm_out);
+/* leaf_start of the finest level (length 4^(L+1) + 1). */
+IMQ_API int imq_ext_operator_leaf_start(const imq_operator* op, int* out, size_t capacity);
+
+typedef struct {
+  int n, m, levels, device;
+  double origin_x, origin_y, side;
+  double far_pairs;  /* exact #(target, non-empty far source block) pairs */
+  double near_pairs; /* exact #(target, source point) near pairs */
+  long long far_items, near_items;
+} imq_ext_stats;
+IMQ_API int imq_ext_operator_stats(const imq_operator* op, imq_ext_stats* out);
+
+/* GMRES with the per-restart true residual history (SolveReport.cycle_residuals,
+ * reference solver.hpp:14).  cycle_out may be NULL; *n_cycles receives the full
+ * count even when it exceeds max_cycles. */
+IMQ_API int imq_ext_iterative_solve(const imq_operator* op, const double* f, double tol, int max_iter,
+                            int restart, double* c_out, imq_solve_stats* stats_out,
+                            double* cycle_out, int max_cycles, int* n_cycles);
+
+/* Stage-level entry points for sharded (multi-GPU) application: moments of a
+ * Morton-ordered device vector, the device coefficient array, and the far +
+ * near evaluation over work-item ranges writing sorted-order results. */
+IMQ_API int imq_ext_operator_moments(const imq_operator* op, const double* d_us, void* stream);
+IMQ_API int imq_ext_operator_coefficients(const imq_operator* op, void** d_coef, size_t* count,
+                                  long long* level_offsets, int capacity);
+IMQ_API int imq_ext_operator_items(const imq_operator* op, int which, int* items_xyzw, size_t capacity,
+                           size_t* count);
+IMQ_API int imq_ext_operator_far_near(const imq_operator* op, const double* d_us, double* d_bs,
+                              int far_begin, int far_end, int near_begin, int near_end,
+                              void* stream);
+
+/* Measured FP64 FMA-pipe throughput (TFLOP/s) of the current device: the
+ * roofline denominator of the FP64-bound far-field kernel. */
+IMQ_API int imq_ext_fp64_peak(int iters, double* tflops, double* ms);
+
+/* Number of visible CUDA devices; select the device used by later creates. */
+IMQ_API int imq_ext_device_count(int* out);
+IMQ_API int imq_ext_set_device(int device);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* IMQFAST_B200_H */

@@ -1,0 +1,158 @@
+// blas.cu -- vector kernels of the device-resident GMRES (reference
+// solver.cpp:14-28 nrm2/dot/axpy).  Reductions use a fixed grid and a fixed
+// combine order, so every dot product is bitwise reproducible run to run.
+// Scalars produced on the device (MGS coefficients h_ij) are consumed on the
+// device, so the modified Gram-Schmidt chain needs no host round trip.
+#include "imq_kernels.hpp"
+
+namespace imqk {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+__global__ void __launch_bounds__(kThreads) k_dot_partial(const double* __restrict__ a,
+                                                          const double* __restrict__ b,
+                                                          long long n,
+                                                          double* __restrict__ partial) {
+  double s = 0.0;
+  for (long long i = blockIdx.x * (long long)kThreads + threadIdx.x; i < n;
+       i += (long long)gridDim.x * kThreads)
+    s = fma(a[i], b[i], s);
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  __shared__ double red[kThreads / 32];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < kThreads / 32; ++w) t += red[w];
+    partial[blockIdx.x] = t;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) k_dot_final(const double* __restrict__ partial,
+                                                        int nparts, double* out, int take_sqrt) {
+  double s = 0.0;
+  for (int i = threadIdx.x; i < nparts; i += kThreads) s += partial[i];
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  __shared__ double red[kThreads / 32];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < kThreads / 32; ++w) t += red[w];
+    *out = take_sqrt ? sqrt(t) : t;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) k_axpy_dev(double* __restrict__ y,
+                                                       const double* __restrict__ x, long long n,
+                                                       const double* __restrict__ alpha,
+                                                       double sign) {
+  const double a = sign * *alpha;
+  for (long long i = blockIdx.x * (long long)kThreads + threadIdx.x; i < n;
+       i += (long long)gridDim.x * kThreads)
+    y[i] = fma(a, x[i], y[i]);
+}
+__global__ void __launch_bounds__(kThreads) k_axpy(double* __restrict__ y,
+                                                   const double* __restrict__ x, long long n,
+                                                   double a) {
+  for (long long i = blockIdx.x * (long long)kThreads + threadIdx.x; i < n;
+       i += (long long)gridDim.x * kThreads)
+    y[i] = fma(a, x[i], y[i]);
+}
+__global__ void __launch_bounds__(kThreads) k_div(double* __restrict__ out,
+                                                  const double* __restrict__ x, long long n,
+                                                  double d) {
+  for (long long i = blockIdx.x * (long long)kThreads + threadIdx.x; i < n;
+       i += (long long)gridDim.x * kThreads)
+    out[i] = x[i] / d;
+}
+__global__ void __launch_bounds__(kThreads) k_sub(double* __restrict__ r,
+                                                  const double* __restrict__ f,
+                                                  const double* __restrict__ w, long long n) {
+  for (long long i = blockIdx.x * (long long)kThreads + threadIdx.x; i < n;
+       i += (long long)gridDim.x * kThreads)
+    r[i] = f[i] - w[i];
+}
+__global__ void __launch_bounds__(kThreads) k_nonfinite(const double* __restrict__ x,
+                                                        long long n, int* flag) {
+  bool bad = false;
+  for (long long i = blockIdx.x * (long long)kThreads + threadIdx.x; i < n;
+       i += (long long)gridDim.x * kThreads)
+    bad |= !isfinite(x[i]);
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
+// FP64 pipe roofline probe: 8 independent DFMA chains per thread, no memory.
+__global__ void __launch_bounds__(256) k_dfma_peak(int iters, double a, double* out) {
+  double x0 = threadIdx.x * 1e-9, x1 = x0 + 1e-3, x2 = x0 + 2e-3, x3 = x0 + 3e-3;
+  double x4 = x0 + 4e-3, x5 = x0 + 5e-3, x6 = x0 + 6e-3, x7 = x0 + 7e-3;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      x0 = fma(x0, a, 1e-7); x1 = fma(x1, a, 1e-7); x2 = fma(x2, a, 1e-7); x3 = fma(x3, a, 1e-7);
+      x4 = fma(x4, a, 1e-7); x5 = fma(x5, a, 1e-7); x6 = fma(x6, a, 1e-7); x7 = fma(x7, a, 1e-7);
+    }
+  }
+  const double s = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+  if (s == 12345.678) out[0] = s;  // keeps the chains live
+}
+
+inline unsigned grid_for(long long n) {
+  long long b = (n + kThreads * 4 - 1) / (kThreads * 4);
+  return (unsigned)(b < 1 ? 1 : (b > 1184 ? 1184 : b));
+}
+
+}  // namespace
+
+int dot_parts(long long n) { return (int)grid_for(n); }
+
+double measure_dfma_peak(int iters, float* ms_out) {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const unsigned grid = (unsigned)sms * 8;  // 8 x 256 threads resident per SM
+  double* d = nullptr;
+  cudaMalloc(&d, sizeof(double));
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  k_dfma_peak<<<grid, 256>>>(iters / 4 + 1, 0.999999, d);  // warm-up / clocks up
+  cudaEventRecord(e0);
+  k_dfma_peak<<<grid, 256>>>(iters, 0.999999, d);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(d);
+  if (ms_out) *ms_out = ms;
+  const double flops = (double)grid * 256 * iters * 16 * 8 * 2;
+  return flops / (ms * 1e-3) / 1e12;
+}
+
+void launch_dot(const double* a, const double* b, long long n, double* partial, int nparts,
+                double* out, int take_sqrt, cudaStream_t s) {
+  k_dot_partial<<<nparts, kThreads, 0, s>>>(a, b, n, partial);
+  k_dot_final<<<1, kThreads, 0, s>>>(partial, nparts, out, take_sqrt);
+}
+void launch_axpy_dev(double* y, const double* x, long long n, const double* alpha_dev,
+                     double sign, cudaStream_t s) {
+  k_axpy_dev<<<grid_for(n), kThreads, 0, s>>>(y, x, n, alpha_dev, sign);
+}
+void launch_axpy(double* y, const double* x, long long n, double alpha, cudaStream_t s) {
+  k_axpy<<<grid_for(n), kThreads, 0, s>>>(y, x, n, alpha);
+}
+void launch_div(double* out, const double* x, long long n, double d, cudaStream_t s) {
+  k_div<<<grid_for(n), kThreads, 0, s>>>(out, x, n, d);
+}
+void launch_sub(double* r, const double* f, const double* w, long long n, cudaStream_t s) {
+  k_sub<<<grid_for(n), kThreads, 0, s>>>(r, f, w, n);
+}
+void launch_nonfinite(const double* x, long long n, int* flag, cudaStream_t s) {
+  k_nonfinite<<<grid_for(n), kThreads, 0, s>>>(x, n, flag);
+}
+
+}  // namespace imqk

@@ -1,0 +1,640 @@
+// expansion.cu -- far-field pipeline of the fast IMQ product on sm_100a.
+//
+//   P2M (leaf)   raw planar moments of every finest block from its points
+//   M2M          exact binomial translation of child moments to the parent
+//   transform    mu -> far-field coefficients C_{m,k} (one small linear map)
+//   M2P          per (target point, source block) evaluation, the hot kernel
+//
+// All of it is exact in real arithmetic with respect to the reference's
+// per-level moment formation (fastmv.cpp:79-100) and M2P evaluation
+// (fastmv.cpp:104-138, specfun.cpp:73-91): the same bounding square, levels,
+// buckets, interaction lists and truncation order.  What changes is how the
+// arithmetic is organised:
+//   * moments are kept as complex sums mu_{m,i} = sum u |e|^{2i} e^m, which
+//     equal the reference's (w - i v)_{n,m} / P_n^m(0) with n = m + 2i; the
+//     n-m odd moments of the reference are identically zero and not stored;
+//   * d_{n,m} P_n^m(0) and the monomial form of P_n^m(t/rho) rho^-(n+1) are
+//     folded into C_{m,k}, so a far pair is a complex Horner scheme in
+//     conj(xi) = (dx, -dy)/rho^2 with real-Horner inner polynomials in
+//     q = 1/rho^2: ~M^2+4M DFMA per pair instead of a Legendre recurrence
+//     with one division per (n, m).
+#include <cstdio>
+
+#include "imq_device.cuh"
+#include "imq_kernels.hpp"
+
+namespace imqk {
+using namespace imqdev;
+
+namespace {
+
+__host__ __device__ __forceinline__ int mu_offset(int M, int m) {
+  // sum_{m' < m} (floor((M - m') / 2) + 1)
+  int o = 0;
+  for (int mm = 0; mm < m; ++mm) o += (M - mm) / 2 + 1;
+  return o;
+}
+__host__ __device__ __forceinline__ void mu_unindex(int M, int o, int& m, int& i) {
+  m = 0;
+  while (true) {
+    int sz = (M - m) / 2 + 1;
+    if (o < sz) break;
+    o -= sz;
+    ++m;
+  }
+  i = o;
+}
+
+__device__ __forceinline__ int block_count(const TreeParams& P, int level, uint32_t q) {
+  int sh = 2 * (P.L - level);
+  return P.leaf_start[(size_t)(q + 1) << sh] - P.leaf_start[(size_t)q << sh];
+}
+__device__ __forceinline__ int block_first(const TreeParams& P, int level, uint32_t q) {
+  return P.leaf_start[(size_t)q << (2 * (P.L - level))];
+}
+
+// ------------------------------------------------------------------- P2M ---
+// Warp per finest block; lane m accumulates mu_{m,i}, i = 0..(M-m)/2, over
+// the block's points in sorted (= ascending original index) order.
+template <int M>
+__global__ void __launch_bounds__(128) k_p2m_leaf(const TreeParams P, const double* __restrict__ u_s,
+                                                  double2* __restrict__ mu) {
+  constexpr int NI = M / 2 + 1;
+  const int lane = threadIdx.x & 31;
+  const long long leaf = (long long)blockIdx.x * 4 + (threadIdx.x >> 5);
+  const long long n_leaves = 1ll << (2 * (P.L + 1));
+  if (leaf >= n_leaves) return;
+  const int s = P.leaf_start[leaf], e = P.leaf_start[leaf + 1];
+  if (s == e) return;
+  int li, lj;
+  demorton((uint32_t)leaf, li, lj);
+  const double zx = block_center(P.ox, li, P.cell[P.L]);
+  const double zy = block_center(P.oy, lj, P.cell[P.L]);
+  const int m = lane;
+  double ar[NI], ai[NI];
+#pragma unroll
+  for (int i = 0; i < NI; ++i) ar[i] = ai[i] = 0.0;
+  for (int p = s; p < e; ++p) {
+    const double ex = P.xs[p] - zx, ey = P.ys[p] - zy;
+    const double e2 = fma(ex, ex, ey * ey);
+    // u * e^m by binary powering
+    double pr = u_s[p], pi = 0.0, br = ex, bi = ey;
+    int mm = m;
+#pragma unroll
+    for (int b = 0; b < 5; ++b) {
+      if (mm & 1) {
+        const double tr = pr * br - pi * bi;
+        pi = pr * bi + pi * br;
+        pr = tr;
+      }
+      const double sr = br * br - bi * bi;
+      bi = 2.0 * br * bi;
+      br = sr;
+      mm >>= 1;
+    }
+    double e2p = 1.0;
+#pragma unroll
+    for (int i = 0; i < NI; ++i) {
+      ar[i] = fma(pr, e2p, ar[i]);
+      ai[i] = fma(pi, e2p, ai[i]);
+      e2p *= e2;
+    }
+  }
+  if (m <= M) {
+    double2* out = mu + P.mu_off[P.L] + (size_t)leaf * P.Ke + mu_offset(M, m);
+#pragma unroll
+    for (int i = 0; i < NI; ++i)
+      if (m + 2 * i <= M) out[i] = make_double2(ar[i], ai[i]);
+  }
+}
+
+// Generic order: thread per (finest block, moment index), direct powering.
+__global__ void __launch_bounds__(128) k_p2m_leaf_generic(const TreeParams P,
+                                                          const double* __restrict__ u_s,
+                                                          double2* __restrict__ mu) {
+  const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long n_leaves = 1ll << (2 * (P.L + 1));
+  const long long leaf = gid / P.Ke;
+  const int o = (int)(gid % P.Ke);
+  if (leaf >= n_leaves) return;
+  const int s = P.leaf_start[leaf], e = P.leaf_start[leaf + 1];
+  if (s == e) return;
+  int li, lj, m, i;
+  demorton((uint32_t)leaf, li, lj);
+  mu_unindex(P.M, o, m, i);
+  const double zx = block_center(P.ox, li, P.cell[P.L]);
+  const double zy = block_center(P.oy, lj, P.cell[P.L]);
+  double ar = 0.0, ai = 0.0;
+  for (int p = s; p < e; ++p) {
+    const double ex = P.xs[p] - zx, ey = P.ys[p] - zy;
+    const double e2 = fma(ex, ex, ey * ey);
+    double pr = u_s[p], pi = 0.0, br = ex, bi = ey;
+    for (int mm = m; mm; mm >>= 1) {
+      if (mm & 1) {
+        const double tr = pr * br - pi * bi;
+        pi = pr * bi + pi * br;
+        pr = tr;
+      }
+      const double sr = br * br - bi * bi;
+      bi = 2.0 * br * bi;
+      br = sr;
+    }
+    double e2p = 1.0, b2 = e2;
+    for (int ii = i; ii; ii >>= 1) {
+      if (ii & 1) e2p *= b2;
+      b2 *= b2;
+    }
+    ar = fma(pr, e2p, ar);
+    ai = fma(pi, e2p, ai);
+  }
+  mu[P.mu_off[P.L] + (size_t)leaf * P.Ke + o] = make_double2(ar, ai);
+}
+
+// ------------------------------------------------------------------- M2M ---
+// CTA per parent block at `level`; thread per output moment (m, i), i.e.
+// (a, b) = (m + i, i) of sum u e^a conj(e)^b.  With e' = e + d (d = child
+// centre - parent centre):
+//   mu'_{a,b} = sum_{p<=a, r<=b} C(a,p) C(b,r) d^{a-p} conj(d)^{b-r} N_{p,r},
+//   N_{p,r} = mu_{p-r, r} (p >= r) or conj(mu_{r-p, p}) (p < r).
+__global__ void k_m2m(const TreeParams P, int level, double2* __restrict__ mu,
+                      const double* __restrict__ binom) {
+  extern __shared__ double2 sm[];
+  const int M = P.M, Ke = P.Ke;
+  double2* cm = sm;                    // [4][Ke]
+  double2* dp = sm + 4 * Ke;           // [4][M+1] powers of d
+  const uint32_t q = blockIdx.x;
+  if (block_count(P, level, q) == 0) return;
+  int qi, qj;
+  demorton(q, qi, qj);
+  const double zx = block_center(P.ox, qi, P.cell[level]);
+  const double zy = block_center(P.oy, qj, P.cell[level]);
+  int have = 0;
+  for (int c = 0; c < 4; ++c) {
+    const uint32_t ch = 4 * q + c;
+    const bool ne = block_count(P, level + 1, ch) > 0;
+    have |= (ne ? 1 : 0) << c;
+    const double2* src = mu + P.mu_off[level + 1] + (size_t)ch * Ke;
+    for (int o = threadIdx.x; o < Ke; o += blockDim.x)
+      cm[c * Ke + o] = ne ? src[o] : make_double2(0.0, 0.0);
+    if (threadIdx.x == 0) {
+      int ci, cj;
+      demorton(ch, ci, cj);
+      const double dx = block_center(P.ox, ci, P.cell[level + 1]) - zx;
+      const double dy = block_center(P.oy, cj, P.cell[level + 1]) - zy;
+      double pr = 1.0, pi = 0.0;
+      for (int k = 0; k <= M; ++k) {
+        dp[c * (M + 1) + k] = make_double2(pr, pi);
+        const double tr = pr * dx - pi * dy;
+        pi = pr * dy + pi * dx;
+        pr = tr;
+      }
+    }
+  }
+  __syncthreads();
+  for (int o = threadIdx.x; o < Ke; o += blockDim.x) {
+    int m, i;
+    mu_unindex(M, o, m, i);
+    const int a = m + i, b = i;
+    double sr = 0.0, si = 0.0;
+    for (int c = 0; c < 4; ++c) {
+      if (!((have >> c) & 1)) continue;
+      const double2* N = cm + c * Ke;
+      const double2* D = dp + c * (M + 1);
+      for (int p = 0; p <= a; ++p) {
+        // inner: sum_r C(b,r) conj(d)^{b-r} N_{p,r}
+        double ir = 0.0, ii = 0.0;
+        for (int r = 0; r <= b; ++r) {
+          double nr, ni;
+          if (p >= r) {
+            const double2 v = N[mu_offset(M, p - r) + r];
+            nr = v.x; ni = v.y;
+          } else {
+            const double2 v = N[mu_offset(M, r - p) + p];
+            nr = v.x; ni = -v.y;
+          }
+          const double2 d = D[b - r];  // conj(d)^{b-r} = conj(d^{b-r})
+          const double cb = binom[b * (M + 1) + r];
+          const double tr = d.x * nr + d.y * ni;
+          const double ti = d.x * ni - d.y * nr;
+          ir = fma(cb, tr, ir);
+          ii = fma(cb, ti, ii);
+        }
+        const double2 d = D[a - p];
+        const double ca = binom[a * (M + 1) + p];
+        sr = fma(ca, d.x * ir - d.y * ii, sr);
+        si = fma(ca, d.x * ii + d.y * ir, si);
+      }
+    }
+    // m = 0 moments are real by construction (conjugate-symmetric terms);
+    // keep their imaginary part exactly zero as the reference's v_{n,0} are.
+    mu[P.mu_off[level] + (size_t)q * Ke + o] = make_double2(sr, m == 0 ? 0.0 : si);
+  }
+}
+
+// ------------------------------------------------------------- transform ---
+__global__ void k_transform(const TreeParams P, int level, const double2* __restrict__ mu,
+                            double2* __restrict__ coef, const TransformTable T) {
+  extern __shared__ double2 sm[];
+  const uint32_t q = blockIdx.x;
+  if (block_count(P, level, q) == 0) return;
+  const double2* src = mu + P.mu_off[level] + (size_t)q * P.Ke;
+  for (int o = threadIdx.x; o < P.Ke; o += blockDim.x) sm[o] = src[o];
+  __syncthreads();
+  double2* dst = coef + P.coef_off[level] + (size_t)q * P.K;
+  for (int o = threadIdx.x; o < P.K; o += blockDim.x) {
+    double cr = 0.0, ci = 0.0;
+    for (int e = T.off[o]; e < T.off[o + 1]; ++e) {
+      const double2 v = sm[T.idx[e]];
+      cr = fma(T.val[e], v.x, cr);
+      ci = fma(T.val[e], v.y, ci);
+    }
+    dst[o] = make_double2(cr, ci);
+  }
+}
+
+// ------------------------------------------------------------------- M2P ---
+constexpr int kMaxList = 384;  // 12 + 27 (L - 2) + 36 <= 372 for L <= 13
+
+// Builds the warp's source list for a work item: every non-empty source block
+// at levels 1..L-1 of the (shared) ancestor lists, then the level-L union over
+// the children of the parent's 3x3 neighbourhood that some present leaf needs.
+// Entries are (level << 28 | block) in the reference's list order.
+__device__ int build_far_list(const TreeParams& P, uint32_t par, int s, int cnt, uint32_t* list,
+                              int lane) {
+  const int L = P.L;
+  const int e = s + cnt;
+  bool present = false;
+  if (lane < 4) {
+    const uint32_t c = 4 * par + lane;
+    present = P.leaf_start[c] < e && P.leaf_start[c + 1] > s;
+  }
+  const uint32_t pmask = __ballot_sync(0xffffffffu, present) & 0xfu;
+  int n = 0;
+  for (int l = 1; l <= L; ++l) {
+    const int grid = 1 << (l + 1);
+    int ai = 0, aj = 0, wi, wj, lo_i, lo_j;
+    if (l < L) demorton(par >> (2 * (L - 1 - l)), ai, aj);
+    if (l == 1) {
+      lo_i = lo_j = 0;
+      wi = wj = 4;
+    } else {
+      int pi, pj;
+      if (l < L) {
+        pi = ai >> 1;
+        pj = aj >> 1;
+      } else {
+        demorton(par, pi, pj);
+      }
+      lo_i = max(0, 2 * pi - 2);
+      lo_j = max(0, 2 * pj - 2);
+      wi = min(grid - 1, 2 * pi + 3) - lo_i + 1;
+      wj = min(grid - 1, 2 * pj + 3) - lo_j + 1;
+    }
+    const int ncand = wi * wj;
+    for (int base = 0; base < ncand; base += 32) {
+      const int c = base + lane;
+      bool keep = false;
+      uint32_t q = 0;
+      if (c < ncand) {
+        const int qi = lo_i + c / wj, qj = lo_j + c % wj;
+        if (l < L) {
+          keep = max(abs(qi - ai), abs(qj - aj)) >= 2;
+        } else {
+          int pi, pj;
+          demorton(par, pi, pj);
+          for (int ch = 0; ch < 4; ++ch) {
+            if (!((pmask >> ch) & 1)) continue;
+            const int ci = 2 * pi + (ch >> 1), cj = 2 * pj + (ch & 1);
+            if (max(abs(qi - ci), abs(qj - cj)) >= 2) keep = true;
+          }
+        }
+        q = morton(qi, qj);
+        if (keep) keep = block_count(P, l, q) > 0;
+      }
+      const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+      if (keep) list[n + __popc(bal & ((1u << lane) - 1u))] = ((uint32_t)l << 28) | q;
+      n += __popc(bal);
+    }
+  }
+  __syncwarp();
+  return n;
+}
+
+// Complex Horner evaluation of one source block's expansion at two targets.
+// c: K coefficients (double2) in Horner order; returns the far contribution.
+template <int M>
+__device__ __forceinline__ void far_eval2(const double2* __restrict__ c, double dx0, double dy0,
+                                          double dx1, double dy1, double t2, double& v0,
+                                          double& v1) {
+  const double r0 = rsqrt(fma(dx0, dx0, fma(dy0, dy0, t2)));
+  const double r1 = rsqrt(fma(dx1, dx1, fma(dy1, dy1, t2)));
+  const double q0 = r0 * r0, q1 = r1 * r1;
+  if constexpr (M == 0) {
+    v0 = c[0].x * r0;
+    v1 = c[0].x * r1;
+  } else {
+    const double xr0 = dx0 * q0, xi0 = -dy0 * q0;
+    const double xr1 = dx1 * q1, xi1 = -dy1 * q1;
+    double2 cc = c[0];
+    double ar0 = cc.x, ai0 = cc.y, ar1 = cc.x, ai1 = cc.y;
+    int o = 1;
+#pragma unroll
+    for (int m = M - 1; m >= 1; --m) {
+      cc = c[o++];
+      double gr0 = cc.x, gi0 = cc.y, gr1 = cc.x, gi1 = cc.y;
+#pragma unroll
+      for (int k = M - 1; k >= m; --k) {
+        cc = c[o++];
+        gr0 = fma(gr0, q0, cc.x);
+        gi0 = fma(gi0, q0, cc.y);
+        gr1 = fma(gr1, q1, cc.x);
+        gi1 = fma(gi1, q1, cc.y);
+      }
+      const double nr0 = fma(ar0, xr0, fma(-ai0, xi0, gr0));
+      const double ni0 = fma(ar0, xi0, fma(ai0, xr0, gi0));
+      const double nr1 = fma(ar1, xr1, fma(-ai1, xi1, gr1));
+      const double ni1 = fma(ar1, xi1, fma(ai1, xr1, gi1));
+      ar0 = nr0; ai0 = ni0; ar1 = nr1; ai1 = ni1;
+    }
+    // m = 0: real inner polynomial, only the real part of the result is used
+    cc = c[o++];
+    double g0 = cc.x, g1 = cc.x;
+#pragma unroll
+    for (int k = M - 1; k >= 0; --k) {
+      cc = c[o++];
+      g0 = fma(g0, q0, cc.x);
+      g1 = fma(g1, q1, cc.x);
+    }
+    v0 = fma(ar0, xr0, fma(-ai0, xi0, g0)) * r0;
+    v1 = fma(ar1, xr1, fma(-ai1, xi1, g1)) * r1;
+  }
+}
+
+// Runtime-order variant (coefficients read through L1 from global memory).
+__device__ __forceinline__ double far_eval_generic(const double2* __restrict__ c, int M,
+                                                   double dx, double dy, double t2) {
+  const double r = rsqrt(fma(dx, dx, fma(dy, dy, t2)));
+  const double q = r * r;
+  if (M == 0) return __ldg(&c[0].x) * r;
+  const double xr = dx * q, xi = -dy * q;
+  double2 cc = __ldg(&c[0]);
+  double ar = cc.x, ai = cc.y;
+  int o = 1;
+  for (int m = M - 1; m >= 1; --m) {
+    cc = __ldg(&c[o++]);
+    double gr = cc.x, gi = cc.y;
+    for (int k = M - 1; k >= m; --k) {
+      cc = __ldg(&c[o++]);
+      gr = fma(gr, q, cc.x);
+      gi = fma(gi, q, cc.y);
+    }
+    const double nr = fma(ar, xr, fma(-ai, xi, gr));
+    const double ni = fma(ar, xi, fma(ai, xr, gi));
+    ar = nr;
+    ai = ni;
+  }
+  double g = __ldg(&c[o++].x);
+  for (int k = M - 1; k >= 0; --k) g = fma(g, q, __ldg(&c[o++].x));
+  return fma(ar, xr, fma(-ai, xi, g)) * r;
+}
+
+struct Target {
+  double x0, y0, x1, y1;
+  int li0, lj0, li1, lj1;
+  bool v0, v1;
+};
+
+__device__ __forceinline__ Target load_targets(const TreeParams& P, int s, int cnt, int lane) {
+  Target T;
+  const int p0 = s + lane, p1 = s + 32 + lane;
+  T.v0 = lane < cnt;
+  T.v1 = lane + 32 < cnt;
+  const int a0 = T.v0 ? p0 : s, a1 = T.v1 ? p1 : s;
+  T.x0 = P.xs[a0]; T.y0 = P.ys[a0];
+  T.x1 = P.xs[a1]; T.y1 = P.ys[a1];
+  demorton(P.leaf[a0], T.li0, T.lj0);
+  demorton(P.leaf[a1], T.li1, T.lj1);
+  return T;
+}
+
+// Warp per work item (<= 64 targets of one level-(L-1) block, 2 per lane).
+// Source coefficients are staged per warp through a STAGES-deep ring of
+// shared-memory buffers filled by one-instruction TMA bulk copies.
+template <int M, int WARPS, int STAGES>
+__global__ void __launch_bounds__(WARPS * 32) k_m2p_far(const TreeParams P,
+                                                       const int4* __restrict__ items,
+                                                       int n_items,
+                                                       const double2* __restrict__ coef,
+                                                       double* __restrict__ far_s) {
+  constexpr int K = (M + 1) * (M + 2) / 2;
+  constexpr uint32_t kBytes = K * 16;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double2* stage = reinterpret_cast<double2*>(smem_raw) + (size_t)warp * STAGES * K;
+  uint64_t* bars =
+      reinterpret_cast<uint64_t*>(reinterpret_cast<double2*>(smem_raw) + WARPS * STAGES * K) +
+      warp * STAGES;
+  uint32_t* list = reinterpret_cast<uint32_t*>(
+                       reinterpret_cast<uint64_t*>(reinterpret_cast<double2*>(smem_raw) +
+                                                   WARPS * STAGES * K) +
+                       WARPS * STAGES) +
+                   warp * kMaxList;
+  const int it = blockIdx.x * WARPS + warp;
+  if (it >= n_items) return;
+  if (lane == 0) {
+#pragma unroll
+    for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+
+  const int4 item = items[it];
+  const uint32_t par = (uint32_t)item.x;
+  const int s0 = item.y, cnt = item.z;
+  const int n = build_far_list(P, par, s0, cnt, list, lane);
+  const Target T = load_targets(P, s0, cnt, lane);
+  const int L = P.L;
+
+  auto issue = [&](int e, int slot) {
+    const uint32_t ent = list[e];
+    const int l = (int)(ent >> 28);
+    const uint32_t q = ent & 0x0fffffffu;
+    mbar_arrive_expect_tx(&bars[slot], kBytes);
+    tma_load_1d(stage + (size_t)slot * K, coef + P.coef_off[l] + (size_t)q * K, kBytes,
+                &bars[slot]);
+  };
+  if (lane == 0)
+    for (int e = 0; e < STAGES && e < n; ++e) issue(e, e);
+
+  double acc0 = 0.0, acc1 = 0.0;
+  for (int e = 0; e < n; ++e) {
+    const int slot = e % STAGES;
+    const uint32_t ent = list[e];
+    const int l = (int)(ent >> 28);
+    int qi, qj;
+    demorton(ent & 0x0fffffffu, qi, qj);
+    const double zx = block_center(P.ox, qi, P.cell[l]);
+    const double zy = block_center(P.oy, qj, P.cell[l]);
+    bool m0 = T.v0, m1 = T.v1;
+    if (l == L) {
+      m0 = m0 && max(abs(qi - T.li0), abs(qj - T.lj0)) >= 2;
+      m1 = m1 && max(abs(qi - T.li1), abs(qj - T.lj1)) >= 2;
+    }
+    mbar_wait(&bars[slot], (uint32_t)((e / STAGES) & 1));
+    double v0, v1;
+    far_eval2<M>(stage + (size_t)slot * K, T.x0 - zx, T.y0 - zy, T.x1 - zx, T.y1 - zy, P.t2,
+                 v0, v1);
+    acc0 += m0 ? v0 : 0.0;
+    acc1 += m1 ? v1 : 0.0;
+    __syncwarp();
+    if (lane == 0 && e + STAGES < n) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(e + STAGES, slot);
+    }
+  }
+  if (T.v0) far_s[s0 + lane] = acc0;
+  if (T.v1) far_s[s0 + 32 + lane] = acc1;
+}
+
+template <int WARPS>
+__global__ void __launch_bounds__(WARPS * 32) k_m2p_far_generic(const TreeParams P,
+                                                               const int4* __restrict__ items,
+                                                               int n_items,
+                                                               const double2* __restrict__ coef,
+                                                               double* __restrict__ far_s) {
+  __shared__ uint32_t lists[WARPS][kMaxList];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int it = blockIdx.x * WARPS + warp;
+  if (it >= n_items) return;
+  const int4 item = items[it];
+  const uint32_t par = (uint32_t)item.x;
+  const int s0 = item.y, cnt = item.z;
+  uint32_t* list = lists[warp];
+  const int n = build_far_list(P, par, s0, cnt, list, lane);
+  const Target T = load_targets(P, s0, cnt, lane);
+  double acc0 = 0.0, acc1 = 0.0;
+  for (int e = 0; e < n; ++e) {
+    const uint32_t ent = list[e];
+    const int l = (int)(ent >> 28);
+    const uint32_t q = ent & 0x0fffffffu;
+    int qi, qj;
+    demorton(q, qi, qj);
+    const double zx = block_center(P.ox, qi, P.cell[l]);
+    const double zy = block_center(P.oy, qj, P.cell[l]);
+    bool m0 = T.v0, m1 = T.v1;
+    if (l == P.L) {
+      m0 = m0 && max(abs(qi - T.li0), abs(qj - T.lj0)) >= 2;
+      m1 = m1 && max(abs(qi - T.li1), abs(qj - T.lj1)) >= 2;
+    }
+    const double2* c = coef + P.coef_off[l] + (size_t)q * P.K;
+    const double v0 = far_eval_generic(c, P.M, T.x0 - zx, T.y0 - zy, P.t2);
+    const double v1 = far_eval_generic(c, P.M, T.x1 - zx, T.y1 - zy, P.t2);
+    acc0 += m0 ? v0 : 0.0;
+    acc1 += m1 ? v1 : 0.0;
+  }
+  if (T.v0) far_s[s0 + lane] = acc0;
+  if (T.v1) far_s[s0 + 32 + lane] = acc1;
+}
+
+constexpr int kFarWarps = 4;
+constexpr int kFarStages = 4;
+
+template <int M>
+size_t far_smem() {
+  constexpr int K = (M + 1) * (M + 2) / 2;
+  return (size_t)kFarWarps * kFarStages * K * 16 + kFarWarps * kFarStages * 8 +
+         kFarWarps * kMaxList * 4;
+}
+
+template <int M>
+void run_far(const TreeParams& P, const int4* items, int n_items, const double2* coef,
+             double* far_s, cudaStream_t s) {
+  auto kern = k_m2p_far<M, kFarWarps, kFarStages>;
+  const size_t smem = far_smem<M>();
+  static bool configured = false;  // per template instance
+  if (!configured) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    configured = true;
+  }
+  const unsigned grid = (unsigned)((n_items + kFarWarps - 1) / kFarWarps);
+  kern<<<grid, kFarWarps * 32, smem, s>>>(P, items, n_items, coef, far_s);
+}
+
+template <int M>
+void run_p2m(const TreeParams& P, const double* u_s, double2* mu, cudaStream_t s) {
+  const long long n_leaves = 1ll << (2 * (P.L + 1));
+  k_p2m_leaf<M><<<(unsigned)((n_leaves + 3) / 4), 128, 0, s>>>(P, u_s, mu);
+}
+
+#define IMQ_FOR_SPECIALISED_M(X) X(0) X(1) X(2) X(4) X(6) X(8) X(10) X(12) X(14) X(16) X(18) X(20)
+
+}  // namespace
+
+bool m2p_specialised(int M) {
+  switch (M) {
+#define X(m) case m:
+    IMQ_FOR_SPECIALISED_M(X)
+#undef X
+    return true;
+    default:
+      return false;
+  }
+}
+
+void launch_p2m_leaf(const TreeParams& P, const double* u_s, double2* mu, cudaStream_t s) {
+  switch (P.M) {
+#define X(m)                    \
+  case m:                       \
+    run_p2m<m>(P, u_s, mu, s); \
+    return;
+    IMQ_FOR_SPECIALISED_M(X)
+#undef X
+    default: {
+      const long long n = (1ll << (2 * (P.L + 1))) * (long long)P.Ke;
+      k_p2m_leaf_generic<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(P, u_s, mu);
+    }
+  }
+}
+
+void launch_m2m(const TreeParams& P, int level, double2* mu, const double* binom,
+                cudaStream_t s) {
+  const size_t smem = (size_t)(4 * P.Ke + 4 * (P.M + 1)) * sizeof(double2);
+  static size_t configured = 0;
+  if (smem > 48 * 1024 && smem > configured) {
+    cudaFuncSetAttribute(k_m2m, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    configured = smem;
+  }
+  const int threads = ((P.Ke + 31) / 32) * 32 > 1024 ? 1024 : ((P.Ke + 31) / 32) * 32;
+  const unsigned nb = 1u << (2 * (level + 1));
+  k_m2m<<<nb, threads, smem, s>>>(P, level, mu, binom);
+}
+
+void launch_transform(const TreeParams& P, const double2* mu, double2* coef,
+                      const TransformTable& T, cudaStream_t s) {
+  const size_t smem = (size_t)P.Ke * sizeof(double2);
+  const int threads = ((P.K + 31) / 32) * 32 > 1024 ? 1024 : ((P.K + 31) / 32) * 32;
+  for (int l = 1; l <= P.L; ++l) {
+    const unsigned nb = 1u << (2 * (l + 1));
+    k_transform<<<nb, threads, smem, s>>>(P, l, mu, coef, T);
+  }
+}
+
+void launch_m2p_far(const TreeParams& P, const int4* items, int n_items, const double2* coef,
+                    double* far_s, cudaStream_t s) {
+  if (n_items == 0) return;
+  switch (P.M) {
+#define X(m)                                      \
+  case m:                                         \
+    run_far<m>(P, items, n_items, coef, far_s, s); \
+    return;
+    IMQ_FOR_SPECIALISED_M(X)
+#undef X
+    default: {
+      constexpr int W = 4;
+      k_m2p_far_generic<W><<<(unsigned)((n_items + W - 1) / W), W * 32, 0, s>>>(
+          P, items, n_items, coef, far_s);
+    }
+  }
+}
+
+}  // namespace imqk

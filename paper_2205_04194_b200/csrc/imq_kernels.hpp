@@ -1,0 +1,91 @@
+// imq_kernels.hpp -- host-visible launch wrappers for the sm_100a kernels.
+//
+// Data layout in HBM (all device arrays owned by DeviceOperator):
+//   xs, ys      [N]   double  point coordinates in Morton (leaf-major) order
+//   leaf        [N]   uint32  finest-level Morton key of each sorted point
+//   perm        [N]   int32   sorted position -> original index (stable sort,
+//                             so each leaf lists its points in ascending index
+//                             order exactly like BlockTree::buckets,
+//                             partition.cpp:53-54)
+//   leaf_start  [4^(L+1)+1]   first sorted position of every leaf; block q at
+//                             level l covers leaves [q<<2(L-l), (q+1)<<2(L-l))
+//   mu          [sum_l 4^(l+1) * Ke] double2  raw planar moments per block,
+//               mu_{m,i} = sum_j u_j |e_j|^{2i} e_j^m, e_j = y_j - z (complex)
+//   coef        [sum_l 4^(l+1) * K]  double2  far-field coefficients C_{m,k}
+//               in Horner order (m = M..0, k = M..m); see DESIGN.md §3.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace imqk {
+
+constexpr int kMaxLevels = 14;  // 2(L+1) <= 30 Morton bits
+
+struct TreeParams {
+  int N, M, K, Ke, L;
+  double t, t2;
+  double ox, oy;                    // bounding-square origin
+  double cell[kMaxLevels + 1];      // cell[l] = side / 2^(l+1), as partition.cpp:46
+  long long mu_off[kMaxLevels + 1];    // first double2 of level l in mu
+  long long coef_off[kMaxLevels + 1];  // first double2 of level l in coef
+  const double* xs;
+  const double* ys;
+  const uint32_t* leaf;
+  const int* leaf_start;
+};
+
+// Transform table mu -> C: for output slot o (Horner order),
+// C[o] = sum_{e in [off[o], off[o+1])} val[e] * mu[idx[e]].
+struct TransformTable {
+  const int* off;
+  const int* idx;
+  const double* val;
+};
+
+// ---- tree / binning (tree.cu)
+void launch_minmax(const double* xy, long long n, double* partial, int nparts, double* out5,
+                   cudaStream_t s);
+int minmax_parts(long long n);
+void launch_bin(const double* xy, long long n, double ox, double oy, double cellL, int gridL,
+                uint32_t* keys, int* idx, cudaStream_t s);
+void launch_gather_points(const double* xy, const int* perm, long long n, double* xs,
+                          double* ys, cudaStream_t s);
+void launch_leaf_start(const uint32_t* keys_sorted, long long n, long long n_leaves,
+                       int* leaf_start, cudaStream_t s);
+void launch_gather(const double* src, const int* perm, long long n, double* dst,
+                   cudaStream_t s);
+void launch_scatter(const double* src, const int* perm, long long n, double* dst,
+                    cudaStream_t s);
+size_t sort_temp_bytes(long long n, int bits);
+void launch_sort(void* temp, size_t temp_bytes, const uint32_t* k_in, uint32_t* k_out,
+                 const int* v_in, int* v_out, long long n, int bits, cudaStream_t s);
+
+// ---- expansion (expansion.cu)
+void launch_p2m_leaf(const TreeParams& P, const double* u_s, double2* mu, cudaStream_t s);
+void launch_m2m(const TreeParams& P, int level, double2* mu, const double* binom,
+                cudaStream_t s);
+void launch_transform(const TreeParams& P, const double2* mu, double2* coef,
+                      const TransformTable& T, cudaStream_t s);
+void launch_m2p_far(const TreeParams& P, const int4* items, int n_items, const double2* coef,
+                    double* far_s, cudaStream_t s);
+bool m2p_specialised(int M);
+
+// ---- direct interactions (direct.cu)
+void launch_p2p_near(const TreeParams& P, const int4* items, int n_items, const double* u_s,
+                     const double* far_s, double* out, const int* perm, cudaStream_t s);
+void launch_direct(const double* txy, long long nt, const double* sxy, const double* sval,
+                   long long ns, double t2, double* out, cudaStream_t s);
+
+// ---- vector kernels for the device-resident GMRES (blas.cu)
+int dot_parts(long long n);
+void launch_dot(const double* a, const double* b, long long n, double* partial, int nparts,
+                double* out, int take_sqrt, cudaStream_t s);
+void launch_axpy_dev(double* y, const double* x, long long n, const double* alpha_dev,
+                     double sign, cudaStream_t s);
+void launch_axpy(double* y, const double* x, long long n, double alpha, cudaStream_t s);
+void launch_div(double* out, const double* x, long long n, double d, cudaStream_t s);
+void launch_sub(double* r, const double* f, const double* w, long long n, cudaStream_t s);
+void launch_nonfinite(const double* x, long long n, int* flag, cudaStream_t s);
+double measure_dfma_peak(int iters, float* ms_out);  // TFLOP/s of the DFMA pipe
+
+}  // namespace imqk

@@ -1,0 +1,498 @@
+// operator.cu -- build / apply / solve of the device-resident fast operator.
+//
+// Build (reference fastmv.cpp:32-77, partition.cpp:9-85), all on the GPU
+// except O(#leaves) bookkeeping:
+//   H2D points -> min/max + finiteness reduction -> bounding square (host,
+//   reference arithmetic) -> bit-exact finest-level binning to Morton keys ->
+//   stable radix sort (key, index) -> gathered SoA coordinates -> leaf offsets
+//   -> work lists for the far (<= 64 targets of one level-(L-1) block per warp)
+//   and near (<= 32 targets of one leaf per warp) kernels.
+// Interaction lists are never materialised: kernels enumerate them on the fly
+// (the reference's O(grid^4) list build, partition.cpp:56-72, is 151 s at L=8).
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include <new>
+#include <stdexcept>
+
+#include "host_math.hpp"
+#include "imq_device.cuh"
+#include "operator.hpp"
+
+namespace imqh {
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return;
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    throw std::bad_alloc();
+  }
+  throw cuda_error(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+}
+
+namespace {
+
+template <typename T>
+T* dalloc(size_t count, const char* what) {
+  T* p = nullptr;
+  if (count == 0) count = 1;
+  cuda_check(cudaMalloc(&p, count * sizeof(T)), what);
+  return p;
+}
+template <typename T>
+void dfree(T*& p) {
+  if (p) cudaFree(p);
+  p = nullptr;
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+}  // namespace
+
+DeviceOperator::DeviceOperator(const double* xy_host, size_t n, double t, int M, int levels) {
+  if (n == 0) throw std::invalid_argument("build_operator: empty point set");
+  check_t(t);  // KernelParams(t) precedes build_operator (capi.cpp:110)
+  if (n > (size_t)INT_MAX) throw std::invalid_argument("build_operator: too many points");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    throw cuda_error("no CUDA device available: the B200 build has no CPU fallback");
+  }
+  cuda_check(cudaGetDevice(&device_), "cudaGetDevice");
+  N_ = (int)n;
+  M_ = M;
+  t_ = t;
+  cuda_check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "stream create");
+  pending_levels_ = levels;
+  try {
+    build(xy_host);
+  } catch (...) {
+    release();
+    throw;
+  }
+}
+
+DeviceOperator::~DeviceOperator() { release(); }
+
+void DeviceOperator::release() {
+  DeviceGuard g(device_);
+  if (stream_) cudaStreamSynchronize(stream_);
+  dfree(d_xs_); dfree(d_ys_); dfree(d_leaf_); dfree(d_perm_); dfree(d_leaf_start_);
+  dfree(d_far_items_); dfree(d_near_items_);
+  dfree(d_tr_off_); dfree(d_tr_idx_); dfree(d_tr_val_); dfree(d_binom_);
+  dfree(d_mu_); dfree(d_coef_); dfree(d_u_); dfree(d_us_); dfree(d_far_); dfree(d_b_);
+  if (stream_) cudaStreamDestroy(stream_);
+  stream_ = nullptr;
+}
+
+void DeviceOperator::build(const double* xy_host) {
+  cudaStream_t s = stream_;
+  const long long n = N_;
+  double* d_xy = dalloc<double>(2 * (size_t)n, "points");
+  uint32_t* d_keys = nullptr;
+  int* d_idx = nullptr;
+  void* d_tmp = nullptr;
+  double* d_part = nullptr;
+  try {
+    cuda_check(cudaMemcpyAsync(d_xy, xy_host, 2 * (size_t)n * sizeof(double),
+                               cudaMemcpyHostToDevice, s),
+               "H2D points");
+    const int nparts = imqk::minmax_parts(n);
+    d_part = dalloc<double>(5 * (size_t)nparts + 5, "minmax");
+    imqk::launch_minmax(d_xy, n, d_part, nparts, d_part + 5 * (size_t)nparts, s);
+    double ext[5];
+    cuda_check(cudaMemcpyAsync(ext, d_part + 5 * (size_t)nparts, sizeof ext,
+                               cudaMemcpyDeviceToHost, s),
+               "D2H extrema");
+    cuda_check(cudaStreamSynchronize(s), "minmax");
+    if (ext[4] > 0.0) throw std::invalid_argument("build_operator: non-finite coordinate");
+    check_M(M_);
+    K_ = order_K(M_);
+    Ke_ = order_Ke(M_);
+    square_from_extrema(ext[0], ext[1], ext[2], ext[3], sq_);
+    if (L_ <= 0) L_ = pending_levels_ > 0 ? pending_levels_ : auto_level(N_, M_);
+    if (L_ > imqk::kMaxLevels - 1)
+      throw std::invalid_argument("build_operator: levels must be <= 13 on this build");
+
+    // ---- tree parameters
+    P_.N = N_; P_.M = M_; P_.K = K_; P_.Ke = Ke_; P_.L = L_;
+    P_.t = t_; P_.t2 = t_ * t_;
+    P_.ox = sq_[0]; P_.oy = sq_[1];
+    long long mo = 0, co = 0;
+    for (int l = 1; l <= L_; ++l) {
+      const int grid = 1 << (l + 1);
+      P_.cell[l] = sq_[2] / grid;  // partition.cpp:46 (double / int)
+      P_.mu_off[l] = mo;
+      P_.coef_off[l] = co;
+      mo += (long long)grid * grid * Ke_;
+      co += (long long)grid * grid * K_;
+    }
+    coef_count_ = (size_t)co;
+
+    // ---- bin + stable Morton sort
+    const int gridL = 1 << (L_ + 1);
+    const int bits = 2 * (L_ + 1);
+    d_keys = dalloc<uint32_t>((size_t)n, "keys");
+    d_idx = dalloc<int>((size_t)n, "idx");
+    d_leaf_ = dalloc<uint32_t>((size_t)n, "leaf");
+    d_perm_ = dalloc<int>((size_t)n, "perm");
+    imqk::launch_bin(d_xy, n, sq_[0], sq_[1], P_.cell[L_], gridL, d_keys, d_idx, s);
+    const size_t tb = imqk::sort_temp_bytes(n, bits);
+    d_tmp = dalloc<unsigned char>(tb, "sort temp");
+    imqk::launch_sort(d_tmp, tb, d_keys, d_leaf_, d_idx, d_perm_, n, bits, s);
+    d_xs_ = dalloc<double>((size_t)n, "xs");
+    d_ys_ = dalloc<double>((size_t)n, "ys");
+    imqk::launch_gather_points(d_xy, d_perm_, n, d_xs_, d_ys_, s);
+    const long long n_leaves = 1ll << (2 * (L_ + 1));
+    d_leaf_start_ = dalloc<int>((size_t)n_leaves + 1, "leaf_start");
+    imqk::launch_leaf_start(d_leaf_, n, n_leaves, d_leaf_start_, s);
+    std::vector<int> ls((size_t)n_leaves + 1);
+    cuda_check(cudaMemcpyAsync(ls.data(), d_leaf_start_, ls.size() * sizeof(int),
+                               cudaMemcpyDeviceToHost, s),
+               "D2H leaf_start");
+    cuda_check(cudaStreamSynchronize(s), "tree build");
+    cuda_check(cudaGetLastError(), "tree kernels");
+
+    // ---- work lists
+    const long long n_par = 1ll << (2 * L_);  // level L-1 (level 0 = 2x2 for L = 1)
+    far_items_h_.clear();
+    near_items_h_.clear();
+    for (long long p = 0; p < n_par; ++p) {
+      const int a = ls[(size_t)(4 * p)], b = ls[(size_t)(4 * p + 4)];
+      for (int c = a; c < b; c += 64) far_items_h_.push_back(make_int4((int)p, c, std::min(64, b - c), 0));
+    }
+    for (long long q = 0; q < n_leaves; ++q) {
+      const int a = ls[(size_t)q], b = ls[(size_t)q + 1];
+      for (int c = a; c < b; c += 32) near_items_h_.push_back(make_int4((int)q, c, std::min(32, b - c), 0));
+    }
+    n_far_ = (int)far_items_h_.size();
+    n_near_ = (int)near_items_h_.size();
+    d_far_items_ = dalloc<int4>(far_items_h_.size(), "far items");
+    d_near_items_ = dalloc<int4>(near_items_h_.size(), "near items");
+    cuda_check(cudaMemcpyAsync(d_far_items_, far_items_h_.data(), far_items_h_.size() * sizeof(int4),
+                               cudaMemcpyHostToDevice, s), "H2D far items");
+    cuda_check(cudaMemcpyAsync(d_near_items_, near_items_h_.data(),
+                               near_items_h_.size() * sizeof(int4), cudaMemcpyHostToDevice, s),
+               "H2D near items");
+
+    // ---- tables
+    const Transform tr = build_transform(M_, t_);
+    const std::vector<double> bn = binomials(M_);
+    d_tr_off_ = dalloc<int>(tr.off.size(), "transform");
+    d_tr_idx_ = dalloc<int>(tr.idx.size(), "transform");
+    d_tr_val_ = dalloc<double>(tr.val.size(), "transform");
+    d_binom_ = dalloc<double>(bn.size(), "binomials");
+    cuda_check(cudaMemcpyAsync(d_tr_off_, tr.off.data(), tr.off.size() * sizeof(int),
+                               cudaMemcpyHostToDevice, s), "H2D transform");
+    cuda_check(cudaMemcpyAsync(d_tr_idx_, tr.idx.data(), tr.idx.size() * sizeof(int),
+                               cudaMemcpyHostToDevice, s), "H2D transform");
+    cuda_check(cudaMemcpyAsync(d_tr_val_, tr.val.data(), tr.val.size() * sizeof(double),
+                               cudaMemcpyHostToDevice, s), "H2D transform");
+    cuda_check(cudaMemcpyAsync(d_binom_, bn.data(), bn.size() * sizeof(double),
+                               cudaMemcpyHostToDevice, s), "H2D binomials");
+    T_.off = d_tr_off_;
+    T_.idx = d_tr_idx_;
+    T_.val = d_tr_val_;
+
+    // ---- expansion storage + workspace
+    d_mu_ = dalloc<double2>((size_t)mo, "moments");
+    d_coef_ = dalloc<double2>((size_t)co, "coefficients");
+    d_u_ = dalloc<double>((size_t)n, "u");
+    d_us_ = dalloc<double>((size_t)n, "u sorted");
+    d_far_ = dalloc<double>((size_t)n, "far");
+    d_b_ = dalloc<double>((size_t)n, "b");
+
+    P_.xs = d_xs_;
+    P_.ys = d_ys_;
+    P_.leaf = d_leaf_;
+    P_.leaf_start = d_leaf_start_;
+    cuda_check(cudaStreamSynchronize(s), "operator build");
+  } catch (...) {
+    dfree(d_xy); dfree(d_keys); dfree(d_idx); dfree(d_tmp); dfree(d_part);
+    throw;
+  }
+  dfree(d_xy); dfree(d_keys); dfree(d_idx); dfree(d_tmp); dfree(d_part);
+}
+
+void DeviceOperator::moments(const double* d_us, cudaStream_t s) {
+  imqk::launch_p2m_leaf(P_, d_us, d_mu_, s);
+  for (int l = L_ - 1; l >= 1; --l) imqk::launch_m2m(P_, l, d_mu_, d_binom_, s);
+  imqk::launch_transform(P_, d_mu_, d_coef_, T_, s);
+}
+
+void DeviceOperator::far_near(const double* d_us, double* d_out, const int* perm,
+                              cudaStream_t s, int far_begin, int far_end, int near_begin,
+                              int near_end) {
+  far_begin = std::max(0, far_begin);
+  far_end = std::min(far_end, n_far_);
+  near_begin = std::max(0, near_begin);
+  near_end = std::min(near_end, n_near_);
+  if (far_end > far_begin)
+    imqk::launch_m2p_far(P_, d_far_items_ + far_begin, far_end - far_begin, d_coef_, d_far_, s);
+  if (near_end > near_begin)
+    imqk::launch_p2p_near(P_, d_near_items_ + near_begin, near_end - near_begin, d_us, d_far_,
+                          d_out, perm, s);
+}
+
+void DeviceOperator::apply_sorted_locked(const double* d_us, double* d_out, const int* perm,
+                                         cudaStream_t s) {
+  moments(d_us, s);
+  far_near(d_us, d_out, perm, s, 0, n_far_, 0, n_near_);
+}
+
+void DeviceOperator::apply_sorted(const double* d_us, double* d_bs, cudaStream_t stream) {
+  std::lock_guard<std::mutex> lk(mtx_);
+  DeviceGuard g(device_);
+  cudaStream_t s = stream ? stream : stream_;
+  apply_sorted_locked(d_us, d_bs, nullptr, s);
+  cuda_check(cudaGetLastError(), "apply_sorted launch");
+}
+
+void DeviceOperator::apply_device(const double* d_u, double* d_b, cudaStream_t stream) {
+  std::lock_guard<std::mutex> lk(mtx_);
+  DeviceGuard g(device_);
+  cudaStream_t s = stream ? stream : stream_;
+  imqk::launch_gather(d_u, d_perm_, N_, d_us_, s);
+  apply_sorted_locked(d_us_, d_b, d_perm_, s);
+  cuda_check(cudaGetLastError(), "apply_device launch");
+}
+
+void DeviceOperator::apply_host(const double* u, double* b) {
+  std::lock_guard<std::mutex> lk(mtx_);
+  DeviceGuard g(device_);
+  cudaStream_t s = stream_;
+  cuda_check(cudaMemcpyAsync(d_u_, u, (size_t)N_ * sizeof(double), cudaMemcpyHostToDevice, s),
+             "H2D u");
+  imqk::launch_gather(d_u_, d_perm_, N_, d_us_, s);
+  apply_sorted_locked(d_us_, d_b_, d_perm_, s);
+  cuda_check(cudaMemcpyAsync(b, d_b_, (size_t)N_ * sizeof(double), cudaMemcpyDeviceToHost, s),
+             "D2H b");
+  cuda_check(cudaStreamSynchronize(s), "apply");
+  cuda_check(cudaGetLastError(), "apply kernels");
+}
+
+void DeviceOperator::copy_permutation(int* perm_host) const {
+  DeviceGuard g(device_);
+  cuda_check(cudaMemcpy(perm_host, d_perm_, (size_t)N_ * sizeof(int), cudaMemcpyDeviceToHost),
+             "D2H perm");
+}
+void DeviceOperator::copy_leaf_start(std::vector<int>& out) const {
+  DeviceGuard g(device_);
+  const long long n_leaves = 1ll << (2 * (L_ + 1));
+  out.resize((size_t)n_leaves + 1);
+  cuda_check(cudaMemcpy(out.data(), d_leaf_start_, out.size() * sizeof(int),
+                        cudaMemcpyDeviceToHost),
+             "D2H leaf_start");
+}
+
+// Exact far / near pair counts of this tree (the flop model's P_far, P_near).
+PairCounts DeviceOperator::pair_counts() {
+  std::lock_guard<std::mutex> lk(mtx_);
+  if (have_counts_) return counts_;
+  std::vector<int> ls;
+  copy_leaf_start(ls);
+  const int L = L_;
+  auto count = [&](int l, int i, int j) -> long long {
+    const uint32_t q = imqdev::morton((uint32_t)i, (uint32_t)j);
+    const int sh = 2 * (L - l);
+    return (long long)ls[(size_t)(q + 1) << sh] - ls[(size_t)q << sh];
+  };
+  double far = 0, near = 0;
+  for (int l = 1; l <= L; ++l) {
+    const int grid = 1 << (l + 1);
+    for (int i = 0; i < grid; ++i)
+      for (int j = 0; j < grid; ++j) {
+        const long long nt = count(l, i, j);
+        if (!nt) continue;
+        int lo_i = 0, hi_i = grid - 1, lo_j = 0, hi_j = grid - 1;
+        if (l >= 2) {
+          lo_i = std::max(0, 2 * (i / 2 - 1)); hi_i = std::min(grid - 1, 2 * (i / 2 + 1) + 1);
+          lo_j = std::max(0, 2 * (j / 2 - 1)); hi_j = std::min(grid - 1, 2 * (j / 2 + 1) + 1);
+        }
+        long long ns = 0;
+        for (int qi = lo_i; qi <= hi_i; ++qi)
+          for (int qj = lo_j; qj <= hi_j; ++qj)
+            if (std::max(std::abs(qi - i), std::abs(qj - j)) >= 2 && count(l, qi, qj) > 0) ++ns;
+        far += (double)nt * (double)ns;
+        if (l == L) {
+          long long nn = 0;
+          for (int qi = std::max(0, i - 1); qi <= std::min(grid - 1, i + 1); ++qi)
+            for (int qj = std::max(0, j - 1); qj <= std::min(grid - 1, j + 1); ++qj)
+              nn += count(l, qi, qj);
+          near += (double)nt * (double)nn;
+        }
+      }
+  }
+  counts_.far_pairs = far;
+  counts_.near_pairs = near;
+  counts_.far_items = n_far_;
+  counts_.near_items = n_near_;
+  have_counts_ = true;
+  return counts_;
+}
+
+// ------------------------------------------------------------------ GMRES --
+// solver.cpp:41-159 with every N-vector resident on the device in Morton
+// order.  MGS coefficients are produced and consumed on the device; the host
+// sees only the (j+2)-entry Hessenberg column per Arnoldi step.
+SolveResult DeviceOperator::solve_host(const double* f, double tol, int max_iter, int restart,
+                                       double* c) {
+  if (!(tol > 0.0) || !std::isfinite(tol))
+    throw std::invalid_argument("iterative_solve: tol must be positive");
+  if (max_iter < 0) throw std::invalid_argument("iterative_solve: max_iter must be >= 0");
+  if (restart < 1) throw std::invalid_argument("iterative_solve: restart must be >= 1");
+  const size_t n = (size_t)N_;
+  for (size_t i = 0; i < n; ++i)
+    if (!std::isfinite(f[i]))
+      throw std::runtime_error("iterative_solve: non-finite value at iteration 0");
+
+  std::lock_guard<std::mutex> lk(mtx_);
+  DeviceGuard g(device_);
+  cudaStream_t s = stream_;
+  SolveResult rep;
+  std::fill(c, c + n, 0.0);
+
+  const int mcap = std::max(1, std::min(restart, max_iter));
+  const int nparts = imqk::dot_parts(N_);
+  double *d_f = nullptr, *d_x = nullptr, *d_r = nullptr, *d_w = nullptr, *d_V = nullptr;
+  double *d_h = nullptr, *d_part = nullptr;
+  int* d_flag = nullptr;
+  auto cleanup = [&]() {
+    dfree(d_f); dfree(d_x); dfree(d_r); dfree(d_w); dfree(d_V); dfree(d_h); dfree(d_part);
+    dfree(d_flag);
+  };
+  try {
+    d_f = dalloc<double>(n, "gmres f");
+    d_x = dalloc<double>(n, "gmres x");
+    d_r = dalloc<double>(n, "gmres r");
+    d_w = dalloc<double>(n, "gmres w");
+    d_V = dalloc<double>(n * (size_t)(mcap + 1), "gmres basis");
+    d_h = dalloc<double>((size_t)mcap + 2, "gmres h");
+    d_part = dalloc<double>((size_t)nparts, "gmres partials");
+    d_flag = dalloc<int>(1, "gmres flag");
+    // f in Morton order
+    cuda_check(cudaMemcpyAsync(d_u_, f, n * sizeof(double), cudaMemcpyHostToDevice, s), "H2D f");
+    imqk::launch_gather(d_u_, d_perm_, N_, d_f, s);
+    auto nrm2 = [&](const double* v) {
+      double out;
+      imqk::launch_dot(v, v, N_, d_part, nparts, d_h + mcap + 1, 1, s);
+      cuda_check(cudaMemcpyAsync(&out, d_h + mcap + 1, sizeof(double), cudaMemcpyDeviceToHost, s),
+                 "D2H norm");
+      cuda_check(cudaStreamSynchronize(s), "norm");
+      return out;
+    };
+    auto matvec = [&](const double* in, double* out) { apply_sorted_locked(in, out, nullptr, s); };
+
+    const double bnorm = nrm2(d_f);
+    if (bnorm == 0.0) {
+      rep.converged = true;
+      rep.cycle_residuals.push_back(0.0);
+      cleanup();
+      return rep;
+    }
+    cuda_check(cudaMemsetAsync(d_x, 0, n * sizeof(double), s), "memset x");
+    cuda_check(cudaMemcpyAsync(d_r, d_f, n * sizeof(double), cudaMemcpyDeviceToDevice, s), "r=f");
+    int total = 0;
+    double rel = 1.0;
+    std::vector<std::vector<double>> hcol((size_t)mcap);
+    std::vector<double> cs((size_t)mcap), sn((size_t)mcap), gv((size_t)mcap + 1), y((size_t)mcap),
+        hbuf((size_t)mcap + 2);
+    while (true) {
+      if (total > 0) {
+        matvec(d_x, d_w);
+        imqk::launch_sub(d_r, d_f, d_w, N_, s);
+      }
+      rel = nrm2(d_r) / bnorm;
+      rep.cycle_residuals.push_back(rel);
+      if (!std::isfinite(rel))
+        throw std::runtime_error("iterative_solve: non-finite value at iteration " +
+                                 std::to_string(total));
+      if (rel <= tol || total >= max_iter) break;
+      const int m = std::min(restart, max_iter - total);
+      const double beta = rel * bnorm;
+      imqk::launch_div(d_V, d_r, N_, beta, s);
+      std::fill(gv.begin(), gv.end(), 0.0);
+      gv[0] = beta;
+      int k = 0;
+      for (int j = 0; j < m; ++j) {
+        double* Vj = d_V + (size_t)j * n;
+        matvec(Vj, d_w);
+        ++total;
+        cuda_check(cudaMemsetAsync(d_flag, 0, sizeof(int), s), "flag");
+        imqk::launch_nonfinite(d_w, N_, d_flag, s);
+        for (int i = 0; i <= j; ++i) {
+          const double* Vi = d_V + (size_t)i * n;
+          imqk::launch_dot(d_w, Vi, N_, d_part, nparts, d_h + i, 0, s);
+          imqk::launch_axpy_dev(d_w, Vi, N_, d_h + i, -1.0, s);
+        }
+        imqk::launch_dot(d_w, d_w, N_, d_part, nparts, d_h + j + 1, 1, s);
+        int flag = 0;
+        cuda_check(cudaMemcpyAsync(hbuf.data(), d_h, (size_t)(j + 2) * sizeof(double),
+                                   cudaMemcpyDeviceToHost, s), "D2H h");
+        cuda_check(cudaMemcpyAsync(&flag, d_flag, sizeof(int), cudaMemcpyDeviceToHost, s),
+                   "D2H flag");
+        cuda_check(cudaStreamSynchronize(s), "arnoldi step");
+        if (flag)
+          throw std::runtime_error("iterative_solve: non-finite value at iteration " +
+                                   std::to_string(total));
+        auto& h = hcol[(size_t)j];
+        h.assign(hbuf.begin(), hbuf.begin() + j + 2);
+        const double hh = h[(size_t)j + 1];
+        for (int i = 0; i < j; ++i) {
+          const double t0 = cs[(size_t)i] * h[(size_t)i] + sn[(size_t)i] * h[(size_t)i + 1];
+          h[(size_t)i + 1] = -sn[(size_t)i] * h[(size_t)i] + cs[(size_t)i] * h[(size_t)i + 1];
+          h[(size_t)i] = t0;
+        }
+        const double denom = std::hypot(h[(size_t)j], hh);
+        if (denom == 0.0) {
+          k = j;
+          break;
+        }
+        cs[(size_t)j] = h[(size_t)j] / denom;
+        sn[(size_t)j] = hh / denom;
+        h[(size_t)j] = denom;
+        h[(size_t)j + 1] = 0.0;
+        gv[(size_t)j + 1] = -sn[(size_t)j] * gv[(size_t)j];
+        gv[(size_t)j] = cs[(size_t)j] * gv[(size_t)j];
+        k = j + 1;
+        const double rel_est = std::fabs(gv[(size_t)j + 1]) / bnorm;
+        if (rel_est <= tol || hh == 0.0) break;
+        if (j + 1 < m) imqk::launch_div(d_V + (size_t)(j + 1) * n, d_w, N_, hh, s);
+      }
+      if (k == 0) break;
+      for (int i = k - 1; i >= 0; --i) {
+        double sacc = gv[(size_t)i];
+        for (int l = i + 1; l < k; ++l) sacc -= hcol[(size_t)l][(size_t)i] * y[(size_t)l];
+        y[(size_t)i] = sacc / hcol[(size_t)i][(size_t)i];
+      }
+      for (int i = 0; i < k; ++i) imqk::launch_axpy(d_x, d_V + (size_t)i * n, N_, y[(size_t)i], s);
+    }
+    imqk::launch_scatter(d_x, d_perm_, N_, d_b_, s);
+    cuda_check(cudaMemcpyAsync(c, d_b_, n * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H c");
+    cuda_check(cudaStreamSynchronize(s), "gmres");
+    cuda_check(cudaGetLastError(), "gmres kernels");
+    rep.iterations = total;
+    rep.final_relative_residual = rel;
+    rep.converged = rel <= tol;
+  } catch (...) {
+    cudaStreamSynchronize(s);
+    cleanup();
+    throw;
+  }
+  cleanup();
+  return rep;
+}
+
+}  // namespace imqh

@@ -1,0 +1,117 @@
+// operator.hpp -- the device-resident fast operator behind imq_operator.
+//
+// B200 counterpart of imq::FastOperator (reference fastmv.hpp:19-38):
+// immutable after build; holds the Morton-sorted points, leaf offsets, work
+// lists and transform tables in HBM plus the per-apply workspace.  apply()
+// and solve() serialise on an internal mutex, which keeps the reference's
+// "safe for concurrent application to distinct vectors" contract
+// (fastmv.hpp:17-18) without duplicating the ~GB workspace.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "imq_kernels.hpp"
+
+namespace imqh {
+
+struct cuda_error : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+void cuda_check(cudaError_t e, const char* what);
+
+struct SolveResult {
+  int iterations = 0;
+  double final_relative_residual = 0.0;
+  bool converged = false;
+  std::vector<double> cycle_residuals;
+};
+
+struct PairCounts {
+  double far_pairs = 0, near_pairs = 0;  // exact, from the built tree
+  int64_t far_items = 0, near_items = 0;
+};
+
+class DeviceOperator {
+ public:
+  DeviceOperator(const double* xy_host, size_t n, double t, int M, int levels);
+  ~DeviceOperator();
+  DeviceOperator(const DeviceOperator&) = delete;
+  DeviceOperator& operator=(const DeviceOperator&) = delete;
+
+  int size() const { return N_; }
+  int levels() const { return L_; }
+  int order() const { return M_; }
+  double shape() const { return t_; }
+  int device() const { return device_; }
+  const double* square() const { return sq_; }
+
+  // Host vectors in original point order (imq_operator_apply semantics).
+  void apply_host(const double* u, double* b);
+  // Device vectors in original order; enqueued on `stream` (nullptr: the
+  // operator's own stream), no host synchronisation.
+  void apply_device(const double* d_u, double* d_b, cudaStream_t stream);
+  // Device vectors already in Morton order (no gather/scatter).
+  void apply_sorted(const double* d_us, double* d_bs, cudaStream_t stream);
+
+  SolveResult solve_host(const double* f, double tol, int max_iter, int restart, double* c);
+
+  // Sorted-order helpers exposed for tests / multi-GPU orchestration.
+  void copy_permutation(int* perm_host) const;
+  void copy_leaf_start(std::vector<int>& out) const;
+  PairCounts pair_counts();
+
+  // Stage-by-stage access (multi-GPU sharding drives these individually).
+  void moments(const double* d_us, cudaStream_t s);  // P2M + M2M + transform
+  void far_near(const double* d_us, double* d_out, const int* perm, cudaStream_t s,
+                int far_begin, int far_end, int near_begin, int near_end);
+  double2* coef_ptr() const { return d_coef_; }
+  size_t coef_count() const { return coef_count_; }
+  const imqk::TreeParams& params() const { return P_; }
+  cudaStream_t stream() const { return stream_; }
+  const std::vector<int4>& far_items_host() const { return far_items_h_; }
+  const std::vector<int4>& near_items_host() const { return near_items_h_; }
+
+ private:
+  void build(const double* xy_host);
+  void release();
+  void apply_sorted_locked(const double* d_us, double* d_bs, const int* perm,
+                           cudaStream_t s);
+
+  int device_ = 0;
+  cudaStream_t stream_ = nullptr;
+  int N_ = 0, M_ = 0, K_ = 0, Ke_ = 0, L_ = 0, pending_levels_ = 0;
+  double t_ = 0.0;
+  double sq_[3] = {0, 0, 0};
+  imqk::TreeParams P_{};
+  imqk::TransformTable T_{};
+  std::mutex mtx_;
+
+  double* d_xs_ = nullptr;
+  double* d_ys_ = nullptr;
+  uint32_t* d_leaf_ = nullptr;
+  int* d_perm_ = nullptr;
+  int* d_leaf_start_ = nullptr;
+  int4* d_far_items_ = nullptr;
+  int4* d_near_items_ = nullptr;
+  int n_far_ = 0, n_near_ = 0;
+  std::vector<int4> far_items_h_, near_items_h_;
+  int* d_tr_off_ = nullptr;
+  int* d_tr_idx_ = nullptr;
+  double* d_tr_val_ = nullptr;
+  double* d_binom_ = nullptr;
+  double2* d_mu_ = nullptr;
+  double2* d_coef_ = nullptr;
+  size_t coef_count_ = 0;
+  double* d_u_ = nullptr;   // original-order input staging
+  double* d_us_ = nullptr;  // sorted input
+  double* d_far_ = nullptr; // sorted far field
+  double* d_b_ = nullptr;   // original-order output staging
+  bool have_counts_ = false;
+  PairCounts counts_{};
+};
+
+}  // namespace imqh

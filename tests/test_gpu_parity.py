@@ -1,0 +1,244 @@
+"""GPU parity of the CUDA product against the oracle and the reference's own
+golden outputs.  Everything goes through the C ABI (libimqfast.so).
+
+Tolerances: bit-exact for binning / bucket membership / ordering (integer
+work); rel_err_inf <= 1e-10 for the fast product vs the reference fast product
+(north_star); |gpu - dense| <= 2 |ref - dense| + 1e-12 against the direct sum.
+"""
+import numpy as np
+import pytest
+
+from conftest import rel_err_inf
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+
+
+def morton(i, j):
+    i = np.asarray(i, dtype=np.uint64)
+    j = np.asarray(j, dtype=np.uint64)
+    out = np.zeros_like(i)
+    for b in range(16):
+        out |= ((i >> np.uint64(b)) & np.uint64(1)) << np.uint64(2 * b + 1)
+        out |= ((j >> np.uint64(b)) & np.uint64(1)) << np.uint64(2 * b)
+    return out
+
+
+def check_binning(imq, oracle, xy, t, m, L):
+    op = imq.FastOperator(xy, t, m, L)
+    L = op.levels
+    perm = op.permutation()
+    ls = op.leaf_start()
+    n = xy.size // 2
+    assert np.array_equal(np.sort(perm), np.arange(n))
+    leaf_of_sorted = np.repeat(np.arange(ls.size - 1), np.diff(ls))
+    leaf = np.empty(n, dtype=np.int64)
+    leaf[perm] = leaf_of_sorted
+    for lvl in range(1, L + 1):
+        g = 1 << (lvl + 1)
+        ids = oracle.block_ids(xy, lvl).astype(np.int64)
+        want = morton(ids // g, ids % g).astype(np.int64)
+        got = leaf >> (2 * (L - lvl))
+        assert np.array_equal(got, want), f"level {lvl}"
+    # within every bucket the points keep ascending original index
+    # (BlockTree::buckets order, partition.cpp:53-54)
+    for c in range(ls.size - 1):
+        seg = perm[ls[c]:ls[c + 1]]
+        assert np.all(np.diff(seg) > 0)
+    return op
+
+
+def test_binning_bit_exact(imq, oracle, golden):
+    c = golden("cfg1")
+    check_binning(imq, oracle, c["xy"], 0.1, 10, 2)
+    cl = golden("clustered")
+    check_binning(imq, oracle, cl["xy"], 0.02, 14, 5)
+    # lattice points sitting exactly on cell edges (upper edges go up)
+    g = np.linspace(0.0, 1.0, 33)
+    X, Y = np.meshgrid(g, g, indexing="ij")
+    xy = np.stack([X.ravel(), Y.ravel()], 1).ravel()
+    check_binning(imq, oracle, xy, 0.5, 4, 4)
+    # degenerate square (all points equal) and a thin strip (dy = 0)
+    check_binning(imq, oracle, np.tile([0.3, 0.4], 50), 0.7, 4, 2)
+    strip = np.stack([np.linspace(-3, 5, 400), np.full(400, 2.0)], 1).ravel()
+    check_binning(imq, oracle, strip, 0.1, 6, 3)
+
+
+def test_config1_fast_matches_reference(imq, golden):
+    c = golden("cfg1")
+    op = imq.FastOperator(c["xy"], 0.1, 10, 2)
+    b = op.apply(c["u"])
+    assert rel_err_inf(b, c["b_fast"]) <= TOL
+    ref_err = rel_err_inf(c["b_fast"], c["b_dense"])
+    assert abs(rel_err_inf(b, c["b_dense"]) - ref_err) <= ref_err  # same truncation error
+    d = imq.dense_matvec(c["xy"], 0.1, c["u"])
+    assert rel_err_inf(d, c["b_dense"]) <= 1e-13
+
+
+def test_families_vs_golden(imq, golden):
+    g = golden("family600")
+    for name in ("halton", "random"):
+        for t in (0.5, 1.0, 2.0):
+            for L in (1, 2):
+                b = imq.FastOperator(g[name], t, 10, L).apply(g["u"])
+                assert rel_err_inf(b, g[f"{name}_t{t}_L{L}"]) <= TOL, (name, t, L)
+
+
+def test_clustered_vs_golden(imq, golden):
+    c = golden("clustered")
+    b = imq.FastOperator(c["xy"], 0.02, 14, 3).apply(c["u"])
+    assert rel_err_inf(b, c["b_fast"]) <= TOL
+    ref = rel_err_inf(c["b_fast"], c["b_dense"])
+    assert rel_err_inf(b, c["b_dense"]) <= 2 * ref + 1e-12
+
+
+def test_order_shape_sweep_vs_golden(imq, golden):
+    s = golden("sweep2048")
+    for cc in (0.001, 0.01, 0.1, 1.0):
+        for p in (4, 8, 12, 16, 20):
+            b = imq.FastOperator(s["xy"], cc, p, 3).apply(s["u"])
+            assert rel_err_inf(b, s[f"c{cc}_p{p}"]) <= TOL, (cc, p)
+
+
+def test_generic_orders_vs_oracle(imq, oracle, golden):
+    h = golden("highm")
+    assert rel_err_inf(imq.FastOperator(h["xy"], 0.03, 30, 0).apply(h["u"]), h["b_m30"]) <= TOL
+    assert rel_err_inf(imq.FastOperator(h["xy"], 0.03, 0, 2).apply(h["u"]), h["b_m0"]) <= TOL
+    assert rel_err_inf(imq.FastOperator(h["xy"], 0.03, 1, 2).apply(h["u"]), h["b_m1"]) <= TOL
+    xy = oracle.random_vector(2 * 3000, 9) * 0.5 + 0.5
+    u = oracle.random_vector(3000, 10)
+    for m in (3, 5, 7, 9, 11, 13, 15, 17, 19, 22, 25, 40):
+        b = imq.FastOperator(xy, 0.2, m, 3).apply(u)
+        assert rel_err_inf(b, oracle.fast_matvec(xy, 0.2, m, 3, u)) <= TOL, m
+
+
+def test_degenerate_trees(imq, golden):
+    d = golden("degenerate")
+    b = imq.FastOperator(d["same"], 0.7, 10, 1).apply(d["u12"])
+    assert rel_err_inf(b, d["b_same"]) <= 1e-14
+    one = imq.FastOperator(np.array([0.3, 0.4]), 2.0, 10, 1).apply([3.0])
+    assert one[0] == pytest.approx(1.5, rel=1e-15)
+
+
+def test_linearity_determinism_symmetry(imq, oracle):
+    xy = oracle.halton2d(3000)
+    op = imq.FastOperator(xy, 1.0, 10, 2)
+    u1, u2 = oracle.random_vector(3000, 7), oracle.random_vector(3000, 8)
+    a, c = 0.7, -1.3
+    b1, b2, bm = op.apply(u1), op.apply(u2), op.apply(a * u1 + c * u2)
+    assert rel_err_inf(bm, a * b1 + c * b2) <= 1e-12
+    assert np.array_equal(op.apply(u1), b1)
+    op2 = imq.FastOperator(xy, 1.0, 10, 2)
+    assert np.array_equal(op2.apply(u1), b1)
+    utAv, vtAu = u1 @ b2, u2 @ b1
+    scale = np.abs(u1 * b2).sum() + np.abs(u2 * b1).sum()
+    assert abs(utAv - vtAu) <= 5e-8 * scale
+
+
+def test_basis_columns_within_level1_bound(imq, oracle):
+    # test_fastmv.cpp:146-164
+    n = 400
+    xy = oracle.halton2d(n)
+    op = imq.FastOperator(xy, 1.0, 10, 1)
+    for j in (0, 57, 399):
+        e = np.zeros(n)
+        e[j] = 1.0
+        col = op.apply(e)
+        d = xy.reshape(-1, 2) - xy.reshape(-1, 2)[j]
+        exact = 1.0 / np.sqrt(1.0 + (d ** 2).sum(1))
+        assert np.max(np.abs(col - exact)) <= 2.8668e-9 * (1 + 1e-6)
+
+
+def test_dense_and_interpolant_vs_oracle(imq, oracle):
+    xy = oracle.random_vector(2 * 5000, 3) * 0.5 + 0.5
+    u = oracle.random_vector(5000, 4)
+    assert rel_err_inf(imq.dense_matvec(xy, 0.01, u), oracle.dense_matvec(xy, 0.01, u)) <= 1e-13
+    q = oracle.halton2d(777)
+    got = imq.evaluate_interpolant(xy, u, 0.05, q)
+    assert rel_err_inf(got, oracle.evaluate_interpolant(xy, u, 0.05, q)) <= 1e-13
+
+
+def test_gmres_against_reference(imq, golden):
+    g = golden("gmres")
+    op = imq.FastOperator(g["xy400"], 0.03, 12, 0)
+    r = op.solve(g["f400"], 1e-10, 300, 50)
+    assert r.converged and r.final_relative_residual <= 1e-10
+    assert abs(r.iterations - int(g["it400"])) <= 2
+    assert rel_err_inf(r.c, g["c400"]) <= 1e-6
+    # config-2 shape: iteration-matched comparison (SURVEY 8(d) protocol)
+    op2 = imq.FastOperator(g["xy2"], 0.05, 12, 0)
+    r2 = op2.solve(g["f2"], 1e-8, 100, 50)
+    assert r2.iterations == int(g["it2"])
+    assert abs(r2.final_relative_residual - float(g["res2"])) <= 1e-3 * float(g["res2"])
+    assert r2.cycle_residuals == sorted(r2.cycle_residuals, reverse=True)
+
+
+def test_gmres_semantics(imq, oracle):
+    # test_solver.cpp:26-43, 93-123
+    op = imq.FastOperator(np.array([0.4, 0.6]), 2.5, 4, 1)
+    r = op.solve(np.array([3.0]), 1e-12)
+    assert r.converged and r.iterations == 1 and r.c[0] == pytest.approx(7.5, rel=1e-12)
+    op = imq.FastOperator(oracle.halton2d(50), 1.0, 6, 1)
+    r = op.solve(np.ones(50), 1e-10, 0)
+    assert not r.converged and r.iterations == 0 and np.all(r.c == 0.0)
+    assert r.final_relative_residual == pytest.approx(1.0, rel=1e-15)
+    f = np.ones(50)
+    f[4] = np.nan
+    with pytest.raises(imq.IMQError) as e:
+        op.solve(f)
+    assert "iteration" in e.value.msg and e.value.code == 4
+    for bad in (dict(tol=0.0), dict(max_iter=-1), dict(restart=0)):
+        with pytest.raises(imq.IMQError) as e:
+            op.solve(np.ones(50), **{**dict(tol=1e-8, max_iter=10, restart=5), **bad})
+        assert e.value.code == 1
+    # restart-boundary residuals never increase (test_solver.cpp:93-105)
+    op = imq.FastOperator(oracle.halton2d(300), 0.02, 30, 0)
+    f = oracle.random_vector(300, 11)
+    r = op.solve(f, 1e-12, 60, 10)
+    cr = r.cycle_residuals
+    assert len(cr) >= 2 and all(cr[i] <= cr[i - 1] * (1 + 1e-10) for i in range(1, len(cr)))
+    assert r.final_relative_residual == pytest.approx(cr[-1], rel=1e-12)
+    res = np.linalg.norm(f - op.apply(r.c)) / np.linalg.norm(f)
+    assert res == pytest.approx(r.final_relative_residual, rel=1e-9)
+
+
+def test_device_pointer_path_matches_host_path(imq, golden):
+    torch = pytest.importorskip("torch")
+    c = golden("cfg1")
+    op = imq.FastOperator(c["xy"], 0.1, 10, 2)
+    b_host = op.apply(c["u"])
+    du = torch.tensor(c["u"], device="cuda")
+    db = torch.empty_like(du)
+    s = torch.cuda.current_stream()
+    op.apply_device(du, db, s)
+    s.synchronize()
+    assert np.array_equal(db.cpu().numpy(), b_host)
+    perm = torch.tensor(op.permutation().astype(np.int64), device="cuda")
+    dbs = torch.empty_like(du)
+    op.apply_sorted_device(du[perm].contiguous(), dbs, s)
+    s.synchronize()
+    out = torch.empty_like(du)
+    out[perm] = dbs
+    assert np.array_equal(out.cpu().numpy(), b_host)
+
+
+def test_verify_suite_passes(imq, oracle):
+    fails, rows = imq.verify(oracle.halton2d(2000), 1.0, 10, 0, 42)
+    names = [r[0] for r in rows]
+    assert names == ["separation_ratio", "separation_ratio_planar", "interaction_counts",
+                     "exact_cover", "oracle_equivalence", "m0_sine_moments", "linearity",
+                     "determinism"]
+    assert fails == 0, rows
+
+
+def test_operator_errors(imq):
+    with pytest.raises(imq.IMQError) as e:
+        imq.FastOperator(np.array([0.1, np.inf]), 1.0, 4, 1)
+    assert e.value.code == 1 and "non-finite" in e.value.msg
+    with pytest.raises(imq.IMQError) as e:
+        imq.FastOperator(np.array([0.1, 0.2]), 1.0, -1, 1)
+    assert e.value.code == 1
+    op = imq.FastOperator(imq.halton2d(10), 1.0, 4, 0)
+    assert op.size == 10 and op.levels == imq.auto_level(10, 4)
+    with pytest.raises(imq.IMQError):
+        op.apply(np.ones(9))
