@@ -1,0 +1,405 @@
+#!/usr/bin/env python
+"""Headline benchmark: fast IMQ matvec points/s at config 4 (BASELINE.json).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+Workload (BASELINE.json configs[3]): N = 16,777,216 uniform points in [0,1)^2
+(seed 0), c = t = 0.01, p = M = 16, leaf <= 128 -> L = 8 (mean 64 per leaf);
+step k applies the operator to u_k = random_vector(N, 1000 + k).  A step is
+one full fast product (P2M + M2M + transform + M2P far + P2P near); operator
+setup is reported separately.  Inputs (134 MB per vector, 855 MB of far-field
+coefficients) exceed the 126 MB L2, so no flush is needed between steps.
+
+N > 1 GPUs (torchrun): every rank holds the Morton-sorted points, computes the
+moments of the (replicated) source vector and evaluates its contiguous range
+of far/near work items -- the target points are sharded, the work per rank
+shrinks with N ("strong" scaling).  value = N points / max-over-ranks time.
+
+--impl reference: the reference's own CPU implementation (oracle/_ref, the
+unmodified /root/reference sources compiled by oracle/Makefile) on the host
+cores, on a bounded sample of the same workload (see cpu_sample()).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CFG = dict(n=16_777_216, t=0.01, m=16, levels=8, seed=0)
+METRIC = "fast IMQ matvec points/sec at N=16M"
+UNIT = "points/s"
+
+
+def f_pair(M):
+    """SURVEY 8(d) algorithmic flops per far (point, block) pair (FMA = 2)."""
+    K = (M + 1) * (M + 2) // 2
+    Ke = sum(n // 2 + 1 for n in range(M + 1))
+    return 4 * K + 6 * Ke + 6 * (M + 1) + 12
+
+
+def f_p2m(M):
+    Ke = sum(n // 2 + 1 for n in range(M + 1))
+    return 5 * Ke + 7 * (M + 1) + 4
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# --------------------------------------------------------------- CPU side
+def cpu_sample(total_steps: int):
+    """Bounded sample of the config-4 workload for the CPU reference: same
+    point distribution, c, p and leaf occupancy (mean 64 per leaf), smaller N."""
+    if total_steps <= 20:
+        return dict(n=262_144, t=0.01, m=16, levels=5, seed=0)
+    return dict(n=65_536, t=0.01, m=16, levels=4, seed=0)
+
+
+def run_cpu_reference(steps: int, warmup: int):
+    """Times the reference fast matvec on the host cores; returns a dict."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from paper_2205_04194_b200 import inputs
+    s = cpu_sample(steps + warmup)
+    xy = inputs.uniform_points(s["n"], s["seed"])
+    cores = os.cpu_count() or 1
+    try:
+        from oracle import Reference  # the unmodified reference, compiled (oracle/_ref)
+        R = Reference()
+        R.set_threads(cores)
+        kind = "reference"
+        t0 = time.perf_counter()
+        h = R.create(xy, s["t"], s["m"], s["levels"])
+        setup = time.perf_counter() - t0
+
+        def step(k):
+            R.apply(h, inputs.random_vector(s["n"], 1000 + k))
+    except FileNotFoundError:
+        from oracle import Oracle  # restatement (port) when the reference was not built
+        O = Oracle()
+        kind = "port"
+        setup = 0.0
+        h = None
+
+        def step(k):
+            O.fast_matvec(xy, s["t"], s["m"], s["levels"], inputs.random_vector(s["n"], 1000 + k))
+    times = []
+    for k in range(warmup + steps):
+        t0 = time.perf_counter()
+        step(k)
+        dt = time.perf_counter() - t0
+        if k >= warmup:
+            times.append(dt)
+    if h is not None:
+        R.destroy(h)
+    mean = sum(times) / len(times)
+    sample = (f"N={s['n']} uniform seed 0, c={s['t']}, p={s['m']}, L={s['levels']} "
+              f"(mean 64 pts/leaf like cfg 4), {len(times)} matvec(s) after {warmup} warm-up; "
+              f"operator build {setup:.2f}s excluded")
+    return dict(value=s["n"] / mean, unit=UNIT, cores=cores, kind=kind, sample=sample,
+                sec_per_step=mean)
+
+
+def reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    r = run_cpu_reference(args.steps, args.warmup)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": r["value"], "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": r["sec_per_step"] * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "cfg4-shaped CPU sample: " + r["sample"]},
+        "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------- GPU side
+def b200_arm(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2205_04194_b200 as P
+    from paper_2205_04194_b200 import inputs
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    P.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    n = args.n or CFG["n"]
+    L = CFG["levels"] if n == CFG["n"] else 0
+    t, M = CFG["t"], CFG["m"]
+    xy = inputs.uniform_points(n, CFG["seed"])
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    op = P.FastOperator(xy, t, M, L)
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t0
+    st = op.stats()
+    L = op.levels
+    far_items, near_items = len(op.items("far")), len(op.items("near"))
+    fr = (far_items * rank // world, far_items * (rank + 1) // world)
+    nr = (near_items * rank // world, near_items * (rank + 1) // world)
+
+    stream = torch.cuda.current_stream()
+    nvec = min(args.steps + args.warmup, 8)
+    host_u = [torch.from_numpy(inputs.random_vector(n, 1000 + k)) for k in range(nvec)]
+    dev_u = [h.cuda() for h in host_u]
+    d_b = torch.empty(n, dtype=torch.float64, device="cuda")
+    d_us = torch.empty_like(d_b)
+    perm = torch.from_numpy(op.permutation().astype(np.int64)).cuda()
+
+    def step(k):
+        u = dev_u[k % nvec]
+        if world == 1:
+            op.apply_device(u, d_b, stream)
+        else:
+            torch.index_select(u, 0, perm, out=d_us)
+            op.moments(d_us, stream)
+            op.far_near(d_us, d_b, fr, nr, stream)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for k in range(args.warmup):
+        step(k)
+    barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for k in range(args.steps):
+            step(args.warmup + k)
+        e1.record(stream)
+        barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    ms_t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms = float(ms_t.item())
+    value = n / (ms * 1e-3)
+
+    # ---- e2e: the public call with host buffers (pinned), copies included
+    pin_u = [torch.empty(n, dtype=torch.float64, pin_memory=True) for _ in range(2)]
+    pin_b = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    for i in range(2):
+        pin_u[i].copy_(host_u[i])
+    e2e_steps = max(3, min(args.steps, 10))
+
+    def e2e_step(k):
+        if world == 1:
+            P.capi.check(P.capi.lib().imq_operator_apply(
+                op.handle, P.api.C.cast(pin_u[k % 2].data_ptr(), P.api._dp),
+                P.api.C.cast(pin_b.data_ptr(), P.api._dp)))
+        else:
+            d_u = dev_u[0]
+            d_u.copy_(pin_u[k % 2], non_blocking=True)
+            torch.index_select(d_u, 0, perm, out=d_us)
+            op.moments(d_us, stream)
+            op.far_near(d_us, d_b, fr, nr, stream)
+            lo, hi = (n * rank // world, n * (rank + 1) // world)
+            pin_b[lo:hi].copy_(d_b[lo:hi], non_blocking=True)
+            torch.cuda.synchronize()
+
+    e2e_step(0)
+    barrier()
+    t0 = time.perf_counter()
+    for k in range(e2e_steps):
+        e2e_step(k)
+    barrier()
+    e2e_s = torch.tensor([(time.perf_counter() - t0) / e2e_steps], device="cuda",
+                         dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
+    e2e_value = n / float(e2e_s.item())
+
+    # ---- roofline of the dominant kernel (M2P far field), timed live
+    torch.index_select(dev_u[0], 0, perm, out=d_us)
+    op.moments(d_us, stream)
+    nf = far_items
+    op.far_near(d_us, d_b, (0, nf), (0, 0), stream)
+    torch.cuda.synchronize()
+    reps = 3
+    e0.record(stream)
+    for _ in range(reps):
+        op.far_near(d_us, d_b, (0, nf), (0, 0), stream)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    far_ms = e0.elapsed_time(e1) / reps
+    e0.record(stream)
+    op.far_near(d_us, d_b, (0, 0), (0, near_items), stream)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    near_ms = e0.elapsed_time(e1)
+    e0.record(stream)
+    op.moments(d_us, stream)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    mom_ms = e0.elapsed_time(e1)
+    peak_tf, _ = P.api.fp64_peak(8192)
+    far_flops = st["far_pairs"] * f_pair(M)
+    achieved = far_flops / (far_ms * 1e-3) / 1e12
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "far_kernel_ncu.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+        except (OSError, ValueError):
+            traffic = None
+
+    # ---- secondary: config-2 GMRES (iteration-capped; 1e-8 is not reachable)
+    gm = None
+    if rank == 0 and world == 1 and not args.no_gmres:
+        xy2 = inputs.uniform_points(65536, 0)
+        f2 = inputs.cfg2_rhs(xy2)
+        with P.FastOperator(xy2, 0.05, 12, 0) as op2:
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            r = op2.solve(f2, 1e-8, args.gmres_iters, 50)
+            gs = time.perf_counter() - t0
+        cr = r.cycle_residuals
+        gm = {"config": "cfg2: N=65536 uniform, c=0.05, p=12, L=auto(2), GMRES(50), x0=0",
+              "tol": 1e-8, "max_iter": args.gmres_iters, "iterations": r.iterations,
+              "time_s": gs, "ms_per_iteration": gs * 1e3 / max(1, r.iterations),
+              "final_relative_residual": r.final_relative_residual,
+              "converged": r.converged,
+              "cycle_residuals_head": cr[:6], "cycle_residuals_tail": cr[-3:]}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = run_cpu_reference(1, 0)
+        cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+
+    if rank == 0:
+        launches_per_step = (1 if world == 1 else 0) + 1 + (L - 1) + L + 1 + 1
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "cfg4: fast IMQ matvec, N=16777216 uniform [0,1)^2 seed 0, "
+                                   "c=0.01, p=16, L=8 (leaf<=128, mean 64), "
+                                   "u_k=random_vector(N,1000+k)" if n == CFG["n"] else
+                                   f"cfg4-shaped, N={n}, L={L}",
+                       "n_points": n, "levels": L, "order": M, "shape": t,
+                       "far_pairs": st["far_pairs"], "near_pairs": st["near_pairs"],
+                       "setup_s": setup_s, "l2": "inputs larger than L2 (no flush)",
+                       "parallelism": f"points sharded {world}-way (Morton ranges)"},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * n * world,
+                    "d2h_bytes_per_step": 8 * n,
+                    "path": "imq_operator_apply (C ABI, pinned host u/b)" if world == 1 else
+                            "sharded ext API, pinned host buffers"},
+            "roofline": {"bound": "fp64", "kernel": "k_m2p_far (M2P far field)",
+                         "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
+                         "frac": achieved / peak_tf, "traffic": traffic,
+                         "peak_source": "measured live: DFMA probe (imq_ext_fp64_peak); "
+                                        "MEASURED_PEAKS.json has no FP64 entry",
+                         "flops_per_launch": far_flops,
+                         "flop_model": "SURVEY 8(d): P_far x (4K+6Ke+6(M+1)+12)",
+                         "far_ms": far_ms, "near_ms": near_ms, "moments_ms": mom_ms,
+                         "far_share_of_step": far_ms / ms if world == 1 else None},
+            "cpu_baseline": cpu,
+            "clocks": clk.summary(),
+            "gpu_launches": launches_per_step * args.steps,
+            "gmres": gm,
+        }
+        print(json.dumps(line), flush=True)
+    op.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
+    ap.add_argument("--n", type=int, default=0, help="override N (development only)")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-gmres", action="store_true")
+    ap.add_argument("--gmres-iters", type=int, default=2000)
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "b200":
+        args.warmup = 3
+    if args.impl == "reference":
+        return reference_arm(args)
+    return b200_arm(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -124,7 +124,9 @@ IMQ_API int imq_verify(const imq_verify_config* cfg, imq_verify_callback cb, voi
  * ---------------------------------------------------------------------- */
 
 /* b = A u on device buffers (original point order) enqueued on `stream`
- * (a cudaStream_t, NULL = the operator's stream); no host synchronisation. */
+ * (a cudaStream_t; NULL = the legacy default stream, as in the CUDA runtime);
+ * no host synchronisation.  Stream-ordered calls on one operator share its
+ * workspace: issue them on one stream (or synchronise between streams). */
 IMQ_API int imq_ext_operator_apply_device(const imq_operator* op, const double* d_u, double* d_b,
                                   void* stream);
 /* Same on vectors already permuted into the operator's Morton order. */

@@ -255,17 +255,15 @@ void DeviceOperator::apply_sorted_locked(const double* d_us, double* d_out, cons
 void DeviceOperator::apply_sorted(const double* d_us, double* d_bs, cudaStream_t stream) {
   std::lock_guard<std::mutex> lk(mtx_);
   DeviceGuard g(device_);
-  cudaStream_t s = stream ? stream : stream_;
-  apply_sorted_locked(d_us, d_bs, nullptr, s);
+  apply_sorted_locked(d_us, d_bs, nullptr, stream);
   cuda_check(cudaGetLastError(), "apply_sorted launch");
 }
 
 void DeviceOperator::apply_device(const double* d_u, double* d_b, cudaStream_t stream) {
   std::lock_guard<std::mutex> lk(mtx_);
   DeviceGuard g(device_);
-  cudaStream_t s = stream ? stream : stream_;
-  imqk::launch_gather(d_u, d_perm_, N_, d_us_, s);
-  apply_sorted_locked(d_us_, d_b, d_perm_, s);
+  imqk::launch_gather(d_u, d_perm_, N_, d_us_, stream);
+  apply_sorted_locked(d_us_, d_b, d_perm_, stream);
   cuda_check(cudaGetLastError(), "apply_device launch");
 }
 

@@ -51,8 +51,8 @@ class DeviceOperator {
 
   // Host vectors in original point order (imq_operator_apply semantics).
   void apply_host(const double* u, double* b);
-  // Device vectors in original order; enqueued on `stream` (nullptr: the
-  // operator's own stream), no host synchronisation.
+  // Device vectors in original order; enqueued on `stream` (0 = the legacy
+  // default stream, as everywhere in CUDA), no host synchronisation.
   void apply_device(const double* d_u, double* d_b, cudaStream_t stream);
   // Device vectors already in Morton order (no gather/scatter).
   void apply_sorted(const double* d_us, double* d_bs, cudaStream_t stream);
