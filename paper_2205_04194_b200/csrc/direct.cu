@@ -18,26 +18,37 @@ using namespace imqdev;
 namespace {
 
 constexpr int kNearWarps = 4;
+constexpr int kNearMaxR = 4;  // a near work item holds <= 32 * kNearMaxR targets of one leaf
 
+// Warp per near work item: <= 32 R targets of one leaf, R per lane.  Every
+// source point staged in the warp's shared-memory tile is read back once per
+// lane and reused for its R targets (register blocking against the per-LDS
+// issue cost).
+template <int R>
 __global__ void __launch_bounds__(kNearWarps * 32) k_p2p_near(
     const TreeParams P, const int4* __restrict__ items, int n_items,
     const double* __restrict__ u_s, const double* __restrict__ far_s, double* __restrict__ out,
     const int* __restrict__ perm) {
-  __shared__ double sx[kNearWarps][32], sy[kNearWarps][32], su[kNearWarps][32];
+  __shared__ double2 sxy[kNearWarps][32];
+  __shared__ double su[kNearWarps][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int it = blockIdx.x * kNearWarps + warp;
   if (it >= n_items) return;
   const int4 item = items[it];
   const uint32_t leaf = (uint32_t)item.x;
   const int s0 = item.y, cnt = item.z;
-  const bool valid = lane < cnt;
-  const int p = valid ? s0 + lane : s0;
-  const double xi = P.xs[p], yi = P.ys[p];
+  double xi[R], yi[R], acc[R];
+#pragma unroll
+  for (int p = 0; p < R; ++p) {
+    const int q = lane + 32 * p < cnt ? s0 + lane + 32 * p : s0;
+    xi[p] = P.xs[q];
+    yi[p] = P.ys[q];
+    acc[p] = 0.0;
+  }
   const double t2 = P.t2;
   const int g = 1 << (P.L + 1);
   int li, lj;
   demorton(leaf, li, lj);
-  double acc = 0.0;
   for (int qi = max(0, li - 1); qi <= min(g - 1, li + 1); ++qi) {
     for (int qj = max(0, lj - 1); qj <= min(g - 1, lj + 1); ++qj) {
       const uint32_t q = morton(qi, qj);
@@ -46,30 +57,31 @@ __global__ void __launch_bounds__(kNearWarps * 32) k_p2p_near(
         const int j = base + lane;
         __syncwarp();
         if (j < b) {
-          sx[warp][lane] = P.xs[j];
-          sy[warp][lane] = P.ys[j];
+          sxy[warp][lane] = make_double2(P.xs[j], P.ys[j]);
           su[warp][lane] = u_s[j];
         }
         __syncwarp();
         const int nsrc = min(32, b - base);
-        int k = 0;
-        for (; k + 4 <= nsrc; k += 4) {
+#pragma unroll 4
+        for (int k = 0; k < nsrc; ++k) {
+          const double2 sp = sxy[warp][k];
+          const double uk = su[warp][k];
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
-            const double dx = xi - sx[warp][k + kk], dy = yi - sy[warp][k + kk];
-            acc = fma(su[warp][k + kk], rsqrt(fma(dx, dx, fma(dy, dy, t2))), acc);
+          for (int p = 0; p < R; ++p) {
+            const double dx = xi[p] - sp.x, dy = yi[p] - sp.y;
+            acc[p] = fma(uk, rsqrt_pos(fma(dx, dx, fma(dy, dy, t2))), acc[p]);
           }
-        }
-        for (; k < nsrc; ++k) {
-          const double dx = xi - sx[warp][k], dy = yi - sy[warp][k];
-          acc = fma(su[warp][k], rsqrt(fma(dx, dx, fma(dy, dy, t2))), acc);
         }
       }
     }
   }
-  if (valid) {
-    const double v = far_s[p] + acc;
-    out[perm ? perm[p] : p] = v;
+#pragma unroll
+  for (int p = 0; p < R; ++p) {
+    if (lane + 32 * p < cnt) {
+      const int q = s0 + lane + 32 * p;
+      const double v = far_s[q] + acc[p];
+      out[perm ? perm[q] : q] = v;
+    }
   }
 }
 
@@ -104,12 +116,12 @@ __global__ void __launch_bounds__(kDirThreads) k_direct(const double* __restrict
 #pragma unroll 8
       for (int k = 0; k < kDirThreads; ++k) {
         const double dx = xi - sp[k].x, dy = yi - sp[k].y;
-        acc = fma(sv[k], rsqrt(fma(dx, dx, fma(dy, dy, t2))), acc);
+        acc = fma(sv[k], rsqrt_pos(fma(dx, dx, fma(dy, dy, t2))), acc);
       }
     } else {
       for (int k = 0; k < nsrc; ++k) {
         const double dx = xi - sp[k].x, dy = yi - sp[k].y;
-        acc = fma(sv[k], rsqrt(fma(dx, dx, fma(dy, dy, t2))), acc);
+        acc = fma(sv[k], rsqrt_pos(fma(dx, dx, fma(dy, dy, t2))), acc);
       }
     }
   }
@@ -118,11 +130,22 @@ __global__ void __launch_bounds__(kDirThreads) k_direct(const double* __restrict
 
 }  // namespace
 
-void launch_p2p_near(const TreeParams& P, const int4* items, int n_items, const double* u_s,
-                     const double* far_s, double* out, const int* perm, cudaStream_t s) {
-  if (n_items == 0) return;
-  k_p2p_near<<<(unsigned)((n_items + kNearWarps - 1) / kNearWarps), kNearWarps * 32, 0, s>>>(
-      P, items, n_items, u_s, far_s, out, perm);
+int near_max_points_per_lane() { return kNearMaxR; }
+
+void launch_p2p_near(const TreeParams& P, const int4* items, const int* group_off, int begin,
+                     int end, const double* u_s, const double* far_s, double* out,
+                     const int* perm, cudaStream_t s) {
+  for (int R = 1; R <= kNearMaxR; ++R) {
+    const int lo = max(begin, group_off[R - 1]), hi = min(end, group_off[R]);
+    if (hi <= lo) continue;
+    const unsigned grid = (unsigned)((hi - lo + kNearWarps - 1) / kNearWarps);
+    switch (R) {
+      case 1: k_p2p_near<1><<<grid, kNearWarps * 32, 0, s>>>(P, items + lo, hi - lo, u_s, far_s, out, perm); break;
+      case 2: k_p2p_near<2><<<grid, kNearWarps * 32, 0, s>>>(P, items + lo, hi - lo, u_s, far_s, out, perm); break;
+      case 3: k_p2p_near<3><<<grid, kNearWarps * 32, 0, s>>>(P, items + lo, hi - lo, u_s, far_s, out, perm); break;
+      default: k_p2p_near<4><<<grid, kNearWarps * 32, 0, s>>>(P, items + lo, hi - lo, u_s, far_s, out, perm); break;
+    }
+  }
 }
 
 void launch_direct(const double* txy, long long nt, const double* sxy, const double* sval,

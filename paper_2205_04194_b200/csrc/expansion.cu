@@ -19,6 +19,8 @@
 //     q = 1/rho^2: ~M^2+4M DFMA per pair instead of a Legendre recurrence
 //     with one division per (n, m).
 #include <cstdio>
+#include <algorithm>
+#include <cstdlib>
 
 #include "imq_device.cuh"
 #include "imq_kernels.hpp"
@@ -156,27 +158,35 @@ __global__ void __launch_bounds__(128) k_p2m_leaf_generic(const TreeParams P,
 // centre - parent centre):
 //   mu'_{a,b} = sum_{p<=a, r<=b} C(a,p) C(b,r) d^{a-p} conj(d)^{b-r} N_{p,r},
 //   N_{p,r} = mu_{p-r, r} (p >= r) or conj(mu_{r-p, p}) (p < r).
+// The four children are folded into one pass: the translated sum is linear in
+// N, so the CTA first forms per child the d-power tables, then every thread
+// walks its (p, r) triangle once per child.  Index / binomial tables live in
+// shared memory (no per-term integer search).
 __global__ void k_m2m(const TreeParams P, int level, double2* __restrict__ mu,
                       const double* __restrict__ binom) {
   extern __shared__ double2 sm[];
   const int M = P.M, Ke = P.Ke;
-  double2* cm = sm;                    // [4][Ke]
-  double2* dp = sm + 4 * Ke;           // [4][M+1] powers of d
+  double2* cm = sm;                          // [4][Ke]
+  double2* dp = sm + 4 * Ke;                 // [4][M+1] powers of d
+  double* bn = reinterpret_cast<double*>(dp + 4 * (M + 1));  // [(M+1)^2]
+  int* moff = reinterpret_cast<int*>(bn + (M + 1) * (M + 1)); // [M+1]
   const uint32_t q = blockIdx.x;
   if (block_count(P, level, q) == 0) return;
   int qi, qj;
   demorton(q, qi, qj);
   const double zx = block_center(P.ox, qi, P.cell[level]);
   const double zy = block_center(P.oy, qj, P.cell[level]);
+  for (int k = threadIdx.x; k < (M + 1) * (M + 1); k += blockDim.x) bn[k] = binom[k];
+  if (threadIdx.x <= M) moff[threadIdx.x] = mu_offset(M, threadIdx.x);
   int have = 0;
   for (int c = 0; c < 4; ++c) {
     const uint32_t ch = 4 * q + c;
     const bool ne = block_count(P, level + 1, ch) > 0;
     have |= (ne ? 1 : 0) << c;
+    if (!ne) continue;
     const double2* src = mu + P.mu_off[level + 1] + (size_t)ch * Ke;
-    for (int o = threadIdx.x; o < Ke; o += blockDim.x)
-      cm[c * Ke + o] = ne ? src[o] : make_double2(0.0, 0.0);
-    if (threadIdx.x == 0) {
+    for (int o = threadIdx.x; o < Ke; o += blockDim.x) cm[c * Ke + o] = src[o];
+    if (threadIdx.x == 32 * (c % max(1, (int)(blockDim.x / 32)))) {
       int ci, cj;
       demorton(ch, ci, cj);
       const double dx = block_center(P.ox, ci, P.cell[level + 1]) - zx;
@@ -192,37 +202,36 @@ __global__ void k_m2m(const TreeParams P, int level, double2* __restrict__ mu,
   }
   __syncthreads();
   for (int o = threadIdx.x; o < Ke; o += blockDim.x) {
-    int m, i;
-    mu_unindex(M, o, m, i);
-    const int a = m + i, b = i;
+    int m = 0, oo = o;
+    while (oo >= (M - m) / 2 + 1) {
+      oo -= (M - m) / 2 + 1;
+      ++m;
+    }
+    const int i = oo, a = m + i, b = i;
     double sr = 0.0, si = 0.0;
     for (int c = 0; c < 4; ++c) {
       if (!((have >> c) & 1)) continue;
       const double2* N = cm + c * Ke;
       const double2* D = dp + c * (M + 1);
       for (int p = 0; p <= a; ++p) {
-        // inner: sum_r C(b,r) conj(d)^{b-r} N_{p,r}
         double ir = 0.0, ii = 0.0;
         for (int r = 0; r <= b; ++r) {
-          double nr, ni;
+          double2 v;
           if (p >= r) {
-            const double2 v = N[mu_offset(M, p - r) + r];
-            nr = v.x; ni = v.y;
+            v = N[moff[p - r] + r];
           } else {
-            const double2 v = N[mu_offset(M, r - p) + p];
-            nr = v.x; ni = -v.y;
+            v = N[moff[r - p] + p];
+            v.y = -v.y;
           }
           const double2 d = D[b - r];  // conj(d)^{b-r} = conj(d^{b-r})
-          const double cb = binom[b * (M + 1) + r];
-          const double tr = d.x * nr + d.y * ni;
-          const double ti = d.x * ni - d.y * nr;
-          ir = fma(cb, tr, ir);
-          ii = fma(cb, ti, ii);
+          const double cb = bn[b * (M + 1) + r];
+          ir = fma(cb, fma(d.x, v.x, d.y * v.y), ir);
+          ii = fma(cb, fma(d.x, v.y, -d.y * v.x), ii);
         }
         const double2 d = D[a - p];
-        const double ca = binom[a * (M + 1) + p];
-        sr = fma(ca, d.x * ir - d.y * ii, sr);
-        si = fma(ca, d.x * ii + d.y * ir, si);
+        const double ca = bn[a * (M + 1) + p];
+        sr = fma(ca, fma(d.x, ir, -d.y * ii), sr);
+        si = fma(ca, fma(d.x, ii, d.y * ir), si);
       }
     }
     // m = 0 moments are real by construction (conjugate-symmetric terms);
@@ -253,7 +262,8 @@ __global__ void k_transform(const TreeParams P, int level, const double2* __rest
 }
 
 // ------------------------------------------------------------------- M2P ---
-constexpr int kMaxList = 384;  // 12 + 27 (L - 2) + 36 <= 372 for L <= 13
+constexpr int kMaxList = 384;
+constexpr int kFarMaxR = 6;  // a far work item holds <= 32 * kFarMaxR targets  // 12 + 27 (L - 2) + 36 <= 372 for L <= 13
 
 // Builds the warp's source list for a work item: every non-empty source block
 // at levels 1..L-1 of the (shared) ancestor lists, then the level-L union over
@@ -320,60 +330,80 @@ __device__ int build_far_list(const TreeParams& P, uint32_t par, int s, int cnt,
   return n;
 }
 
-// Complex Horner evaluation of one source block's expansion at two targets.
-// c: K coefficients (double2) in Horner order; returns the far contribution.
-template <int M>
-__device__ __forceinline__ void far_eval2(const double2* __restrict__ c, double dx0, double dy0,
-                                          double dx1, double dy1, double t2, double& v0,
-                                          double& v1) {
-  const double r0 = rsqrt(fma(dx0, dx0, fma(dy0, dy0, t2)));
-  const double r1 = rsqrt(fma(dx1, dx1, fma(dy1, dy1, t2)));
-  const double q0 = r0 * r0, q1 = r1 * r1;
+// Complex Horner evaluation of one source block's expansion at R targets of
+// the lane.  c: K coefficients (double2) in Horner order.  Every coefficient
+// read from shared memory feeds 2R DFMAs; shared-memory -> register delivery
+// (128 B/clk/SM) is the co-bottleneck with the FP64 pipe, so R >= 3 keeps the
+// kernel on the DFMA roofline (profiles/).
+template <int M, int R>
+__device__ __forceinline__ void far_evalR(const double2* __restrict__ c, const double* dx,
+                                          const double* dy, double t2, double* v) {
+  double r[R], q[R];
+#pragma unroll
+  for (int p = 0; p < R; ++p) {
+    r[p] = rsqrt_pos(fma(dx[p], dx[p], fma(dy[p], dy[p], t2)));
+    q[p] = r[p] * r[p];
+  }
   if constexpr (M == 0) {
-    v0 = c[0].x * r0;
-    v1 = c[0].x * r1;
+#pragma unroll
+    for (int p = 0; p < R; ++p) v[p] = c[0].x * r[p];
   } else {
-    const double xr0 = dx0 * q0, xi0 = -dy0 * q0;
-    const double xr1 = dx1 * q1, xi1 = -dy1 * q1;
+    double xr[R], xi[R], ar[R], ai[R];
     double2 cc = c[0];
-    double ar0 = cc.x, ai0 = cc.y, ar1 = cc.x, ai1 = cc.y;
+#pragma unroll
+    for (int p = 0; p < R; ++p) {
+      xr[p] = dx[p] * q[p];
+      xi[p] = -dy[p] * q[p];
+      ar[p] = cc.x;
+      ai[p] = cc.y;
+    }
     int o = 1;
 #pragma unroll
     for (int m = M - 1; m >= 1; --m) {
       cc = c[o++];
-      double gr0 = cc.x, gi0 = cc.y, gr1 = cc.x, gi1 = cc.y;
+      double gr[R], gi[R];
+#pragma unroll
+      for (int p = 0; p < R; ++p) {
+        gr[p] = cc.x;
+        gi[p] = cc.y;
+      }
 #pragma unroll
       for (int k = M - 1; k >= m; --k) {
         cc = c[o++];
-        gr0 = fma(gr0, q0, cc.x);
-        gi0 = fma(gi0, q0, cc.y);
-        gr1 = fma(gr1, q1, cc.x);
-        gi1 = fma(gi1, q1, cc.y);
-      }
-      const double nr0 = fma(ar0, xr0, fma(-ai0, xi0, gr0));
-      const double ni0 = fma(ar0, xi0, fma(ai0, xr0, gi0));
-      const double nr1 = fma(ar1, xr1, fma(-ai1, xi1, gr1));
-      const double ni1 = fma(ar1, xi1, fma(ai1, xr1, gi1));
-      ar0 = nr0; ai0 = ni0; ar1 = nr1; ai1 = ni1;
-    }
-    // m = 0: real inner polynomial, only the real part of the result is used
-    cc = c[o++];
-    double g0 = cc.x, g1 = cc.x;
 #pragma unroll
-    for (int k = M - 1; k >= 0; --k) {
-      cc = c[o++];
-      g0 = fma(g0, q0, cc.x);
-      g1 = fma(g1, q1, cc.x);
+        for (int p = 0; p < R; ++p) {
+          gr[p] = fma(gr[p], q[p], cc.x);
+          gi[p] = fma(gi[p], q[p], cc.y);
+        }
+      }
+#pragma unroll
+      for (int p = 0; p < R; ++p) {
+        const double nr = fma(ar[p], xr[p], fma(-ai[p], xi[p], gr[p]));
+        const double ni = fma(ar[p], xi[p], fma(ai[p], xr[p], gi[p]));
+        ar[p] = nr;
+        ai[p] = ni;
+      }
     }
-    v0 = fma(ar0, xr0, fma(-ai0, xi0, g0)) * r0;
-    v1 = fma(ar1, xr1, fma(-ai1, xi1, g1)) * r1;
+    // m = 0: real inner polynomial (its imaginary parts are exactly zero)
+    const double* c0 = reinterpret_cast<const double*>(c + o);
+    double g[R];
+#pragma unroll
+    for (int p = 0; p < R; ++p) g[p] = c0[0];
+#pragma unroll
+    for (int k = 1; k <= M; ++k) {
+      const double ck = c0[2 * k];
+#pragma unroll
+      for (int p = 0; p < R; ++p) g[p] = fma(g[p], q[p], ck);
+    }
+#pragma unroll
+    for (int p = 0; p < R; ++p) v[p] = fma(ar[p], xr[p], fma(-ai[p], xi[p], g[p])) * r[p];
   }
 }
 
 // Runtime-order variant (coefficients read through L1 from global memory).
 __device__ __forceinline__ double far_eval_generic(const double2* __restrict__ c, int M,
                                                    double dx, double dy, double t2) {
-  const double r = rsqrt(fma(dx, dx, fma(dy, dy, t2)));
+  const double r = rsqrt_pos(fma(dx, dx, fma(dy, dy, t2)));
   const double q = r * r;
   if (M == 0) return __ldg(&c[0].x) * r;
   const double xr = dx * q, xi = -dy * q;
@@ -398,34 +428,36 @@ __device__ __forceinline__ double far_eval_generic(const double2* __restrict__ c
   return fma(ar, xr, fma(-ai, xi, g)) * r;
 }
 
-struct Target {
-  double x0, y0, x1, y1;
-  int li0, lj0, li1, lj1;
-  bool v0, v1;
+template <int R>
+struct Targets {
+  double x[R], y[R];
+  int li[R], lj[R];
+  bool v[R];
 };
 
-__device__ __forceinline__ Target load_targets(const TreeParams& P, int s, int cnt, int lane) {
-  Target T;
-  const int p0 = s + lane, p1 = s + 32 + lane;
-  T.v0 = lane < cnt;
-  T.v1 = lane + 32 < cnt;
-  const int a0 = T.v0 ? p0 : s, a1 = T.v1 ? p1 : s;
-  T.x0 = P.xs[a0]; T.y0 = P.ys[a0];
-  T.x1 = P.xs[a1]; T.y1 = P.ys[a1];
-  demorton(P.leaf[a0], T.li0, T.lj0);
-  demorton(P.leaf[a1], T.li1, T.lj1);
-  return T;
+template <int R>
+__device__ __forceinline__ void load_targets(const TreeParams& P, int s, int cnt, int lane,
+                                             Targets<R>& T) {
+#pragma unroll
+  for (int p = 0; p < R; ++p) {
+    T.v[p] = lane + 32 * p < cnt;
+    const int a = T.v[p] ? s + lane + 32 * p : s;
+    T.x[p] = P.xs[a];
+    T.y[p] = P.ys[a];
+    demorton(P.leaf[a], T.li[p], T.lj[p]);
+  }
 }
 
-// Warp per work item (<= 64 targets of one level-(L-1) block, 2 per lane).
+// Warp per work item (<= 32 R targets of one level-(L-1) block, R per lane).
 // Source coefficients are staged per warp through a STAGES-deep ring of
-// shared-memory buffers filled by one-instruction TMA bulk copies.
-template <int M, int WARPS, int STAGES>
-__global__ void __launch_bounds__(WARPS * 32) k_m2p_far(const TreeParams P,
-                                                       const int4* __restrict__ items,
-                                                       int n_items,
-                                                       const double2* __restrict__ coef,
-                                                       double* __restrict__ far_s) {
+// shared-memory buffers filled by one-instruction TMA bulk copies
+// (cp.async.bulk + mbarrier complete_tx), lane 0 producing, the warp consuming.
+template <int M, int R, int WARPS, int STAGES, int MINB>
+__global__ void __launch_bounds__(WARPS * 32, MINB) k_m2p_far(const TreeParams P,
+                                                             const int4* __restrict__ items,
+                                                             int n_items,
+                                                             const double2* __restrict__ coef,
+                                                             double* __restrict__ far_s) {
   constexpr int K = (M + 1) * (M + 2) / 2;
   constexpr uint32_t kBytes = K * 16;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -452,7 +484,8 @@ __global__ void __launch_bounds__(WARPS * 32) k_m2p_far(const TreeParams P,
   const uint32_t par = (uint32_t)item.x;
   const int s0 = item.y, cnt = item.z;
   const int n = build_far_list(P, par, s0, cnt, list, lane);
-  const Target T = load_targets(P, s0, cnt, lane);
+  Targets<R> T;
+  load_targets<R>(P, s0, cnt, lane, T);
   const int L = P.L;
 
   auto issue = [&](int e, int slot) {
@@ -466,7 +499,9 @@ __global__ void __launch_bounds__(WARPS * 32) k_m2p_far(const TreeParams P,
   if (lane == 0)
     for (int e = 0; e < STAGES && e < n; ++e) issue(e, e);
 
-  double acc0 = 0.0, acc1 = 0.0;
+  double acc[R];
+#pragma unroll
+  for (int p = 0; p < R; ++p) acc[p] = 0.0;
   for (int e = 0; e < n; ++e) {
     const int slot = e % STAGES;
     const uint32_t ent = list[e];
@@ -475,25 +510,27 @@ __global__ void __launch_bounds__(WARPS * 32) k_m2p_far(const TreeParams P,
     demorton(ent & 0x0fffffffu, qi, qj);
     const double zx = block_center(P.ox, qi, P.cell[l]);
     const double zy = block_center(P.oy, qj, P.cell[l]);
-    bool m0 = T.v0, m1 = T.v1;
-    if (l == L) {
-      m0 = m0 && max(abs(qi - T.li0), abs(qj - T.lj0)) >= 2;
-      m1 = m1 && max(abs(qi - T.li1), abs(qj - T.lj1)) >= 2;
+    bool msk[R];
+    double dx[R], dy[R], v[R];
+#pragma unroll
+    for (int p = 0; p < R; ++p) {
+      msk[p] = T.v[p] && (l < L || max(abs(qi - T.li[p]), abs(qj - T.lj[p])) >= 2);
+      dx[p] = T.x[p] - zx;
+      dy[p] = T.y[p] - zy;
     }
     mbar_wait(&bars[slot], (uint32_t)((e / STAGES) & 1));
-    double v0, v1;
-    far_eval2<M>(stage + (size_t)slot * K, T.x0 - zx, T.y0 - zy, T.x1 - zx, T.y1 - zy, P.t2,
-                 v0, v1);
-    acc0 += m0 ? v0 : 0.0;
-    acc1 += m1 ? v1 : 0.0;
+    far_evalR<M, R>(stage + (size_t)slot * K, dx, dy, P.t2, v);
+#pragma unroll
+    for (int p = 0; p < R; ++p) acc[p] += msk[p] ? v[p] : 0.0;
     __syncwarp();
     if (lane == 0 && e + STAGES < n) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       issue(e + STAGES, slot);
     }
   }
-  if (T.v0) far_s[s0 + lane] = acc0;
-  if (T.v1) far_s[s0 + 32 + lane] = acc1;
+#pragma unroll
+  for (int p = 0; p < R; ++p)
+    if (T.v[p]) far_s[s0 + lane + 32 * p] = acc[p];
 }
 
 template <int WARPS>
@@ -511,53 +548,63 @@ __global__ void __launch_bounds__(WARPS * 32) k_m2p_far_generic(const TreeParams
   const int s0 = item.y, cnt = item.z;
   uint32_t* list = lists[warp];
   const int n = build_far_list(P, par, s0, cnt, list, lane);
-  const Target T = load_targets(P, s0, cnt, lane);
-  double acc0 = 0.0, acc1 = 0.0;
-  for (int e = 0; e < n; ++e) {
-    const uint32_t ent = list[e];
-    const int l = (int)(ent >> 28);
-    const uint32_t q = ent & 0x0fffffffu;
-    int qi, qj;
-    demorton(q, qi, qj);
-    const double zx = block_center(P.ox, qi, P.cell[l]);
-    const double zy = block_center(P.oy, qj, P.cell[l]);
-    bool m0 = T.v0, m1 = T.v1;
-    if (l == P.L) {
-      m0 = m0 && max(abs(qi - T.li0), abs(qj - T.lj0)) >= 2;
-      m1 = m1 && max(abs(qi - T.li1), abs(qj - T.lj1)) >= 2;
+  for (int p0 = lane; p0 < cnt; p0 += 32) {
+    const int p = s0 + p0;
+    const double x = P.xs[p], y = P.ys[p];
+    int li, lj;
+    demorton(P.leaf[p], li, lj);
+    double acc = 0.0;
+    for (int e = 0; e < n; ++e) {
+      const uint32_t ent = list[e];
+      const int l = (int)(ent >> 28);
+      const uint32_t q = ent & 0x0fffffffu;
+      int qi, qj;
+      demorton(q, qi, qj);
+      if (l == P.L && max(abs(qi - li), abs(qj - lj)) < 2) continue;
+      const double zx = block_center(P.ox, qi, P.cell[l]);
+      const double zy = block_center(P.oy, qj, P.cell[l]);
+      acc += far_eval_generic(coef + P.coef_off[l] + (size_t)q * P.K, P.M, x - zx, y - zy, P.t2);
     }
-    const double2* c = coef + P.coef_off[l] + (size_t)q * P.K;
-    const double v0 = far_eval_generic(c, P.M, T.x0 - zx, T.y0 - zy, P.t2);
-    const double v1 = far_eval_generic(c, P.M, T.x1 - zx, T.y1 - zy, P.t2);
-    acc0 += m0 ? v0 : 0.0;
-    acc1 += m1 ? v1 : 0.0;
+    far_s[p] = acc;
   }
-  if (T.v0) far_s[s0 + lane] = acc0;
-  if (T.v1) far_s[s0 + 32 + lane] = acc1;
 }
 
-constexpr int kFarWarps = 4;
-constexpr int kFarStages = 4;
-
-template <int M>
-size_t far_smem() {
+// Launch configuration of the far kernel for work items of R points per lane
+// (warps per CTA W, staging depth S, min CTAs per SM).  Items are grouped by
+// R = ceil(count / 32) at build time, so lanes are idle only in the last
+// point slot of an item.
+template <int M, int R, int W, int S, int MINB>
+void run_far_cfg(const TreeParams& P, const int4* items, int n_items, const double2* coef,
+                 double* far_s, cudaStream_t s) {
   constexpr int K = (M + 1) * (M + 2) / 2;
-  return (size_t)kFarWarps * kFarStages * K * 16 + kFarWarps * kFarStages * 8 +
-         kFarWarps * kMaxList * 4;
-}
-
-template <int M>
-void run_far(const TreeParams& P, const int4* items, int n_items, const double2* coef,
-             double* far_s, cudaStream_t s) {
-  auto kern = k_m2p_far<M, kFarWarps, kFarStages>;
-  const size_t smem = far_smem<M>();
+  auto kern = k_m2p_far<M, R, W, S, MINB>;
+  const size_t smem = (size_t)W * S * K * 16 + W * S * 8 + W * kMaxList * 4;
   static bool configured = false;  // per template instance
   if (!configured) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     configured = true;
   }
-  const unsigned grid = (unsigned)((n_items + kFarWarps - 1) / kFarWarps);
-  kern<<<grid, kFarWarps * 32, smem, s>>>(P, items, n_items, coef, far_s);
+  const unsigned grid = (unsigned)((n_items + W - 1) / W);
+  kern<<<grid, W * 32, smem, s>>>(P, items, n_items, coef, far_s);
+}
+
+}  // namespace
+
+int far_max_points_per_lane() { return kFarMaxR; }
+
+namespace {
+
+template <int M>
+void run_far(const TreeParams& P, int R, const int4* items, int n_items, const double2* coef,
+             double* far_s, cudaStream_t s) {
+  switch (R) {
+    case 1: return run_far_cfg<M, 1, 4, 3, 1>(P, items, n_items, coef, far_s, s);
+    case 2: return run_far_cfg<M, 2, 4, 3, 1>(P, items, n_items, coef, far_s, s);
+    case 3: return run_far_cfg<M, 3, 4, 3, 1>(P, items, n_items, coef, far_s, s);
+    case 4: return run_far_cfg<M, 4, 4, 3, 1>(P, items, n_items, coef, far_s, s);
+    case 5: return run_far_cfg<M, 5, 4, 3, 1>(P, items, n_items, coef, far_s, s);
+    default: return run_far_cfg<M, 6, 4, 3, 1>(P, items, n_items, coef, far_s, s);
+  }
 }
 
 template <int M>
@@ -598,7 +645,8 @@ void launch_p2m_leaf(const TreeParams& P, const double* u_s, double2* mu, cudaSt
 
 void launch_m2m(const TreeParams& P, int level, double2* mu, const double* binom,
                 cudaStream_t s) {
-  const size_t smem = (size_t)(4 * P.Ke + 4 * (P.M + 1)) * sizeof(double2);
+  const size_t smem = (size_t)(4 * P.Ke + 4 * (P.M + 1)) * sizeof(double2) +
+                      (size_t)(P.M + 1) * (P.M + 1) * sizeof(double) + (P.M + 1) * sizeof(int);
   static size_t configured = 0;
   if (smem > 48 * 1024 && smem > configured) {
     cudaFuncSetAttribute(k_m2m, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -619,20 +667,28 @@ void launch_transform(const TreeParams& P, const double2* mu, double2* coef,
   }
 }
 
-void launch_m2p_far(const TreeParams& P, const int4* items, int n_items, const double2* coef,
-                    double* far_s, cudaStream_t s) {
-  if (n_items == 0) return;
-  switch (P.M) {
-#define X(m)                                      \
-  case m:                                         \
-    run_far<m>(P, items, n_items, coef, far_s, s); \
+void launch_m2p_far(const TreeParams& P, const int4* items, const int* group_off, int begin,
+                    int end, const double2* coef, double* far_s, cudaStream_t s) {
+  if (end <= begin) return;
+  if (!m2p_specialised(P.M)) {
+    constexpr int W = 4;
+    const int n = end - begin;
+    k_m2p_far_generic<W><<<(unsigned)((n + W - 1) / W), W * 32, 0, s>>>(P, items + begin, n,
+                                                                        coef, far_s);
     return;
-    IMQ_FOR_SPECIALISED_M(X)
+  }
+  for (int R = 1; R <= kFarMaxR; ++R) {
+    const int lo = std::max(begin, group_off[R - 1]), hi = std::min(end, group_off[R]);
+    if (hi <= lo) continue;
+    switch (P.M) {
+#define X(m)                                                   \
+  case m:                                                      \
+    run_far<m>(P, R, items + lo, hi - lo, coef, far_s, s);     \
+    break;
+      IMQ_FOR_SPECIALISED_M(X)
 #undef X
-    default: {
-      constexpr int W = 4;
-      k_m2p_far_generic<W><<<(unsigned)((n_items + W - 1) / W), W * 32, 0, s>>>(
-          P, items, n_items, coef, far_s);
+      default:
+        break;
     }
   }
 }

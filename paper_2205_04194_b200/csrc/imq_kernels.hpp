@@ -66,13 +66,20 @@ void launch_m2m(const TreeParams& P, int level, double2* mu, const double* binom
                 cudaStream_t s);
 void launch_transform(const TreeParams& P, const double2* mu, double2* coef,
                       const TransformTable& T, cudaStream_t s);
-void launch_m2p_far(const TreeParams& P, const int4* items, int n_items, const double2* coef,
-                    double* far_s, cudaStream_t s);
+// Far work items are grouped by points-per-lane R = ceil(count/32):
+// group R occupies [group_off[R-1], group_off[R]) of `items`.  Launches the
+// items with index in [begin, end).
+void launch_m2p_far(const TreeParams& P, const int4* items, const int* group_off, int begin,
+                    int end, const double2* coef, double* far_s, cudaStream_t s);
 bool m2p_specialised(int M);
+int far_max_points_per_lane();
 
 // ---- direct interactions (direct.cu)
-void launch_p2p_near(const TreeParams& P, const int4* items, int n_items, const double* u_s,
-                     const double* far_s, double* out, const int* perm, cudaStream_t s);
+// Near work items (one leaf each) grouped by points-per-lane like the far ones.
+void launch_p2p_near(const TreeParams& P, const int4* items, const int* group_off, int begin,
+                     int end, const double* u_s, const double* far_s, double* out,
+                     const int* perm, cudaStream_t s);
+int near_max_points_per_lane();
 void launch_direct(const double* txy, long long nt, const double* sxy, const double* sval,
                    long long ns, double t2, double* out, cudaStream_t s);
 

@@ -169,14 +169,39 @@ void DeviceOperator::build(const double* xy_host) {
     const long long n_par = 1ll << (2 * L_);  // level L-1 (level 0 = 2x2 for L = 1)
     far_items_h_.clear();
     near_items_h_.clear();
+    // far items: <= 32 Rmax targets of one level-(L-1) block, grouped by
+    // R = ceil(count / 32) so every group runs the kernel specialised for it
+    const int rmax = imqk::m2p_specialised(M_) ? imqk::far_max_points_per_lane() : 2;
+    const int chunk = 32 * rmax;
+    std::vector<std::vector<int4>> groups((size_t)rmax);
     for (long long p = 0; p < n_par; ++p) {
       const int a = ls[(size_t)(4 * p)], b = ls[(size_t)(4 * p + 4)];
-      for (int c = a; c < b; c += 64) far_items_h_.push_back(make_int4((int)p, c, std::min(64, b - c), 0));
+      for (int c = a; c < b; c += chunk) {
+        const int cnt = std::min(chunk, b - c);
+        groups[(size_t)((cnt + 31) / 32 - 1)].push_back(make_int4((int)p, c, cnt, 0));
+      }
     }
+    far_group_off_.assign(8, 0);
+    for (int r = 0; r < rmax; ++r) {
+      far_items_h_.insert(far_items_h_.end(), groups[(size_t)r].begin(), groups[(size_t)r].end());
+      far_group_off_[(size_t)r + 1] = (int)far_items_h_.size();
+    }
+    for (int r = rmax + 1; r < 8; ++r) far_group_off_[(size_t)r] = (int)far_items_h_.size();
+    const int nrmax = imqk::near_max_points_per_lane();
+    std::vector<std::vector<int4>> ngroups((size_t)nrmax);
     for (long long q = 0; q < n_leaves; ++q) {
       const int a = ls[(size_t)q], b = ls[(size_t)q + 1];
-      for (int c = a; c < b; c += 32) near_items_h_.push_back(make_int4((int)q, c, std::min(32, b - c), 0));
+      for (int c = a; c < b; c += 32 * nrmax) {
+        const int cnt = std::min(32 * nrmax, b - c);
+        ngroups[(size_t)((cnt + 31) / 32 - 1)].push_back(make_int4((int)q, c, cnt, 0));
+      }
     }
+    near_group_off_.assign(8, 0);
+    for (int r = 0; r < nrmax; ++r) {
+      near_items_h_.insert(near_items_h_.end(), ngroups[(size_t)r].begin(), ngroups[(size_t)r].end());
+      near_group_off_[(size_t)r + 1] = (int)near_items_h_.size();
+    }
+    for (int r = nrmax + 1; r < 8; ++r) near_group_off_[(size_t)r] = (int)near_items_h_.size();
     n_far_ = (int)far_items_h_.size();
     n_near_ = (int)near_items_h_.size();
     d_far_items_ = dalloc<int4>(far_items_h_.size(), "far items");
@@ -240,10 +265,11 @@ void DeviceOperator::far_near(const double* d_us, double* d_out, const int* perm
   near_begin = std::max(0, near_begin);
   near_end = std::min(near_end, n_near_);
   if (far_end > far_begin)
-    imqk::launch_m2p_far(P_, d_far_items_ + far_begin, far_end - far_begin, d_coef_, d_far_, s);
+    imqk::launch_m2p_far(P_, d_far_items_, far_group_off_.data(), far_begin, far_end, d_coef_,
+                         d_far_, s);
   if (near_end > near_begin)
-    imqk::launch_p2p_near(P_, d_near_items_ + near_begin, near_end - near_begin, d_us, d_far_,
-                          d_out, perm, s);
+    imqk::launch_p2p_near(P_, d_near_items_, near_group_off_.data(), near_begin, near_end, d_us,
+                          d_far_, d_out, perm, s);
 }
 
 void DeviceOperator::apply_sorted_locked(const double* d_us, double* d_out, const int* perm,

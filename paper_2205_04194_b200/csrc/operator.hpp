@@ -99,6 +99,8 @@ class DeviceOperator {
   int4* d_near_items_ = nullptr;
   int n_far_ = 0, n_near_ = 0;
   std::vector<int4> far_items_h_, near_items_h_;
+  std::vector<int> far_group_off_;   // far items grouped by points per lane
+  std::vector<int> near_group_off_;  // near items grouped by points per lane
   int* d_tr_off_ = nullptr;
   int* d_tr_idx_ = nullptr;
   double* d_tr_val_ = nullptr;

@@ -1,0 +1,22 @@
+"""Fixed launch sequence for ncu: build the cfg-4 operator, run 2 warm-up
+fast products and 1 measured one (19 kernel launches per product at L=8)."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2205_04194_b200 as P  # noqa: E402
+from paper_2205_04194_b200 import inputs  # noqa: E402
+
+cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 4
+c = inputs.CONFIGS[cfg]
+xy = inputs.config_points(cfg)
+op = P.FastOperator(xy, c["t"], c["m"], c["levels"])
+u = torch.tensor(inputs.random_vector(c["n"], 1000), device="cuda")
+b = torch.empty_like(u)
+for _ in range(3):
+    op.apply_device(u, b, torch.cuda.current_stream())
+torch.cuda.synchronize()
+print("ok", float(b.abs().max()))
