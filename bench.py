@@ -10,10 +10,12 @@ one full fast product (P2M + M2M + transform + M2P far + P2P near); operator
 setup is reported separately.  Inputs (134 MB per vector, 855 MB of far-field
 coefficients) exceed the 126 MB L2, so no flush is needed between steps.
 
-N > 1 GPUs (torchrun): every rank holds the Morton-sorted points, computes the
-moments of the (replicated) source vector and evaluates its contiguous range
-of far/near work items -- the target points are sharded, the work per rank
-shrinks with N ("strong" scaling).  value = N points / max-over-ranks time.
+N > 1 GPUs (torchrun): every rank holds the Morton-sorted points and the full
+source vector, forms the moments, and evaluates the far + near field of its own
+contiguous Morton range of targets (paper_2205_04194_b200/parallel.py, cut at
+level-(L-1) blocks); no collective on the data path.  The target points are
+sharded, the work per rank shrinks with N ("strong" scaling).
+value = N points / max-over-ranks time.
 
 --impl reference: the reference's own CPU implementation (oracle/_ref, the
 unmodified /root/reference sources compiled by oracle/Makefile) on the host
@@ -208,9 +210,13 @@ def b200_arm(args):
     setup_s = time.perf_counter() - t0
     st = op.stats()
     L = op.levels
+    share = 1.0
+    if world > 1:
+        from paper_2205_04194_b200.parallel import ShardedOperator
+        sh = ShardedOperator(op, rank, world)   # far/near restricted to own targets
+        owned = torch.from_numpy(sh.owned_original_indices().astype(np.int64)).cuda()
+        share = (sh.hi - sh.lo) / n
     far_items, near_items = len(op.items("far")), len(op.items("near"))
-    fr = (far_items * rank // world, far_items * (rank + 1) // world)
-    nr = (near_items * rank // world, near_items * (rank + 1) // world)
 
     stream = torch.cuda.current_stream()
     nvec = min(args.steps + args.warmup, 8)
@@ -221,13 +227,7 @@ def b200_arm(args):
     perm = torch.from_numpy(op.permutation().astype(np.int64)).cuda()
 
     def step(k):
-        u = dev_u[k % nvec]
-        if world == 1:
-            op.apply_device(u, d_b, stream)
-        else:
-            torch.index_select(u, 0, perm, out=d_us)
-            op.moments(d_us, stream)
-            op.far_near(d_us, d_b, fr, nr, stream)
+        op.apply_device(dev_u[k % nvec], d_b, stream)
 
     def barrier():
         if world > 1:
@@ -267,11 +267,9 @@ def b200_arm(args):
         else:
             d_u = dev_u[0]
             d_u.copy_(pin_u[k % 2], non_blocking=True)
-            torch.index_select(d_u, 0, perm, out=d_us)
-            op.moments(d_us, stream)
-            op.far_near(d_us, d_b, fr, nr, stream)
-            lo, hi = (n * rank // world, n * (rank + 1) // world)
-            pin_b[lo:hi].copy_(d_b[lo:hi], non_blocking=True)
+            op.apply_device(d_u, d_b, stream)
+            mine = torch.index_select(d_b, 0, owned)
+            pin_b[:mine.numel()].copy_(mine, non_blocking=True)
             torch.cuda.synchronize()
 
     e2e_step(0)
@@ -310,7 +308,7 @@ def b200_arm(args):
     torch.cuda.synchronize()
     mom_ms = e0.elapsed_time(e1)
     peak_tf, _ = P.api.fp64_peak(8192)
-    far_flops = st["far_pairs"] * f_pair(M)
+    far_flops = st["far_pairs"] * f_pair(M) * share  # this rank's targets
     achieved = far_flops / (far_ms * 1e-3) / 1e12
     traffic = None
     prof = os.path.join(ROOT, "profiles", "far_kernel_ncu.json")
@@ -368,7 +366,11 @@ def b200_arm(args):
                          "peak_source": "measured live: DFMA probe (imq_ext_fp64_peak); "
                                         "MEASURED_PEAKS.json has no FP64 entry",
                          "flops_per_launch": far_flops,
-                         "flop_model": "SURVEY 8(d): P_far x (4K+6Ke+6(M+1)+12)",
+                         "flop_model": "SURVEY 8(d): P_far x (4K+6Ke+6(M+1)+12)"
+                                       + ("" if world == 1 else " x rank-0 target share"),
+                         "executed_flops_per_pair": 2 * (M * M + 4 * M + 12),
+                         "executed_frac": st["far_pairs"] * share * 2 * (M * M + 4 * M + 12)
+                                          / (far_ms * 1e-3) / 1e12 / peak_tf,
                          "far_ms": far_ms, "near_ms": near_ms, "moments_ms": mom_ms,
                          "far_share_of_step": far_ms / ms if world == 1 else None},
             "cpu_baseline": cpu,

@@ -167,6 +167,13 @@ IMQ_API int imq_ext_operator_far_near(const imq_operator* op, const double* d_us
                               int far_begin, int far_end, int near_begin, int near_end,
                               void* stream);
 
+/* Sharded application over `world` GPUs: sorted-position bounds (world+1
+ * entries) cut at level-(L-1) block boundaries with balanced point counts,
+ * computed from an operator's leaf_start (pure host function), and the
+ * restriction of an operator's far/near evaluation to one such range. */
+IMQ_API int imq_ext_shard_bounds(const int* leaf_start, int levels, int world, int* bounds_out);
+IMQ_API int imq_ext_operator_restrict(const imq_operator* op, int sorted_lo, int sorted_hi);
+
 /* Measured FP64 FMA-pipe throughput (TFLOP/s) of the current device: the
  * roofline denominator of the FP64-bound far-field kernel. */
 IMQ_API int imq_ext_fp64_peak(int iters, double* tflops, double* ms);

@@ -578,6 +578,26 @@ int imq_ext_operator_far_near(const imq_operator* op, const double* d_us, double
   });
 }
 
+int imq_ext_shard_bounds(const int* leaf_start, int levels, int world, int* bounds_out) {
+  if (!leaf_start || !bounds_out || levels < 1 || levels > 13 || world < 1)
+    return fail(IMQ_ERR_INVALID_ARG, "imq_ext_shard_bounds: bad argument");
+  return guard([&] {
+    const size_t n = ((size_t)1 << (2 * (levels + 1))) + 1;
+    std::vector<int> ls(leaf_start, leaf_start + n);
+    std::vector<int> b = imqh::shard_bounds(ls, levels, world);
+    std::copy(b.begin(), b.end(), bounds_out);
+    return IMQ_OK;
+  });
+}
+
+int imq_ext_operator_restrict(const imq_operator* op, int sorted_lo, int sorted_hi) {
+  if (!op) return fail(IMQ_ERR_INVALID_ARG, "imq_ext_operator_restrict: null argument");
+  return guard([&] {
+    op->op->restrict_targets(sorted_lo, sorted_hi);
+    return IMQ_OK;
+  });
+}
+
 int imq_ext_fp64_peak(int iters, double* tflops, double* ms) {
   if (!tflops || iters < 1) return fail(IMQ_ERR_INVALID_ARG, "imq_ext_fp64_peak: bad argument");
   return guard([&] {

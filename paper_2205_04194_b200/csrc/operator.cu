@@ -165,52 +165,9 @@ void DeviceOperator::build(const double* xy_host) {
     cuda_check(cudaStreamSynchronize(s), "tree build");
     cuda_check(cudaGetLastError(), "tree kernels");
 
-    // ---- work lists
-    const long long n_par = 1ll << (2 * L_);  // level L-1 (level 0 = 2x2 for L = 1)
-    far_items_h_.clear();
-    near_items_h_.clear();
-    // far items: <= 32 Rmax targets of one level-(L-1) block, grouped by
-    // R = ceil(count / 32) so every group runs the kernel specialised for it
-    const int rmax = imqk::m2p_specialised(M_) ? imqk::far_max_points_per_lane() : 2;
-    const int chunk = 32 * rmax;
-    std::vector<std::vector<int4>> groups((size_t)rmax);
-    for (long long p = 0; p < n_par; ++p) {
-      const int a = ls[(size_t)(4 * p)], b = ls[(size_t)(4 * p + 4)];
-      for (int c = a; c < b; c += chunk) {
-        const int cnt = std::min(chunk, b - c);
-        groups[(size_t)((cnt + 31) / 32 - 1)].push_back(make_int4((int)p, c, cnt, 0));
-      }
-    }
-    far_group_off_.assign(8, 0);
-    for (int r = 0; r < rmax; ++r) {
-      far_items_h_.insert(far_items_h_.end(), groups[(size_t)r].begin(), groups[(size_t)r].end());
-      far_group_off_[(size_t)r + 1] = (int)far_items_h_.size();
-    }
-    for (int r = rmax + 1; r < 8; ++r) far_group_off_[(size_t)r] = (int)far_items_h_.size();
-    const int nrmax = imqk::near_max_points_per_lane();
-    std::vector<std::vector<int4>> ngroups((size_t)nrmax);
-    for (long long q = 0; q < n_leaves; ++q) {
-      const int a = ls[(size_t)q], b = ls[(size_t)q + 1];
-      for (int c = a; c < b; c += 32 * nrmax) {
-        const int cnt = std::min(32 * nrmax, b - c);
-        ngroups[(size_t)((cnt + 31) / 32 - 1)].push_back(make_int4((int)q, c, cnt, 0));
-      }
-    }
-    near_group_off_.assign(8, 0);
-    for (int r = 0; r < nrmax; ++r) {
-      near_items_h_.insert(near_items_h_.end(), ngroups[(size_t)r].begin(), ngroups[(size_t)r].end());
-      near_group_off_[(size_t)r + 1] = (int)near_items_h_.size();
-    }
-    for (int r = nrmax + 1; r < 8; ++r) near_group_off_[(size_t)r] = (int)near_items_h_.size();
-    n_far_ = (int)far_items_h_.size();
-    n_near_ = (int)near_items_h_.size();
-    d_far_items_ = dalloc<int4>(far_items_h_.size(), "far items");
-    d_near_items_ = dalloc<int4>(near_items_h_.size(), "near items");
-    cuda_check(cudaMemcpyAsync(d_far_items_, far_items_h_.data(), far_items_h_.size() * sizeof(int4),
-                               cudaMemcpyHostToDevice, s), "H2D far items");
-    cuda_check(cudaMemcpyAsync(d_near_items_, near_items_h_.data(),
-                               near_items_h_.size() * sizeof(int4), cudaMemcpyHostToDevice, s),
-               "H2D near items");
+    // ---- work lists (all targets)
+    leaf_start_h_ = std::move(ls);
+    build_items(0, N_);
 
     // ---- tables
     const Transform tr = build_transform(M_, t_);
@@ -249,6 +206,88 @@ void DeviceOperator::build(const double* xy_host) {
     throw;
   }
   dfree(d_xy); dfree(d_keys); dfree(d_idx); dfree(d_tmp); dfree(d_part);
+}
+
+// Far items: <= 32 Rmax targets of one level-(L-1) block; near items: <= 32 Rn
+// targets of one leaf.  Both are grouped by R = ceil(count / 32) so each group
+// runs the kernel specialised for it.  Only targets in [p_lo, p_hi) (aligned
+// to level-(L-1) block boundaries by the caller) get items.
+void DeviceOperator::build_items(int p_lo, int p_hi) {
+  const std::vector<int>& ls = leaf_start_h_;
+  const long long n_par = 1ll << (2 * L_);  // level L-1 (level 0 = 2x2 for L = 1)
+  const long long n_leaves = 1ll << (2 * (L_ + 1));
+  far_items_h_.clear();
+  near_items_h_.clear();
+  auto grouped = [](std::vector<std::vector<int4>>& g, std::vector<int4>& out,
+                    std::vector<int>& off) {
+    off.assign(8, 0);
+    for (size_t r = 0; r < g.size(); ++r) {
+      out.insert(out.end(), g[r].begin(), g[r].end());
+      off[r + 1] = (int)out.size();
+    }
+    for (size_t r = g.size() + 1; r < 8; ++r) off[r] = (int)out.size();
+  };
+  const int rmax = imqk::m2p_specialised(M_) ? imqk::far_max_points_per_lane() : 2;
+  std::vector<std::vector<int4>> groups((size_t)rmax);
+  for (long long p = 0; p < n_par; ++p) {
+    const int a = std::max(p_lo, ls[(size_t)(4 * p)]), b = std::min(p_hi, ls[(size_t)(4 * p + 4)]);
+    for (int c = a; c < b; c += 32 * rmax) {
+      const int cnt = std::min(32 * rmax, b - c);
+      groups[(size_t)((cnt + 31) / 32 - 1)].push_back(make_int4((int)p, c, cnt, 0));
+    }
+  }
+  grouped(groups, far_items_h_, far_group_off_);
+  const int nrmax = imqk::near_max_points_per_lane();
+  std::vector<std::vector<int4>> ngroups((size_t)nrmax);
+  for (long long q = 0; q < n_leaves; ++q) {
+    const int a = std::max(p_lo, ls[(size_t)q]), b = std::min(p_hi, ls[(size_t)q + 1]);
+    for (int c = a; c < b; c += 32 * nrmax) {
+      const int cnt = std::min(32 * nrmax, b - c);
+      ngroups[(size_t)((cnt + 31) / 32 - 1)].push_back(make_int4((int)q, c, cnt, 0));
+    }
+  }
+  grouped(ngroups, near_items_h_, near_group_off_);
+  n_far_ = (int)far_items_h_.size();
+  n_near_ = (int)near_items_h_.size();
+  dfree(d_far_items_);
+  dfree(d_near_items_);
+  d_far_items_ = dalloc<int4>(far_items_h_.size(), "far items");
+  d_near_items_ = dalloc<int4>(near_items_h_.size(), "near items");
+  cuda_check(cudaMemcpy(d_far_items_, far_items_h_.data(), far_items_h_.size() * sizeof(int4),
+                        cudaMemcpyHostToDevice), "H2D far items");
+  cuda_check(cudaMemcpy(d_near_items_, near_items_h_.data(), near_items_h_.size() * sizeof(int4),
+                        cudaMemcpyHostToDevice), "H2D near items");
+  target_lo_ = p_lo;
+  target_hi_ = p_hi;
+}
+
+void DeviceOperator::restrict_targets(int p_lo, int p_hi) {
+  std::lock_guard<std::mutex> lk(mtx_);
+  DeviceGuard g(device_);
+  if (p_lo < 0 || p_hi > N_ || p_lo > p_hi)
+    throw std::invalid_argument("restrict_targets: bad sorted-position range");
+  cuda_check(cudaStreamSynchronize(stream_), "restrict");
+  build_items(p_lo, p_hi);
+}
+
+// World+1 sorted-position bounds, cut at level-(L-1) block boundaries, with
+// near-equal point counts per rank (far work per target is ~uniform).
+std::vector<int> shard_bounds(const std::vector<int>& ls, int L, int world) {
+  if (world < 1) throw std::invalid_argument("shard_bounds: world must be >= 1");
+  const long long n_par = 1ll << (2 * L);
+  const int n = ls.back();
+  std::vector<int> b((size_t)world + 1, n);
+  b[0] = 0;
+  long long p = 0;
+  for (int r = 1; r < world; ++r) {
+    const double want = (double)n * r / world;
+    while (p < n_par && ls[(size_t)(4 * (p + 1))] <= want) ++p;
+    // choose the closer of the two parent boundaries around `want`
+    int lo = ls[(size_t)(4 * p)], hi = p < n_par ? ls[(size_t)(4 * (p + 1))] : n;
+    b[(size_t)r] = (want - lo <= hi - want) ? lo : hi;
+    if (b[(size_t)r] < b[(size_t)r - 1]) b[(size_t)r] = b[(size_t)r - 1];
+  }
+  return b;
 }
 
 void DeviceOperator::moments(const double* d_us, cudaStream_t s) {

@@ -35,6 +35,8 @@ struct PairCounts {
   int64_t far_items = 0, near_items = 0;
 };
 
+std::vector<int> shard_bounds(const std::vector<int>& leaf_start, int L, int world);
+
 class DeviceOperator {
  public:
   DeviceOperator(const double* xy_host, size_t n, double t, int M, int levels);
@@ -63,6 +65,11 @@ class DeviceOperator {
   void copy_permutation(int* perm_host) const;
   void copy_leaf_start(std::vector<int>& out) const;
   PairCounts pair_counts();
+  // Restricts far/near evaluation to targets at sorted positions [lo, hi)
+  // (sharded application); b entries of other targets are left untouched.
+  void restrict_targets(int p_lo, int p_hi);
+  int target_lo() const { return target_lo_; }
+  int target_hi() const { return target_hi_; }
 
   // Stage-by-stage access (multi-GPU sharding drives these individually).
   void moments(const double* d_us, cudaStream_t s);  // P2M + M2M + transform
@@ -77,6 +84,7 @@ class DeviceOperator {
 
  private:
   void build(const double* xy_host);
+  void build_items(int p_lo, int p_hi);
   void release();
   void apply_sorted_locked(const double* d_us, double* d_bs, const int* perm,
                            cudaStream_t s);
@@ -112,6 +120,8 @@ class DeviceOperator {
   double* d_us_ = nullptr;  // sorted input
   double* d_far_ = nullptr; // sorted far field
   double* d_b_ = nullptr;   // original-order output staging
+  std::vector<int> leaf_start_h_;
+  int target_lo_ = 0, target_hi_ = 0;
   bool have_counts_ = false;
   PairCounts counts_{};
 };

@@ -1,0 +1,79 @@
+"""Multi-GPU application of the fast operator (one process per GPU).
+
+Targets are sharded by contiguous Morton ranges cut at level-(L-1) block
+boundaries (imq_ext_shard_bounds); every rank holds the full sorted point set
+(setup is sub-second) and the full source vector, forms the moments, and
+evaluates the far + near field of its own targets only
+(imq_ext_operator_restrict).  The data path needs no collective; gather_b()
+assembles the full product when a caller wants it (all_gather over NCCL on
+GPUs, gloo on CPU in the tests).
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from .capi import check, lib
+
+
+def shard_bounds(leaf_start, levels: int, world: int) -> np.ndarray:
+    """world+1 sorted-position bounds, balanced, aligned to level-(L-1) blocks."""
+    ls = np.ascontiguousarray(leaf_start, dtype=np.int32)
+    if ls.size != (1 << (2 * (levels + 1))) + 1:
+        raise ValueError("leaf_start has the wrong length for `levels`")
+    out = np.empty(world + 1, dtype=np.int32)
+    check(lib().imq_ext_shard_bounds(ls.ctypes.data_as(C.POINTER(C.c_int)), levels, world,
+                                     out.ctypes.data_as(C.POINTER(C.c_int))))
+    return out
+
+
+def leaf_start_from_keys(leaf_keys_sorted, levels: int) -> np.ndarray:
+    """leaf_start (lower bounds) of a sorted array of finest Morton keys."""
+    n_leaves = 1 << (2 * (levels + 1))
+    return np.searchsorted(np.asarray(leaf_keys_sorted), np.arange(n_leaves + 1),
+                           side="left").astype(np.int32)
+
+
+class ShardedOperator:
+    """FastOperator whose far/near evaluation covers this rank's targets."""
+
+    def __init__(self, op, rank: int, world: int):
+        self.op = op
+        self.rank, self.world = rank, world
+        self.bounds = shard_bounds(op.leaf_start(), op.levels, world)
+        self.lo, self.hi = int(self.bounds[rank]), int(self.bounds[rank + 1])
+        check(lib().imq_ext_operator_restrict(op.handle, self.lo, self.hi))
+        self.perm = op.permutation()
+
+    def apply_device(self, d_u, d_b, stream=None):
+        """b[perm[p]] for p in [lo, hi) (original order); other entries untouched."""
+        self.op.apply_device(d_u, d_b, stream)
+
+    def owned_original_indices(self) -> np.ndarray:
+        return self.perm[self.lo:self.hi]
+
+
+def gather_b(local_b, owned_idx, n: int, group=None):
+    """Assemble the full product from every rank's owned entries (torch.distributed)."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    dev = local_b.device
+    vals = local_b[torch.as_tensor(owned_idx, device=dev, dtype=torch.long)]
+    sizes = [torch.zeros(1, dtype=torch.long, device=dev) for _ in range(world)]
+    dist.all_gather(sizes, torch.tensor([vals.numel()], device=dev), group=group)
+    m = int(max(s.item() for s in sizes))
+    pad_v = torch.zeros(m, dtype=vals.dtype, device=dev)
+    pad_i = torch.full((m,), -1, dtype=torch.long, device=dev)
+    pad_v[:vals.numel()] = vals
+    pad_i[:vals.numel()] = torch.as_tensor(owned_idx, device=dev, dtype=torch.long)
+    all_v = [torch.empty_like(pad_v) for _ in range(world)]
+    all_i = [torch.empty_like(pad_i) for _ in range(world)]
+    dist.all_gather(all_v, pad_v, group=group)
+    dist.all_gather(all_i, pad_i, group=group)
+    out = torch.empty(n, dtype=vals.dtype, device=dev)
+    for v, i in zip(all_v, all_i):
+        k = i >= 0
+        out[i[k]] = v[k]
+    return out
