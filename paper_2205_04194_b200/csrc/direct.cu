@@ -23,12 +23,15 @@ constexpr int kNearMaxR = 4;  // a near work item holds <= 32 * kNearMaxR target
 // Warp per near work item: <= 32 R targets of one leaf, R per lane.  Every
 // source point staged in the warp's shared-memory tile is read back once per
 // lane and reused for its R targets (register blocking against the per-LDS
-// issue cost).
+// issue cost).  item.w = 3: all three neighbour rows, the
+// epilogue adds the far field and scatters; item.w = r in {0,1,2}: only source
+// row li-1+r, partial sums to part[r][.] (small problems split the sources
+// three ways for parallelism; k_near_combine adds them in a fixed order).
 template <int R>
 __global__ void __launch_bounds__(kNearWarps * 32) k_p2p_near(
     const TreeParams P, const int4* __restrict__ items, int n_items,
     const double* __restrict__ u_s, const double* __restrict__ far_s, double* __restrict__ out,
-    const int* __restrict__ perm) {
+    const int* __restrict__ perm, double* __restrict__ part) {
   __shared__ double2 sxy[kNearWarps][32];
   __shared__ double su[kNearWarps][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -36,7 +39,7 @@ __global__ void __launch_bounds__(kNearWarps * 32) k_p2p_near(
   if (it >= n_items) return;
   const int4 item = items[it];
   const uint32_t leaf = (uint32_t)item.x;
-  const int s0 = item.y, cnt = item.z;
+  const int s0 = item.y, cnt = item.z, srow = item.w;
   double xi[R], yi[R], acc[R];
 #pragma unroll
   for (int p = 0; p < R; ++p) {
@@ -49,7 +52,10 @@ __global__ void __launch_bounds__(kNearWarps * 32) k_p2p_near(
   const int g = 1 << (P.L + 1);
   int li, lj;
   demorton(leaf, li, lj);
-  for (int qi = max(0, li - 1); qi <= min(g - 1, li + 1); ++qi) {
+  const int qlo = srow == 3 ? max(0, li - 1) : li - 1 + srow;
+  const int qhi = srow == 3 ? min(g - 1, li + 1) : li - 1 + srow;
+  for (int qi = qlo; qi <= qhi; ++qi) {
+    if (qi < 0 || qi > g - 1) continue;
     for (int qj = max(0, lj - 1); qj <= min(g - 1, lj + 1); ++qj) {
       const uint32_t q = morton(qi, qj);
       const int a = P.leaf_start[q], b = P.leaf_start[q + 1];
@@ -79,10 +85,25 @@ __global__ void __launch_bounds__(kNearWarps * 32) k_p2p_near(
   for (int p = 0; p < R; ++p) {
     if (lane + 32 * p < cnt) {
       const int q = s0 + lane + 32 * p;
-      const double v = far_s[q] + acc[p];
-      out[perm ? perm[q] : q] = v;
+      if (srow == 3) {
+        const double v = far_s[q] + acc[p];
+        out[perm ? perm[q] : q] = v;
+      } else {
+        part[(size_t)srow * P.N + q] = acc[p];
+      }
     }
   }
+}
+
+__global__ void __launch_bounds__(256) k_near_combine(int lo, int hi, int N,
+                                                      const double* __restrict__ far_s,
+                                                      const double* __restrict__ part,
+                                                      double* __restrict__ out,
+                                                      const int* __restrict__ perm) {
+  const int q = lo + blockIdx.x * 256 + threadIdx.x;
+  if (q >= hi) return;
+  const double v = far_s[q] + ((part[q] + part[(size_t)N + q]) + part[2 * (size_t)N + q]);
+  out[perm ? perm[q] : q] = v;
 }
 
 constexpr int kDirThreads = 256;
@@ -132,18 +153,25 @@ __global__ void __launch_bounds__(kDirThreads) k_direct(const double* __restrict
 
 int near_max_points_per_lane() { return kNearMaxR; }
 
+void launch_near_combine(int lo, int hi, int N, const double* far_s, const double* part,
+                         double* out, const int* perm, cudaStream_t s) {
+  if (hi <= lo) return;
+  k_near_combine<<<(unsigned)((hi - lo + 255) / 256), 256, 0, s>>>(lo, hi, N, far_s, part, out,
+                                                                   perm);
+}
+
 void launch_p2p_near(const TreeParams& P, const int4* items, const int* group_off, int begin,
                      int end, const double* u_s, const double* far_s, double* out,
-                     const int* perm, cudaStream_t s) {
+                     const int* perm, double* part, cudaStream_t s) {
   for (int R = 1; R <= kNearMaxR; ++R) {
     const int lo = max(begin, group_off[R - 1]), hi = min(end, group_off[R]);
     if (hi <= lo) continue;
     const unsigned grid = (unsigned)((hi - lo + kNearWarps - 1) / kNearWarps);
     switch (R) {
-      case 1: k_p2p_near<1><<<grid, kNearWarps * 32, 0, s>>>(P, items + lo, hi - lo, u_s, far_s, out, perm); break;
-      case 2: k_p2p_near<2><<<grid, kNearWarps * 32, 0, s>>>(P, items + lo, hi - lo, u_s, far_s, out, perm); break;
-      case 3: k_p2p_near<3><<<grid, kNearWarps * 32, 0, s>>>(P, items + lo, hi - lo, u_s, far_s, out, perm); break;
-      default: k_p2p_near<4><<<grid, kNearWarps * 32, 0, s>>>(P, items + lo, hi - lo, u_s, far_s, out, perm); break;
+      case 1: k_p2p_near<1><<<grid, kNearWarps * 32, 0, s>>>(P, items + lo, hi - lo, u_s, far_s, out, perm, part); break;
+      case 2: k_p2p_near<2><<<grid, kNearWarps * 32, 0, s>>>(P, items + lo, hi - lo, u_s, far_s, out, perm, part); break;
+      case 3: k_p2p_near<3><<<grid, kNearWarps * 32, 0, s>>>(P, items + lo, hi - lo, u_s, far_s, out, perm, part); break;
+      default: k_p2p_near<4><<<grid, kNearWarps * 32, 0, s>>>(P, items + lo, hi - lo, u_s, far_s, out, perm, part); break;
     }
   }
 }

@@ -78,7 +78,9 @@ int far_max_points_per_lane();
 // Near work items (one leaf each) grouped by points-per-lane like the far ones.
 void launch_p2p_near(const TreeParams& P, const int4* items, const int* group_off, int begin,
                      int end, const double* u_s, const double* far_s, double* out,
-                     const int* perm, cudaStream_t s);
+                     const int* perm, double* part, cudaStream_t s);
+void launch_near_combine(int lo, int hi, int N, const double* far_s, const double* part,
+                         double* out, const int* perm, cudaStream_t s);
 int near_max_points_per_lane();
 void launch_direct(const double* txy, long long nt, const double* sxy, const double* sval,
                    long long ns, double t2, double* out, cudaStream_t s);

@@ -93,6 +93,7 @@ void DeviceOperator::release() {
   dfree(d_far_items_); dfree(d_near_items_);
   dfree(d_tr_off_); dfree(d_tr_idx_); dfree(d_tr_val_); dfree(d_binom_);
   dfree(d_mu_); dfree(d_coef_); dfree(d_u_); dfree(d_us_); dfree(d_far_); dfree(d_b_);
+  dfree(d_part_);
   if (stream_) cudaStreamDestroy(stream_);
   stream_ = nullptr;
 }
@@ -227,7 +228,12 @@ void DeviceOperator::build_items(int p_lo, int p_hi) {
     }
     for (size_t r = g.size() + 1; r < 8; ++r) off[r] = (int)out.size();
   };
-  const int rmax = imqk::m2p_specialised(M_) ? imqk::far_max_points_per_lane() : 2;
+  // Points per lane: as large as the kernels allow (register blocking), but
+  // small enough that the GPU still gets >= ~8 waves of warps (kWarpsWanted).
+  constexpr double kWarpsWanted = 148.0 * 64;
+  const double nt = (double)(p_hi - p_lo);
+  const int rfit = (int)std::max(1.0, std::floor(nt / (32.0 * kWarpsWanted)));
+  const int rmax = imqk::m2p_specialised(M_) ? std::min(rfit, imqk::far_max_points_per_lane()) : 2;
   std::vector<std::vector<int4>> groups((size_t)rmax);
   for (long long p = 0; p < n_par; ++p) {
     const int a = std::max(p_lo, ls[(size_t)(4 * p)]), b = std::min(p_hi, ls[(size_t)(4 * p + 4)]);
@@ -237,15 +243,20 @@ void DeviceOperator::build_items(int p_lo, int p_hi) {
     }
   }
   grouped(groups, far_items_h_, far_group_off_);
-  const int nrmax = imqk::near_max_points_per_lane();
+  const int nrmax = std::min(rfit, imqk::near_max_points_per_lane());
+  // small problems: split each leaf's 3x3 sources into three rows
+  near_split_ = nt / (32.0 * nrmax) < kWarpsWanted ? 3 : 1;
   std::vector<std::vector<int4>> ngroups((size_t)nrmax);
   for (long long q = 0; q < n_leaves; ++q) {
     const int a = std::max(p_lo, ls[(size_t)q]), b = std::min(p_hi, ls[(size_t)q + 1]);
     for (int c = a; c < b; c += 32 * nrmax) {
       const int cnt = std::min(32 * nrmax, b - c);
-      ngroups[(size_t)((cnt + 31) / 32 - 1)].push_back(make_int4((int)q, c, cnt, 0));
+      for (int r = 0; r < near_split_; ++r)
+        ngroups[(size_t)((cnt + 31) / 32 - 1)].push_back(
+            make_int4((int)q, c, cnt, near_split_ == 1 ? 3 : r));
     }
   }
+  if (near_split_ > 1 && !d_part_) d_part_ = dalloc<double>(3 * (size_t)N_, "near partials");
   grouped(ngroups, near_items_h_, near_group_off_);
   n_far_ = (int)far_items_h_.size();
   n_near_ = (int)near_items_h_.size();
@@ -308,7 +319,9 @@ void DeviceOperator::far_near(const double* d_us, double* d_out, const int* perm
                          d_far_, s);
   if (near_end > near_begin)
     imqk::launch_p2p_near(P_, d_near_items_, near_group_off_.data(), near_begin, near_end, d_us,
-                          d_far_, d_out, perm, s);
+                          d_far_, d_out, perm, d_part_, s);
+  if (near_split_ > 1 && near_end > near_begin)
+    imqk::launch_near_combine(target_lo_, target_hi_, N_, d_far_, d_part_, d_out, perm, s);
 }
 
 void DeviceOperator::apply_sorted_locked(const double* d_us, double* d_out, const int* perm,

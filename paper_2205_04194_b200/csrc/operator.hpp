@@ -120,6 +120,8 @@ class DeviceOperator {
   double* d_us_ = nullptr;  // sorted input
   double* d_far_ = nullptr; // sorted far field
   double* d_b_ = nullptr;   // original-order output staging
+  double* d_part_ = nullptr;  // [3][N] near-field row partials (small problems)
+  int near_split_ = 1;
   std::vector<int> leaf_start_h_;
   int target_lo_ = 0, target_hi_ = 0;
   bool have_counts_ = false;
