@@ -110,6 +110,92 @@ __global__ void __launch_bounds__(128) k_p2m_leaf(const TreeParams P, const doub
   }
 }
 
+// Warp per finest block, G lanes per point (32/G points of the block per
+// pass): lane g of a group accumulates the moments of m in {g, g+G, g+2G, ...}
+// (m <= M).  e^g comes from binary powering of e (log2 G steps, whose last
+// base is e^G), e^{g+kG} from one complex product each.  After the pass the
+// 32/G groups are folded by shuffles in a fixed order (deterministic).
+template <int M, int G>
+__global__ void __launch_bounds__(128) k_p2m_leaf_g(const TreeParams P,
+                                                    const double* __restrict__ u_s,
+                                                    double2* __restrict__ mu) {
+  constexpr int NI = M / 2 + 1;
+  constexpr int NM = (M + G) / G;  // m values per lane
+  constexpr int LOGG = G == 8 ? 3 : (G == 16 ? 4 : 5);
+  const int lane = threadIdx.x & 31;
+  const int g = lane % G, grp = lane / G;
+  const long long leaf = (long long)blockIdx.x * 4 + (threadIdx.x >> 5);
+  const long long n_leaves = 1ll << (2 * (P.L + 1));
+  if (leaf >= n_leaves) return;
+  const int s = P.leaf_start[leaf], e = P.leaf_start[leaf + 1];
+  if (s == e) return;
+  int li, lj;
+  demorton((uint32_t)leaf, li, lj);
+  const double zx = block_center(P.ox, li, P.cell[P.L]);
+  const double zy = block_center(P.oy, lj, P.cell[P.L]);
+  double ar[NM][NI], ai[NM][NI];
+#pragma unroll
+  for (int k = 0; k < NM; ++k)
+#pragma unroll
+    for (int i = 0; i < NI; ++i) ar[k][i] = ai[k][i] = 0.0;
+  for (int p = s + grp; p < e; p += 32 / G) {
+    const double ex = P.xs[p] - zx, ey = P.ys[p] - zy;
+    const double e2 = fma(ex, ex, ey * ey);
+    double pr = u_s[p], pi = 0.0, br = ex, bi = ey;
+#pragma unroll
+    for (int b = 0; b < LOGG; ++b) {
+      if ((g >> b) & 1) {
+        const double tr = pr * br - pi * bi;
+        pi = pr * bi + pi * br;
+        pr = tr;
+      }
+      const double sr = br * br - bi * bi;
+      bi = 2.0 * br * bi;
+      br = sr;
+    }
+    // br + i bi = e^G;  pr + i pi = u e^g
+#pragma unroll
+    for (int k = 0; k < NM; ++k) {
+      double e2p = 1.0;
+#pragma unroll
+      for (int i = 0; i < NI; ++i) {
+        if (k * G + 2 * i <= M) {  // compile-time bound for the largest m of slot k
+          ar[k][i] = fma(pr, e2p, ar[k][i]);
+          ai[k][i] = fma(pi, e2p, ai[k][i]);
+        }
+        e2p *= e2;
+      }
+      if (k + 1 < NM) {
+        const double tr = pr * br - pi * bi;
+        pi = pr * bi + pi * br;
+        pr = tr;
+      }
+    }
+  }
+  // fold the 32/G point groups onto lanes 0..G-1
+#pragma unroll
+  for (int off = G; off < 32; off <<= 1)
+#pragma unroll
+    for (int k = 0; k < NM; ++k)
+#pragma unroll
+      for (int i = 0; i < NI; ++i) {
+        ar[k][i] += __shfl_down_sync(0xffffffffu, ar[k][i], off);
+        ai[k][i] += __shfl_down_sync(0xffffffffu, ai[k][i], off);
+      }
+  if (grp == 0) {
+    double2* out = mu + P.mu_off[P.L] + (size_t)leaf * P.Ke;
+#pragma unroll
+    for (int k = 0; k < NM; ++k) {
+      const int m = g + k * G;
+      if (m > M) continue;
+      const int o = mu_offset(M, m);
+#pragma unroll
+      for (int i = 0; i < NI; ++i)
+        if (m + 2 * i <= M) out[o + i] = make_double2(ar[k][i], ai[k][i]);
+    }
+  }
+}
+
 // Generic order: thread per (finest block, moment index), direct powering.
 __global__ void __launch_bounds__(128) k_p2m_leaf_generic(const TreeParams P,
                                                           const double* __restrict__ u_s,
@@ -610,7 +696,11 @@ void run_far(const TreeParams& P, int R, const int4* items, int n_items, const d
 template <int M>
 void run_p2m(const TreeParams& P, const double* u_s, double2* mu, cudaStream_t s) {
   const long long n_leaves = 1ll << (2 * (P.L + 1));
-  k_p2m_leaf<M><<<(unsigned)((n_leaves + 3) / 4), 128, 0, s>>>(P, u_s, mu);
+  // 8 lanes per point (4 points per pass) for M < 24, else the 32-lane form
+  if constexpr (M < 24)
+    k_p2m_leaf_g<M, 8><<<(unsigned)((n_leaves + 3) / 4), 128, 0, s>>>(P, u_s, mu);
+  else
+    k_p2m_leaf<M><<<(unsigned)((n_leaves + 3) / 4), 128, 0, s>>>(P, u_s, mu);
 }
 
 #define IMQ_FOR_SPECIALISED_M(X) X(0) X(1) X(2) X(4) X(6) X(8) X(10) X(12) X(14) X(16) X(18) X(20)

@@ -22,6 +22,8 @@
 
 namespace imqh {
 
+constexpr int kGemmM2MMaxKe = 256;  // M <= 30: dense translation matrices stay <= 8 MB/level
+
 void cuda_check(cudaError_t e, const char* what) {
   if (e == cudaSuccess) return;
   if (e == cudaErrorMemoryAllocation) {
@@ -91,7 +93,9 @@ void DeviceOperator::release() {
   if (stream_) cudaStreamSynchronize(stream_);
   dfree(d_xs_); dfree(d_ys_); dfree(d_leaf_); dfree(d_perm_); dfree(d_leaf_start_);
   dfree(d_far_items_); dfree(d_near_items_);
-  dfree(d_tr_off_); dfree(d_tr_idx_); dfree(d_tr_val_); dfree(d_binom_);
+  dfree(d_tr_off_); dfree(d_tr_idx_); dfree(d_tr_val_); dfree(d_binom_); dfree(d_m2m_);
+  if (blas_) cublasDestroy(blas_);
+  blas_ = nullptr;
   dfree(d_mu_); dfree(d_coef_); dfree(d_u_); dfree(d_us_); dfree(d_far_); dfree(d_b_);
   dfree(d_part_);
   if (stream_) cudaStreamDestroy(stream_);
@@ -185,12 +189,26 @@ void DeviceOperator::build(const double* xy_host) {
                                cudaMemcpyHostToDevice, s), "H2D transform");
     cuda_check(cudaMemcpyAsync(d_binom_, bn.data(), bn.size() * sizeof(double),
                                cudaMemcpyHostToDevice, s), "H2D binomials");
+    if (L_ >= 2 && Ke_ <= kGemmM2MMaxKe) {
+      // M2M translation matrices (one per parent level, exact child offsets
+      // +-cell_{l+1}/2), applied as DGEMM [parents x 8Ke] x [8Ke x 2Ke]
+      const size_t msz = (size_t)8 * Ke_ * 2 * Ke_;
+      d_m2m_ = dalloc<double>(msz * (size_t)(L_ - 1), "m2m matrices");
+      for (int l = 1; l <= L_ - 1; ++l) {
+        const std::vector<double> T = m2m_matrix(M_, 0.5 * P_.cell[l + 1]);
+        cuda_check(cudaMemcpy(d_m2m_ + msz * (size_t)(l - 1), T.data(), msz * sizeof(double),
+                              cudaMemcpyHostToDevice), "H2D m2m");
+      }
+      if (cublasCreate(&blas_) != CUBLAS_STATUS_SUCCESS) throw cuda_error("cublasCreate failed");
+    }
     T_.off = d_tr_off_;
     T_.idx = d_tr_idx_;
     T_.val = d_tr_val_;
 
     // ---- expansion storage + workspace
     d_mu_ = dalloc<double2>((size_t)mo, "moments");
+    // empty blocks keep zero moments forever (P2M never writes them)
+    cuda_check(cudaMemsetAsync(d_mu_, 0, (size_t)mo * sizeof(double2), s), "memset mu");
     d_coef_ = dalloc<double2>((size_t)co, "coefficients");
     d_u_ = dalloc<double>((size_t)n, "u");
     d_us_ = dalloc<double>((size_t)n, "u sorted");
@@ -303,7 +321,23 @@ std::vector<int> shard_bounds(const std::vector<int>& ls, int L, int world) {
 
 void DeviceOperator::moments(const double* d_us, cudaStream_t s) {
   imqk::launch_p2m_leaf(P_, d_us, d_mu_, s);
-  for (int l = L_ - 1; l >= 1; --l) imqk::launch_m2m(P_, l, d_mu_, d_binom_, s);
+  if (d_m2m_) {
+    cublasSetStream(blas_, s);
+    const size_t msz = (size_t)8 * Ke_ * 2 * Ke_;
+    const double one = 1.0, zero = 0.0;
+    for (int l = L_ - 1; l >= 1; --l) {
+      const int parents = 1 << (2 * (l + 1));
+      // row-major C[parents x 2Ke] = A[parents x 8Ke] * T[8Ke x 2Ke]
+      const cublasStatus_t st = cublasDgemm(
+          blas_, CUBLAS_OP_N, CUBLAS_OP_N, 2 * Ke_, parents, 8 * Ke_, &one,
+          d_m2m_ + msz * (size_t)(l - 1), 2 * Ke_,
+          reinterpret_cast<const double*>(d_mu_ + P_.mu_off[l + 1]), 8 * Ke_, &zero,
+          reinterpret_cast<double*>(d_mu_ + P_.mu_off[l]), 2 * Ke_);
+      if (st != CUBLAS_STATUS_SUCCESS) throw cuda_error("cublasDgemm (M2M) failed");
+    }
+  } else {
+    for (int l = L_ - 1; l >= 1; --l) imqk::launch_m2m(P_, l, d_mu_, d_binom_, s);
+  }
   imqk::launch_transform(P_, d_mu_, d_coef_, T_, s);
 }
 

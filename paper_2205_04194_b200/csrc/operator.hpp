@@ -7,6 +7,7 @@
 // "safe for concurrent application to distinct vectors" contract
 // (fastmv.hpp:17-18) without duplicating the ~GB workspace.
 #pragma once
+#include <cublas_v2.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -113,6 +114,8 @@ class DeviceOperator {
   int* d_tr_idx_ = nullptr;
   double* d_tr_val_ = nullptr;
   double* d_binom_ = nullptr;
+  double* d_m2m_ = nullptr;           // per parent level: [8 Ke][2 Ke] translation
+  cublasHandle_t blas_ = nullptr;     // M2M as one DGEMM per level
   double2* d_mu_ = nullptr;
   double2* d_coef_ = nullptr;
   size_t coef_count_ = 0;
