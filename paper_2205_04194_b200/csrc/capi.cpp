@@ -409,7 +409,7 @@ int imq_verify(const imq_verify_config* cfg, imq_verify_callback cb, void* user_
           const int sh = 2 * (P.L - l);
           for (long long q = 0; q < nb; ++q) {
             if (ls[(size_t)(q + 1) << sh] == ls[(size_t)q << sh]) continue;
-            for (int k = 0; k <= P.M; ++k) {
+            for (int k = 0; k <= imqh::horner_top(P.M, 0); ++k) {
               const double2 v = coef[(size_t)P.coef_off[l] + (size_t)q * P.K +
                                      (size_t)imqh::horner_index(P.M, 0, k)];
               worst = std::max(worst, std::fabs(v.y));

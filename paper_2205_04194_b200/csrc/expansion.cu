@@ -47,6 +47,12 @@ __host__ __device__ __forceinline__ void mu_unindex(int M, int o, int& m, int& i
   i = o;
 }
 
+// Horner layout (host_math.hpp): group m holds k = top(m)..m.
+__host__ __device__ constexpr int hz_top(int M, int m) { return M - ((M - m) & 1); }
+__host__ __device__ constexpr int hz_count(int M) {
+  return (M + 1) * (M + 2) / 2 - (M + 1) / 2;
+}
+
 __device__ __forceinline__ int block_count(const TreeParams& P, int level, uint32_t q) {
   int sh = 2 * (P.L - level);
   return P.leaf_start[(size_t)(q + 1) << sh] - P.leaf_start[(size_t)q << sh];
@@ -349,7 +355,7 @@ __global__ void k_transform(const TreeParams P, int level, const double2* __rest
 
 // ------------------------------------------------------------------- M2P ---
 constexpr int kMaxList = 384;
-constexpr int kFarMaxR = 6;  // a far work item holds <= 32 * kFarMaxR targets  // 12 + 27 (L - 2) + 36 <= 372 for L <= 13
+constexpr int kFarMaxR = 8;  // a far work item holds <= 32 * kFarMaxR targets  // 12 + 27 (L - 2) + 36 <= 372 for L <= 13
 
 // Builds the warp's source list for a work item: every non-empty source block
 // at levels 1..L-1 of the (shared) ancestor lists, then the level-L union over
@@ -435,7 +441,7 @@ __device__ __forceinline__ void far_evalR(const double2* __restrict__ c, const d
     for (int p = 0; p < R; ++p) v[p] = c[0].x * r[p];
   } else {
     double xr[R], xi[R], ar[R], ai[R];
-    double2 cc = c[0];
+    double2 cc = c[0];  // group m = M: the single coefficient C_{M,M}
 #pragma unroll
     for (int p = 0; p < R; ++p) {
       xr[p] = dx[p] * q[p];
@@ -446,7 +452,7 @@ __device__ __forceinline__ void far_evalR(const double2* __restrict__ c, const d
     int o = 1;
 #pragma unroll
     for (int m = M - 1; m >= 1; --m) {
-      cc = c[o++];
+      cc = c[o++];  // C_{m, top(m)}
       double gr[R], gi[R];
 #pragma unroll
       for (int p = 0; p < R; ++p) {
@@ -454,7 +460,7 @@ __device__ __forceinline__ void far_evalR(const double2* __restrict__ c, const d
         gi[p] = cc.y;
       }
 #pragma unroll
-      for (int k = M - 1; k >= m; --k) {
+      for (int k = hz_top(M, m) - 1; k >= m; --k) {
         cc = c[o++];
 #pragma unroll
         for (int p = 0; p < R; ++p) {
@@ -476,7 +482,7 @@ __device__ __forceinline__ void far_evalR(const double2* __restrict__ c, const d
 #pragma unroll
     for (int p = 0; p < R; ++p) g[p] = c0[0];
 #pragma unroll
-    for (int k = 1; k <= M; ++k) {
+    for (int k = 1; k <= hz_top(M, 0); ++k) {
       const double ck = c0[2 * k];
 #pragma unroll
       for (int p = 0; p < R; ++p) g[p] = fma(g[p], q[p], ck);
@@ -499,7 +505,7 @@ __device__ __forceinline__ double far_eval_generic(const double2* __restrict__ c
   for (int m = M - 1; m >= 1; --m) {
     cc = __ldg(&c[o++]);
     double gr = cc.x, gi = cc.y;
-    for (int k = M - 1; k >= m; --k) {
+    for (int k = hz_top(M, m) - 1; k >= m; --k) {
       cc = __ldg(&c[o++]);
       gr = fma(gr, q, cc.x);
       gi = fma(gi, q, cc.y);
@@ -510,27 +516,33 @@ __device__ __forceinline__ double far_eval_generic(const double2* __restrict__ c
     ai = ni;
   }
   double g = __ldg(&c[o++].x);
-  for (int k = M - 1; k >= 0; --k) g = fma(g, q, __ldg(&c[o++].x));
+  for (int k = hz_top(M, 0) - 1; k >= 0; --k) g = fma(g, q, __ldg(&c[o++].x));
   return fma(ar, xr, fma(-ai, xi, g)) * r;
 }
 
+// Targets of a lane: coordinates in registers; the leaf of each target is one
+// of the four children of the item's level-(L-1) block, packed 2 bits each,
+// with a validity bit (slots past the item's count).
 template <int R>
 struct Targets {
   double x[R], y[R];
-  int li[R], lj[R];
-  bool v[R];
+  uint32_t child;  // 2 bits per slot
+  uint32_t valid;  // 1 bit per slot
 };
 
 template <int R>
 __device__ __forceinline__ void load_targets(const TreeParams& P, int s, int cnt, int lane,
                                              Targets<R>& T) {
+  T.child = 0;
+  T.valid = 0;
 #pragma unroll
   for (int p = 0; p < R; ++p) {
-    T.v[p] = lane + 32 * p < cnt;
-    const int a = T.v[p] ? s + lane + 32 * p : s;
+    const bool v = lane + 32 * p < cnt;
+    const int a = v ? s + lane + 32 * p : s;
     T.x[p] = P.xs[a];
     T.y[p] = P.ys[a];
-    demorton(P.leaf[a], T.li[p], T.lj[p]);
+    T.child |= (P.leaf[a] & 3u) << (2 * p);
+    T.valid |= (v ? 1u : 0u) << p;
   }
 }
 
@@ -544,7 +556,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_m2p_far(const TreeParams P
                                                              int n_items,
                                                              const double2* __restrict__ coef,
                                                              double* __restrict__ far_s) {
-  constexpr int K = (M + 1) * (M + 2) / 2;
+  constexpr int K = hz_count(M);
   constexpr uint32_t kBytes = K * 16;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -573,6 +585,10 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_m2p_far(const TreeParams P
   Targets<R> T;
   load_targets<R>(P, s0, cnt, lane, T);
   const int L = P.L;
+  int pi2, pj2;  // finest-level index of the item's first child
+  demorton(par, pi2, pj2);
+  pi2 *= 2;
+  pj2 *= 2;
 
   auto issue = [&](int e, int slot) {
     const uint32_t ent = list[e];
@@ -596,11 +612,20 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_m2p_far(const TreeParams P
     demorton(ent & 0x0fffffffu, qi, qj);
     const double zx = block_center(P.ox, qi, P.cell[l]);
     const double zy = block_center(P.oy, qj, P.cell[l]);
+    // level-L sources: usable by the children of `par` at Chebyshev
+    // distance >= 2 (4-bit mask over the children), others by every target
+    uint32_t cmask = 0xfu;
+    if (l == L) {
+      cmask = 0;
+#pragma unroll
+      for (int ch = 0; ch < 4; ++ch)
+        cmask |= (max(abs(qi - (pi2 + (ch >> 1))), abs(qj - (pj2 + (ch & 1)))) >= 2 ? 1u : 0u) << ch;
+    }
     bool msk[R];
     double dx[R], dy[R], v[R];
 #pragma unroll
     for (int p = 0; p < R; ++p) {
-      msk[p] = T.v[p] && (l < L || max(abs(qi - T.li[p]), abs(qj - T.lj[p])) >= 2);
+      msk[p] = ((T.valid >> p) & 1u) && ((cmask >> ((T.child >> (2 * p)) & 3u)) & 1u);
       dx[p] = T.x[p] - zx;
       dy[p] = T.y[p] - zy;
     }
@@ -616,7 +641,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_m2p_far(const TreeParams P
   }
 #pragma unroll
   for (int p = 0; p < R; ++p)
-    if (T.v[p]) far_s[s0 + lane + 32 * p] = acc[p];
+    if ((T.valid >> p) & 1u) far_s[s0 + lane + 32 * p] = acc[p];
 }
 
 template <int WARPS>
@@ -662,7 +687,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_m2p_far_generic(const TreeParams
 template <int M, int R, int W, int S, int MINB>
 void run_far_cfg(const TreeParams& P, const int4* items, int n_items, const double2* coef,
                  double* far_s, cudaStream_t s) {
-  constexpr int K = (M + 1) * (M + 2) / 2;
+  constexpr int K = hz_count(M);
   auto kern = k_m2p_far<M, R, W, S, MINB>;
   const size_t smem = (size_t)W * S * K * 16 + W * S * 8 + W * kMaxList * 4;
   static bool configured = false;  // per template instance
@@ -689,7 +714,9 @@ void run_far(const TreeParams& P, int R, const int4* items, int n_items, const d
     case 3: return run_far_cfg<M, 3, 4, 3, 1>(P, items, n_items, coef, far_s, s);
     case 4: return run_far_cfg<M, 4, 4, 3, 1>(P, items, n_items, coef, far_s, s);
     case 5: return run_far_cfg<M, 5, 4, 3, 1>(P, items, n_items, coef, far_s, s);
-    default: return run_far_cfg<M, 6, 4, 3, 1>(P, items, n_items, coef, far_s, s);
+    case 6: return run_far_cfg<M, 6, 4, 3, 1>(P, items, n_items, coef, far_s, s);
+    case 7: return run_far_cfg<M, 7, 4, 3, 1>(P, items, n_items, coef, far_s, s);
+    default: return run_far_cfg<M, 8, 4, 3, 1>(P, items, n_items, coef, far_s, s);
   }
 }
 
@@ -767,7 +794,7 @@ void launch_m2p_far(const TreeParams& P, const int4* items, const int* group_off
                                                                         coef, far_s);
     return;
   }
-  for (int R = 1; R <= kFarMaxR; ++R) {
+  for (int R = kFarMaxR; R >= 1; --R) {  // longest items first
     const int lo = std::max(begin, group_off[R - 1]), hi = std::min(end, group_off[R]);
     if (hi <= lo) continue;
     switch (P.M) {

@@ -218,20 +218,20 @@ void write_points(const std::string& path, const double* xy, size_t n) {
 // Derivation: P_n^m(x) = sin^m(theta) (-1)^m D^m P_n(x), x = t/rho,
 // sin(theta) e^{-i m w} = conj(dx + i dy)/rho; see DESIGN.md §3.
 Transform build_transform(int M, double t) {
-  const int K = order_K(M);
+  const int K = horner_count(M);
   std::vector<long double> pascal((size_t)(2 * M + 2) * (2 * M + 2), 0.0L);
   auto Cb = [&](int a, int b) -> long double & { return pascal[(size_t)a * (2 * M + 2) + b]; };
   for (int a = 0; a <= 2 * M + 1; ++a) {
     Cb(a, 0) = 1.0L;
     for (int b = 1; b <= a; ++b) Cb(a, b) = Cb(a - 1, b - 1) + (b <= a - 1 ? Cb(a - 1, b) : 0.0L);
   }
-  std::vector<double> pn0((size_t)K);
+  std::vector<double> pn0((size_t)order_K(M));
   legendre_table(M, 0.0, 1.0, pn0.data());
   Transform T;
   T.off.assign((size_t)K + 1, 0);
   std::vector<std::vector<std::pair<int, double>>> rows((size_t)K);
   for (int m = 0; m <= M; ++m)
-    for (int k = m; k <= M; ++k) {
+    for (int k = m; k <= horner_top(M, m); ++k) {
       const int o = horner_index(M, m, k);
       for (int n = k; n <= std::min(M, 2 * k - m); ++n) {
         if ((n - m) % 2) continue;

@@ -25,7 +25,16 @@ struct singular_error : std::runtime_error {
 inline int order_K(int M) { return (M + 1) * (M + 2) / 2; }
 int order_Ke(int M);  // #{(n, m) : n - m even, 0 <= m <= n <= M}
 int mu_offset(int M, int m);
-inline int horner_index(int M, int m, int k) { return (M - m) * (M - m + 1) / 2 + (M - k); }
+// Far-field coefficient layout ("Horner order"): groups m = M..0, inside a
+// group k = top(m)..m.  C_{m,M} vanishes identically when M - m is odd (no n
+// with n = m mod 2 fits in [M, min(M, 2M - m)]), so such groups start at M-1.
+inline int horner_top(int M, int m) { return M - ((M - m) & 1); }
+inline int horner_count(int M) { return order_K(M) - (M + 1) / 2; }
+inline int horner_index(int M, int m, int k) {
+  int o = 0;
+  for (int mm = M; mm > m; --mm) o += horner_top(M, mm) - mm + 1;
+  return o + (horner_top(M, m) - k);
+}
 
 void check_t(double t);  // expansion.cpp:11-13
 void check_M(int M);     // specfun.cpp:8-10

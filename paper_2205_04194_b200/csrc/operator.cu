@@ -124,7 +124,7 @@ void DeviceOperator::build(const double* xy_host) {
     cuda_check(cudaStreamSynchronize(s), "minmax");
     if (ext[4] > 0.0) throw std::invalid_argument("build_operator: non-finite coordinate");
     check_M(M_);
-    K_ = order_K(M_);
+    K_ = horner_count(M_);  // stored far coefficients per block (zero slots dropped)
     Ke_ = order_Ke(M_);
     square_from_extrema(ext[0], ext[1], ext[2], ext[3], sq_);
     if (L_ <= 0) L_ = pending_levels_ > 0 ? pending_levels_ : auto_level(N_, M_);
@@ -239,12 +239,12 @@ void DeviceOperator::build_items(int p_lo, int p_hi) {
   near_items_h_.clear();
   auto grouped = [](std::vector<std::vector<int4>>& g, std::vector<int4>& out,
                     std::vector<int>& off) {
-    off.assign(8, 0);
+    off.assign(16, 0);
     for (size_t r = 0; r < g.size(); ++r) {
       out.insert(out.end(), g[r].begin(), g[r].end());
       off[r + 1] = (int)out.size();
     }
-    for (size_t r = g.size() + 1; r < 8; ++r) off[r] = (int)out.size();
+    for (size_t r = g.size() + 1; r < 16; ++r) off[r] = (int)out.size();
   };
   // Points per lane: as large as the kernels allow (register blocking), but
   // small enough that the GPU still gets >= ~8 waves of warps (kWarpsWanted).
@@ -255,8 +255,12 @@ void DeviceOperator::build_items(int p_lo, int p_hi) {
   std::vector<std::vector<int4>> groups((size_t)rmax);
   for (long long p = 0; p < n_par; ++p) {
     const int a = std::max(p_lo, ls[(size_t)(4 * p)]), b = std::min(p_hi, ls[(size_t)(4 * p + 4)]);
-    for (int c = a; c < b; c += 32 * rmax) {
-      const int cnt = std::min(32 * rmax, b - c);
+    if (b <= a) continue;
+    // balanced chunks: fewest items of <= 32 rmax targets, sizes multiple of 32
+    const int nchunk = (b - a + 32 * rmax - 1) / (32 * rmax);
+    const int size = 32 * ((b - a + 32 * nchunk - 1) / (32 * nchunk));
+    for (int c = a; c < b; c += size) {
+      const int cnt = std::min(size, b - c);
       groups[(size_t)((cnt + 31) / 32 - 1)].push_back(make_int4((int)p, c, cnt, 0));
     }
   }
