@@ -42,3 +42,52 @@ def test_config4_full_size(imq, oracle):
     bm = op.apply(0.25 * u - 2.0 * u2)
     assert rel_err_inf(bm, 0.25 * b - 2.0 * b2) <= 1e-12
     assert np.array_equal(op.apply(u), b)
+
+
+def test_config5_sweep_sampled(imq, oracle):
+    """4,194,304 uniform points, L=7: p x c corners of the sweep, sampled rows vs
+    the oracle (<=1e-10) and vs the direct sum at the truncation error."""
+    from paper_2205_04194_b200 import inputs
+    n = 1 << 22
+    xy = inputs.uniform_points(n, 0)
+    u = inputs.random_vector(n, 42)
+    rows = (np.arange(4096) * n) // 4096  # i_r = floor(r N / 4096)
+    sub = rows[::64]
+    dense = {}
+    for p, c in ((4, 0.001), (12, 0.1), (16, 0.01), (20, 1.0)):
+        op = imq.FastOperator(xy, c, p, 7)
+        b = op.apply(u)
+        ref = oracle.fast_matvec_rows(xy, c, p, 7, u, sub)
+        assert np.max(np.abs(b[sub] - ref)) / np.max(np.abs(ref)) <= 1e-10, (p, c)
+        if c not in dense:
+            dense[c] = oracle.dense_matvec(xy, c, u, sub)
+        d = dense[c]
+        assert np.max(np.abs(b[sub] - d)) <= 2 * np.max(np.abs(ref - d)) + 1e-12 * np.max(np.abs(d))
+        op.close()
+
+
+def test_dense_262144(imq, oracle):
+    """Config 5's direct O(N^2) reference point at N = 262,144."""
+    from paper_2205_04194_b200 import inputs
+    n = 262144
+    xy = inputs.uniform_points(n, 0)
+    u = inputs.random_vector(n, 42)
+    b = imq.dense_matvec(xy, 0.01, u)
+    rows = np.arange(0, n, n // 256)
+    ref = oracle.dense_matvec(xy, 0.01, u, rows)
+    assert np.max(np.abs(b[rows] - ref)) / np.max(np.abs(ref)) <= 1e-12
+
+
+def test_config2_gmres_iteration_matched(imq, oracle):
+    """SURVEY 8(d) protocol: same cap, compare the restart-boundary residuals."""
+    from paper_2205_04194_b200 import inputs
+    xy = inputs.uniform_points(65536, 0)
+    f = inputs.cfg2_rhs(xy)
+    op = imq.FastOperator(xy, 0.05, 12, 0)
+    assert op.levels == 2  # auto level of the reference for N = 65536, M = 12
+    r = op.solve(f, 1e-8, 100, 50)
+    ref = oracle.iterative_solve(xy, 0.05, 12, 0, f, 1e-8, 100, 50)
+    assert r.iterations == ref["iterations"] == 100
+    cr, rr = np.array(r.cycle_residuals), ref["cycle_residuals"]
+    assert cr.size == rr.size
+    assert np.max(np.abs(cr - rr) / rr) <= 1e-6
