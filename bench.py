@@ -342,7 +342,12 @@ def b200_arm(args):
         cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
 
     if rank == 0:
-        launches_per_step = (1 if world == 1 else 0) + 1 + (L - 1) + L + 1 + 1
+        fi, ni = op.items("far"), op.items("near")
+        groups = lambda it: len(set(((it[:, 2] + 31) // 32).tolist())) if len(it) else 0
+        split = int(len(ni) and (ni[:, 3] != 3).any())
+        # ours per step: gather, leaf P2M, L transforms, far groups, near groups
+        # (+ combine when the near sources are split); the L-1 M2M DGEMMs are cuBLAS
+        launches_per_step = 1 + 1 + L + groups(fi) + groups(ni) + split
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
