@@ -194,10 +194,15 @@ def b200_arm(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    P.set_device(local)
+    dev = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(dev)
+    P.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("IMQ_DIST_BACKEND", "nccl")  # gloo: code-path checks on 1 GPU
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
 
     n = args.n or CFG["n"]
     L = CFG["levels"] if n == CFG["n"] else 0
@@ -227,7 +232,10 @@ def b200_arm(args):
     perm = torch.from_numpy(op.permutation().astype(np.int64)).cuda()
 
     def step(k):
-        op.apply_device(dev_u[k % nvec], d_b, stream)
+        if world == 1:
+            op.apply_device(dev_u[k % nvec], d_b, stream)
+        else:
+            sh.apply_device(dev_u[k % nvec], d_b, stream)
 
     def barrier():
         if world > 1:
@@ -239,7 +247,7 @@ def b200_arm(args):
     barrier()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
+    with ClockSampler(dev) as clk:
         e0.record(stream)
         for k in range(args.steps):
             step(args.warmup + k)
@@ -267,7 +275,7 @@ def b200_arm(args):
         else:
             d_u = dev_u[0]
             d_u.copy_(pin_u[k % 2], non_blocking=True)
-            op.apply_device(d_u, d_b, stream)
+            sh.apply_device(d_u, d_b, stream)
             mine = torch.index_select(d_b, 0, owned)
             pin_b[:mine.numel()].copy_(mine, non_blocking=True)
             torch.cuda.synchronize()
@@ -286,7 +294,10 @@ def b200_arm(args):
 
     # ---- roofline of the dominant kernel (M2P far field), timed live
     torch.index_select(dev_u[0], 0, perm, out=d_us)
-    op.moments(d_us, stream)
+    if world == 1:
+        op.moments(d_us, stream)
+    else:
+        sh.moments(dev_u[0], stream)
     nf = far_items
     op.far_near(d_us, d_b, (0, nf), (0, 0), stream)
     torch.cuda.synchronize()
@@ -303,7 +314,10 @@ def b200_arm(args):
     torch.cuda.synchronize()
     near_ms = e0.elapsed_time(e1)
     e0.record(stream)
-    op.moments(d_us, stream)
+    if world == 1:
+        op.moments(d_us, stream)
+    else:
+        sh.moments(dev_u[0], stream)
     e1.record(stream)
     torch.cuda.synchronize()
     mom_ms = e0.elapsed_time(e1)
@@ -396,7 +410,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
-    ap.add_argument("--n", type=int, default=0, help="override N (development only)")
+    ap.add_argument("--points", dest="n", type=int, default=0, help="override N (development only)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-gmres", action="store_true")
     ap.add_argument("--gmres-iters", type=int, default=2000)

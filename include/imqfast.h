@@ -165,7 +165,20 @@ IMQ_API int imq_ext_operator_items(const imq_operator* op, int which, int* items
                            size_t* count);
 IMQ_API int imq_ext_operator_far_near(const imq_operator* op, const double* d_us, double* d_bs,
                               int far_begin, int far_end, int near_begin, int near_end,
-                              void* stream);
+                              int scatter, void* stream);
+/* u (original order) -> Morton order. */
+IMQ_API int imq_ext_operator_gather(const imq_operator* op, const double* d_u, double* d_us,
+                                    void* stream);
+/* Sharded moments (after imq_ext_operator_restrict): own + halo fine levels and
+ * own-only coarse partial moments; all-reduce (sum) the coarse region returned
+ * by imq_ext_operator_coarse_moments over the ranks, then moments_finish.
+ * Unrestricted operators: moments_local forms the full moments, the coarse
+ * region is empty and moments_finish is a no-op. */
+IMQ_API int imq_ext_operator_moments_local(const imq_operator* op, const double* d_us,
+                                           void* stream);
+IMQ_API int imq_ext_operator_coarse_moments(const imq_operator* op, void** d_ptr,
+                                            size_t* n_doubles);
+IMQ_API int imq_ext_operator_moments_finish(const imq_operator* op, void* stream);
 
 /* Sharded application over `world` GPUs: sorted-position bounds (world+1
  * entries) cut at level-(L-1) block boundaries with balanced point counts,

@@ -280,10 +280,27 @@ class FastOperator:
                                            n.value, C.byref(n)))
         return out
 
-    def far_near(self, d_us, d_bs, far_range, near_range, stream=None) -> None:
+    def far_near(self, d_us, d_bs, far_range, near_range, stream=None, scatter=False) -> None:
         check(lib().imq_ext_operator_far_near(self._h, _addr(d_us), _addr(d_bs), far_range[0],
                                               far_range[1], near_range[0], near_range[1],
-                                              _stream(stream)))
+                                              1 if scatter else 0, _stream(stream)))
+
+    def gather(self, d_u, d_us, stream=None) -> None:
+        check(lib().imq_ext_operator_gather(self._h, _addr(d_u), _addr(d_us), _stream(stream)))
+
+    def moments_local(self, d_us, stream=None) -> None:
+        check(lib().imq_ext_operator_moments_local(self._h, _addr(d_us), _stream(stream)))
+
+    def coarse_moments(self):
+        """(device pointer, number of doubles) of the coarse moment region that
+        sharded ranks all-reduce; 0 doubles when the operator is not sharded."""
+        p = C.c_void_p()
+        n = C.c_size_t()
+        check(lib().imq_ext_operator_coarse_moments(self._h, C.byref(p), C.byref(n)))
+        return p.value, n.value
+
+    def moments_finish(self, stream=None) -> None:
+        check(lib().imq_ext_operator_moments_finish(self._h, _stream(stream)))
 
 
 def _addr(x) -> int:

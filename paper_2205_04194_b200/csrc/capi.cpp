@@ -542,6 +542,46 @@ int imq_ext_operator_moments(const imq_operator* op, const double* d_us, void* s
   });
 }
 
+int imq_ext_operator_gather(const imq_operator* op, const double* d_u, double* d_us,
+                            void* stream) {
+  if (!op || !d_u || !d_us) return fail(IMQ_ERR_INVALID_ARG, "imq_ext_operator_gather: null argument");
+  return guard([&] {
+    imqk::launch_gather(d_u, op->op->perm_ptr(), op->op->size(), d_us,
+                        static_cast<cudaStream_t>(stream));
+    imqh::cuda_check(cudaGetLastError(), "gather launch");
+    return IMQ_OK;
+  });
+}
+
+int imq_ext_operator_moments_local(const imq_operator* op, const double* d_us, void* stream) {
+  if (!op || !d_us) return fail(IMQ_ERR_INVALID_ARG, "imq_ext_operator_moments_local: null argument");
+  return guard([&] {
+    op->op->moments_local(d_us, static_cast<cudaStream_t>(stream));
+    imqh::cuda_check(cudaGetLastError(), "moments_local launch");
+    return IMQ_OK;
+  });
+}
+
+int imq_ext_operator_coarse_moments(const imq_operator* op, void** d_ptr, size_t* n_doubles) {
+  if (!op || !d_ptr || !n_doubles)
+    return fail(IMQ_ERR_INVALID_ARG, "imq_ext_operator_coarse_moments: null argument");
+  double2* p = nullptr;
+  size_t n = 0;
+  op->op->coarse_moments(&p, &n);
+  *d_ptr = p;
+  *n_doubles = 2 * n;
+  return IMQ_OK;
+}
+
+int imq_ext_operator_moments_finish(const imq_operator* op, void* stream) {
+  if (!op) return fail(IMQ_ERR_INVALID_ARG, "imq_ext_operator_moments_finish: null argument");
+  return guard([&] {
+    op->op->moments_finish(static_cast<cudaStream_t>(stream));
+    imqh::cuda_check(cudaGetLastError(), "moments_finish launch");
+    return IMQ_OK;
+  });
+}
+
 int imq_ext_operator_coefficients(const imq_operator* op, void** d_coef, size_t* count,
                                   long long* level_offsets, int capacity) {
   if (!op || !d_coef || !count)
@@ -568,11 +608,11 @@ int imq_ext_operator_items(const imq_operator* op, int which, int* items_xyzw, s
 
 int imq_ext_operator_far_near(const imq_operator* op, const double* d_us, double* d_bs,
                               int far_begin, int far_end, int near_begin, int near_end,
-                              void* stream) {
+                              int scatter, void* stream) {
   if (!op || !d_us || !d_bs) return fail(IMQ_ERR_INVALID_ARG, "imq_ext_operator_far_near: null argument");
   return guard([&] {
-    op->op->far_near(d_us, d_bs, nullptr, static_cast<cudaStream_t>(stream), far_begin, far_end,
-                     near_begin, near_end);
+    op->op->far_near(d_us, d_bs, scatter ? op->op->perm_ptr() : nullptr,
+                     static_cast<cudaStream_t>(stream), far_begin, far_end, near_begin, near_end);
     imqh::cuda_check(cudaGetLastError(), "far_near launch");
     return IMQ_OK;
   });

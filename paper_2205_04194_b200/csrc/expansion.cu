@@ -66,12 +66,14 @@ __device__ __forceinline__ int block_first(const TreeParams& P, int level, uint3
 // the block's points in sorted (= ascending original index) order.
 template <int M>
 __global__ void __launch_bounds__(128) k_p2m_leaf(const TreeParams P, const double* __restrict__ u_s,
-                                                  double2* __restrict__ mu) {
+                                                  double2* __restrict__ mu,
+                                                  const int* __restrict__ leaf_list, int n_list) {
   constexpr int NI = M / 2 + 1;
   const int lane = threadIdx.x & 31;
-  const long long leaf = (long long)blockIdx.x * 4 + (threadIdx.x >> 5);
-  const long long n_leaves = 1ll << (2 * (P.L + 1));
-  if (leaf >= n_leaves) return;
+  const long long wid = (long long)blockIdx.x * 4 + (threadIdx.x >> 5);
+  const long long n_leaves = leaf_list ? n_list : 1ll << (2 * (P.L + 1));
+  if (wid >= n_leaves) return;
+  const long long leaf = leaf_list ? leaf_list[wid] : wid;
   const int s = P.leaf_start[leaf], e = P.leaf_start[leaf + 1];
   if (s == e) return;
   int li, lj;
@@ -124,15 +126,18 @@ __global__ void __launch_bounds__(128) k_p2m_leaf(const TreeParams P, const doub
 template <int M, int G>
 __global__ void __launch_bounds__(128) k_p2m_leaf_g(const TreeParams P,
                                                     const double* __restrict__ u_s,
-                                                    double2* __restrict__ mu) {
+                                                    double2* __restrict__ mu,
+                                                    const int* __restrict__ leaf_list,
+                                                    int n_list) {
   constexpr int NI = M / 2 + 1;
   constexpr int NM = (M + G) / G;  // m values per lane
   constexpr int LOGG = G == 8 ? 3 : (G == 16 ? 4 : 5);
   const int lane = threadIdx.x & 31;
   const int g = lane % G, grp = lane / G;
-  const long long leaf = (long long)blockIdx.x * 4 + (threadIdx.x >> 5);
-  const long long n_leaves = 1ll << (2 * (P.L + 1));
-  if (leaf >= n_leaves) return;
+  const long long wid = (long long)blockIdx.x * 4 + (threadIdx.x >> 5);
+  const long long n_leaves = leaf_list ? n_list : 1ll << (2 * (P.L + 1));
+  if (wid >= n_leaves) return;
+  const long long leaf = leaf_list ? leaf_list[wid] : wid;
   const int s = P.leaf_start[leaf], e = P.leaf_start[leaf + 1];
   if (s == e) return;
   int li, lj;
@@ -205,12 +210,15 @@ __global__ void __launch_bounds__(128) k_p2m_leaf_g(const TreeParams P,
 // Generic order: thread per (finest block, moment index), direct powering.
 __global__ void __launch_bounds__(128) k_p2m_leaf_generic(const TreeParams P,
                                                           const double* __restrict__ u_s,
-                                                          double2* __restrict__ mu) {
+                                                          double2* __restrict__ mu,
+                                                          const int* __restrict__ leaf_list,
+                                                          int n_list) {
   const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long long n_leaves = 1ll << (2 * (P.L + 1));
-  const long long leaf = gid / P.Ke;
+  const long long n_leaves = leaf_list ? n_list : 1ll << (2 * (P.L + 1));
+  const long long wid = gid / P.Ke;
   const int o = (int)(gid % P.Ke);
-  if (leaf >= n_leaves) return;
+  if (wid >= n_leaves) return;
+  const long long leaf = leaf_list ? leaf_list[wid] : wid;
   const int s = P.leaf_start[leaf], e = P.leaf_start[leaf + 1];
   if (s == e) return;
   int li, lj, m, i;
@@ -334,9 +342,10 @@ __global__ void k_m2m(const TreeParams P, int level, double2* __restrict__ mu,
 
 // ------------------------------------------------------------- transform ---
 __global__ void k_transform(const TreeParams P, int level, const double2* __restrict__ mu,
-                            double2* __restrict__ coef, const TransformTable T) {
+                            double2* __restrict__ coef, const TransformTable T,
+                            const int* __restrict__ block_list) {
   extern __shared__ double2 sm[];
-  const uint32_t q = blockIdx.x;
+  const uint32_t q = block_list ? (uint32_t)block_list[blockIdx.x] : blockIdx.x;
   if (block_count(P, level, q) == 0) return;
   const double2* src = mu + P.mu_off[level] + (size_t)q * P.Ke;
   for (int o = threadIdx.x; o < P.Ke; o += blockDim.x) sm[o] = src[o];
@@ -721,13 +730,14 @@ void run_far(const TreeParams& P, int R, const int4* items, int n_items, const d
 }
 
 template <int M>
-void run_p2m(const TreeParams& P, const double* u_s, double2* mu, cudaStream_t s) {
-  const long long n_leaves = 1ll << (2 * (P.L + 1));
+void run_p2m(const TreeParams& P, const double* u_s, double2* mu, const int* list, int n_list,
+             cudaStream_t s) {
+  const long long n_leaves = list ? n_list : 1ll << (2 * (P.L + 1));
   // 8 lanes per point (4 points per pass) for M < 24, else the 32-lane form
   if constexpr (M < 24)
-    k_p2m_leaf_g<M, 8><<<(unsigned)((n_leaves + 3) / 4), 128, 0, s>>>(P, u_s, mu);
+    k_p2m_leaf_g<M, 8><<<(unsigned)((n_leaves + 3) / 4), 128, 0, s>>>(P, u_s, mu, list, n_list);
   else
-    k_p2m_leaf<M><<<(unsigned)((n_leaves + 3) / 4), 128, 0, s>>>(P, u_s, mu);
+    k_p2m_leaf<M><<<(unsigned)((n_leaves + 3) / 4), 128, 0, s>>>(P, u_s, mu, list, n_list);
 }
 
 #define IMQ_FOR_SPECIALISED_M(X) X(0) X(1) X(2) X(4) X(6) X(8) X(10) X(12) X(14) X(16) X(18) X(20)
@@ -745,17 +755,20 @@ bool m2p_specialised(int M) {
   }
 }
 
-void launch_p2m_leaf(const TreeParams& P, const double* u_s, double2* mu, cudaStream_t s) {
+void launch_p2m_leaf(const TreeParams& P, const double* u_s, double2* mu, const int* leaf_list,
+                     int n_list, cudaStream_t s) {
   switch (P.M) {
-#define X(m)                    \
-  case m:                       \
-    run_p2m<m>(P, u_s, mu, s); \
+#define X(m)                                      \
+  case m:                                         \
+    run_p2m<m>(P, u_s, mu, leaf_list, n_list, s); \
     return;
     IMQ_FOR_SPECIALISED_M(X)
 #undef X
     default: {
-      const long long n = (1ll << (2 * (P.L + 1))) * (long long)P.Ke;
-      k_p2m_leaf_generic<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(P, u_s, mu);
+      const long long n =
+          (leaf_list ? (long long)n_list : (1ll << (2 * (P.L + 1)))) * (long long)P.Ke;
+      k_p2m_leaf_generic<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(P, u_s, mu, leaf_list,
+                                                                    n_list);
     }
   }
 }
@@ -775,13 +788,44 @@ void launch_m2m(const TreeParams& P, int level, double2* mu, const double* binom
 }
 
 void launch_transform(const TreeParams& P, const double2* mu, double2* coef,
-                      const TransformTable& T, cudaStream_t s) {
+                      const TransformTable& T, cudaStream_t s, int l_lo, int l_hi,
+                      const int* block_list, int n_list) {
   const size_t smem = (size_t)P.Ke * sizeof(double2);
   const int threads = ((P.K + 31) / 32) * 32 > 1024 ? 1024 : ((P.K + 31) / 32) * 32;
-  for (int l = 1; l <= P.L; ++l) {
-    const unsigned nb = 1u << (2 * (l + 1));
-    k_transform<<<nb, threads, smem, s>>>(P, l, mu, coef, T);
+  if (l_lo < 1) l_lo = 1;
+  if (l_hi < 1 || l_hi > P.L) l_hi = P.L;
+  for (int l = l_lo; l <= l_hi; ++l) {
+    const unsigned nb = block_list ? (unsigned)n_list : 1u << (2 * (l + 1));
+    if (nb) k_transform<<<nb, threads, smem, s>>>(P, l, mu, coef, T, block_list);
   }
+}
+
+// rows[i] <- src[idx[i]] (row = `width` doubles); used to pack / unpack the
+// M2M DGEMM operands of a block subset.
+__global__ void k_gather_rows(const double* __restrict__ src, const int* __restrict__ idx,
+                              int n, int width, double* __restrict__ dst) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long long)n * width) return;
+  const int r = (int)(t / width), c = (int)(t % width);
+  dst[t] = src[(size_t)idx[r] * width + c];
+}
+__global__ void k_scatter_rows(const double* __restrict__ src, const int* __restrict__ idx,
+                               int n, int width, double* __restrict__ dst) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long long)n * width) return;
+  const int r = (int)(t / width), c = (int)(t % width);
+  dst[(size_t)idx[r] * width + c] = src[t];
+}
+
+void launch_gather_rows(const double* src, const int* idx, int n, int width, double* dst,
+                        cudaStream_t s) {
+  const long long t = (long long)n * width;
+  if (t) k_gather_rows<<<(unsigned)((t + 255) / 256), 256, 0, s>>>(src, idx, n, width, dst);
+}
+void launch_scatter_rows(const double* src, const int* idx, int n, int width, double* dst,
+                         cudaStream_t s) {
+  const long long t = (long long)n * width;
+  if (t) k_scatter_rows<<<(unsigned)((t + 255) / 256), 256, 0, s>>>(src, idx, n, width, dst);
 }
 
 void launch_m2p_far(const TreeParams& P, const int4* items, const int* group_off, int begin,

@@ -61,11 +61,19 @@ void launch_sort(void* temp, size_t temp_bytes, const uint32_t* k_in, uint32_t* 
                  const int* v_in, int* v_out, long long n, int bits, cudaStream_t s);
 
 // ---- expansion (expansion.cu)
-void launch_p2m_leaf(const TreeParams& P, const double* u_s, double2* mu, cudaStream_t s);
+// leaf_list == nullptr: every finest block; else the n_list listed leaves.
+void launch_p2m_leaf(const TreeParams& P, const double* u_s, double2* mu, const int* leaf_list,
+                     int n_list, cudaStream_t s);
 void launch_m2m(const TreeParams& P, int level, double2* mu, const double* binom,
                 cudaStream_t s);
+// Levels [l_lo, l_hi] (<= 0: all); block_list restricts one level's blocks.
 void launch_transform(const TreeParams& P, const double2* mu, double2* coef,
-                      const TransformTable& T, cudaStream_t s);
+                      const TransformTable& T, cudaStream_t s, int l_lo = 0, int l_hi = 0,
+                      const int* block_list = nullptr, int n_list = 0);
+void launch_gather_rows(const double* src, const int* idx, int n, int width, double* dst,
+                        cudaStream_t s);
+void launch_scatter_rows(const double* src, const int* idx, int n, int width, double* dst,
+                         cudaStream_t s);
 // Far work items are grouped by points-per-lane R = ceil(count/32):
 // group R occupies [group_off[R-1], group_off[R]) of `items`.  Launches the
 // items with index in [begin, end).

@@ -98,6 +98,7 @@ void DeviceOperator::release() {
   blas_ = nullptr;
   dfree(d_mu_); dfree(d_coef_); dfree(d_u_); dfree(d_us_); dfree(d_far_); dfree(d_b_);
   dfree(d_part_);
+  dfree(d_need_par_); dfree(d_local_leaves_); dfree(d_pack_a_); dfree(d_pack_c_); dfree(d_own_lvl_);
   if (stream_) cudaStreamDestroy(stream_);
   stream_ = nullptr;
 }
@@ -301,6 +302,7 @@ void DeviceOperator::restrict_targets(int p_lo, int p_hi) {
     throw std::invalid_argument("restrict_targets: bad sorted-position range");
   cuda_check(cudaStreamSynchronize(stream_), "restrict");
   build_items(p_lo, p_hi);
+  setup_sharded_moments(p_lo, p_hi);
 }
 
 // World+1 sorted-position bounds, cut at level-(L-1) block boundaries, with
@@ -324,7 +326,7 @@ std::vector<int> shard_bounds(const std::vector<int>& ls, int L, int world) {
 }
 
 void DeviceOperator::moments(const double* d_us, cudaStream_t s) {
-  imqk::launch_p2m_leaf(P_, d_us, d_mu_, s);
+  imqk::launch_p2m_leaf(P_, d_us, d_mu_, nullptr, 0, s);
   if (d_m2m_) {
     cublasSetStream(blas_, s);
     const size_t msz = (size_t)8 * Ke_ * 2 * Ke_;
@@ -343,6 +345,120 @@ void DeviceOperator::moments(const double* d_us, cudaStream_t s) {
     for (int l = L_ - 1; l >= 1; --l) imqk::launch_m2m(P_, l, d_mu_, d_binom_, s);
   }
   imqk::launch_transform(P_, d_mu_, d_coef_, T_, s);
+}
+
+// ---------------------------------------------------------------------------
+// Sharded moments (one rank of a multi-GPU application).  The rank owns the
+// level-(L-1) blocks [par_lo, par_hi) (its targets).  Its far field needs, at
+// levels L-1 and L, only blocks inside the children of the 3x3 neighbourhoods
+// of its blocks' parents ("local" = own + halo), which it forms itself from
+// its copy of u; at levels <= L-2 it contributes the moments of its OWN points
+// (M2M of its own level-(L-1) blocks) and the caller sums those coarse levels
+// over ranks (one all-reduce of mu[levels 1..L-2]) before moments_finish().
+// ---------------------------------------------------------------------------
+bool DeviceOperator::sharded() const { return !need_par_h_.empty(); }
+
+void DeviceOperator::setup_sharded_moments(int p_lo, int p_hi) {
+  dfree(d_need_par_); dfree(d_local_leaves_); dfree(d_pack_a_); dfree(d_pack_c_); dfree(d_own_lvl_);
+  need_par_h_.clear();
+  local_leaves_h_.clear();
+  if ((p_lo == 0 && p_hi == N_) || L_ < 3 || !d_m2m_) return;
+  const std::vector<int>& ls = leaf_start_h_;
+  const int G = 1 << L_;  // level L-1 grid
+  const long long npar = (long long)G * G;
+  par_lo_ = (int)npar;
+  par_hi_ = 0;
+  for (long long p = 0; p < npar; ++p)
+    if (ls[(size_t)(4 * p)] >= p_lo && ls[(size_t)(4 * p + 4)] <= p_hi && ls[(size_t)(4 * p)] < p_hi) {
+      par_lo_ = std::min<long long>(par_lo_, p);
+      par_hi_ = std::max<long long>(par_hi_, p + 1);
+    }
+  if (par_hi_ <= par_lo_) {
+    par_lo_ = par_hi_ = 0;
+  }
+  std::vector<char> need((size_t)npar, 0);
+  for (int p = par_lo_; p < par_hi_; ++p) {
+    int pi, pj;
+    imqdev::demorton((uint32_t)p, pi, pj);
+    const int gi = pi >> 1, gj = pj >> 1;  // grandparent block (level L-2)
+    for (int a = std::max(0, 2 * gi - 2); a <= std::min(G - 1, 2 * gi + 3); ++a)
+      for (int b = std::max(0, 2 * gj - 2); b <= std::min(G - 1, 2 * gj + 3); ++b)
+        need[imqdev::morton((uint32_t)a, (uint32_t)b)] = 1;
+  }
+  for (long long p = 0; p < npar; ++p) {
+    if (!need[(size_t)p] || ls[(size_t)(4 * p)] == ls[(size_t)(4 * p + 4)]) continue;
+    need_par_h_.push_back((int)p);
+    for (int c = 0; c < 4; ++c)
+      if (ls[(size_t)(4 * p + c)] < ls[(size_t)(4 * p + c + 1)]) local_leaves_h_.push_back((int)(4 * p + c));
+  }
+  if (need_par_h_.empty()) need_par_h_.push_back(0);  // keeps "sharded" set; zero-work lists
+  d_need_par_ = dalloc<int>(need_par_h_.size(), "need par");
+  d_local_leaves_ = dalloc<int>(std::max<size_t>(1, local_leaves_h_.size()), "local leaves");
+  cuda_check(cudaMemcpy(d_need_par_, need_par_h_.data(), need_par_h_.size() * sizeof(int),
+                        cudaMemcpyHostToDevice), "H2D need par");
+  if (!local_leaves_h_.empty())
+    cuda_check(cudaMemcpy(d_local_leaves_, local_leaves_h_.data(),
+                          local_leaves_h_.size() * sizeof(int), cudaMemcpyHostToDevice),
+               "H2D local leaves");
+  d_pack_a_ = dalloc<double>(need_par_h_.size() * (size_t)8 * Ke_, "m2m pack A");
+  d_pack_c_ = dalloc<double>(need_par_h_.size() * (size_t)2 * Ke_, "m2m pack C");
+  d_own_lvl_ = dalloc<double2>((size_t)npar * Ke_, "own level moments");
+}
+
+void DeviceOperator::moments_local(const double* d_us, cudaStream_t s) {
+  if (!sharded()) {  // unsharded: the full moments, nothing to reduce
+    moments(d_us, s);
+    return;
+  }
+  const int G = 1 << L_;
+  const long long npar = (long long)G * G;
+  const int nneed = (int)need_par_h_.size();
+  imqk::launch_p2m_leaf(P_, d_us, d_mu_, d_local_leaves_, (int)local_leaves_h_.size(), s);
+  cublasSetStream(blas_, s);
+  const size_t msz = (size_t)8 * Ke_ * 2 * Ke_;
+  const double one = 1.0, zero = 0.0;
+  // level L-1 for own + halo blocks: packed DGEMM over the needed parents
+  imqk::launch_gather_rows(reinterpret_cast<const double*>(d_mu_ + P_.mu_off[L_]), d_need_par_,
+                           nneed, 8 * Ke_, d_pack_a_, s);
+  if (cublasDgemm(blas_, CUBLAS_OP_N, CUBLAS_OP_N, 2 * Ke_, nneed, 8 * Ke_, &one,
+                  d_m2m_ + msz * (size_t)(L_ - 2), 2 * Ke_, d_pack_a_, 8 * Ke_, &zero,
+                  d_pack_c_, 2 * Ke_) != CUBLAS_STATUS_SUCCESS)
+    throw cuda_error("cublasDgemm (M2M, level L-1) failed");
+  imqk::launch_scatter_rows(d_pack_c_, d_need_par_, nneed, 2 * Ke_,
+                            reinterpret_cast<double*>(d_mu_ + P_.mu_off[L_ - 1]), s);
+  // own-only level L-1 -> coarse levels (partial sums, reduced by the caller)
+  cuda_check(cudaMemsetAsync(d_own_lvl_, 0, (size_t)npar * Ke_ * sizeof(double2), s), "memset");
+  if (par_hi_ > par_lo_)
+    cuda_check(cudaMemcpyAsync(d_own_lvl_ + (size_t)par_lo_ * Ke_,
+                               d_mu_ + P_.mu_off[L_ - 1] + (size_t)par_lo_ * Ke_,
+                               (size_t)(par_hi_ - par_lo_) * Ke_ * sizeof(double2),
+                               cudaMemcpyDeviceToDevice, s),
+               "own level copy");
+  for (int l = L_ - 2; l >= 1; --l) {
+    const int parents = 1 << (2 * (l + 1));
+    const double* A = l == L_ - 2 ? reinterpret_cast<const double*>(d_own_lvl_)
+                                  : reinterpret_cast<const double*>(d_mu_ + P_.mu_off[l + 1]);
+    if (cublasDgemm(blas_, CUBLAS_OP_N, CUBLAS_OP_N, 2 * Ke_, parents, 8 * Ke_, &one,
+                    d_m2m_ + msz * (size_t)(l - 1), 2 * Ke_, A, 8 * Ke_, &zero,
+                    reinterpret_cast<double*>(d_mu_ + P_.mu_off[l]), 2 * Ke_) !=
+        CUBLAS_STATUS_SUCCESS)
+      throw cuda_error("cublasDgemm (M2M, coarse) failed");
+  }
+}
+
+void DeviceOperator::coarse_moments(double2** ptr, size_t* count) const {
+  *ptr = d_mu_ + P_.mu_off[1];
+  *count = sharded() ? (size_t)(P_.mu_off[L_ - 1] - P_.mu_off[1]) : 0;
+}
+
+void DeviceOperator::moments_finish(cudaStream_t s) {
+  if (!sharded()) return;  // moments_local already transformed everything
+  imqk::launch_transform(P_, d_mu_, d_coef_, T_, s, 1, L_ - 2);
+  imqk::launch_transform(P_, d_mu_, d_coef_, T_, s, L_ - 1, L_ - 1, d_need_par_,
+                         (int)need_par_h_.size());
+  if (!local_leaves_h_.empty())
+    imqk::launch_transform(P_, d_mu_, d_coef_, T_, s, L_, L_, d_local_leaves_,
+                           (int)local_leaves_h_.size());
 }
 
 void DeviceOperator::far_near(const double* d_us, double* d_out, const int* perm,

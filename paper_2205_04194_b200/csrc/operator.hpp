@@ -74,9 +74,16 @@ class DeviceOperator {
 
   // Stage-by-stage access (multi-GPU sharding drives these individually).
   void moments(const double* d_us, cudaStream_t s);  // P2M + M2M + transform
+  // Sharded ranks: own + halo moments and own-only coarse partials; the caller
+  // all-reduces coarse_moments() over ranks, then calls moments_finish().
+  void moments_local(const double* d_us, cudaStream_t s);
+  void coarse_moments(double2** ptr, size_t* count) const;
+  void moments_finish(cudaStream_t s);
+  bool sharded() const;
   void far_near(const double* d_us, double* d_out, const int* perm, cudaStream_t s,
                 int far_begin, int far_end, int near_begin, int near_end);
   double2* coef_ptr() const { return d_coef_; }
+  const int* perm_ptr() const { return d_perm_; }
   size_t coef_count() const { return coef_count_; }
   const imqk::TreeParams& params() const { return P_; }
   cudaStream_t stream() const { return stream_; }
@@ -86,6 +93,7 @@ class DeviceOperator {
  private:
   void build(const double* xy_host);
   void build_items(int p_lo, int p_hi);
+  void setup_sharded_moments(int p_lo, int p_hi);
   void release();
   void apply_sorted_locked(const double* d_us, double* d_bs, const int* perm,
                            cudaStream_t s);
@@ -126,6 +134,13 @@ class DeviceOperator {
   double* d_part_ = nullptr;  // [3][N] near-field row partials (small problems)
   int near_split_ = 1;
   std::vector<int> leaf_start_h_;
+  std::vector<int> need_par_h_, local_leaves_h_;  // sharded moments (own + halo)
+  int par_lo_ = 0, par_hi_ = 0;
+  int* d_need_par_ = nullptr;
+  int* d_local_leaves_ = nullptr;
+  double* d_pack_a_ = nullptr;
+  double* d_pack_c_ = nullptr;
+  double2* d_own_lvl_ = nullptr;
   int target_lo_ = 0, target_hi_ = 0;
   bool have_counts_ = false;
   PairCounts counts_{};

@@ -2,11 +2,18 @@
 
 Targets are sharded by contiguous Morton ranges cut at level-(L-1) block
 boundaries (imq_ext_shard_bounds); every rank holds the full sorted point set
-(setup is sub-second) and the full source vector, forms the moments, and
-evaluates the far + near field of its own targets only
-(imq_ext_operator_restrict).  The data path needs no collective; gather_b()
-assembles the full product when a caller wants it (all_gather over NCCL on
-GPUs, gloo on CPU in the tests).
+(setup is sub-second) and the full source vector.  After
+imq_ext_operator_restrict a rank
+
+  * forms the fine-level (L-1, L) moments of its own blocks and of the halo its
+    far field reads (children of the 3x3 neighbourhoods of its blocks'
+    parents) locally -- no exchange of fine moments or halo points;
+  * forms the coarse-level (1..L-2) moments of its OWN points only; one
+    all-reduce (sum) over NVLink of that coarse region (28 MB at config 4)
+    makes them global;
+  * evaluates the far + near field of its own targets.
+
+gather_b() assembles the full product when a caller wants it.
 """
 from __future__ import annotations
 
@@ -35,20 +42,47 @@ def leaf_start_from_keys(leaf_keys_sorted, levels: int) -> np.ndarray:
                            side="left").astype(np.int32)
 
 
+class _DeviceView:
+    """__cuda_array_interface__ view of library-owned device memory (float64)."""
+
+    def __init__(self, ptr: int, n: int):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f8", "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
 class ShardedOperator:
-    """FastOperator whose far/near evaluation covers this rank's targets."""
+    """FastOperator whose moments and far/near evaluation cover this rank."""
 
     def __init__(self, op, rank: int, world: int):
+        import torch
         self.op = op
         self.rank, self.world = rank, world
         self.bounds = shard_bounds(op.leaf_start(), op.levels, world)
         self.lo, self.hi = int(self.bounds[rank]), int(self.bounds[rank + 1])
         check(lib().imq_ext_operator_restrict(op.handle, self.lo, self.hi))
         self.perm = op.permutation()
+        self.n_far, self.n_near = len(op.items("far")), len(op.items("near"))
+        self.d_us = torch.empty(op.size, dtype=torch.float64, device="cuda")
+        ptr, n = op.coarse_moments()
+        self.coarse = torch.as_tensor(_DeviceView(ptr, n), device="cuda") if n else None
 
-    def apply_device(self, d_u, d_b, stream=None):
+    def moments(self, d_u, stream=None, group=None, reduce=True):
+        """Gather u, local + coarse-partial moments, coarse all-reduce, transform."""
+        import torch.distributed as dist
+        self.op.gather(d_u, self.d_us, stream)
+        self.op.moments_local(self.d_us, stream)
+        if reduce and self.coarse is not None and self.world > 1:
+            dist.all_reduce(self.coarse, group=group)
+        if reduce:
+            self.op.moments_finish(stream)
+
+    def evaluate(self, d_b, stream=None):
         """b[perm[p]] for p in [lo, hi) (original order); other entries untouched."""
-        self.op.apply_device(d_u, d_b, stream)
+        self.op.far_near(self.d_us, d_b, (0, self.n_far), (0, self.n_near), stream, scatter=True)
+
+    def apply_device(self, d_u, d_b, stream=None, group=None):
+        self.moments(d_u, stream, group)
+        self.evaluate(d_b, stream)
 
     def owned_original_indices(self) -> np.ndarray:
         return self.perm[self.lo:self.hi]

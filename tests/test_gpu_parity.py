@@ -242,3 +242,37 @@ def test_operator_errors(imq):
     assert op.size == 10 and op.levels == imq.auto_level(10, 4)
     with pytest.raises(imq.IMQError):
         op.apply(np.ones(9))
+
+
+@pytest.mark.parametrize("world", [2, 3, 5])
+def test_sharded_application_emulated(imq, world):
+    """The multi-GPU algorithm on one GPU: `world` restricted operators (own +
+    halo moments, own-only coarse partials), the coarse all-reduce done by a
+    sum, then each rank's far/near field; the union must equal the unsharded
+    product.  (NCCL itself is exercised by bench.py under torchrun.)"""
+    torch = pytest.importorskip("torch")
+    from paper_2205_04194_b200 import inputs
+    from paper_2205_04194_b200.parallel import ShardedOperator
+    n, t, m, L = 1 << 18, 0.01, 12, 5
+    for xy in (inputs.uniform_points(n, 3), inputs.gaussian_mixture(n, 1)):
+        u = torch.tensor(inputs.random_vector(n, 7), device="cuda")
+        full = imq.FastOperator(xy, t, m, L)
+        b_ref = torch.empty_like(u)
+        full.apply_device(u, b_ref)
+        torch.cuda.synchronize()
+        ranks = [ShardedOperator(imq.FastOperator(xy, t, m, L), r, world) for r in range(world)]
+        for sh in ranks:
+            sh.moments(u, reduce=False)
+        torch.cuda.synchronize()
+        total = sum(sh.coarse.clone() for sh in ranks)   # the all-reduce
+        b = torch.full_like(u, float("nan"))
+        for sh in ranks:
+            sh.coarse.copy_(total)
+            sh.op.moments_finish()
+            sh.evaluate(b)
+        torch.cuda.synchronize()
+        assert not torch.isnan(b).any()
+        err = float((b - b_ref).abs().max() / b_ref.abs().max())
+        assert err <= 1e-13, err
+        owned = np.concatenate([sh.owned_original_indices() for sh in ranks])
+        assert np.array_equal(np.sort(owned), np.arange(n))
