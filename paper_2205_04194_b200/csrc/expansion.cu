@@ -829,8 +829,11 @@ void launch_scatter_rows(const double* src, const int* idx, int n, int width, do
 }
 
 void launch_m2p_far(const TreeParams& P, const int4* items, const int* group_off, int begin,
-                    int end, const double2* coef, double* far_s, cudaStream_t s) {
+                    int end, const double2* coef, double* far_s, const cudaStream_t* streams,
+                    int nstreams) {
   if (end <= begin) return;
+  cudaStream_t s = streams[0];
+  int launched = 0;
   if (!m2p_specialised(P.M)) {
     constexpr int W = 4;
     const int n = end - begin;
@@ -844,7 +847,8 @@ void launch_m2p_far(const TreeParams& P, const int4* items, const int* group_off
     switch (P.M) {
 #define X(m)                                                   \
   case m:                                                      \
-    run_far<m>(P, R, items + lo, hi - lo, coef, far_s, s);     \
+    run_far<m>(P, R, items + lo, hi - lo, coef, far_s,          \
+               streams[launched++ % nstreams]);               \
     break;
       IMQ_FOR_SPECIALISED_M(X)
 #undef X

@@ -76,9 +76,12 @@ void launch_scatter_rows(const double* src, const int* idx, int n, int width, do
                          cudaStream_t s);
 // Far work items are grouped by points-per-lane R = ceil(count/32):
 // group R occupies [group_off[R-1], group_off[R]) of `items`.  Launches the
-// items with index in [begin, end).
+// items with index in [begin, end).  Group launches are spread round-robin
+// over `streams` (streams[0] first, largest R first) so that small groups run
+// in the tail of the large ones; the caller forks/joins the streams.
 void launch_m2p_far(const TreeParams& P, const int4* items, const int* group_off, int begin,
-                    int end, const double2* coef, double* far_s, cudaStream_t s);
+                    int end, const double2* coef, double* far_s, const cudaStream_t* streams,
+                    int nstreams);
 bool m2p_specialised(int M);
 int far_max_points_per_lane();
 

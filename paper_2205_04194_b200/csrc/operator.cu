@@ -77,6 +77,11 @@ DeviceOperator::DeviceOperator(const double* xy_host, size_t n, double t, int M,
   M_ = M;
   t_ = t;
   cuda_check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "stream create");
+  for (int k = 0; k < kAuxStreams; ++k) {
+    cuda_check(cudaStreamCreateWithFlags(&aux_[k], cudaStreamNonBlocking), "stream create");
+    cuda_check(cudaEventCreateWithFlags(&ev_join_[k], cudaEventDisableTiming), "event create");
+  }
+  cuda_check(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming), "event create");
   pending_levels_ = levels;
   try {
     build(xy_host);
@@ -101,6 +106,14 @@ void DeviceOperator::release() {
   dfree(d_need_par_); dfree(d_local_leaves_); dfree(d_pack_a_); dfree(d_pack_c_); dfree(d_own_lvl_);
   if (stream_) cudaStreamDestroy(stream_);
   stream_ = nullptr;
+  for (int k = 0; k < kAuxStreams; ++k) {
+    if (aux_[k]) cudaStreamDestroy(aux_[k]);
+    if (ev_join_[k]) cudaEventDestroy(ev_join_[k]);
+    aux_[k] = nullptr;
+    ev_join_[k] = nullptr;
+  }
+  if (ev_fork_) cudaEventDestroy(ev_fork_);
+  ev_fork_ = nullptr;
 }
 
 void DeviceOperator::build(const double* xy_host) {
@@ -468,9 +481,21 @@ void DeviceOperator::far_near(const double* d_us, double* d_out, const int* perm
   far_end = std::min(far_end, n_far_);
   near_begin = std::max(0, near_begin);
   near_end = std::min(near_end, n_near_);
-  if (far_end > far_begin)
+  if (far_end > far_begin) {
+    // fork: group launches on s + the aux streams, joined back into s
+    cudaStream_t ss[1 + kAuxStreams] = {s};
+    cuda_check(cudaEventRecord(ev_fork_, s), "fork");
+    for (int k = 0; k < kAuxStreams; ++k) {
+      ss[k + 1] = aux_[k];
+      cuda_check(cudaStreamWaitEvent(aux_[k], ev_fork_, 0), "fork wait");
+    }
     imqk::launch_m2p_far(P_, d_far_items_, far_group_off_.data(), far_begin, far_end, d_coef_,
-                         d_far_, s);
+                         d_far_, ss, 1 + kAuxStreams);
+    for (int k = 0; k < kAuxStreams; ++k) {
+      cuda_check(cudaEventRecord(ev_join_[k], aux_[k]), "join");
+      cuda_check(cudaStreamWaitEvent(s, ev_join_[k], 0), "join wait");
+    }
+  }
   if (near_end > near_begin)
     imqk::launch_p2p_near(P_, d_near_items_, near_group_off_.data(), near_begin, near_end, d_us,
                           d_far_, d_out, perm, d_part_, s);

@@ -100,6 +100,10 @@ class DeviceOperator {
 
   int device_ = 0;
   cudaStream_t stream_ = nullptr;
+  static constexpr int kAuxStreams = 3;  // far-field work groups run concurrently
+  cudaStream_t aux_[kAuxStreams] = {};
+  cudaEvent_t ev_fork_ = nullptr;
+  cudaEvent_t ev_join_[kAuxStreams] = {};
   int N_ = 0, M_ = 0, K_ = 0, Ke_ = 0, L_ = 0, pending_levels_ = 0;
   double t_ = 0.0;
   double sq_[3] = {0, 0, 0};
