@@ -107,7 +107,10 @@ __global__ void __launch_bounds__(256) k_near_combine(int lo, int hi, int N,
 }
 
 constexpr int kDirThreads = 256;
+constexpr int kDirR = 4;  // targets per thread (register blocking)
 
+// b_q = sum_j c_j / sqrt(t^2 + |x_q - y_j|^2): each thread owns kDirR targets
+// and sums its rows in ascending j over source tiles staged in shared memory.
 __global__ void __launch_bounds__(kDirThreads) k_direct(const double* __restrict__ txy,
                                                         long long nt,
                                                         const double* __restrict__ sxy,
@@ -116,14 +119,17 @@ __global__ void __launch_bounds__(kDirThreads) k_direct(const double* __restrict
                                                         double* __restrict__ out) {
   __shared__ double2 sp[kDirThreads];
   __shared__ double sv[kDirThreads];
-  const long long i = (long long)blockIdx.x * kDirThreads + threadIdx.x;
-  double xi = 0.0, yi = 0.0;
-  if (i < nt) {
-    const double2 v = reinterpret_cast<const double2*>(txy)[i];
-    xi = v.x;
-    yi = v.y;
+  const long long i0 = (long long)blockIdx.x * kDirThreads * kDirR + threadIdx.x;
+  double xi[kDirR], yi[kDirR], acc[kDirR];
+#pragma unroll
+  for (int r = 0; r < kDirR; ++r) {
+    const long long i = i0 + (long long)r * kDirThreads;
+    double2 v = make_double2(0.0, 0.0);
+    if (i < nt) v = reinterpret_cast<const double2*>(txy)[i];
+    xi[r] = v.x;
+    yi[r] = v.y;
+    acc[r] = 0.0;
   }
-  double acc = 0.0;
   for (long long base = 0; base < ns; base += kDirThreads) {
     const long long j = base + threadIdx.x;
     __syncthreads();
@@ -133,20 +139,22 @@ __global__ void __launch_bounds__(kDirThreads) k_direct(const double* __restrict
     }
     __syncthreads();
     const int nsrc = (int)min((long long)kDirThreads, ns - base);
-    if (nsrc == kDirThreads) {
-#pragma unroll 8
-      for (int k = 0; k < kDirThreads; ++k) {
-        const double dx = xi - sp[k].x, dy = yi - sp[k].y;
-        acc = fma(sv[k], rsqrt_pos(fma(dx, dx, fma(dy, dy, t2))), acc);
-      }
-    } else {
-      for (int k = 0; k < nsrc; ++k) {
-        const double dx = xi - sp[k].x, dy = yi - sp[k].y;
-        acc = fma(sv[k], rsqrt_pos(fma(dx, dx, fma(dy, dy, t2))), acc);
+#pragma unroll 4
+    for (int k = 0; k < nsrc; ++k) {
+      const double2 p = sp[k];
+      const double c = sv[k];
+#pragma unroll
+      for (int r = 0; r < kDirR; ++r) {
+        const double dx = xi[r] - p.x, dy = yi[r] - p.y;
+        acc[r] = fma(c, rsqrt_pos(fma(dx, dx, fma(dy, dy, t2))), acc[r]);
       }
     }
   }
-  if (i < nt) out[i] = acc;
+#pragma unroll
+  for (int r = 0; r < kDirR; ++r) {
+    const long long i = i0 + (long long)r * kDirThreads;
+    if (i < nt) out[i] = acc[r];
+  }
 }
 
 }  // namespace
@@ -179,8 +187,9 @@ void launch_p2p_near(const TreeParams& P, const int4* items, const int* group_of
 void launch_direct(const double* txy, long long nt, const double* sxy, const double* sval,
                    long long ns, double t2, double* out, cudaStream_t s) {
   if (nt == 0) return;
-  k_direct<<<(unsigned)((nt + kDirThreads - 1) / kDirThreads), kDirThreads, 0, s>>>(
-      txy, nt, sxy, sval, ns, t2, out);
+  const long long per = (long long)kDirThreads * kDirR;
+  k_direct<<<(unsigned)((nt + per - 1) / per), kDirThreads, 0, s>>>(txy, nt, sxy, sval, ns, t2,
+                                                                    out);
 }
 
 }  // namespace imqk
