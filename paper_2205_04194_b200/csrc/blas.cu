@@ -3,7 +3,11 @@
 // combine order, so every dot product is bitwise reproducible run to run.
 // Scalars produced on the device (MGS coefficients h_ij) are consumed on the
 // device, so the modified Gram-Schmidt chain needs no host round trip.
+#include <cooperative_groups.h>
+
 #include "imq_kernels.hpp"
+
+namespace cg = cooperative_groups;
 
 namespace imqk {
 
@@ -99,6 +103,65 @@ __global__ void __launch_bounds__(256) k_dfma_peak(int iters, double a, double* 
   if (s == 12345.678) out[0] = s;  // keeps the chains live
 }
 
+// One Arnoldi step's modified Gram-Schmidt in a single cooperative launch:
+// for i = 0..j: h_i = <w, V_i> (fixed-order grid reduction, every CTA forms
+// the same total), w -= h_i V_i; then h_{j+1} = ||w||.  Each thread owns a
+// fixed slice of w, so only the reductions need the grid barrier (one per
+// projection, partials double-buffered).  Also flags non-finite w.
+constexpr int kMgsThreads = 256;
+__global__ void __launch_bounds__(kMgsThreads) k_mgs(const double* __restrict__ V, double* w,
+                                                     long long n, long long ld, int j,
+                                                     double* __restrict__ partial,
+                                                     double* __restrict__ h, int* flag) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double red[kMgsThreads / 32];
+  __shared__ double total_sh;
+  const long long stride = (long long)gridDim.x * kMgsThreads;
+  const long long t0 = blockIdx.x * (long long)kMgsThreads + threadIdx.x;
+  auto block_sum = [&](double v) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    double t = 0.0;
+    if (threadIdx.x == 0)
+      for (int k = 0; k < kMgsThreads / 32; ++k) t += red[k];
+    __syncthreads();
+    return t;  // valid in thread 0
+  };
+  auto grid_total = [&](int buf) {
+    // every CTA sums the partials in the same order -> identical totals
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      const double* pp = partial + (size_t)buf * gridDim.x;
+      for (unsigned b = 0; b < gridDim.x; ++b) t += pp[b];
+      total_sh = t;
+    }
+    __syncthreads();
+    return total_sh;
+  };
+  bool bad = false;
+  for (long long k = t0; k < n; k += stride) bad |= !isfinite(w[k]);
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+  for (int i = 0; i <= j + 1; ++i) {
+    const double* Vi = V + (size_t)i * ld;
+    double acc = 0.0;
+    if (i <= j)
+      for (long long k = t0; k < n; k += stride) acc = fma(w[k], Vi[k], acc);
+    else
+      for (long long k = t0; k < n; k += stride) acc = fma(w[k], w[k], acc);
+    const double bs = block_sum(acc);
+    if (threadIdx.x == 0) partial[(size_t)(i & 1) * gridDim.x + blockIdx.x] = bs;
+    grid.sync();
+    const double hi = grid_total(i & 1);
+    if (i <= j) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) h[i] = hi;
+      for (long long k = t0; k < n; k += stride) w[k] = fma(-hi, Vi[k], w[k]);
+    } else if (blockIdx.x == 0 && threadIdx.x == 0) {
+      h[j + 1] = sqrt(hi);
+    }
+  }
+}
+
 inline unsigned grid_for(long long n) {
   long long b = (n + kThreads * 4 - 1) / (kThreads * 4);
   return (unsigned)(b < 1 ? 1 : (b > 1184 ? 1184 : b));
@@ -131,6 +194,27 @@ double measure_dfma_peak(int iters, float* ms_out) {
   if (ms_out) *ms_out = ms;
   const double flops = (double)grid * 256 * iters * 16 * 8 * 2;
   return flops / (ms * 1e-3) / 1e12;
+}
+
+int mgs_grid(long long n) {
+  static int max_blocks = 0;
+  if (!max_blocks) {
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mgs, kMgsThreads, 0);
+    max_blocks = sms * (per_sm > 2 ? 2 : per_sm);
+  }
+  const long long want = (n + kMgsThreads * 4 - 1) / (kMgsThreads * 4);
+  return (int)(want < 1 ? 1 : (want > max_blocks ? max_blocks : want));
+}
+
+cudaError_t launch_mgs(const double* V, double* w, long long n, long long ld, int j,
+                       double* partial, int nparts, double* h, int* flag, cudaStream_t s) {
+  void* args[] = {(void*)&V, (void*)&w, (void*)&n, (void*)&ld, (void*)&j,
+                  (void*)&partial, (void*)&h, (void*)&flag};
+  return cudaLaunchCooperativeKernel((const void*)k_mgs, dim3(nparts), dim3(kMgsThreads), args, 0,
+                                     s);
 }
 
 void launch_dot(const double* a, const double* b, long long n, double* partial, int nparts,

@@ -23,10 +23,12 @@ constexpr int kNearMaxR = 4;  // a near work item holds <= 32 * kNearMaxR target
 // Warp per near work item: <= 32 R targets of one leaf, R per lane.  Every
 // source point staged in the warp's shared-memory tile is read back once per
 // lane and reused for its R targets (register blocking against the per-LDS
-// issue cost).  item.w = 3: all three neighbour rows, the
-// epilogue adds the far field and scatters; item.w = r in {0,1,2}: only source
-// row li-1+r, partial sums to part[r][.] (small problems split the sources
-// three ways for parallelism; k_near_combine adds them in a fixed order).
+// issue cost).  item.w encodes the source subset:
+//   15       all 3x3 neighbour leaves; the epilogue adds the far field, scatters;
+//   16 + r   neighbour row li-1+r   -> partial sums part[r][.]      (3-way split)
+//   32 + k   neighbour leaf k of 9  -> partial sums part[k][.]      (9-way split)
+// Small problems split the sources for parallelism; k_near_combine adds the
+// partials in a fixed order (deterministic).
 template <int R>
 __global__ void __launch_bounds__(kNearWarps * 32) k_p2p_near(
     const TreeParams P, const int4* __restrict__ items, int n_items,
@@ -39,7 +41,7 @@ __global__ void __launch_bounds__(kNearWarps * 32) k_p2p_near(
   if (it >= n_items) return;
   const int4 item = items[it];
   const uint32_t leaf = (uint32_t)item.x;
-  const int s0 = item.y, cnt = item.z, srow = item.w;
+  const int s0 = item.y, cnt = item.z, sel = item.w;
   double xi[R], yi[R], acc[R];
 #pragma unroll
   for (int p = 0; p < R; ++p) {
@@ -52,32 +54,63 @@ __global__ void __launch_bounds__(kNearWarps * 32) k_p2p_near(
   const int g = 1 << (P.L + 1);
   int li, lj;
   demorton(leaf, li, lj);
-  const int qlo = srow == 3 ? max(0, li - 1) : li - 1 + srow;
-  const int qhi = srow == 3 ? min(g - 1, li + 1) : li - 1 + srow;
-  for (int qi = qlo; qi <= qhi; ++qi) {
-    if (qi < 0 || qi > g - 1) continue;
-    for (int qj = max(0, lj - 1); qj <= min(g - 1, lj + 1); ++qj) {
-      const uint32_t q = morton(qi, qj);
-      const int a = P.leaf_start[q], b = P.leaf_start[q + 1];
-      for (int base = a; base < b; base += 32) {
-        const int j = base + lane;
-        __syncwarp();
-        if (j < b) {
-          sxy[warp][lane] = make_double2(P.xs[j], P.ys[j]);
-          su[warp][lane] = u_s[j];
-        }
-        __syncwarp();
-        const int nsrc = min(32, b - base);
-#pragma unroll 4
-        for (int k = 0; k < nsrc; ++k) {
-          const double2 sp = sxy[warp][k];
-          const double uk = su[warp][k];
+  int qilo = li - 1, qihi = li + 1, qjlo = lj - 1, qjhi = lj + 1, slot = 0;
+  if (sel >= 32) {
+    slot = sel - 32;
+    qilo = qihi = li - 1 + slot / 3;
+    qjlo = qjhi = lj - 1 + slot % 3;
+  } else if (sel >= 16) {
+    slot = sel - 16;
+    qilo = qihi = li - 1 + slot;
+  }
+  // the (<= 9) source leaves as one virtual range, streamed in tiles of 32
+  int rs[9], rc[9], total = 0;
 #pragma unroll
-          for (int p = 0; p < R; ++p) {
-            const double dx = xi[p] - sp.x, dy = yi[p] - sp.y;
-            acc[p] = fma(uk, rsqrt_pos(fma(dx, dx, fma(dy, dy, t2))), acc[p]);
-          }
-        }
+  for (int k = 0; k < 9; ++k) {  // static indexing keeps the ranges in registers
+    const int qi = li - 1 + k / 3, qj = lj - 1 + k % 3;
+    rs[k] = rc[k] = 0;
+    if (qi >= max(0, qilo) && qi <= min(g - 1, qihi) && qj >= max(0, qjlo) &&
+        qj <= min(g - 1, qjhi)) {
+      const uint32_t q = morton(qi, qj);
+      rs[k] = P.leaf_start[q];
+      rc[k] = P.leaf_start[q + 1] - rs[k];
+      total += rc[k];
+    }
+  }
+  auto fetch = [&](int v, double& x, double& y, double& u) {
+    // virtual index -> sorted position; padding slots carry u = 0
+    int pos = -1;
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+      if (pos < 0 && v < rc[k]) pos = rs[k] + v;
+      if (pos < 0) v -= rc[k];
+    }
+    if (pos < 0) {
+      x = xi[0];
+      y = yi[0];
+      u = 0.0;
+    } else {
+      x = P.xs[pos];
+      y = P.ys[pos];
+      u = u_s[pos];
+    }
+  };
+  double nx, ny, nu;
+  fetch(lane, nx, ny, nu);
+  for (int v = 0; v < total; v += 32) {
+    __syncwarp();
+    sxy[warp][lane] = make_double2(nx, ny);
+    su[warp][lane] = nu;
+    __syncwarp();
+    if (v + 32 < total) fetch(v + 32 + lane, nx, ny, nu);  // in flight during the tile
+#pragma unroll 8
+    for (int k = 0; k < 32; ++k) {
+      const double2 sp = sxy[warp][k];
+      const double uk = su[warp][k];
+#pragma unroll
+      for (int p = 0; p < R; ++p) {
+        const double dx = xi[p] - sp.x, dy = yi[p] - sp.y;
+        acc[p] = fma(uk, rsqrt_pos(fma(dx, dx, fma(dy, dy, t2))), acc[p]);
       }
     }
   }
@@ -85,25 +118,26 @@ __global__ void __launch_bounds__(kNearWarps * 32) k_p2p_near(
   for (int p = 0; p < R; ++p) {
     if (lane + 32 * p < cnt) {
       const int q = s0 + lane + 32 * p;
-      if (srow == 3) {
+      if (sel == 15) {
         const double v = far_s[q] + acc[p];
         out[perm ? perm[q] : q] = v;
       } else {
-        part[(size_t)srow * P.N + q] = acc[p];
+        part[(size_t)slot * P.N + q] = acc[p];
       }
     }
   }
 }
 
-__global__ void __launch_bounds__(256) k_near_combine(int lo, int hi, int N,
+__global__ void __launch_bounds__(256) k_near_combine(int lo, int hi, int N, int nparts,
                                                       const double* __restrict__ far_s,
                                                       const double* __restrict__ part,
                                                       double* __restrict__ out,
                                                       const int* __restrict__ perm) {
   const int q = lo + blockIdx.x * 256 + threadIdx.x;
   if (q >= hi) return;
-  const double v = far_s[q] + ((part[q] + part[(size_t)N + q]) + part[2 * (size_t)N + q]);
-  out[perm ? perm[q] : q] = v;
+  double nsum = 0.0;
+  for (int k = 0; k < nparts; ++k) nsum += part[(size_t)k * N + q];
+  out[perm ? perm[q] : q] = far_s[q] + nsum;
 }
 
 constexpr int kDirThreads = 256;
@@ -161,11 +195,11 @@ __global__ void __launch_bounds__(kDirThreads) k_direct(const double* __restrict
 
 int near_max_points_per_lane() { return kNearMaxR; }
 
-void launch_near_combine(int lo, int hi, int N, const double* far_s, const double* part,
-                         double* out, const int* perm, cudaStream_t s) {
+void launch_near_combine(int lo, int hi, int N, int nparts, const double* far_s,
+                         const double* part, double* out, const int* perm, cudaStream_t s) {
   if (hi <= lo) return;
-  k_near_combine<<<(unsigned)((hi - lo + 255) / 256), 256, 0, s>>>(lo, hi, N, far_s, part, out,
-                                                                   perm);
+  k_near_combine<<<(unsigned)((hi - lo + 255) / 256), 256, 0, s>>>(lo, hi, N, nparts, far_s,
+                                                                   part, out, perm);
 }
 
 void launch_p2p_near(const TreeParams& P, const int4* items, const int* group_off, int begin,

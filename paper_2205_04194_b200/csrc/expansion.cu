@@ -123,23 +123,27 @@ __global__ void __launch_bounds__(128) k_p2m_leaf(const TreeParams P, const doub
 // (m <= M).  e^g comes from binary powering of e (log2 G steps, whose last
 // base is e^G), e^{g+kG} from one complex product each.  After the pass the
 // 32/G groups are folded by shuffles in a fixed order (deterministic).
-template <int M, int G>
-__global__ void __launch_bounds__(128) k_p2m_leaf_g(const TreeParams P,
-                                                    const double* __restrict__ u_s,
-                                                    double2* __restrict__ mu,
-                                                    const int* __restrict__ leaf_list,
-                                                    int n_list) {
+template <int M, int G, int WPL>
+__global__ void __launch_bounds__(32 * (WPL > 4 ? WPL : 4)) k_p2m_leaf_g(
+    const TreeParams P, const double* __restrict__ u_s, double2* __restrict__ mu,
+    const int* __restrict__ leaf_list, int n_list) {
+  // WPL warps per leaf (large leaves split their points over several warps;
+  // the partial sums are combined through shared memory in a fixed order)
   constexpr int NI = M / 2 + 1;
   constexpr int NM = (M + G) / G;  // m values per lane
   constexpr int LOGG = G == 8 ? 3 : (G == 16 ? 4 : 5);
-  const int lane = threadIdx.x & 31;
+  constexpr int WARPS = WPL > 4 ? WPL : 4;
+  constexpr int LPC = WARPS / WPL;  // leaves per CTA
+  __shared__ double2 red[WPL > 1 ? WARPS : 1][G][NM][NI];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane % G, grp = lane / G;
-  const long long wid = (long long)blockIdx.x * 4 + (threadIdx.x >> 5);
+  const int sub = warp % WPL;
+  const long long wid = (long long)blockIdx.x * LPC + warp / WPL;
   const long long n_leaves = leaf_list ? n_list : 1ll << (2 * (P.L + 1));
-  if (wid >= n_leaves) return;
-  const long long leaf = leaf_list ? leaf_list[wid] : wid;
-  const int s = P.leaf_start[leaf], e = P.leaf_start[leaf + 1];
-  if (s == e) return;
+  const bool live = wid < n_leaves;
+  const long long leaf = live ? (leaf_list ? leaf_list[wid] : wid) : 0;
+  const int s = live ? P.leaf_start[leaf] : 0, e = live ? P.leaf_start[leaf + 1] : 0;
+  if (WPL == 1 && s == e) return;
   int li, lj;
   demorton((uint32_t)leaf, li, lj);
   const double zx = block_center(P.ox, li, P.cell[P.L]);
@@ -149,7 +153,7 @@ __global__ void __launch_bounds__(128) k_p2m_leaf_g(const TreeParams P,
   for (int k = 0; k < NM; ++k)
 #pragma unroll
     for (int i = 0; i < NI; ++i) ar[k][i] = ai[k][i] = 0.0;
-  for (int p = s + grp; p < e; p += 32 / G) {
+  for (int p = s + grp + sub * (32 / G); p < e; p += WPL * (32 / G)) {
     const double ex = P.xs[p] - zx, ey = P.ys[p] - zy;
     const double e2 = fma(ex, ex, ey * ey);
     double pr = u_s[p], pi = 0.0, br = ex, bi = ey;
@@ -193,6 +197,29 @@ __global__ void __launch_bounds__(128) k_p2m_leaf_g(const TreeParams P,
         ar[k][i] += __shfl_down_sync(0xffffffffu, ar[k][i], off);
         ai[k][i] += __shfl_down_sync(0xffffffffu, ai[k][i], off);
       }
+  if constexpr (WPL > 1) {  // combine the leaf's warps in a fixed order
+    if (grp == 0)
+#pragma unroll
+      for (int k = 0; k < NM; ++k)
+#pragma unroll
+        for (int i = 0; i < NI; ++i) red[warp][g][k][i] = make_double2(ar[k][i], ai[k][i]);
+    __syncthreads();
+    if (sub != 0 || !live || s == e) return;
+    if (grp == 0)
+#pragma unroll
+      for (int k = 0; k < NM; ++k)
+#pragma unroll
+        for (int i = 0; i < NI; ++i) {
+          double sr = 0.0, si = 0.0;
+          for (int w = 0; w < WPL; ++w) {
+            const double2 v = red[warp + w][g][k][i];
+            sr += v.x;
+            si += v.y;
+          }
+          ar[k][i] = sr;
+          ai[k][i] = si;
+        }
+  }
   if (grp == 0) {
     double2* out = mu + P.mu_off[P.L] + (size_t)leaf * P.Ke;
 #pragma unroll
@@ -729,14 +756,30 @@ void run_far(const TreeParams& P, int R, const int4* items, int n_items, const d
   }
 }
 
+template <int M, int WPL>
+void run_p2m_w(const TreeParams& P, const double* u_s, double2* mu, const int* list, int n_list,
+               cudaStream_t s) {
+  const long long n_leaves = list ? n_list : 1ll << (2 * (P.L + 1));
+  constexpr int WARPS = WPL > 4 ? WPL : 4;
+  constexpr int LPC = WARPS / WPL;
+  k_p2m_leaf_g<M, 8, WPL><<<(unsigned)((n_leaves + LPC - 1) / LPC), 32 * WARPS, 0, s>>>(
+      P, u_s, mu, list, n_list);
+}
+
 template <int M>
 void run_p2m(const TreeParams& P, const double* u_s, double2* mu, const int* list, int n_list,
              cudaStream_t s) {
   const long long n_leaves = list ? n_list : 1ll << (2 * (P.L + 1));
-  // 8 lanes per point (4 points per pass) for M < 24, else the 32-lane form
-  if constexpr (M < 24)
-    k_p2m_leaf_g<M, 8><<<(unsigned)((n_leaves + 3) / 4), 128, 0, s>>>(P, u_s, mu, list, n_list);
-  else
+  // 8 lanes per point (4 points per pass) for M < 24, else the 32-lane form;
+  // warps per leaf from the mean leaf occupancy (P.p2m_wpl)
+  if constexpr (M < 24) {
+    switch (P.p2m_wpl) {
+      case 1: return run_p2m_w<M, 1>(P, u_s, mu, list, n_list, s);
+      case 2: return run_p2m_w<M, 2>(P, u_s, mu, list, n_list, s);
+      case 4: return run_p2m_w<M, 4>(P, u_s, mu, list, n_list, s);
+      default: return run_p2m_w<M, 8>(P, u_s, mu, list, n_list, s);
+    }
+  } else
     k_p2m_leaf<M><<<(unsigned)((n_leaves + 3) / 4), 128, 0, s>>>(P, u_s, mu, list, n_list);
 }
 

@@ -32,6 +32,7 @@ struct TreeParams {
   const double* ys;
   const uint32_t* leaf;
   const int* leaf_start;
+  int p2m_wpl;  // warps per leaf in the leaf P2M (1, 2, 4, 8)
 };
 
 // Transform table mu -> C: for output slot o (Horner order),
@@ -90,8 +91,8 @@ int far_max_points_per_lane();
 void launch_p2p_near(const TreeParams& P, const int4* items, const int* group_off, int begin,
                      int end, const double* u_s, const double* far_s, double* out,
                      const int* perm, double* part, cudaStream_t s);
-void launch_near_combine(int lo, int hi, int N, const double* far_s, const double* part,
-                         double* out, const int* perm, cudaStream_t s);
+void launch_near_combine(int lo, int hi, int N, int nparts, const double* far_s,
+                         const double* part, double* out, const int* perm, cudaStream_t s);
 int near_max_points_per_lane();
 void launch_direct(const double* txy, long long nt, const double* sxy, const double* sval,
                    long long ns, double t2, double* out, cudaStream_t s);
@@ -107,5 +108,10 @@ void launch_div(double* out, const double* x, long long n, double d, cudaStream_
 void launch_sub(double* r, const double* f, const double* w, long long n, cudaStream_t s);
 void launch_nonfinite(const double* x, long long n, int* flag, cudaStream_t s);
 double measure_dfma_peak(int iters, float* ms_out);  // TFLOP/s of the DFMA pipe
+// Whole MGS of one Arnoldi step (h[0..j+1], non-finite flag) in one
+// cooperative launch; partial holds 2 * mgs_grid(n) doubles.
+int mgs_grid(long long n);
+cudaError_t launch_mgs(const double* V, double* w, long long n, long long ld, int j,
+                       double* partial, int nparts, double* h, int* flag, cudaStream_t s);
 
 }  // namespace imqk

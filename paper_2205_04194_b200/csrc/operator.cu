@@ -10,6 +10,9 @@
 // Interaction lists are never materialised: kernels enumerate them on the fly
 // (the reference's O(grid^4) list build, partition.cpp:56-72, is 151 s at L=8).
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <climits>
 #include <cmath>
 #include <cstring>
@@ -184,6 +187,15 @@ void DeviceOperator::build(const double* xy_host) {
     cuda_check(cudaStreamSynchronize(s), "tree build");
     cuda_check(cudaGetLastError(), "tree kernels");
 
+    // leaf P2M parallelism: ~64 points per warp on average over non-empty leaves
+    {
+      long long ne = 0;
+      for (long long q = 0; q < n_leaves; ++q) ne += ls[(size_t)q + 1] > ls[(size_t)q];
+      const double mean = ne ? (double)N_ / (double)ne : 1.0;
+      int w = 1;
+      while (w < 8 && mean > 64.0 * w * 1.5) w *= 2;
+      P_.p2m_wpl = w;
+    }
     // ---- work lists (all targets)
     leaf_start_h_ = std::move(ls);
     build_items(0, N_);
@@ -279,20 +291,47 @@ void DeviceOperator::build_items(int p_lo, int p_hi) {
     }
   }
   grouped(groups, far_items_h_, far_group_off_);
-  const int nrmax = std::min(rfit, imqk::near_max_points_per_lane());
-  // small problems: split each leaf's 3x3 sources into three rows
-  near_split_ = nt / (32.0 * nrmax) < kWarpsWanted ? 3 : 1;
+  // near items: one leaf each; R from the mean leaf occupancy (a typical leaf
+  // in one item), then the smallest source split (1, 3 or 9 ways) that gives
+  // the GPU enough warps
+  long long ne = 0;
+  for (long long q = 0; q < n_leaves; ++q) ne += std::min(p_hi, ls[(size_t)q + 1]) > std::max(p_lo, ls[(size_t)q]);
+  const double occ = ne ? nt / (double)ne : 1.0;
+  // (measured: the near kernel wants many warps more than register blocking;
+  // split the sources 3 or 9 ways until ~4 x kWarpsWanted items exist, and
+  // drop to one target per lane if even the 9-way split is short of that)
+  constexpr double kNearWarps = 4 * kWarpsWanted;
+  int nrmax = std::max(1, std::min(3, (int)std::ceil(1.25 * occ / 32.0)));
+  auto count_items = [&](int r) {
+    long long c = 0;
+    for (long long q = 0; q < n_leaves; ++q) {
+      const int a = std::max(p_lo, ls[(size_t)q]), b = std::min(p_hi, ls[(size_t)q + 1]);
+      if (b > a) c += (b - a + 32 * r - 1) / (32 * r);
+    }
+    return (double)c;
+  };
+  double nitems = count_items(nrmax);
+  near_split_ = nitems >= kNearWarps ? 1 : (3 * nitems >= kNearWarps ? 3 : 9);
+  if (near_split_ == 9 && 9 * nitems < kNearWarps && nrmax > 1) {
+    nrmax = 1;
+    nitems = count_items(1);
+  }
+  if (const char* e = getenv("IMQ_NEAR_R")) nrmax = std::max(1, std::min(4, atoi(e)));  // tuning
+  if (const char* e = getenv("IMQ_NEAR_SPLIT")) near_split_ = atoi(e) >= 9 ? 9 : (atoi(e) >= 3 ? 3 : 1);
   std::vector<std::vector<int4>> ngroups((size_t)nrmax);
   for (long long q = 0; q < n_leaves; ++q) {
     const int a = std::max(p_lo, ls[(size_t)q]), b = std::min(p_hi, ls[(size_t)q + 1]);
     for (int c = a; c < b; c += 32 * nrmax) {
       const int cnt = std::min(32 * nrmax, b - c);
       for (int r = 0; r < near_split_; ++r)
-        ngroups[(size_t)((cnt + 31) / 32 - 1)].push_back(
-            make_int4((int)q, c, cnt, near_split_ == 1 ? 3 : r));
+        ngroups[(size_t)((cnt + 31) / 32 - 1)].push_back(make_int4(
+            (int)q, c, cnt, near_split_ == 1 ? 15 : (near_split_ == 3 ? 16 + r : 32 + r)));
     }
   }
-  if (near_split_ > 1 && !d_part_) d_part_ = dalloc<double>(3 * (size_t)N_, "near partials");
+  if (near_split_ > 1) {
+    dfree(d_part_);
+    d_part_ = dalloc<double>((size_t)near_split_ * (size_t)N_, "near partials");
+  }
   grouped(ngroups, near_items_h_, near_group_off_);
   n_far_ = (int)far_items_h_.size();
   n_near_ = (int)near_items_h_.size();
@@ -500,7 +539,8 @@ void DeviceOperator::far_near(const double* d_us, double* d_out, const int* perm
     imqk::launch_p2p_near(P_, d_near_items_, near_group_off_.data(), near_begin, near_end, d_us,
                           d_far_, d_out, perm, d_part_, s);
   if (near_split_ > 1 && near_end > near_begin)
-    imqk::launch_near_combine(target_lo_, target_hi_, N_, d_far_, d_part_, d_out, perm, s);
+    imqk::launch_near_combine(target_lo_, target_hi_, N_, near_split_, d_far_, d_part_, d_out,
+                              perm, s);
 }
 
 void DeviceOperator::apply_sorted_locked(const double* d_us, double* d_out, const int* perm,
@@ -621,11 +661,13 @@ SolveResult DeviceOperator::solve_host(const double* f, double tol, int max_iter
 
   const int mcap = std::max(1, std::min(restart, max_iter));
   const int nparts = imqk::dot_parts(N_);
+  const int mgs_parts = imqk::mgs_grid(N_);
   double *d_f = nullptr, *d_x = nullptr, *d_r = nullptr, *d_w = nullptr, *d_V = nullptr;
-  double *d_h = nullptr, *d_part = nullptr;
+  double *d_h = nullptr, *d_part = nullptr, *d_mgs = nullptr;
   int* d_flag = nullptr;
   auto cleanup = [&]() {
     dfree(d_f); dfree(d_x); dfree(d_r); dfree(d_w); dfree(d_V); dfree(d_h); dfree(d_part);
+    dfree(d_mgs);
     dfree(d_flag);
   };
   try {
@@ -636,6 +678,7 @@ SolveResult DeviceOperator::solve_host(const double* f, double tol, int max_iter
     d_V = dalloc<double>(n * (size_t)(mcap + 1), "gmres basis");
     d_h = dalloc<double>((size_t)mcap + 2, "gmres h");
     d_part = dalloc<double>((size_t)nparts, "gmres partials");
+    d_mgs = dalloc<double>(2 * (size_t)mgs_parts, "mgs partials");
     d_flag = dalloc<int>(1, "gmres flag");
     // f in Morton order
     cuda_check(cudaMemcpyAsync(d_u_, f, n * sizeof(double), cudaMemcpyHostToDevice, s), "H2D f");
@@ -657,6 +700,12 @@ SolveResult DeviceOperator::solve_host(const double* f, double tol, int max_iter
       cleanup();
       return rep;
     }
+    const bool trace = getenv("IMQ_TRACE") != nullptr;
+    cudaEvent_t tev[3];
+    double t_mv = 0, t_mgs = 0;
+    const auto t_start = std::chrono::steady_clock::now();
+    if (trace)
+      for (auto& e : tev) cudaEventCreate(&e);
     cuda_check(cudaMemsetAsync(d_x, 0, n * sizeof(double), s), "memset x");
     cuda_check(cudaMemcpyAsync(d_r, d_f, n * sizeof(double), cudaMemcpyDeviceToDevice, s), "r=f");
     int total = 0;
@@ -683,22 +732,28 @@ SolveResult DeviceOperator::solve_host(const double* f, double tol, int max_iter
       int k = 0;
       for (int j = 0; j < m; ++j) {
         double* Vj = d_V + (size_t)j * n;
+        if (trace) cudaEventRecord(tev[0], s);
         matvec(Vj, d_w);
         ++total;
+        if (trace) cudaEventRecord(tev[1], s);
         cuda_check(cudaMemsetAsync(d_flag, 0, sizeof(int), s), "flag");
-        imqk::launch_nonfinite(d_w, N_, d_flag, s);
-        for (int i = 0; i <= j; ++i) {
-          const double* Vi = d_V + (size_t)i * n;
-          imqk::launch_dot(d_w, Vi, N_, d_part, nparts, d_h + i, 0, s);
-          imqk::launch_axpy_dev(d_w, Vi, N_, d_h + i, -1.0, s);
-        }
-        imqk::launch_dot(d_w, d_w, N_, d_part, nparts, d_h + j + 1, 1, s);
+        cuda_check(imqk::launch_mgs(d_V, d_w, N_, (long long)n, j, d_mgs, mgs_parts, d_h, d_flag,
+                                    s),
+                   "MGS launch");
+        if (trace) cudaEventRecord(tev[2], s);
         int flag = 0;
         cuda_check(cudaMemcpyAsync(hbuf.data(), d_h, (size_t)(j + 2) * sizeof(double),
                                    cudaMemcpyDeviceToHost, s), "D2H h");
         cuda_check(cudaMemcpyAsync(&flag, d_flag, sizeof(int), cudaMemcpyDeviceToHost, s),
                    "D2H flag");
         cuda_check(cudaStreamSynchronize(s), "arnoldi step");
+        if (trace) {
+          float a = 0, b2 = 0;
+          cudaEventElapsedTime(&a, tev[0], tev[1]);
+          cudaEventElapsedTime(&b2, tev[1], tev[2]);
+          t_mv += a;
+          t_mgs += b2;
+        }
         if (flag)
           throw std::runtime_error("iterative_solve: non-finite value at iteration " +
                                    std::to_string(total));
@@ -733,6 +788,13 @@ SolveResult DeviceOperator::solve_host(const double* f, double tol, int max_iter
         y[(size_t)i] = sacc / hcol[(size_t)i][(size_t)i];
       }
       for (int i = 0; i < k; ++i) imqk::launch_axpy(d_x, d_V + (size_t)i * n, N_, y[(size_t)i], s);
+    }
+    if (trace) {
+      const double wall = std::chrono::duration<double, std::milli>(
+                              std::chrono::steady_clock::now() - t_start).count();
+      fprintf(stderr, "[imq trace] gmres %d its: wall %.1f ms, matvec %.1f ms, mgs %.1f ms\n",
+              total, wall, t_mv, t_mgs);
+      for (auto& e : tev) cudaEventDestroy(e);
     }
     imqk::launch_scatter(d_x, d_perm_, N_, d_b_, s);
     cuda_check(cudaMemcpyAsync(c, d_b_, n * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H c");

@@ -276,3 +276,34 @@ def test_sharded_application_emulated(imq, world):
         assert err <= 1e-13, err
         owned = np.concatenate([sh.owned_original_indices() for sh in ranks])
         assert np.array_equal(np.sort(owned), np.arange(n))
+
+
+@pytest.mark.parametrize("case", ["shifted_scaled", "strip", "duplicates", "two_points",
+                                  "tiny_t", "large_t", "sparse_clusters"])
+def test_unusual_geometry_vs_oracle(imq, oracle, case):
+    """Edge geometries: far-from-origin squares, degenerate aspect ratios,
+    coincident points, extreme shape parameters, mostly-empty trees."""
+    rng = np.random.default_rng(5)
+    if case == "shifted_scaled":
+        xy, t, m, L = 1000.0 * rng.random(6000) - 12345.0, 7.5, 10, 3
+    elif case == "strip":
+        x = rng.random(3000)
+        xy, t, m, L = np.stack([x, 1e-6 * x], 1).ravel(), 0.01, 12, 4
+    elif case == "duplicates":
+        base = rng.random(400)
+        xy, t, m, L = np.concatenate([base, base, base]), 0.05, 8, 3
+    elif case == "two_points":
+        xy, t, m, L = np.array([0.1, 0.2, 0.9, 0.7]), 0.3, 6, 1
+    elif case == "tiny_t":
+        xy, t, m, L = rng.random(4000), 1e-5, 16, 3
+    elif case == "large_t":
+        xy, t, m, L = rng.random(4000), 40.0, 12, 3
+    else:  # a few tight clusters in a large empty square
+        c = rng.random((5, 2)) * 100.0
+        xy = (c[rng.integers(0, 5, 3000)] + 0.01 * rng.standard_normal((3000, 2))).ravel()
+        t, m, L = 0.002, 14, 6
+    n = xy.size // 2
+    u = rng.uniform(-1, 1, n)
+    b = imq.FastOperator(xy, t, m, L).apply(u)
+    ref = oracle.fast_matvec(xy, t, m, L, u)
+    assert rel_err_inf(b, ref) <= 1e-10, case
