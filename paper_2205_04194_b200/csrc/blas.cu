@@ -5,6 +5,8 @@
 // device, so the modified Gram-Schmidt chain needs no host round trip.
 #include <cooperative_groups.h>
 
+#include <cstdlib>
+
 #include "imq_kernels.hpp"
 
 namespace cg = cooperative_groups;
@@ -162,6 +164,74 @@ __global__ void __launch_bounds__(kMgsThreads) k_mgs(const double* __restrict__ 
   }
 }
 
+// Small vectors (N <= 8 * 1024 * 16): the same MGS in ONE thread-block
+// cluster of 8 CTAs x 1024 threads.  w lives in registers (E elements per
+// thread); each projection's reduction crosses the cluster through distributed
+// shared memory with one cluster barrier (partials double-buffered), so a
+// projection costs ~1 us instead of a grid-wide barrier.
+constexpr int kClusterCtas = 8;
+template <int E>
+__global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(1024)
+    k_mgs_cluster(const double* __restrict__ V, double* w, int n, long long ld, int j,
+                  double* __restrict__ h, int* flag) {
+  cg::cluster_group cl = cg::this_cluster();
+  __shared__ double red[32];
+  __shared__ double slot[2];
+  __shared__ double bcast;
+  constexpr int T = kClusterCtas * 1024;
+  const int tid = (int)cl.block_rank() * 1024 + threadIdx.x;
+  double wr[E];
+  bool bad = false;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int k = tid + e * T;
+    wr[e] = k < n ? w[k] : 0.0;
+    bad |= k < n && !isfinite(wr[e]);
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+  for (int i = 0; i <= j + 1; ++i) {
+    const double* Vi = V + (size_t)i * ld;
+    double acc = 0.0;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int k = tid + e * T;
+      if (k < n) acc = fma(wr[e], i <= j ? Vi[k] : wr[e], acc);
+    }
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int k = 0; k < 32; ++k) t += red[k];
+      slot[i & 1] = t;
+    }
+    cl.sync();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int r = 0; r < kClusterCtas; ++r) t += *cl.map_shared_rank(&slot[i & 1], r);
+      bcast = t;
+    }
+    __syncthreads();
+    const double tot = bcast;
+    if (i <= j) {
+      if (tid == 0) h[i] = tot;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int k = tid + e * T;
+        if (k < n) wr[e] = fma(-tot, Vi[k], wr[e]);
+      }
+    } else if (tid == 0) {
+      h[j + 1] = sqrt(tot);
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int k = tid + e * T;
+    if (k < n) w[k] = wr[e];
+  }
+  cl.sync();  // keep every CTA's shared memory alive until all remote reads are done
+}
+
 inline unsigned grid_for(long long n) {
   long long b = (n + kThreads * 4 - 1) / (kThreads * 4);
   return (unsigned)(b < 1 ? 1 : (b > 1184 ? 1184 : b));
@@ -205,12 +275,25 @@ int mgs_grid(long long n) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mgs, kMgsThreads, 0);
     max_blocks = sms * (per_sm > 2 ? 2 : per_sm);
   }
-  const long long want = (n + kMgsThreads * 4 - 1) / (kMgsThreads * 4);
+  long long per = 4;
+  if (const char* e = getenv("IMQ_MGS_PER")) per = atoi(e);  // elements per thread (tuning)
+  const long long want = (n + kMgsThreads * per - 1) / (kMgsThreads * per);
   return (int)(want < 1 ? 1 : (want > max_blocks ? max_blocks : want));
 }
 
 cudaError_t launch_mgs(const double* V, double* w, long long n, long long ld, int j,
                        double* partial, int nparts, double* h, int* flag, cudaStream_t s) {
+  constexpr long long T = kClusterCtas * 1024;
+  if (!getenv("IMQ_MGS_COOP") && n <= 16 * T) {
+    const int ni = (int)n;
+    const dim3 g(kClusterCtas), b(1024);
+    if (n <= T) k_mgs_cluster<1><<<g, b, 0, s>>>(V, w, ni, ld, j, h, flag);
+    else if (n <= 2 * T) k_mgs_cluster<2><<<g, b, 0, s>>>(V, w, ni, ld, j, h, flag);
+    else if (n <= 4 * T) k_mgs_cluster<4><<<g, b, 0, s>>>(V, w, ni, ld, j, h, flag);
+    else if (n <= 8 * T) k_mgs_cluster<8><<<g, b, 0, s>>>(V, w, ni, ld, j, h, flag);
+    else k_mgs_cluster<16><<<g, b, 0, s>>>(V, w, ni, ld, j, h, flag);
+    return cudaGetLastError();
+  }
   void* args[] = {(void*)&V, (void*)&w, (void*)&n, (void*)&ld, (void*)&j,
                   (void*)&partial, (void*)&h, (void*)&flag};
   return cudaLaunchCooperativeKernel((const void*)k_mgs, dim3(nparts), dim3(kMgsThreads), args, 0,
