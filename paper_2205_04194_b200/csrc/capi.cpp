@@ -536,7 +536,7 @@ int imq_ext_iterative_solve(const imq_operator* op, const double* f, double tol,
 int imq_ext_operator_moments(const imq_operator* op, const double* d_us, void* stream) {
   if (!op || !d_us) return fail(IMQ_ERR_INVALID_ARG, "imq_ext_operator_moments: null argument");
   return guard([&] {
-    op->op->moments(d_us, static_cast<cudaStream_t>(stream));
+    op->op->moments_locked(d_us, static_cast<cudaStream_t>(stream));
     imqh::cuda_check(cudaGetLastError(), "moments launch");
     return IMQ_OK;
   });
@@ -611,8 +611,9 @@ int imq_ext_operator_far_near(const imq_operator* op, const double* d_us, double
                               int scatter, void* stream) {
   if (!op || !d_us || !d_bs) return fail(IMQ_ERR_INVALID_ARG, "imq_ext_operator_far_near: null argument");
   return guard([&] {
-    op->op->far_near(d_us, d_bs, scatter ? op->op->perm_ptr() : nullptr,
-                     static_cast<cudaStream_t>(stream), far_begin, far_end, near_begin, near_end);
+    op->op->far_near_locked(d_us, d_bs, scatter ? op->op->perm_ptr() : nullptr,
+                            static_cast<cudaStream_t>(stream), far_begin, far_end, near_begin,
+                            near_end);
     imqh::cuda_check(cudaGetLastError(), "far_near launch");
     return IMQ_OK;
   });

@@ -21,6 +21,9 @@
 #include <cstdio>
 #include <algorithm>
 #include <cstdlib>
+#include <mutex>
+#include <set>
+#include <tuple>
 
 #include "imq_device.cuh"
 #include "imq_kernels.hpp"
@@ -51,6 +54,18 @@ __host__ __device__ __forceinline__ void mu_unindex(int M, int o, int& m, int& i
 __host__ __device__ constexpr int hz_top(int M, int m) { return M - ((M - m) & 1); }
 __host__ __device__ constexpr int hz_count(int M) {
   return (M + 1) * (M + 2) / 2 - (M + 1) / 2;
+}
+
+// Opt a kernel into > 48 KB of dynamic shared memory, once per (kernel,
+// device, size); the attribute is per device context.
+void ensure_smem_attr(const void* kern, size_t bytes) {
+  static std::mutex mtx;
+  static std::set<std::tuple<const void*, int, size_t>> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mtx);
+  if (done.insert({kern, dev, bytes}).second)
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
 __device__ __forceinline__ int block_count(const TreeParams& P, int level, uint32_t q) {
@@ -726,11 +741,7 @@ void run_far_cfg(const TreeParams& P, const int4* items, int n_items, const doub
   constexpr int K = hz_count(M);
   auto kern = k_m2p_far<M, R, W, S, MINB>;
   const size_t smem = (size_t)W * S * K * 16 + W * S * 8 + W * kMaxList * 4;
-  static bool configured = false;  // per template instance
-  if (!configured) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    configured = true;
-  }
+  if (smem > 48 * 1024) ensure_smem_attr((const void*)kern, smem);
   const unsigned grid = (unsigned)((n_items + W - 1) / W);
   kern<<<grid, W * 32, smem, s>>>(P, items, n_items, coef, far_s);
 }
@@ -820,11 +831,7 @@ void launch_m2m(const TreeParams& P, int level, double2* mu, const double* binom
                 cudaStream_t s) {
   const size_t smem = (size_t)(4 * P.Ke + 4 * (P.M + 1)) * sizeof(double2) +
                       (size_t)(P.M + 1) * (P.M + 1) * sizeof(double) + (P.M + 1) * sizeof(int);
-  static size_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
-    cudaFuncSetAttribute(k_m2m, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    configured = smem;
-  }
+  if (smem > 48 * 1024) ensure_smem_attr((const void*)k_m2m, smem);
   const int threads = ((P.Ke + 31) / 32) * 32 > 1024 ? 1024 : ((P.Ke + 31) / 32) * 32;
   const unsigned nb = 1u << (2 * (level + 1));
   k_m2m<<<nb, threads, smem, s>>>(P, level, mu, binom);

@@ -458,6 +458,8 @@ void DeviceOperator::setup_sharded_moments(int p_lo, int p_hi) {
 }
 
 void DeviceOperator::moments_local(const double* d_us, cudaStream_t s) {
+  std::lock_guard<std::mutex> lk(mtx_);
+  DeviceGuard g(device_);
   if (!sharded()) {  // unsharded: the full moments, nothing to reduce
     moments(d_us, s);
     return;
@@ -504,6 +506,8 @@ void DeviceOperator::coarse_moments(double2** ptr, size_t* count) const {
 }
 
 void DeviceOperator::moments_finish(cudaStream_t s) {
+  std::lock_guard<std::mutex> lk(mtx_);
+  DeviceGuard g(device_);
   if (!sharded()) return;  // moments_local already transformed everything
   imqk::launch_transform(P_, d_mu_, d_coef_, T_, s, 1, L_ - 2);
   imqk::launch_transform(P_, d_mu_, d_coef_, T_, s, L_ - 1, L_ - 1, d_need_par_,

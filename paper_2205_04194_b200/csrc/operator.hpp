@@ -72,7 +72,17 @@ class DeviceOperator {
   int target_lo() const { return target_lo_; }
   int target_hi() const { return target_hi_; }
 
-  // Stage-by-stage access (multi-GPU sharding drives these individually).
+  // Stage-by-stage access (multi-GPU sharding drives these individually);
+  // the *_locked variants are the thread-safe entry points of the C ABI.
+  void moments_locked(const double* d_us, cudaStream_t s) {
+    std::lock_guard<std::mutex> lk(mtx_);
+    moments(d_us, s);
+  }
+  void far_near_locked(const double* d_us, double* d_out, const int* perm, cudaStream_t s,
+                       int fb, int fe, int nb, int ne) {
+    std::lock_guard<std::mutex> lk(mtx_);
+    far_near(d_us, d_out, perm, s, fb, fe, nb, ne);
+  }
   void moments(const double* d_us, cudaStream_t s);  // P2M + M2M + transform
   // Sharded ranks: own + halo moments and own-only coarse partials; the caller
   // all-reduces coarse_moments() over ranks, then calls moments_finish().
