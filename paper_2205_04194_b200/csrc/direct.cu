@@ -128,6 +128,109 @@ __global__ void __launch_bounds__(kNearWarps * 32) k_p2p_near(
   }
 }
 
+// Symmetric near field (every leaf <= 32 R points, unsharded): the item of
+// leaf C evaluates its self tile and each unordered pair {C, B} with B one of
+// its four "forward" neighbours (0,+1), (+1,-1), (+1,0), (+1,+1) once:
+// forward sums sum_j u_j phi_ij accumulate in registers (slot 0), and the
+// reverse sums sum_i u_i phi_ij for B's points are formed by a register that
+// rotates through the lanes with one shuffle per step (lane l evaluates source
+// (l + k) mod 32 at step k), ending in lane j for source j; they go to B's
+// slot 1 + dir.  Slots are combined with the far field in a fixed order.
+template <int R>
+__global__ void __launch_bounds__(kNearWarps * 32) k_p2p_near_sym(
+    const TreeParams P, const int4* __restrict__ items, int n_items,
+    const double* __restrict__ u_s, double* __restrict__ part) {
+  __shared__ double2 sxy[kNearWarps][32];
+  __shared__ double su[kNearWarps][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int it = blockIdx.x * kNearWarps + warp;
+  if (it >= n_items) return;
+  const int4 item = items[it];
+  const uint32_t leaf = (uint32_t)item.x;
+  const int s0 = item.y, cnt = item.z;
+  const size_t N = (size_t)P.N;
+  double xi[R], yi[R], ui[R], acc[R];
+#pragma unroll
+  for (int p = 0; p < R; ++p) {
+    const bool v = lane + 32 * p < cnt;
+    const int q = v ? s0 + lane + 32 * p : s0;
+    xi[p] = P.xs[q];
+    yi[p] = P.ys[q];
+    ui[p] = v ? u_s[q] : 0.0;  // padded targets must not feed reverse sums
+    acc[p] = 0.0;
+  }
+  const double t2 = P.t2;
+  const int g = 1 << (P.L + 1);
+  int li, lj;
+  demorton(leaf, li, lj);
+  // self tile: forward sums only (cnt <= 32 R: whole leaf in this item)
+  for (int base = s0; base < s0 + cnt; base += 32) {
+    const int j = base + lane;
+    __syncwarp();
+    if (j < s0 + cnt) {
+      sxy[warp][lane] = make_double2(P.xs[j], P.ys[j]);
+      su[warp][lane] = u_s[j];
+    } else {
+      sxy[warp][lane] = make_double2(xi[0], yi[0]);
+      su[warp][lane] = 0.0;
+    }
+    __syncwarp();
+#pragma unroll 8
+    for (int k = 0; k < 32; ++k) {
+      const double2 sp = sxy[warp][k];
+      const double uk = su[warp][k];
+#pragma unroll
+      for (int p = 0; p < R; ++p) {
+        const double dx = xi[p] - sp.x, dy = yi[p] - sp.y;
+        acc[p] = fma(uk, rsqrt_pos(fma(dx, dx, fma(dy, dy, t2))), acc[p]);
+      }
+    }
+  }
+  // forward neighbours: forward + reverse sums
+#pragma unroll 1
+  for (int dir = 0; dir < 4; ++dir) {
+    const int bi = li + (dir == 0 ? 0 : 1);
+    const int bj = lj + (dir == 0 ? 1 : dir - 2);
+    if (bi > g - 1 || bj < 0 || bj > g - 1) continue;
+    const uint32_t q = morton(bi, bj);
+    const int a = P.leaf_start[q], b = P.leaf_start[q + 1];
+    double* rev = part + (size_t)(1 + dir) * N;
+    for (int base = a; base < b; base += 32) {
+      const int j = base + lane;
+      __syncwarp();
+      if (j < b) {
+        sxy[warp][lane] = make_double2(P.xs[j], P.ys[j]);
+        su[warp][lane] = u_s[j];
+      } else {
+        sxy[warp][lane] = make_double2(xi[0], yi[0]);
+        su[warp][lane] = 0.0;
+      }
+      __syncwarp();
+      double racc = 0.0;
+#pragma unroll 8
+      for (int k = 0; k < 32; ++k) {
+        const int jj = (lane + k) & 31;
+        const double2 sp = sxy[warp][jj];
+        const double uk = su[warp][jj];
+        double r = 0.0;
+#pragma unroll
+        for (int p = 0; p < R; ++p) {
+          const double dx = xi[p] - sp.x, dy = yi[p] - sp.y;
+          const double phi = rsqrt_pos(fma(dx, dx, fma(dy, dy, t2)));
+          acc[p] = fma(uk, phi, acc[p]);
+          r = fma(ui[p], phi, r);
+        }
+        racc += r;
+        racc = __shfl_sync(0xffffffffu, racc, (lane + 1) & 31);
+      }
+      if (j < b) rev[j] = racc;  // lane j now holds source j's reverse sum
+    }
+  }
+#pragma unroll
+  for (int p = 0; p < R; ++p)
+    if (lane + 32 * p < cnt) part[s0 + lane + 32 * p] = acc[p];
+}
+
 __global__ void __launch_bounds__(256) k_near_combine(int lo, int hi, int N, int nparts,
                                                       const double* __restrict__ far_s,
                                                       const double* __restrict__ part,
@@ -194,6 +297,21 @@ __global__ void __launch_bounds__(kDirThreads) k_direct(const double* __restrict
 }  // namespace
 
 int near_max_points_per_lane() { return kNearMaxR; }
+
+void launch_p2p_near_sym(const TreeParams& P, const int4* items, const int* group_off, int begin,
+                         int end, const double* u_s, double* part, cudaStream_t s) {
+  for (int R = 1; R <= kNearMaxR; ++R) {
+    const int lo = max(begin, group_off[R - 1]), hi = min(end, group_off[R]);
+    if (hi <= lo) continue;
+    const unsigned grid = (unsigned)((hi - lo + kNearWarps - 1) / kNearWarps);
+    switch (R) {
+      case 1: k_p2p_near_sym<1><<<grid, kNearWarps * 32, 0, s>>>(P, items + lo, hi - lo, u_s, part); break;
+      case 2: k_p2p_near_sym<2><<<grid, kNearWarps * 32, 0, s>>>(P, items + lo, hi - lo, u_s, part); break;
+      case 3: k_p2p_near_sym<3><<<grid, kNearWarps * 32, 0, s>>>(P, items + lo, hi - lo, u_s, part); break;
+      default: k_p2p_near_sym<4><<<grid, kNearWarps * 32, 0, s>>>(P, items + lo, hi - lo, u_s, part); break;
+    }
+  }
+}
 
 void launch_near_combine(int lo, int hi, int N, int nparts, const double* far_s,
                          const double* part, double* out, const int* perm, cudaStream_t s) {

@@ -94,6 +94,11 @@ void launch_p2p_near(const TreeParams& P, const int4* items, const int* group_of
 void launch_near_combine(int lo, int hi, int N, int nparts, const double* far_s,
                          const double* part, double* out, const int* perm, cudaStream_t s);
 int near_max_points_per_lane();
+// Symmetric near field (all leaves <= 32 * near_max_points_per_lane() points,
+// whole point set): part holds 5 N-vectors (slot 0 forward, 1..4 reverse),
+// slots 1..4 zeroed by the caller; combine with launch_near_combine(..., 5).
+void launch_p2p_near_sym(const TreeParams& P, const int4* items, const int* group_off, int begin,
+                         int end, const double* u_s, double* part, cudaStream_t s);
 void launch_direct(const double* txy, long long nt, const double* sxy, const double* sval,
                    long long ns, double t2, double* out, cudaStream_t s);
 

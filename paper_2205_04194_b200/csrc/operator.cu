@@ -318,6 +318,13 @@ void DeviceOperator::build_items(int p_lo, int p_hi) {
   }
   if (const char* e = getenv("IMQ_NEAR_R")) nrmax = std::max(1, std::min(4, atoi(e)));  // tuning
   if (const char* e = getenv("IMQ_NEAR_SPLIT")) near_split_ = atoi(e) >= 9 ? 9 : (atoi(e) >= 3 ? 3 : 1);
+  // symmetric near field: whole point set, every leaf within one item
+  int max_leaf = 0;
+  for (long long q = 0; q < n_leaves; ++q)
+    max_leaf = std::max(max_leaf, ls[(size_t)q + 1] - ls[(size_t)q]);
+  near_sym_ = p_lo == 0 && p_hi == N_ && near_split_ == 1 &&
+              max_leaf <= 32 * imqk::near_max_points_per_lane() && !getenv("IMQ_NEAR_NOSYM");
+  if (near_sym_) nrmax = imqk::near_max_points_per_lane();
   std::vector<std::vector<int4>> ngroups((size_t)nrmax);
   for (long long q = 0; q < n_leaves; ++q) {
     const int a = std::max(p_lo, ls[(size_t)q]), b = std::min(p_hi, ls[(size_t)q + 1]);
@@ -328,9 +335,10 @@ void DeviceOperator::build_items(int p_lo, int p_hi) {
             (int)q, c, cnt, near_split_ == 1 ? 15 : (near_split_ == 3 ? 16 + r : 32 + r)));
     }
   }
-  if (near_split_ > 1) {
+  const int nslots = near_sym_ ? 5 : near_split_;
+  if (nslots > 1) {
     dfree(d_part_);
-    d_part_ = dalloc<double>((size_t)near_split_ * (size_t)N_, "near partials");
+    d_part_ = dalloc<double>((size_t)nslots * (size_t)N_, "near partials");
   }
   grouped(ngroups, near_items_h_, near_group_off_);
   n_far_ = (int)far_items_h_.size();
@@ -538,6 +546,15 @@ void DeviceOperator::far_near(const double* d_us, double* d_out, const int* perm
       cuda_check(cudaEventRecord(ev_join_[k], aux_[k]), "join");
       cuda_check(cudaStreamWaitEvent(s, ev_join_[k], 0), "join wait");
     }
+  }
+  if (near_sym_) {
+    if (near_end > near_begin) {
+      cuda_check(cudaMemsetAsync(d_part_ + N_, 0, 4 * (size_t)N_ * sizeof(double), s), "memset");
+      imqk::launch_p2p_near_sym(P_, d_near_items_, near_group_off_.data(), near_begin, near_end,
+                                d_us, d_part_, s);
+      imqk::launch_near_combine(target_lo_, target_hi_, N_, 5, d_far_, d_part_, d_out, perm, s);
+    }
+    return;
   }
   if (near_end > near_begin)
     imqk::launch_p2p_near(P_, d_near_items_, near_group_off_.data(), near_begin, near_end, d_us,

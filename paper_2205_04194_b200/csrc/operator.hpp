@@ -147,6 +147,7 @@ class DeviceOperator {
   double* d_b_ = nullptr;   // original-order output staging
   double* d_part_ = nullptr;  // [3][N] near-field row partials (small problems)
   int near_split_ = 1;
+  bool near_sym_ = false;  // symmetric near-field evaluation (small leaves)
   std::vector<int> leaf_start_h_;
   std::vector<int> need_par_h_, local_leaves_h_;  // sharded moments (own + halo)
   int par_lo_ = 0, par_hi_ = 0;
