@@ -229,6 +229,19 @@ __global__ void __launch_bounds__(kNearWarps * 32) k_p2p_near_sym(
 #pragma unroll
   for (int p = 0; p < R; ++p)
     if (lane + 32 * p < cnt) part[s0 + lane + 32 * p] = acc[p];
+  // reverse slots nobody writes (no / empty backward neighbour): zero them here
+#pragma unroll 1
+  for (int dir = 0; dir < 4; ++dir) {
+    const int ci = li - (dir == 0 ? 0 : 1);
+    const int cj = lj - (dir == 0 ? 1 : dir - 2);
+    bool has = ci >= 0 && cj >= 0 && cj <= g - 1;
+    if (has) {
+      const uint32_t q = morton(ci, cj);
+      has = P.leaf_start[q + 1] > P.leaf_start[q];
+    }
+    if (!has)
+      for (int p = lane; p < cnt; p += 32) part[(size_t)(1 + dir) * N + s0 + p] = 0.0;
+  }
 }
 
 __global__ void __launch_bounds__(256) k_near_combine(int lo, int hi, int N, int nparts,

@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(128) k_p2m_leaf(const TreeParams P, const doub
 // base is e^G), e^{g+kG} from one complex product each.  After the pass the
 // 32/G groups are folded by shuffles in a fixed order (deterministic).
 template <int M, int G, int WPL>
-__global__ void __launch_bounds__(32 * (WPL > 4 ? WPL : 4)) k_p2m_leaf_g(
+__global__ void __launch_bounds__(32 * (WPL > 4 ? WPL : 4), WPL == 1 ? 4 : 1) k_p2m_leaf_g(
     const TreeParams P, const double* __restrict__ u_s, double2* __restrict__ mu,
     const int* __restrict__ leaf_list, int n_list) {
   // WPL warps per leaf (large leaves split their points over several warps;
@@ -168,6 +168,7 @@ __global__ void __launch_bounds__(32 * (WPL > 4 ? WPL : 4)) k_p2m_leaf_g(
   for (int k = 0; k < NM; ++k)
 #pragma unroll
     for (int i = 0; i < NI; ++i) ar[k][i] = ai[k][i] = 0.0;
+#pragma unroll 1
   for (int p = s + grp + sub * (32 / G); p < e; p += WPL * (32 / G)) {
     const double ex = P.xs[p] - zx, ey = P.ys[p] - zy;
     const double e2 = fma(ex, ex, ey * ey);
@@ -383,30 +384,47 @@ __global__ void k_m2m(const TreeParams P, int level, double2* __restrict__ mu,
 }
 
 // ------------------------------------------------------------- transform ---
+// CTA per kTrBlocks consecutive blocks: the sparse table is staged once in
+// shared memory, then each block's K_e moments -> K coefficients.
+constexpr int kTrBlocks = 8;
 __global__ void k_transform(const TreeParams P, int level, const double2* __restrict__ mu,
                             double2* __restrict__ coef, const TransformTable T,
-                            const int* __restrict__ block_list) {
+                            const int* __restrict__ block_list, int n_blocks, int nnz) {
   extern __shared__ double2 sm[];
-  const uint32_t q = block_list ? (uint32_t)block_list[blockIdx.x] : blockIdx.x;
-  if (block_count(P, level, q) == 0) return;
-  const double2* src = mu + P.mu_off[level] + (size_t)q * P.Ke;
-  for (int o = threadIdx.x; o < P.Ke; o += blockDim.x) sm[o] = src[o];
-  __syncthreads();
-  double2* dst = coef + P.coef_off[level] + (size_t)q * P.K;
-  for (int o = threadIdx.x; o < P.K; o += blockDim.x) {
-    double cr = 0.0, ci = 0.0;
-    for (int e = T.off[o]; e < T.off[o + 1]; ++e) {
-      const double2 v = sm[T.idx[e]];
-      cr = fma(T.val[e], v.x, cr);
-      ci = fma(T.val[e], v.y, ci);
+  double2* smu = sm;                                          // [Ke]
+  double* sval = reinterpret_cast<double*>(sm + P.Ke);        // [nnz]
+  int* soff = reinterpret_cast<int*>(sval + nnz);             // [K + 1]
+  int* sidx = soff + P.K + 1;                                 // [nnz]
+  for (int e = threadIdx.x; e < nnz; e += blockDim.x) {
+    sval[e] = T.val[e];
+    sidx[e] = T.idx[e];
+  }
+  for (int o = threadIdx.x; o <= P.K; o += blockDim.x) soff[o] = T.off[o];
+  for (int bb = 0; bb < kTrBlocks; ++bb) {
+    const int b = blockIdx.x * kTrBlocks + bb;
+    if (b >= n_blocks) break;
+    const uint32_t q = block_list ? (uint32_t)block_list[b] : (uint32_t)b;
+    if (block_count(P, level, q) == 0) continue;  // uniform across the CTA
+    __syncthreads();
+    const double2* src = mu + P.mu_off[level] + (size_t)q * P.Ke;
+    for (int o = threadIdx.x; o < P.Ke; o += blockDim.x) smu[o] = src[o];
+    __syncthreads();
+    double2* dst = coef + P.coef_off[level] + (size_t)q * P.K;
+    for (int o = threadIdx.x; o < P.K; o += blockDim.x) {
+      double cr = 0.0, ci = 0.0;
+      for (int e = soff[o]; e < soff[o + 1]; ++e) {
+        const double2 v = smu[sidx[e]];
+        cr = fma(sval[e], v.x, cr);
+        ci = fma(sval[e], v.y, ci);
+      }
+      dst[o] = make_double2(cr, ci);
     }
-    dst[o] = make_double2(cr, ci);
   }
 }
 
 // ------------------------------------------------------------------- M2P ---
-constexpr int kMaxList = 384;
-constexpr int kFarMaxR = 8;  // a far work item holds <= 32 * kFarMaxR targets  // 12 + 27 (L - 2) + 36 <= 372 for L <= 13
+constexpr int kMaxList = 384;  // 12 + 27 (L - 2) + 36 <= 372 for L <= 13
+constexpr int kFarMaxR = 8;    // a far work item holds <= 32 * kFarMaxR targets
 
 // Builds the warp's source list for a work item: every non-empty source block
 // at levels 1..L-1 of the (shared) ancestor lists, then the level-L union over
@@ -601,12 +619,33 @@ __device__ __forceinline__ void load_targets(const TreeParams& P, int s, int cnt
 // Source coefficients are staged per warp through a STAGES-deep ring of
 // shared-memory buffers filled by one-instruction TMA bulk copies
 // (cp.async.bulk + mbarrier complete_tx), lane 0 producing, the warp consuming.
+// Epilogue: far_s[q] = far field (near_part == nullptr), or, when the
+// symmetric near field already ran, out[perm[q]] = far + sum of its 5 slots.
+struct FarOut {
+  double* far_s;
+  const double* near_part;  // [nslots][N] or nullptr
+  int nslots;
+  double* out;
+  const int* perm;
+};
+
+__device__ __forceinline__ void far_store(const TreeParams& P, const FarOut& O, int q,
+                                          double acc) {
+  if (!O.near_part) {
+    O.far_s[q] = acc;
+    return;
+  }
+  double nsum = 0.0;
+  for (int k = 0; k < O.nslots; ++k) nsum += O.near_part[(size_t)k * P.N + q];
+  O.out[O.perm ? O.perm[q] : q] = acc + nsum;
+}
+
 template <int M, int R, int WARPS, int STAGES, int MINB>
 __global__ void __launch_bounds__(WARPS * 32, MINB) k_m2p_far(const TreeParams P,
                                                              const int4* __restrict__ items,
                                                              int n_items,
                                                              const double2* __restrict__ coef,
-                                                             double* __restrict__ far_s) {
+                                                             const FarOut O) {
   constexpr int K = hz_count(M);
   constexpr uint32_t kBytes = K * 16;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -692,7 +731,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_m2p_far(const TreeParams P
   }
 #pragma unroll
   for (int p = 0; p < R; ++p)
-    if ((T.valid >> p) & 1u) far_s[s0 + lane + 32 * p] = acc[p];
+    if ((T.valid >> p) & 1u) far_store(P, O, s0 + lane + 32 * p, acc[p]);
 }
 
 template <int WARPS>
@@ -700,7 +739,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_m2p_far_generic(const TreeParams
                                                                const int4* __restrict__ items,
                                                                int n_items,
                                                                const double2* __restrict__ coef,
-                                                               double* __restrict__ far_s) {
+                                                               const FarOut O) {
   __shared__ uint32_t lists[WARPS][kMaxList];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int it = blockIdx.x * WARPS + warp;
@@ -727,7 +766,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_m2p_far_generic(const TreeParams
       const double zy = block_center(P.oy, qj, P.cell[l]);
       acc += far_eval_generic(coef + P.coef_off[l] + (size_t)q * P.K, P.M, x - zx, y - zy, P.t2);
     }
-    far_s[p] = acc;
+    far_store(P, O, p, acc);
   }
 }
 
@@ -737,7 +776,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_m2p_far_generic(const TreeParams
 // point slot of an item.
 template <int M, int R, int W, int S, int MINB>
 void run_far_cfg(const TreeParams& P, const int4* items, int n_items, const double2* coef,
-                 double* far_s, cudaStream_t s) {
+                 const FarOut& far_s, cudaStream_t s) {
   constexpr int K = hz_count(M);
   auto kern = k_m2p_far<M, R, W, S, MINB>;
   const size_t smem = (size_t)W * S * K * 16 + W * S * 8 + W * kMaxList * 4;
@@ -754,7 +793,7 @@ namespace {
 
 template <int M>
 void run_far(const TreeParams& P, int R, const int4* items, int n_items, const double2* coef,
-             double* far_s, cudaStream_t s) {
+             const FarOut& far_s, cudaStream_t s) {
   switch (R) {
     case 1: return run_far_cfg<M, 1, 4, 3, 1>(P, items, n_items, coef, far_s, s);
     case 2: return run_far_cfg<M, 2, 4, 3, 1>(P, items, n_items, coef, far_s, s);
@@ -840,13 +879,18 @@ void launch_m2m(const TreeParams& P, int level, double2* mu, const double* binom
 void launch_transform(const TreeParams& P, const double2* mu, double2* coef,
                       const TransformTable& T, cudaStream_t s, int l_lo, int l_hi,
                       const int* block_list, int n_list) {
-  const size_t smem = (size_t)P.Ke * sizeof(double2);
+  const int nnz = T.nnz;
+  const size_t smem = (size_t)P.Ke * sizeof(double2) + (size_t)nnz * (sizeof(double) + sizeof(int)) +
+                      (size_t)(P.K + 1) * sizeof(int);
+  if (smem > 48 * 1024) ensure_smem_attr((const void*)k_transform, smem);
   const int threads = ((P.K + 31) / 32) * 32 > 1024 ? 1024 : ((P.K + 31) / 32) * 32;
   if (l_lo < 1) l_lo = 1;
   if (l_hi < 1 || l_hi > P.L) l_hi = P.L;
   for (int l = l_lo; l <= l_hi; ++l) {
-    const unsigned nb = block_list ? (unsigned)n_list : 1u << (2 * (l + 1));
-    if (nb) k_transform<<<nb, threads, smem, s>>>(P, l, mu, coef, T, block_list);
+    const int nb = block_list ? n_list : 1 << (2 * (l + 1));
+    if (nb)
+      k_transform<<<(unsigned)((nb + kTrBlocks - 1) / kTrBlocks), threads, smem, s>>>(
+          P, l, mu, coef, T, block_list, nb, nnz);
   }
 }
 
@@ -879,9 +923,11 @@ void launch_scatter_rows(const double* src, const int* idx, int n, int width, do
 }
 
 void launch_m2p_far(const TreeParams& P, const int4* items, const int* group_off, int begin,
-                    int end, const double2* coef, double* far_s, const cudaStream_t* streams,
-                    int nstreams) {
+                    int end, const double2* coef, double* far_s_ptr, const cudaStream_t* streams,
+                    int nstreams, const double* near_part, int nslots, double* out,
+                    const int* perm) {
   if (end <= begin) return;
+  const FarOut far_s{far_s_ptr, near_part, nslots, out, perm};
   cudaStream_t s = streams[0];
   int launched = 0;
   if (!m2p_specialised(P.M)) {

@@ -41,6 +41,7 @@ struct TransformTable {
   const int* off;
   const int* idx;
   const double* val;
+  int nnz;
 };
 
 // ---- tree / binning (tree.cu)
@@ -80,9 +81,12 @@ void launch_scatter_rows(const double* src, const int* idx, int n, int width, do
 // items with index in [begin, end).  Group launches are spread round-robin
 // over `streams` (streams[0] first, largest R first) so that small groups run
 // in the tail of the large ones; the caller forks/joins the streams.
+// near_part != nullptr: the symmetric near field already ran; the far kernel's
+// epilogue writes out[perm[q]] = far + sum of the nslots near partials.
 void launch_m2p_far(const TreeParams& P, const int4* items, const int* group_off, int begin,
                     int end, const double2* coef, double* far_s, const cudaStream_t* streams,
-                    int nstreams);
+                    int nstreams, const double* near_part = nullptr, int nslots = 0,
+                    double* out = nullptr, const int* perm = nullptr);
 bool m2p_specialised(int M);
 int far_max_points_per_lane();
 

@@ -230,6 +230,7 @@ void DeviceOperator::build(const double* xy_host) {
     T_.off = d_tr_off_;
     T_.idx = d_tr_idx_;
     T_.val = d_tr_val_;
+    T_.nnz = (int)tr.val.size();
 
     // ---- expansion storage + workspace
     d_mu_ = dalloc<double2>((size_t)mo, "moments");
@@ -532,6 +533,10 @@ void DeviceOperator::far_near(const double* d_us, double* d_out, const int* perm
   far_end = std::min(far_end, n_far_);
   near_begin = std::max(0, near_begin);
   near_end = std::min(near_end, n_near_);
+  const bool sym = near_sym_ && near_end > near_begin;
+  if (sym)  // symmetric near field first; the far epilogue combines and scatters
+    imqk::launch_p2p_near_sym(P_, d_near_items_, near_group_off_.data(), near_begin, near_end,
+                              d_us, d_part_, s);
   if (far_end > far_begin) {
     // fork: group launches on s + the aux streams, joined back into s
     cudaStream_t ss[1 + kAuxStreams] = {s};
@@ -541,21 +546,13 @@ void DeviceOperator::far_near(const double* d_us, double* d_out, const int* perm
       cuda_check(cudaStreamWaitEvent(aux_[k], ev_fork_, 0), "fork wait");
     }
     imqk::launch_m2p_far(P_, d_far_items_, far_group_off_.data(), far_begin, far_end, d_coef_,
-                         d_far_, ss, 1 + kAuxStreams);
+                         d_far_, ss, 1 + kAuxStreams, sym ? d_part_ : nullptr, 5, d_out, perm);
     for (int k = 0; k < kAuxStreams; ++k) {
       cuda_check(cudaEventRecord(ev_join_[k], aux_[k]), "join");
       cuda_check(cudaStreamWaitEvent(s, ev_join_[k], 0), "join wait");
     }
   }
-  if (near_sym_) {
-    if (near_end > near_begin) {
-      cuda_check(cudaMemsetAsync(d_part_ + N_, 0, 4 * (size_t)N_ * sizeof(double), s), "memset");
-      imqk::launch_p2p_near_sym(P_, d_near_items_, near_group_off_.data(), near_begin, near_end,
-                                d_us, d_part_, s);
-      imqk::launch_near_combine(target_lo_, target_hi_, N_, 5, d_far_, d_part_, d_out, perm, s);
-    }
-    return;
-  }
+  if (near_sym_) return;
   if (near_end > near_begin)
     imqk::launch_p2p_near(P_, d_near_items_, near_group_off_.data(), near_begin, near_end, d_us,
                           d_far_, d_out, perm, d_part_, s);
