@@ -307,3 +307,26 @@ def test_unusual_geometry_vs_oracle(imq, oracle, case):
     b = imq.FastOperator(xy, t, m, L).apply(u)
     ref = oracle.fast_matvec(xy, t, m, L, u)
     assert rel_err_inf(b, ref) <= 1e-10, case
+
+
+def test_concurrent_apply_from_threads(imq, golden):
+    """fastmv.hpp:17-18: the operator is safe for concurrent application to
+    distinct vectors (ctypes releases the GIL; the library serialises)."""
+    import threading
+    c = golden("cfg1")
+    op = imq.FastOperator(c["xy"], 0.1, 10, 2)
+    us = [imq.random_vector(4096, 100 + k) for k in range(8)]
+    want = [op.apply(u) for u in us]
+    got = [None] * 8
+
+    def work(k):
+        for _ in range(3):
+            got[k] = op.apply(us[k])
+
+    ts = [threading.Thread(target=work, args=(k,)) for k in range(8)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for k in range(8):
+        assert np.array_equal(got[k], want[k])
