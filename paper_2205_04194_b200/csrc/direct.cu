@@ -19,6 +19,7 @@ namespace {
 
 constexpr int kNearWarps = 4;
 constexpr int kNearMaxR = 4;  // a near work item holds <= 32 * kNearMaxR targets of one leaf
+constexpr int kPairR = 4;     // chunk size 32 * kPairR of the chunk-pair near field
 
 // Warp per near work item: <= 32 R targets of one leaf, R per lane.  Every
 // source point staged in the warp's shared-memory tile is read back once per
@@ -244,6 +245,102 @@ __global__ void __launch_bounds__(kNearWarps * 32) k_p2p_near_sym(
   }
 }
 
+// Symmetric near field for large leaves: items are unordered pairs of leaf
+// chunks (<= 32 R points each) {A, B} -- A's chunk with itself, with the later
+// chunks of its own leaf, and with every chunk of its four forward neighbour
+// leaves.  Each pair's kernel values are evaluated once: forward sums for A's
+// points and (pairs A != B) reverse sums for B's points, via the lane rotation
+// of k_p2p_near_sym, are written to the item's two partial rows; a reduction
+// kernel then adds, for every chunk, its rows in a fixed order.
+template <int R>
+__global__ void __launch_bounds__(kNearWarps * 32) k_p2p_pair(
+    const TreeParams P, const int4* __restrict__ items, int n_items,
+    const double* __restrict__ u_s, double* __restrict__ part) {
+  __shared__ double2 sxy[kNearWarps][32];
+  __shared__ double su[kNearWarps][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int it = blockIdx.x * kNearWarps + warp;
+  if (it >= n_items) return;
+  const int4 item = items[it];
+  const int a0 = item.x, na = item.y, b0 = item.z, nb = item.w;
+  const bool self = a0 == b0;
+  double* fwd = part + (size_t)it * (64 * R);
+  double* rev = fwd + 32 * R;
+  double xi[R], yi[R], ui[R], acc[R];
+#pragma unroll
+  for (int p = 0; p < R; ++p) {
+    const bool v = lane + 32 * p < na;
+    const int q = v ? a0 + lane + 32 * p : a0;
+    xi[p] = P.xs[q];
+    yi[p] = P.ys[q];
+    ui[p] = v ? u_s[q] : 0.0;
+    acc[p] = 0.0;
+  }
+  const double t2 = P.t2;
+  for (int base = 0; base < nb; base += 32) {
+    const int j = b0 + base + lane;
+    __syncwarp();
+    if (base + lane < nb) {
+      sxy[warp][lane] = make_double2(P.xs[j], P.ys[j]);
+      su[warp][lane] = u_s[j];
+    } else {
+      sxy[warp][lane] = make_double2(xi[0], yi[0]);
+      su[warp][lane] = 0.0;
+    }
+    __syncwarp();
+    if (self) {
+#pragma unroll 8
+      for (int k = 0; k < 32; ++k) {
+        const double2 sp = sxy[warp][k];
+        const double uk = su[warp][k];
+#pragma unroll
+        for (int p = 0; p < R; ++p) {
+          const double dx = xi[p] - sp.x, dy = yi[p] - sp.y;
+          acc[p] = fma(uk, rsqrt_pos(fma(dx, dx, fma(dy, dy, t2))), acc[p]);
+        }
+      }
+    } else {
+      double racc = 0.0;
+#pragma unroll 8
+      for (int k = 0; k < 32; ++k) {
+        const int jj = (lane + k) & 31;
+        const double2 sp = sxy[warp][jj];
+        const double uk = su[warp][jj];
+        double r = 0.0;
+#pragma unroll
+        for (int p = 0; p < R; ++p) {
+          const double dx = xi[p] - sp.x, dy = yi[p] - sp.y;
+          const double phi = rsqrt_pos(fma(dx, dx, fma(dy, dy, t2)));
+          acc[p] = fma(uk, phi, acc[p]);
+          r = fma(ui[p], phi, r);
+        }
+        racc += r;
+        racc = __shfl_sync(0xffffffffu, racc, (lane + 1) & 31);
+      }
+      if (base + lane < nb) rev[base + lane] = racc;
+    }
+  }
+#pragma unroll
+  for (int p = 0; p < R; ++p)
+    if (lane + 32 * p < na) fwd[lane + 32 * p] = acc[p];
+}
+
+// Block per chunk, thread per point: near = sum of the chunk's partial rows
+// (contrib entries = row offsets into part) in their fixed list order.
+__global__ void __launch_bounds__(128) k_pair_reduce(const int2* __restrict__ chunks,
+                                                     const int* __restrict__ contrib_off,
+                                                     const int* __restrict__ contrib,
+                                                     const double* __restrict__ part,
+                                                     double* __restrict__ near_s) {
+  const int2 c = chunks[blockIdx.x];
+  for (int k = threadIdx.x; k < c.y; k += blockDim.x) {
+    double sum = 0.0;
+    for (int e = contrib_off[blockIdx.x]; e < contrib_off[blockIdx.x + 1]; ++e)
+      sum += part[(size_t)contrib[e] + k];
+    near_s[c.x + k] = sum;
+  }
+}
+
 __global__ void __launch_bounds__(256) k_near_combine(int lo, int hi, int N, int nparts,
                                                       const double* __restrict__ far_s,
                                                       const double* __restrict__ part,
@@ -324,6 +421,16 @@ void launch_p2p_near_sym(const TreeParams& P, const int4* items, const int* grou
       default: k_p2p_near_sym<4><<<grid, kNearWarps * 32, 0, s>>>(P, items + lo, hi - lo, u_s, part); break;
     }
   }
+}
+
+void launch_p2p_pair(const TreeParams& P, const int4* items, int n_items, const double* u_s,
+                     double* part, const int2* chunks, int n_chunks, const int* contrib_off,
+                     const int* contrib, double* near_s, cudaStream_t s) {
+  if (n_items)
+    k_p2p_pair<kPairR><<<(unsigned)((n_items + kNearWarps - 1) / kNearWarps), kNearWarps * 32, 0,
+                         s>>>(P, items, n_items, u_s, part);
+  if (n_chunks)
+    k_pair_reduce<<<(unsigned)n_chunks, 128, 0, s>>>(chunks, contrib_off, contrib, part, near_s);
 }
 
 void launch_near_combine(int lo, int hi, int N, int nparts, const double* far_s,

@@ -336,7 +336,8 @@ void DeviceOperator::build_items(int p_lo, int p_hi) {
             (int)q, c, cnt, near_split_ == 1 ? 15 : (near_split_ == 3 ? 16 + r : 32 + r)));
     }
   }
-  const int nslots = near_sym_ ? 5 : near_split_;
+  build_pair_items(p_lo, p_hi);
+  const int nslots = near_sym_ ? 5 : (near_pair_ ? 1 : near_split_);
   if (nslots > 1) {
     dfree(d_part_);
     d_part_ = dalloc<double>((size_t)nslots * (size_t)N_, "near partials");
@@ -354,6 +355,75 @@ void DeviceOperator::build_items(int p_lo, int p_hi) {
                         cudaMemcpyHostToDevice), "H2D near items");
   target_lo_ = p_lo;
   target_hi_ = p_hi;
+}
+
+// Chunk-pair symmetric near field for the whole point set when leaves are too
+// large for k_p2p_near_sym (see direct.cu).  Sets near_pair_.
+void DeviceOperator::build_pair_items(int p_lo, int p_hi) {
+  dfree(d_pair_items_); dfree(d_pair_part_); dfree(d_chunks_); dfree(d_contrib_off_);
+  dfree(d_contrib_); dfree(d_near_s_);
+  near_pair_ = false;
+  n_pair_items_ = n_chunks_ = 0;
+  if (near_sym_ || p_lo != 0 || p_hi != N_ || getenv("IMQ_NEAR_NOPAIR")) return;
+  const std::vector<int>& ls = leaf_start_h_;
+  const int g = 1 << (L_ + 1);
+  const long long n_leaves = (long long)g * g;
+  constexpr int CS = imqk::kNearChunk;
+  // chunks of every leaf
+  std::vector<int> leaf_chunk0((size_t)n_leaves + 1, 0);
+  std::vector<int2> chunks;
+  for (long long q = 0; q < n_leaves; ++q) {
+    leaf_chunk0[(size_t)q] = (int)chunks.size();
+    for (int c = ls[(size_t)q]; c < ls[(size_t)q + 1]; c += CS)
+      chunks.push_back(make_int2(c, std::min(CS, ls[(size_t)q + 1] - c)));
+  }
+  leaf_chunk0[(size_t)n_leaves] = (int)chunks.size();
+  std::vector<int4> items;
+  std::vector<std::vector<int>> contrib(chunks.size());
+  auto add = [&](int a, int b) {
+    const int i = (int)items.size();
+    items.push_back(make_int4(chunks[(size_t)a].x, chunks[(size_t)a].y, chunks[(size_t)b].x,
+                              chunks[(size_t)b].y));
+    contrib[(size_t)a].push_back(i * 2 * CS);
+    if (a != b) contrib[(size_t)b].push_back(i * 2 * CS + CS);
+  };
+  for (long long q = 0; q < n_leaves; ++q) {
+    int li, lj;
+    imqdev::demorton((uint32_t)q, li, lj);
+    for (int a = leaf_chunk0[(size_t)q]; a < leaf_chunk0[(size_t)q + 1]; ++a) {
+      for (int b = a; b < leaf_chunk0[(size_t)q + 1]; ++b) add(a, b);
+      for (int dir = 0; dir < 4; ++dir) {
+        const int bi = li + (dir == 0 ? 0 : 1), bj = lj + (dir == 0 ? 1 : dir - 2);
+        if (bi > g - 1 || bj < 0 || bj > g - 1) continue;
+        const uint32_t qb = imqdev::morton((uint32_t)bi, (uint32_t)bj);
+        for (int b = leaf_chunk0[qb]; b < leaf_chunk0[(size_t)qb + 1]; ++b) add(a, b);
+      }
+    }
+    if ((double)items.size() * 2 * CS * sizeof(double) > 2.0e9) return;  // too large: plain path
+  }
+  std::vector<int> off(chunks.size() + 1, 0), flat;
+  for (size_t c = 0; c < chunks.size(); ++c) {
+    off[c + 1] = off[c] + (int)contrib[c].size();
+    flat.insert(flat.end(), contrib[c].begin(), contrib[c].end());
+  }
+  if (flat.empty()) flat.push_back(0);
+  n_pair_items_ = (int)items.size();
+  n_chunks_ = (int)chunks.size();
+  d_pair_items_ = dalloc<int4>(items.size(), "pair items");
+  d_pair_part_ = dalloc<double>(items.size() * 2 * CS, "pair partials");
+  d_chunks_ = dalloc<int2>(chunks.size(), "chunks");
+  d_contrib_off_ = dalloc<int>(off.size(), "contrib off");
+  d_contrib_ = dalloc<int>(flat.size(), "contrib");
+  d_near_s_ = dalloc<double>((size_t)N_, "near");
+  cuda_check(cudaMemcpy(d_pair_items_, items.data(), items.size() * sizeof(int4),
+                        cudaMemcpyHostToDevice), "H2D pair items");
+  cuda_check(cudaMemcpy(d_chunks_, chunks.data(), chunks.size() * sizeof(int2),
+                        cudaMemcpyHostToDevice), "H2D chunks");
+  cuda_check(cudaMemcpy(d_contrib_off_, off.data(), off.size() * sizeof(int),
+                        cudaMemcpyHostToDevice), "H2D contrib off");
+  cuda_check(cudaMemcpy(d_contrib_, flat.data(), flat.size() * sizeof(int),
+                        cudaMemcpyHostToDevice), "H2D contrib");
+  near_pair_ = true;
 }
 
 void DeviceOperator::restrict_targets(int p_lo, int p_hi) {
@@ -533,10 +603,13 @@ void DeviceOperator::far_near(const double* d_us, double* d_out, const int* perm
   far_end = std::min(far_end, n_far_);
   near_begin = std::max(0, near_begin);
   near_end = std::min(near_end, n_near_);
-  const bool sym = near_sym_ && near_end > near_begin;
-  if (sym)  // symmetric near field first; the far epilogue combines and scatters
+  const bool sym = (near_sym_ || near_pair_) && near_end > near_begin;
+  if (sym && near_sym_)  // symmetric near field first; the far epilogue combines and scatters
     imqk::launch_p2p_near_sym(P_, d_near_items_, near_group_off_.data(), near_begin, near_end,
                               d_us, d_part_, s);
+  if (sym && near_pair_)
+    imqk::launch_p2p_pair(P_, d_pair_items_, n_pair_items_, d_us, d_pair_part_, d_chunks_,
+                          n_chunks_, d_contrib_off_, d_contrib_, d_near_s_, s);
   if (far_end > far_begin) {
     // fork: group launches on s + the aux streams, joined back into s
     cudaStream_t ss[1 + kAuxStreams] = {s};
@@ -546,13 +619,15 @@ void DeviceOperator::far_near(const double* d_us, double* d_out, const int* perm
       cuda_check(cudaStreamWaitEvent(aux_[k], ev_fork_, 0), "fork wait");
     }
     imqk::launch_m2p_far(P_, d_far_items_, far_group_off_.data(), far_begin, far_end, d_coef_,
-                         d_far_, ss, 1 + kAuxStreams, sym ? d_part_ : nullptr, 5, d_out, perm);
+                         d_far_, ss, 1 + kAuxStreams,
+                         sym ? (near_pair_ ? d_near_s_ : d_part_) : nullptr, near_pair_ ? 1 : 5,
+                         d_out, perm);
     for (int k = 0; k < kAuxStreams; ++k) {
       cuda_check(cudaEventRecord(ev_join_[k], aux_[k]), "join");
       cuda_check(cudaStreamWaitEvent(s, ev_join_[k], 0), "join wait");
     }
   }
-  if (near_sym_) return;
+  if (near_sym_ || near_pair_) return;
   if (near_end > near_begin)
     imqk::launch_p2p_near(P_, d_near_items_, near_group_off_.data(), near_begin, near_end, d_us,
                           d_far_, d_out, perm, d_part_, s);

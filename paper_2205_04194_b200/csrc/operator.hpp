@@ -103,6 +103,7 @@ class DeviceOperator {
  private:
   void build(const double* xy_host);
   void build_items(int p_lo, int p_hi);
+  void build_pair_items(int p_lo, int p_hi);
   void setup_sharded_moments(int p_lo, int p_hi);
   void release();
   void apply_sorted_locked(const double* d_us, double* d_bs, const int* perm,
@@ -148,6 +149,14 @@ class DeviceOperator {
   double* d_part_ = nullptr;  // [3][N] near-field row partials (small problems)
   int near_split_ = 1;
   bool near_sym_ = false;  // symmetric near-field evaluation (small leaves)
+  bool near_pair_ = false; // chunk-pair symmetric near field (large leaves)
+  int n_pair_items_ = 0, n_chunks_ = 0;
+  int4* d_pair_items_ = nullptr;
+  double* d_pair_part_ = nullptr;
+  int2* d_chunks_ = nullptr;
+  int* d_contrib_off_ = nullptr;
+  int* d_contrib_ = nullptr;
+  double* d_near_s_ = nullptr;
   std::vector<int> leaf_start_h_;
   std::vector<int> need_par_h_, local_leaves_h_;  // sharded moments (own + halo)
   int par_lo_ = 0, par_hi_ = 0;
