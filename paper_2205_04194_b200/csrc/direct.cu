@@ -187,45 +187,52 @@ __global__ void __launch_bounds__(kNearWarps * 32) k_p2p_near_sym(
       }
     }
   }
-  // forward neighbours: forward + reverse sums
-#pragma unroll 1
+  // forward neighbours: forward + reverse sums over the concatenation of the
+  // four neighbour ranges (tiles of 32 sources cross leaf boundaries)
+  int na[4], nb[4];
+#pragma unroll
   for (int dir = 0; dir < 4; ++dir) {
     const int bi = li + (dir == 0 ? 0 : 1);
     const int bj = lj + (dir == 0 ? 1 : dir - 2);
+    na[dir] = nb[dir] = 0;
     if (bi > g - 1 || bj < 0 || bj > g - 1) continue;
     const uint32_t q = morton(bi, bj);
-    const int a = P.leaf_start[q], b = P.leaf_start[q + 1];
-    double* rev = part + (size_t)(1 + dir) * N;
-    for (int base = a; base < b; base += 32) {
-      const int j = base + lane;
-      __syncwarp();
-      if (j < b) {
-        sxy[warp][lane] = make_double2(P.xs[j], P.ys[j]);
-        su[warp][lane] = u_s[j];
-      } else {
-        sxy[warp][lane] = make_double2(xi[0], yi[0]);
-        su[warp][lane] = 0.0;
-      }
-      __syncwarp();
-      double racc = 0.0;
-#pragma unroll 8
-      for (int k = 0; k < 32; ++k) {
-        const int jj = (lane + k) & 31;
-        const double2 sp = sxy[warp][jj];
-        const double uk = su[warp][jj];
-        double r = 0.0;
-#pragma unroll
-        for (int p = 0; p < R; ++p) {
-          const double dx = xi[p] - sp.x, dy = yi[p] - sp.y;
-          const double phi = rsqrt_pos(fma(dx, dx, fma(dy, dy, t2)));
-          acc[p] = fma(uk, phi, acc[p]);
-          r = fma(ui[p], phi, r);
-        }
-        racc += r;
-        racc = __shfl_sync(0xffffffffu, racc, (lane + 1) & 31);
-      }
-      if (j < b) rev[j] = racc;  // lane j now holds source j's reverse sum
+    na[dir] = P.leaf_start[q];
+    nb[dir] = P.leaf_start[q + 1];
+  }
+  const int e1 = nb[0] - na[0], e2 = e1 + nb[1] - na[1], e3 = e2 + nb[2] - na[2];
+  const int total = e3 + nb[3] - na[3];
+  for (int base = 0; base < total; base += 32) {
+    const int v = base + lane;
+    const int dir = v < e1 ? 0 : (v < e2 ? 1 : (v < e3 ? 2 : 3));
+    const int j = na[dir] + v - (dir == 0 ? 0 : (dir == 1 ? e1 : (dir == 2 ? e2 : e3)));
+    __syncwarp();
+    if (v < total) {
+      sxy[warp][lane] = make_double2(P.xs[j], P.ys[j]);
+      su[warp][lane] = u_s[j];
+    } else {
+      sxy[warp][lane] = make_double2(xi[0], yi[0]);
+      su[warp][lane] = 0.0;
     }
+    __syncwarp();
+    double racc = 0.0;
+#pragma unroll 8
+    for (int k = 0; k < 32; ++k) {
+      const int jj = (lane + k) & 31;
+      const double2 sp = sxy[warp][jj];
+      const double uk = su[warp][jj];
+      double r = 0.0;
+#pragma unroll
+      for (int p = 0; p < R; ++p) {
+        const double dx = xi[p] - sp.x, dy = yi[p] - sp.y;
+        const double phi = rsqrt_pos(fma(dx, dx, fma(dy, dy, t2)));
+        acc[p] = fma(uk, phi, acc[p]);
+        r = fma(ui[p], phi, r);
+      }
+      racc += r;
+      racc = __shfl_sync(0xffffffffu, racc, (lane + 1) & 31);
+    }
+    if (v < total) part[(size_t)(1 + dir) * N + j] = racc;  // lane holds its source's reverse sum
   }
 #pragma unroll
   for (int p = 0; p < R; ++p)
