@@ -561,6 +561,95 @@ __device__ __forceinline__ void far_evalR(const double2* __restrict__ c, const d
   }
 }
 
+// Same evaluation with the Horner loops unrolled by template recursion: the
+// compiler otherwise keeps the long inner loops of the low-m groups rolled
+// (4 coefficients per trip, each trip stalling on its own shared loads), and
+// every coefficient becomes an LDS with an immediate offset.
+template <int R, int N>
+__device__ __forceinline__ void horner_inner(const double2* __restrict__ c, double* gr, double* gi,
+                                             const double* q) {
+  if constexpr (N > 0) {
+    const double2 cc = c[0];
+#pragma unroll
+    for (int p = 0; p < R; ++p) {
+      gr[p] = fma(gr[p], q[p], cc.x);
+      gi[p] = fma(gi[p], q[p], cc.y);
+    }
+    horner_inner<R, N - 1>(c + 1, gr, gi, q);
+  }
+}
+
+template <int R, int N>
+__device__ __forceinline__ void horner_real(const double2* __restrict__ c, double* g,
+                                            const double* q) {
+  if constexpr (N > 0) {
+    const double ck = c[0].x;
+#pragma unroll
+    for (int p = 0; p < R; ++p) g[p] = fma(g[p], q[p], ck);
+    horner_real<R, N - 1>(c + 1, g, q);
+  }
+}
+
+// Groups m, m-1, ..., 1 (c points at C_{m, top(m)}); returns the offset past them.
+template <int M, int R, int m>
+__device__ __forceinline__ const double2* horner_groups(const double2* __restrict__ c, double* ar,
+                                                        double* ai, const double* q,
+                                                        const double* xr, const double* xi) {
+  if constexpr (m < 1) {
+    return c;
+  } else {
+    constexpr int n = hz_top(M, m) - m;  // coefficients after the leading one
+    double gr[R], gi[R];
+    const double2 cc = c[0];
+#pragma unroll
+    for (int p = 0; p < R; ++p) {
+      gr[p] = cc.x;
+      gi[p] = cc.y;
+    }
+    horner_inner<R, n>(c + 1, gr, gi, q);
+#pragma unroll
+    for (int p = 0; p < R; ++p) {
+      const double nr = fma(ar[p], xr[p], fma(-ai[p], xi[p], gr[p]));
+      const double ni = fma(ar[p], xi[p], fma(ai[p], xr[p], gi[p]));
+      ar[p] = nr;
+      ai[p] = ni;
+    }
+    return horner_groups<M, R, m - 1>(c + 1 + n, ar, ai, q, xr, xi);
+  }
+}
+
+template <int M, int R>
+__device__ __forceinline__ void far_evalT(const double2* __restrict__ c, const double* dx,
+                                          const double* dy, double t2, double* v) {
+  double r[R], q[R];
+#pragma unroll
+  for (int p = 0; p < R; ++p) {
+    r[p] = rsqrt_pos(fma(dx[p], dx[p], fma(dy[p], dy[p], t2)));
+    q[p] = r[p] * r[p];
+  }
+  if constexpr (M == 0) {
+#pragma unroll
+    for (int p = 0; p < R; ++p) v[p] = c[0].x * r[p];
+  } else {
+    double xr[R], xi[R], ar[R], ai[R];
+    const double2 cc = c[0];
+#pragma unroll
+    for (int p = 0; p < R; ++p) {
+      xr[p] = dx[p] * q[p];
+      xi[p] = -dy[p] * q[p];
+      ar[p] = cc.x;
+      ai[p] = cc.y;
+    }
+    const double2* c0 = horner_groups<M, R, M - 1>(c + 1, ar, ai, q, xr, xi);
+    double g[R];
+#pragma unroll
+    for (int p = 0; p < R; ++p) g[p] = c0[0].x;
+    horner_real<R, hz_top(M, 0)>(c0 + 1, g, q);
+#pragma unroll
+    for (int p = 0; p < R; ++p) v[p] = fma(ar[p], xr[p], fma(-ai[p], xi[p], g[p])) * r[p];
+  }
+}
+
 // Runtime-order variant (coefficients read through L1 from global memory).
 __device__ __forceinline__ double far_eval_generic(const double2* __restrict__ c, int M,
                                                    double dx, double dy, double t2) {
@@ -720,7 +809,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_m2p_far(const TreeParams P
       dy[p] = T.y[p] - zy;
     }
     mbar_wait(&bars[slot], (uint32_t)((e / STAGES) & 1));
-    far_evalR<M, R>(stage + (size_t)slot * K, dx, dy, P.t2, v);
+    far_evalT<M, R>(stage + (size_t)slot * K, dx, dy, P.t2, v);
 #pragma unroll
     for (int p = 0; p < R; ++p) acc[p] += msk[p] ? v[p] : 0.0;
     __syncwarp();
