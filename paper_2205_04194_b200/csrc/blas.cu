@@ -114,7 +114,8 @@ constexpr int kMgsThreads = 256;
 __global__ void __launch_bounds__(kMgsThreads) k_mgs(const double* __restrict__ V, double* w,
                                                      long long n, long long ld, int j,
                                                      double* __restrict__ partial,
-                                                     double* __restrict__ h, int* flag) {
+                                                     double* __restrict__ h, int* flag,
+                                                     double* __restrict__ vnext) {
   cg::grid_group grid = cg::this_grid();
   __shared__ double red[kMgsThreads / 32];
   __shared__ double total_sh;
@@ -158,8 +159,11 @@ __global__ void __launch_bounds__(kMgsThreads) k_mgs(const double* __restrict__ 
     if (i <= j) {
       if (blockIdx.x == 0 && threadIdx.x == 0) h[i] = hi;
       for (long long k = t0; k < n; k += stride) w[k] = fma(-hi, Vi[k], w[k]);
-    } else if (blockIdx.x == 0 && threadIdx.x == 0) {
-      h[j + 1] = sqrt(hi);
+    } else {
+      const double hn = sqrt(hi);
+      if (blockIdx.x == 0 && threadIdx.x == 0) h[j + 1] = hn;
+      if (vnext)  // next basis vector v_{j+1} = w / h_{j+1,j} (own slice)
+        for (long long k = t0; k < n; k += stride) vnext[k] = w[k] / hn;
     }
   }
 }
@@ -173,7 +177,7 @@ constexpr int kClusterCtas = 8;
 template <int E>
 __global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(1024)
     k_mgs_cluster(const double* __restrict__ V, double* w, int n, long long ld, int j,
-                  double* __restrict__ h, int* flag) {
+                  double* __restrict__ h, int* flag, double* __restrict__ vnext) {
   cg::cluster_group cl = cg::this_cluster();
   __shared__ double red[32];
   __shared__ double slot[2];
@@ -220,14 +224,23 @@ __global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(1024)
         const int k = tid + e * T;
         if (k < n) wr[e] = fma(-tot, Vi[k], wr[e]);
       }
-    } else if (tid == 0) {
-      h[j + 1] = sqrt(tot);
+    } else {
+      const double hn = sqrt(tot);
+      if (tid == 0) h[j + 1] = hn;
+      if (vnext) {  // next basis vector v_{j+1} = w / h_{j+1,j}
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int k = tid + e * T;
+          if (k < n) wr[e] = wr[e] / hn;
+        }
+      }
     }
   }
+  double* out = vnext ? vnext : w;
 #pragma unroll
   for (int e = 0; e < E; ++e) {
     const int k = tid + e * T;
-    if (k < n) w[k] = wr[e];
+    if (k < n) out[k] = wr[e];
   }
   cl.sync();  // keep every CTA's shared memory alive until all remote reads are done
 }
@@ -282,20 +295,21 @@ int mgs_grid(long long n) {
 }
 
 cudaError_t launch_mgs(const double* V, double* w, long long n, long long ld, int j,
-                       double* partial, int nparts, double* h, int* flag, cudaStream_t s) {
+                       double* partial, int nparts, double* h, int* flag, double* vnext,
+                       cudaStream_t s) {
   constexpr long long T = kClusterCtas * 1024;
   if (!getenv("IMQ_MGS_COOP") && n <= 16 * T) {
     const int ni = (int)n;
     const dim3 g(kClusterCtas), b(1024);
-    if (n <= T) k_mgs_cluster<1><<<g, b, 0, s>>>(V, w, ni, ld, j, h, flag);
-    else if (n <= 2 * T) k_mgs_cluster<2><<<g, b, 0, s>>>(V, w, ni, ld, j, h, flag);
-    else if (n <= 4 * T) k_mgs_cluster<4><<<g, b, 0, s>>>(V, w, ni, ld, j, h, flag);
-    else if (n <= 8 * T) k_mgs_cluster<8><<<g, b, 0, s>>>(V, w, ni, ld, j, h, flag);
-    else k_mgs_cluster<16><<<g, b, 0, s>>>(V, w, ni, ld, j, h, flag);
+    if (n <= T) k_mgs_cluster<1><<<g, b, 0, s>>>(V, w, ni, ld, j, h, flag, vnext);
+    else if (n <= 2 * T) k_mgs_cluster<2><<<g, b, 0, s>>>(V, w, ni, ld, j, h, flag, vnext);
+    else if (n <= 4 * T) k_mgs_cluster<4><<<g, b, 0, s>>>(V, w, ni, ld, j, h, flag, vnext);
+    else if (n <= 8 * T) k_mgs_cluster<8><<<g, b, 0, s>>>(V, w, ni, ld, j, h, flag, vnext);
+    else k_mgs_cluster<16><<<g, b, 0, s>>>(V, w, ni, ld, j, h, flag, vnext);
     return cudaGetLastError();
   }
   void* args[] = {(void*)&V, (void*)&w, (void*)&n, (void*)&ld, (void*)&j,
-                  (void*)&partial, (void*)&h, (void*)&flag};
+                  (void*)&partial, (void*)&h, (void*)&flag, (void*)&vnext};
   return cudaLaunchCooperativeKernel((const void*)k_mgs, dim3(nparts), dim3(kMgsThreads), args, 0,
                                      s);
 }

@@ -125,9 +125,11 @@ void launch_sub(double* r, const double* f, const double* w, long long n, cudaSt
 void launch_nonfinite(const double* x, long long n, int* flag, cudaStream_t s);
 double measure_dfma_peak(int iters, float* ms_out);  // TFLOP/s of the DFMA pipe
 // Whole MGS of one Arnoldi step (h[0..j+1], non-finite flag) in one
-// cooperative launch; partial holds 2 * mgs_grid(n) doubles.
+// cooperative launch; partial holds 2 * mgs_grid(n) doubles.  With vnext set,
+// the kernel also writes v_{j+1} = w / h[j+1] there (w is then left stale).
 int mgs_grid(long long n);
 cudaError_t launch_mgs(const double* V, double* w, long long n, long long ld, int j,
-                       double* partial, int nparts, double* h, int* flag, cudaStream_t s);
+                       double* partial, int nparts, double* h, int* flag, double* vnext,
+                       cudaStream_t s);
 
 }  // namespace imqk

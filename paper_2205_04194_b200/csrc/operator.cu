@@ -107,6 +107,11 @@ void DeviceOperator::release() {
   dfree(d_mu_); dfree(d_coef_); dfree(d_u_); dfree(d_us_); dfree(d_far_); dfree(d_b_);
   dfree(d_part_);
   dfree(d_need_par_); dfree(d_local_leaves_); dfree(d_pack_a_); dfree(d_pack_c_); dfree(d_own_lvl_);
+  dfree(d_pair_items_); dfree(d_pair_part_); dfree(d_chunks_); dfree(d_contrib_off_);
+  dfree(d_contrib_); dfree(d_near_s_);
+  if (solve_pin_) cudaFreeHost(solve_pin_);
+  solve_pin_ = nullptr;
+  solve_pin_bytes_ = 0;
   if (stream_) cudaStreamDestroy(stream_);
   stream_ = nullptr;
   for (int k = 0; k < kAuxStreams; ++k) {
@@ -750,39 +755,101 @@ SolveResult DeviceOperator::solve_host(const double* f, double tol, int max_iter
   DeviceGuard g(device_);
   cudaStream_t s = stream_;
   SolveResult rep;
+  const auto t_enter = std::chrono::steady_clock::now();
   std::fill(c, c + n, 0.0);
 
   const int mcap = std::max(1, std::min(restart, max_iter));
   const int nparts = imqk::dot_parts(N_);
   const int mgs_parts = imqk::mgs_grid(N_);
+  const size_t hld = (size_t)mcap + 2;  // one Hessenberg column slot per Arnoldi step
+  // Arnoldi steps are enqueued kLookahead ahead of the host's Givens
+  // processing (the basis and the Hessenberg columns never depend on the
+  // rotations), so the GPU does not idle on the per-step host round trip.
+  // A step enqueued past convergence is discarded and never counted.
+  constexpr int kLookahead = 1, kRing = kLookahead + 2;
   double *d_f = nullptr, *d_x = nullptr, *d_r = nullptr, *d_w = nullptr, *d_V = nullptr;
-  double *d_h = nullptr, *d_part = nullptr, *d_mgs = nullptr;
-  int* d_flag = nullptr;
+  double *d_h = nullptr, *d_part = nullptr, *d_mgs = nullptr, *h_pin = nullptr;
+  int *d_flag = nullptr, *flag_pin = nullptr;
+  void* ws = nullptr;
+  cudaEvent_t ev[kRing] = {}, tev[kRing][3] = {};
+  const bool trace = getenv("IMQ_TRACE") != nullptr;
   auto cleanup = [&]() {
-    dfree(d_f); dfree(d_x); dfree(d_r); dfree(d_w); dfree(d_V); dfree(d_h); dfree(d_part);
-    dfree(d_mgs);
-    dfree(d_flag);
+    if (ws) cudaFreeAsync(ws, s);
+    ws = nullptr;
+    for (int i = 0; i < kRing; ++i) {
+      if (ev[i]) cudaEventDestroy(ev[i]);
+      for (auto& e : tev[i])
+        if (e) cudaEventDestroy(e);
+    }
   };
   try {
-    d_f = dalloc<double>(n, "gmres f");
-    d_x = dalloc<double>(n, "gmres x");
-    d_r = dalloc<double>(n, "gmres r");
-    d_w = dalloc<double>(n, "gmres w");
-    d_V = dalloc<double>(n * (size_t)(mcap + 1), "gmres basis");
-    d_h = dalloc<double>((size_t)mcap + 2, "gmres h");
-    d_part = dalloc<double>((size_t)nparts, "gmres partials");
-    d_mgs = dalloc<double>(2 * (size_t)mgs_parts, "mgs partials");
-    d_flag = dalloc<int>(1, "gmres flag");
+    {  // one stream-ordered workspace from the device pool (kept cached by the
+       // pool between solves, so repeated solves do not pay cudaMalloc)
+      size_t off = 0;
+      auto carve = [&](size_t bytes) {
+        const size_t o = off;
+        off += (bytes + 255) & ~(size_t)255;
+        return o;
+      };
+      const size_t o_f = carve(n * 8), o_x = carve(n * 8), o_r = carve(n * 8), o_w = carve(n * 8);
+      const size_t o_V = carve(n * (size_t)(mcap + 1) * 8), o_h = carve(hld * (size_t)(mcap + 1) * 8);
+      const size_t o_p = carve((size_t)nparts * 8), o_m = carve(2 * (size_t)mgs_parts * 8);
+      const size_t o_fl = carve((size_t)mcap * sizeof(int));
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, device_) == cudaSuccess) {
+        uint64_t thr = 0;
+        cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        if (thr < off) {
+          thr = off;
+          cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+      }
+      const cudaError_t e = cudaMallocAsync(&ws, off, s);
+      if (e == cudaErrorMemoryAllocation) {
+        cudaGetLastError();
+        ws = nullptr;
+        throw std::bad_alloc();
+      }
+      cuda_check(e, "gmres workspace");
+      char* b = static_cast<char*>(ws);
+      d_f = reinterpret_cast<double*>(b + o_f);
+      d_x = reinterpret_cast<double*>(b + o_x);
+      d_r = reinterpret_cast<double*>(b + o_r);
+      d_w = reinterpret_cast<double*>(b + o_w);
+      d_V = reinterpret_cast<double*>(b + o_V);
+      d_h = reinterpret_cast<double*>(b + o_h);
+      d_part = reinterpret_cast<double*>(b + o_p);
+      d_mgs = reinterpret_cast<double*>(b + o_m);
+      d_flag = reinterpret_cast<int*>(b + o_fl);
+    }
+    {  // pinned staging for the Hessenberg columns + flags, kept by the operator
+      const size_t bytes = hld * (size_t)(mcap + 1) * sizeof(double) + (size_t)mcap * sizeof(int);
+      if (bytes > solve_pin_bytes_) {  // (cudaMallocHost costs ms: round up generously)
+        if (solve_pin_) cudaFreeHost(solve_pin_);
+        solve_pin_ = nullptr;
+        solve_pin_bytes_ = 0;
+        const size_t cap = std::max(bytes, (size_t)130 * 129 * sizeof(double) + 128 * sizeof(int));
+        cuda_check(cudaMallocHost(&solve_pin_, cap), "pinned h");
+        solve_pin_bytes_ = cap;
+      }
+      h_pin = static_cast<double*>(solve_pin_);
+      flag_pin = reinterpret_cast<int*>(h_pin + hld * (size_t)(mcap + 1));
+    }
+    for (int i = 0; i < kRing; ++i) {
+      cuda_check(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming), "event");
+      if (trace)
+        for (auto& e : tev[i]) cuda_check(cudaEventCreate(&e), "event");
+    }
     // f in Morton order
     cuda_check(cudaMemcpyAsync(d_u_, f, n * sizeof(double), cudaMemcpyHostToDevice, s), "H2D f");
     imqk::launch_gather(d_u_, d_perm_, N_, d_f, s);
+    double* d_scalar = d_h + hld * (size_t)mcap;
     auto nrm2 = [&](const double* v) {
-      double out;
-      imqk::launch_dot(v, v, N_, d_part, nparts, d_h + mcap + 1, 1, s);
-      cuda_check(cudaMemcpyAsync(&out, d_h + mcap + 1, sizeof(double), cudaMemcpyDeviceToHost, s),
-                 "D2H norm");
+      imqk::launch_dot(v, v, N_, d_part, nparts, d_scalar, 1, s);
+      cuda_check(cudaMemcpyAsync(h_pin + hld * (size_t)mcap, d_scalar, sizeof(double),
+                                 cudaMemcpyDeviceToHost, s), "D2H norm");
       cuda_check(cudaStreamSynchronize(s), "norm");
-      return out;
+      return h_pin[hld * (size_t)mcap];
     };
     auto matvec = [&](const double* in, double* out) { apply_sorted_locked(in, out, nullptr, s); };
 
@@ -793,19 +860,33 @@ SolveResult DeviceOperator::solve_host(const double* f, double tol, int max_iter
       cleanup();
       return rep;
     }
-    const bool trace = getenv("IMQ_TRACE") != nullptr;
-    cudaEvent_t tev[3];
     double t_mv = 0, t_mgs = 0;
     const auto t_start = std::chrono::steady_clock::now();
-    if (trace)
-      for (auto& e : tev) cudaEventCreate(&e);
     cuda_check(cudaMemsetAsync(d_x, 0, n * sizeof(double), s), "memset x");
     cuda_check(cudaMemcpyAsync(d_r, d_f, n * sizeof(double), cudaMemcpyDeviceToDevice, s), "r=f");
     int total = 0;
     double rel = 1.0;
-    std::vector<std::vector<double>> hcol((size_t)mcap);
-    std::vector<double> cs((size_t)mcap), sn((size_t)mcap), gv((size_t)mcap + 1), y((size_t)mcap),
-        hbuf((size_t)mcap + 2);
+    std::vector<double> cs((size_t)mcap), sn((size_t)mcap), gv((size_t)mcap + 1), y((size_t)mcap);
+    // Arnoldi step jj on the device: w = A v_jj, MGS against v_0..v_jj,
+    // h column -> slot jj, v_{jj+1} = w / h_{jj+1,jj}; column + flag -> host.
+    auto enqueue = [&](int jj, int m) {
+      const int r = jj % kRing;
+      if (trace) cudaEventRecord(tev[r][0], s);
+      matvec(d_V + (size_t)jj * n, d_w);
+      if (trace) cudaEventRecord(tev[r][1], s);
+      cuda_check(cudaMemsetAsync(d_flag + jj, 0, sizeof(int), s), "flag");
+      cuda_check(imqk::launch_mgs(d_V, d_w, N_, (long long)n, jj, d_mgs, mgs_parts,
+                                  d_h + hld * (size_t)jj, d_flag + jj,
+                                  jj + 1 < m ? d_V + (size_t)(jj + 1) * n : nullptr, s),
+                 "MGS launch");
+      if (trace) cudaEventRecord(tev[r][2], s);
+      cuda_check(cudaMemcpyAsync(h_pin + hld * (size_t)jj, d_h + hld * (size_t)jj,
+                                 (size_t)(jj + 2) * sizeof(double), cudaMemcpyDeviceToHost, s),
+                 "D2H h");
+      cuda_check(cudaMemcpyAsync(flag_pin + jj, d_flag + jj, sizeof(int), cudaMemcpyDeviceToHost,
+                                 s), "D2H flag");
+      cuda_check(cudaEventRecord(ev[r], s), "step event");
+    };
     while (true) {
       if (total > 0) {
         matvec(d_x, d_w);
@@ -822,36 +903,22 @@ SolveResult DeviceOperator::solve_host(const double* f, double tol, int max_iter
       imqk::launch_div(d_V, d_r, N_, beta, s);
       std::fill(gv.begin(), gv.end(), 0.0);
       gv[0] = beta;
-      int k = 0;
+      int k = 0, enq = 0;
       for (int j = 0; j < m; ++j) {
-        double* Vj = d_V + (size_t)j * n;
-        if (trace) cudaEventRecord(tev[0], s);
-        matvec(Vj, d_w);
+        while (enq < m && enq <= j + kLookahead) enqueue(enq++, m);
+        cuda_check(cudaEventSynchronize(ev[j % kRing]), "arnoldi step");
         ++total;
-        if (trace) cudaEventRecord(tev[1], s);
-        cuda_check(cudaMemsetAsync(d_flag, 0, sizeof(int), s), "flag");
-        cuda_check(imqk::launch_mgs(d_V, d_w, N_, (long long)n, j, d_mgs, mgs_parts, d_h, d_flag,
-                                    s),
-                   "MGS launch");
-        if (trace) cudaEventRecord(tev[2], s);
-        int flag = 0;
-        cuda_check(cudaMemcpyAsync(hbuf.data(), d_h, (size_t)(j + 2) * sizeof(double),
-                                   cudaMemcpyDeviceToHost, s), "D2H h");
-        cuda_check(cudaMemcpyAsync(&flag, d_flag, sizeof(int), cudaMemcpyDeviceToHost, s),
-                   "D2H flag");
-        cuda_check(cudaStreamSynchronize(s), "arnoldi step");
         if (trace) {
           float a = 0, b2 = 0;
-          cudaEventElapsedTime(&a, tev[0], tev[1]);
-          cudaEventElapsedTime(&b2, tev[1], tev[2]);
+          cudaEventElapsedTime(&a, tev[j % kRing][0], tev[j % kRing][1]);
+          cudaEventElapsedTime(&b2, tev[j % kRing][1], tev[j % kRing][2]);
           t_mv += a;
           t_mgs += b2;
         }
-        if (flag)
+        if (flag_pin[j])
           throw std::runtime_error("iterative_solve: non-finite value at iteration " +
                                    std::to_string(total));
-        auto& h = hcol[(size_t)j];
-        h.assign(hbuf.begin(), hbuf.begin() + j + 2);
+        double* h = h_pin + hld * (size_t)j;  // rotated in place (host copy)
         const double hh = h[(size_t)j + 1];
         for (int i = 0; i < j; ++i) {
           const double t0 = cs[(size_t)i] * h[(size_t)i] + sn[(size_t)i] * h[(size_t)i + 1];
@@ -872,22 +939,21 @@ SolveResult DeviceOperator::solve_host(const double* f, double tol, int max_iter
         k = j + 1;
         const double rel_est = std::fabs(gv[(size_t)j + 1]) / bnorm;
         if (rel_est <= tol || hh == 0.0) break;
-        if (j + 1 < m) imqk::launch_div(d_V + (size_t)(j + 1) * n, d_w, N_, hh, s);
       }
       if (k == 0) break;
       for (int i = k - 1; i >= 0; --i) {
         double sacc = gv[(size_t)i];
-        for (int l = i + 1; l < k; ++l) sacc -= hcol[(size_t)l][(size_t)i] * y[(size_t)l];
-        y[(size_t)i] = sacc / hcol[(size_t)i][(size_t)i];
+        for (int l = i + 1; l < k; ++l) sacc -= h_pin[hld * (size_t)l + (size_t)i] * y[(size_t)l];
+        y[(size_t)i] = sacc / h_pin[hld * (size_t)i + (size_t)i];
       }
       for (int i = 0; i < k; ++i) imqk::launch_axpy(d_x, d_V + (size_t)i * n, N_, y[(size_t)i], s);
     }
     if (trace) {
       const double wall = std::chrono::duration<double, std::milli>(
                               std::chrono::steady_clock::now() - t_start).count();
-      fprintf(stderr, "[imq trace] gmres %d its: wall %.1f ms, matvec %.1f ms, mgs %.1f ms\n",
-              total, wall, t_mv, t_mgs);
-      for (auto& e : tev) cudaEventDestroy(e);
+      fprintf(stderr, "[imq trace] gmres %d its: wall %.1f ms, matvec %.1f ms, mgs %.1f ms, "
+              "setup %.1f ms\n", total, wall, t_mv, t_mgs,
+              std::chrono::duration<double, std::milli>(t_start - t_enter).count());
     }
     imqk::launch_scatter(d_x, d_perm_, N_, d_b_, s);
     cuda_check(cudaMemcpyAsync(c, d_b_, n * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H c");
@@ -902,6 +968,10 @@ SolveResult DeviceOperator::solve_host(const double* f, double tol, int max_iter
     throw;
   }
   cleanup();
+  if (getenv("IMQ_TRACE"))
+    fprintf(stderr, "[imq trace] gmres total %.1f ms\n",
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_enter)
+                .count());
   return rep;
 }
 

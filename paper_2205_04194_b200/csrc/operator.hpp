@@ -157,6 +157,8 @@ class DeviceOperator {
   int* d_contrib_off_ = nullptr;
   int* d_contrib_ = nullptr;
   double* d_near_s_ = nullptr;
+  void* solve_pin_ = nullptr;  // pinned GMRES staging (Hessenberg columns, flags)
+  size_t solve_pin_bytes_ = 0;
   std::vector<int> leaf_start_h_;
   std::vector<int> need_par_h_, local_leaves_h_;  // sharded moments (own + halo)
   int par_lo_ = 0, par_hi_ = 0;
