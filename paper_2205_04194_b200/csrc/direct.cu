@@ -333,18 +333,25 @@ __global__ void __launch_bounds__(kNearWarps * 32) k_p2p_pair(
 }
 
 // Block per chunk, thread per point: near = sum of the chunk's partial rows
-// (contrib entries = row offsets into part) in their fixed list order.
+// (contrib entries = row offsets into part) in their fixed list order; with
+// far_s set, out[perm[q]] = far_s[q] + near (the product's final combine).
 __global__ void __launch_bounds__(128) k_pair_reduce(const int2* __restrict__ chunks,
                                                      const int* __restrict__ contrib_off,
                                                      const int* __restrict__ contrib,
                                                      const double* __restrict__ part,
-                                                     double* __restrict__ near_s) {
+                                                     double* __restrict__ near_s,
+                                                     const double* __restrict__ far_s,
+                                                     const int* __restrict__ perm) {
   const int2 c = chunks[blockIdx.x];
   for (int k = threadIdx.x; k < c.y; k += blockDim.x) {
     double sum = 0.0;
     for (int e = contrib_off[blockIdx.x]; e < contrib_off[blockIdx.x + 1]; ++e)
       sum += part[(size_t)contrib[e] + k];
-    near_s[c.x + k] = sum;
+    const int q = c.x + k;
+    if (far_s)
+      near_s[perm ? perm[q] : q] = far_s[q] + sum;
+    else
+      near_s[q] = sum;
   }
 }
 
@@ -431,13 +438,18 @@ void launch_p2p_near_sym(const TreeParams& P, const int4* items, const int* grou
 }
 
 void launch_p2p_pair(const TreeParams& P, const int4* items, int n_items, const double* u_s,
-                     double* part, const int2* chunks, int n_chunks, const int* contrib_off,
-                     const int* contrib, double* near_s, cudaStream_t s) {
+                     double* part, cudaStream_t s) {
   if (n_items)
     k_p2p_pair<kPairR><<<(unsigned)((n_items + kNearWarps - 1) / kNearWarps), kNearWarps * 32, 0,
                          s>>>(P, items, n_items, u_s, part);
+}
+
+void launch_pair_reduce(const int2* chunks, int n_chunks, const int* contrib_off,
+                        const int* contrib, const double* part, double* out,
+                        const double* far_s, const int* perm, cudaStream_t s) {
   if (n_chunks)
-    k_pair_reduce<<<(unsigned)n_chunks, 128, 0, s>>>(chunks, contrib_off, contrib, part, near_s);
+    k_pair_reduce<<<(unsigned)n_chunks, 128, 0, s>>>(chunks, contrib_off, contrib, part, out,
+                                                     far_s, perm);
 }
 
 void launch_near_combine(int lo, int hi, int N, int nparts, const double* far_s,

@@ -104,12 +104,15 @@ int near_max_points_per_lane();
 void launch_p2p_near_sym(const TreeParams& P, const int4* items, const int* group_off, int begin,
                          int end, const double* u_s, double* part, cudaStream_t s);
 // Chunk-pair symmetric near field (large leaves): items {a_start, a_cnt,
-// b_start, b_cnt} (chunks <= 128 points), part = n_items x 256 doubles, then
-// near_s[point] = sum of its chunk's rows (contrib CSR over chunks).
+// b_start, b_cnt} (chunks <= 128 points), part = n_items x 256 doubles; the
+// reduction adds each chunk's rows (contrib CSR over chunks): out[q] = near
+// (far_s == nullptr) or out[perm ? perm[q] : q] = far_s[q] + near.
 constexpr int kNearChunk = 128;
 void launch_p2p_pair(const TreeParams& P, const int4* items, int n_items, const double* u_s,
-                     double* part, const int2* chunks, int n_chunks, const int* contrib_off,
-                     const int* contrib, double* near_s, cudaStream_t s);
+                     double* part, cudaStream_t s);
+void launch_pair_reduce(const int2* chunks, int n_chunks, const int* contrib_off,
+                        const int* contrib, const double* part, double* out,
+                        const double* far_s, const int* perm, cudaStream_t s);
 void launch_direct(const double* txy, long long nt, const double* sxy, const double* sval,
                    long long ns, double t2, double* out, cudaStream_t s);
 

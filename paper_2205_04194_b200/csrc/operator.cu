@@ -85,6 +85,9 @@ DeviceOperator::DeviceOperator(const double* xy_host, size_t n, double t, int M,
     cuda_check(cudaEventCreateWithFlags(&ev_join_[k], cudaEventDisableTiming), "event create");
   }
   cuda_check(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming), "event create");
+  cuda_check(cudaStreamCreateWithFlags(&near_stream_, cudaStreamNonBlocking), "stream create");
+  cuda_check(cudaEventCreateWithFlags(&ev_near_fork_, cudaEventDisableTiming), "event create");
+  cuda_check(cudaEventCreateWithFlags(&ev_near_done_, cudaEventDisableTiming), "event create");
   pending_levels_ = levels;
   try {
     build(xy_host);
@@ -122,6 +125,11 @@ void DeviceOperator::release() {
   }
   if (ev_fork_) cudaEventDestroy(ev_fork_);
   ev_fork_ = nullptr;
+  if (near_stream_) cudaStreamDestroy(near_stream_);
+  if (ev_near_fork_) cudaEventDestroy(ev_near_fork_);
+  if (ev_near_done_) cudaEventDestroy(ev_near_done_);
+  near_stream_ = nullptr;
+  ev_near_fork_ = ev_near_done_ = nullptr;
 }
 
 void DeviceOperator::build(const double* xy_host) {
@@ -612,9 +620,11 @@ void DeviceOperator::far_near(const double* d_us, double* d_out, const int* perm
   if (sym && near_sym_)  // symmetric near field first; the far epilogue combines and scatters
     imqk::launch_p2p_near_sym(P_, d_near_items_, near_group_off_.data(), near_begin, near_end,
                               d_us, d_part_, s);
-  if (sym && near_pair_)
-    imqk::launch_p2p_pair(P_, d_pair_items_, n_pair_items_, d_us, d_pair_part_, d_chunks_,
-                          n_chunks_, d_contrib_off_, d_contrib_, d_near_s_, s);
+  if (sym && near_pair_) {
+    imqk::launch_p2p_pair(P_, d_pair_items_, n_pair_items_, d_us, d_pair_part_, s);
+    imqk::launch_pair_reduce(d_chunks_, n_chunks_, d_contrib_off_, d_contrib_, d_pair_part_,
+                             d_near_s_, nullptr, nullptr, s);
+  }
   if (far_end > far_begin) {
     // fork: group launches on s + the aux streams, joined back into s
     cudaStream_t ss[1 + kAuxStreams] = {s};
@@ -643,6 +653,20 @@ void DeviceOperator::far_near(const double* d_us, double* d_out, const int* perm
 
 void DeviceOperator::apply_sorted_locked(const double* d_us, double* d_out, const int* perm,
                                          cudaStream_t s) {
+  if (near_pair_ && n_far_ > 0) {
+    // chunk-pair near field on its own stream, concurrent with the moments
+    // and the far field; the pair reduction adds far + near and unsorts
+    cuda_check(cudaEventRecord(ev_near_fork_, s), "near fork");
+    cuda_check(cudaStreamWaitEvent(near_stream_, ev_near_fork_, 0), "near fork wait");
+    imqk::launch_p2p_pair(P_, d_pair_items_, n_pair_items_, d_us, d_pair_part_, near_stream_);
+    cuda_check(cudaEventRecord(ev_near_done_, near_stream_), "near done");
+    moments(d_us, s);
+    far_near(d_us, d_out, perm, s, 0, n_far_, 0, 0);  // far field only -> d_far_
+    cuda_check(cudaStreamWaitEvent(s, ev_near_done_, 0), "near join");
+    imqk::launch_pair_reduce(d_chunks_, n_chunks_, d_contrib_off_, d_contrib_, d_pair_part_, d_out,
+                             d_far_, perm, s);
+    return;
+  }
   moments(d_us, s);
   far_near(d_us, d_out, perm, s, 0, n_far_, 0, n_near_);
 }

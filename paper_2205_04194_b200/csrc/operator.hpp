@@ -114,6 +114,8 @@ class DeviceOperator {
   static constexpr int kAuxStreams = 3;  // far-field work groups run concurrently
   cudaStream_t aux_[kAuxStreams] = {};
   cudaEvent_t ev_fork_ = nullptr;
+  cudaStream_t near_stream_ = nullptr;  // chunk-pair near field, concurrent with far
+  cudaEvent_t ev_near_fork_ = nullptr, ev_near_done_ = nullptr;
   cudaEvent_t ev_join_[kAuxStreams] = {};
   int N_ = 0, M_ = 0, K_ = 0, Ke_ = 0, L_ = 0, pending_levels_ = 0;
   double t_ = 0.0;
