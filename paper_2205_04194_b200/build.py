@@ -22,6 +22,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-ffp-contract=off,-fvisibility=hidden",
           "-I", CSRC, "-I", os.path.join(ROOT, "include")]
+COMMON += os.environ.get("IMQ_NVCC_EXTRA", "").split()  # development experiments only
 
 
 def sources():

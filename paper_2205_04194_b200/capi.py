@@ -12,7 +12,7 @@ import os
 import re
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libimqfast.so")
+LIB_PATH = os.environ.get("IMQ_LIB_PATH") or os.path.join(HERE, "libimqfast.so")  # override: experiments
 HEADER = os.path.join(os.path.dirname(HERE), "include", "imqfast.h")
 
 IMQ_OK = 0

@@ -85,6 +85,8 @@ DeviceOperator::DeviceOperator(const double* xy_host, size_t n, double t, int M,
     cuda_check(cudaEventCreateWithFlags(&ev_join_[k], cudaEventDisableTiming), "event create");
   }
   cuda_check(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming), "event create");
+  if (const char* e = getenv("IMQ_FAR_STREAMS"))  // tuning: far groups on 1..4 streams
+    far_streams_ = std::max(1, std::min(1 + kAuxStreams, atoi(e)));
   cuda_check(cudaStreamCreateWithFlags(&near_stream_, cudaStreamNonBlocking), "stream create");
   cuda_check(cudaEventCreateWithFlags(&ev_near_fork_, cudaEventDisableTiming), "event create");
   cuda_check(cudaEventCreateWithFlags(&ev_near_done_, cudaEventDisableTiming), "event create");
@@ -634,7 +636,7 @@ void DeviceOperator::far_near(const double* d_us, double* d_out, const int* perm
       cuda_check(cudaStreamWaitEvent(aux_[k], ev_fork_, 0), "fork wait");
     }
     imqk::launch_m2p_far(P_, d_far_items_, far_group_off_.data(), far_begin, far_end, d_coef_,
-                         d_far_, ss, 1 + kAuxStreams,
+                         d_far_, ss, far_streams_,
                          sym ? (near_pair_ ? d_near_s_ : d_part_) : nullptr, near_pair_ ? 1 : 5,
                          d_out, perm);
     for (int k = 0; k < kAuxStreams; ++k) {

@@ -113,6 +113,7 @@ class DeviceOperator {
   cudaStream_t stream_ = nullptr;
   static constexpr int kAuxStreams = 3;  // far-field work groups run concurrently
   cudaStream_t aux_[kAuxStreams] = {};
+  int far_streams_ = 1 + kAuxStreams;
   cudaEvent_t ev_fork_ = nullptr;
   cudaStream_t near_stream_ = nullptr;  // chunk-pair near field, concurrent with far
   cudaEvent_t ev_near_fork_ = nullptr, ev_near_done_ = nullptr;
