@@ -145,6 +145,8 @@ typedef struct {
   double far_pairs;  /* exact #(target, non-empty far source block) pairs */
   double near_pairs; /* exact #(target, source point) near pairs */
   long long far_items, near_items;
+  int near_mode; /* near-field evaluation: 0 = per target (split sources, sharded ranges),
+                    1 = symmetric per leaf (leaves <= 128), 2 = symmetric chunk pairs */
 } imq_ext_stats;
 IMQ_API int imq_ext_operator_stats(const imq_operator* op, imq_ext_stats* out);
 

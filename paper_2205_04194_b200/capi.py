@@ -40,7 +40,8 @@ class imq_ext_stats(C.Structure):
     _fields_ = [("n", C.c_int), ("m", C.c_int), ("levels", C.c_int), ("device", C.c_int),
                 ("origin_x", C.c_double), ("origin_y", C.c_double), ("side", C.c_double),
                 ("far_pairs", C.c_double), ("near_pairs", C.c_double),
-                ("far_items", C.c_longlong), ("near_items", C.c_longlong)]
+                ("far_items", C.c_longlong), ("near_items", C.c_longlong),
+                ("near_mode", C.c_int)]
 
 
 VERIFY_CB = C.CFUNCTYPE(None, C.c_char_p, C.c_int, C.c_double, C.c_void_p)

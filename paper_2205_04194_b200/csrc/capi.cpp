@@ -510,6 +510,7 @@ int imq_ext_operator_stats(const imq_operator* op, imq_ext_stats* out) {
     out->near_pairs = c.near_pairs;
     out->far_items = c.far_items;
     out->near_items = c.near_items;
+    out->near_mode = c.near_mode;
     return IMQ_OK;
   });
 }

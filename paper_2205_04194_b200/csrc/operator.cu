@@ -719,7 +719,12 @@ void DeviceOperator::copy_leaf_start(std::vector<int>& out) const {
 // Exact far / near pair counts of this tree (the flop model's P_far, P_near).
 PairCounts DeviceOperator::pair_counts() {
   std::lock_guard<std::mutex> lk(mtx_);
-  if (have_counts_) return counts_;
+  if (have_counts_) {  // pair counts are fixed; the work lists follow restrict_targets
+    counts_.far_items = n_far_;
+    counts_.near_items = n_near_;
+    counts_.near_mode = near_pair_ ? 2 : (near_sym_ ? 1 : 0);
+    return counts_;
+  }
   std::vector<int> ls;
   copy_leaf_start(ls);
   const int L = L_;
@@ -756,9 +761,10 @@ PairCounts DeviceOperator::pair_counts() {
   }
   counts_.far_pairs = far;
   counts_.near_pairs = near;
+  have_counts_ = true;
   counts_.far_items = n_far_;
   counts_.near_items = n_near_;
-  have_counts_ = true;
+  counts_.near_mode = near_pair_ ? 2 : (near_sym_ ? 1 : 0);
   return counts_;
 }
 

@@ -34,6 +34,7 @@ struct SolveResult {
 struct PairCounts {
   double far_pairs = 0, near_pairs = 0;  // exact, from the built tree
   int64_t far_items = 0, near_items = 0;
+  int near_mode = 0;  // 0 plain (split sources), 1 symmetric per leaf, 2 chunk pairs
 };
 
 std::vector<int> shard_bounds(const std::vector<int>& leaf_start, int L, int world);

@@ -330,3 +330,39 @@ def test_concurrent_apply_from_threads(imq, golden):
         t.join()
     for k in range(8):
         assert np.array_equal(got[k], want[k])
+
+
+@pytest.mark.parametrize("case", ["sym_leaves", "pair_large_leaves", "pair_ragged",
+                                  "pair_small_problem"])
+def test_near_field_modes_vs_oracle(imq, oracle, case):
+    """Each near-field evaluation strategy (imq_ext_stats.near_mode) against
+    the oracle: the symmetric per-leaf kernel (leaves <= 128 and enough leaves
+    to fill the GPU), the chunk-pair kernel for 1,024-point leaves, for ragged
+    cluster leaves with partial chunks, and for a problem too small for the
+    per-leaf kernel."""
+    rng = np.random.default_rng(11)
+    rows = None
+    if case == "sym_leaves":
+        xy, t, m, L, mode = rng.random(2 * (1 << 21)), 0.05, 8, 7, 1
+        rows = np.unique(rng.integers(0, 1 << 21, 512))
+    elif case == "pair_large_leaves":
+        xy, t, m, L, mode = rng.random(2 * 16384), 0.05, 12, 1, 2
+    elif case == "pair_ragged":
+        c = rng.random((6, 2))
+        k = rng.integers(0, 6, 12000)
+        xy = np.clip(c[k] + 0.03 * rng.standard_normal((12000, 2)), 0, 1).ravel()
+        t, m, L, mode = 0.02, 10, 2, 2
+    else:
+        xy, t, m, L, mode = rng.random(2 * 777), 0.3, 8, 1, 2
+    n = xy.size // 2
+    op = imq.FastOperator(xy, t, m, L)
+    assert op.stats()["near_mode"] == mode
+    u = rng.uniform(-1, 1, n)
+    b = op.apply(u)
+    if rows is None:
+        ref = oracle.fast_matvec(xy, t, m, L, u)
+        assert rel_err_inf(b, ref) <= TOL, case
+    else:
+        ref = oracle.fast_matvec_rows(xy, t, m, L, u, rows)
+        assert float(np.max(np.abs(b[rows] - ref)) / np.max(np.abs(ref))) <= TOL, case
+    assert np.array_equal(op.apply(u), b)  # deterministic reductions
