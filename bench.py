@@ -358,10 +358,16 @@ def b200_arm(args):
     if rank == 0:
         fi, ni = op.items("far"), op.items("near")
         groups = lambda it: len(set(((it[:, 2] + 31) // 32).tolist())) if len(it) else 0
-        split = int(len(ni) and (ni[:, 3] != 3).any())
-        # ours per step: gather, leaf P2M, L transforms, far groups, near groups
-        # (+ combine when the near sources are split); the L-1 M2M DGEMMs are cuBLAS
-        launches_per_step = 1 + 1 + L + groups(fi) + groups(ni) + split
+        mode = op.stats()["near_mode"]
+        if mode == 1:    # symmetric per-leaf kernels, combined in the far epilogue
+            near_launches = groups(ni)
+        elif mode == 2:  # chunk-pair kernel + its reduction
+            near_launches = 2
+        else:            # per-target kernels (+ combine when the sources are split)
+            near_launches = groups(ni) + int(len(ni) > 0 and (ni[:, 3] != 15).any())
+        # ours per step: gather, leaf P2M, L transforms, far groups, near kernels;
+        # the L-1 M2M DGEMMs are cuBLAS (not counted)
+        launches_per_step = 1 + 1 + L + groups(fi) + near_launches
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,

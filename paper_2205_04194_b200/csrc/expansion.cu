@@ -431,7 +431,7 @@ constexpr int kFarMaxR = 8;    // a far work item holds <= 32 * kFarMaxR targets
 // the children of the parent's 3x3 neighbourhood that some present leaf needs.
 // Entries are (level << 28 | block) in the reference's list order.
 __device__ int build_far_list(const TreeParams& P, uint32_t par, int s, int cnt, uint32_t* list,
-                              int lane) {
+                              int lane, int lmin, int lmax) {
   const int L = P.L;
   const int e = s + cnt;
   bool present = false;
@@ -441,7 +441,7 @@ __device__ int build_far_list(const TreeParams& P, uint32_t par, int s, int cnt,
   }
   const uint32_t pmask = __ballot_sync(0xffffffffu, present) & 0xfu;
   int n = 0;
-  for (int l = 1; l <= L; ++l) {
+  for (int l = lmin; l <= lmax; ++l) {
     const int grid = 1 << (l + 1);
     int ai = 0, aj = 0, wi, wj, lo_i, lo_j;
     if (l < L) demorton(par >> (2 * (L - 1 - l)), ai, aj);
@@ -710,16 +710,21 @@ __device__ __forceinline__ void load_targets(const TreeParams& P, int s, int cnt
 // (cp.async.bulk + mbarrier complete_tx), lane 0 producing, the warp consuming.
 // Epilogue: far_s[q] = far field (near_part == nullptr), or, when the
 // symmetric near field already ran, out[perm[q]] = far + sum of its 5 slots.
+// Level range: items evaluate the source blocks of levels lmin..lmax; a
+// fine pass (levels L-1..L) adds the coarse pass's far_add[q] first.
 struct FarOut {
   double* far_s;
   const double* near_part;  // [nslots][N] or nullptr
   int nslots;
   double* out;
   const int* perm;
+  const double* far_add;  // or nullptr
+  int lmin, lmax;
 };
 
 __device__ __forceinline__ void far_store(const TreeParams& P, const FarOut& O, int q,
                                           double acc) {
+  if (O.far_add) acc = O.far_add[q] + acc;
   if (!O.near_part) {
     O.far_s[q] = acc;
     return;
@@ -760,7 +765,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_m2p_far(const TreeParams P
   const int4 item = items[it];
   const uint32_t par = (uint32_t)item.x;
   const int s0 = item.y, cnt = item.z;
-  const int n = build_far_list(P, par, s0, cnt, list, lane);
+  const int n = build_far_list(P, par, s0, cnt, list, lane, O.lmin, O.lmax);
   Targets<R> T;
   load_targets<R>(P, s0, cnt, lane, T);
   const int L = P.L;
@@ -837,7 +842,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_m2p_far_generic(const TreeParams
   const uint32_t par = (uint32_t)item.x;
   const int s0 = item.y, cnt = item.z;
   uint32_t* list = lists[warp];
-  const int n = build_far_list(P, par, s0, cnt, list, lane);
+  const int n = build_far_list(P, par, s0, cnt, list, lane, O.lmin, O.lmax);
   for (int p0 = lane; p0 < cnt; p0 += 32) {
     const int p = s0 + p0;
     const double x = P.xs[p], y = P.ys[p];
@@ -1014,9 +1019,11 @@ void launch_scatter_rows(const double* src, const int* idx, int n, int width, do
 void launch_m2p_far(const TreeParams& P, const int4* items, const int* group_off, int begin,
                     int end, const double2* coef, double* far_s_ptr, const cudaStream_t* streams,
                     int nstreams, const double* near_part, int nslots, double* out,
-                    const int* perm) {
+                    const int* perm, const double* far_add, int lmin, int lmax) {
   if (end <= begin) return;
-  const FarOut far_s{far_s_ptr, near_part, nslots, out, perm};
+  if (lmin < 1) lmin = 1;
+  if (lmax < 1 || lmax > P.L) lmax = P.L;
+  const FarOut far_s{far_s_ptr, near_part, nslots, out, perm, far_add, lmin, lmax};
   cudaStream_t s = streams[0];
   int launched = 0;
   if (!m2p_specialised(P.M)) {

@@ -86,7 +86,8 @@ void launch_scatter_rows(const double* src, const int* idx, int n, int width, do
 void launch_m2p_far(const TreeParams& P, const int4* items, const int* group_off, int begin,
                     int end, const double2* coef, double* far_s, const cudaStream_t* streams,
                     int nstreams, const double* near_part = nullptr, int nslots = 0,
-                    double* out = nullptr, const int* perm = nullptr);
+                    double* out = nullptr, const int* perm = nullptr,
+                    const double* far_add = nullptr, int lmin = 1, int lmax = 0);
 bool m2p_specialised(int M);
 int far_max_points_per_lane();
 

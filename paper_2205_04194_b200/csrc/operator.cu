@@ -113,7 +113,7 @@ void DeviceOperator::release() {
   dfree(d_part_);
   dfree(d_need_par_); dfree(d_local_leaves_); dfree(d_pack_a_); dfree(d_pack_c_); dfree(d_own_lvl_);
   dfree(d_pair_items_); dfree(d_pair_part_); dfree(d_chunks_); dfree(d_contrib_off_);
-  dfree(d_contrib_); dfree(d_near_s_);
+  dfree(d_contrib_); dfree(d_near_s_); dfree(d_farc_);
   if (solve_pin_) cudaFreeHost(solve_pin_);
   solve_pin_ = nullptr;
   solve_pin_bytes_ = 0;
@@ -294,19 +294,41 @@ void DeviceOperator::build_items(int p_lo, int p_hi) {
   const double nt = (double)(p_hi - p_lo);
   const int rfit = (int)std::max(1.0, std::floor(nt / (32.0 * kWarpsWanted)));
   const int rmax = imqk::m2p_specialised(M_) ? std::min(rfit, imqk::far_max_points_per_lane()) : 2;
-  std::vector<std::vector<int4>> groups((size_t)rmax);
-  for (long long p = 0; p < n_par; ++p) {
-    const int a = std::max(p_lo, ls[(size_t)(4 * p)]), b = std::min(p_hi, ls[(size_t)(4 * p + 4)]);
-    if (b <= a) continue;
-    // balanced chunks: fewest items of <= 32 rmax targets, sizes multiple of 32
-    const int nchunk = (b - a + 32 * rmax - 1) / (32 * rmax);
-    const int size = 32 * ((b - a + 32 * nchunk - 1) / (32 * nchunk));
-    for (int c = a; c < b; c += size) {
-      const int cnt = std::min(size, b - c);
-      groups[(size_t)((cnt + 31) / 32 - 1)].push_back(make_int4((int)p, c, cnt, 0));
+  // Level split (L >= 4): the lists of levels 1..L-2 are shared by every
+  // target of a level-(L-2) block, so those levels run as a separate "coarse"
+  // pass whose items span whole grandparents (fewer idle lanes), and the
+  // per-parent "fine" pass covers levels L-1..L and adds the coarse partial.
+  far_split_ = L_ >= 4 && !getenv("IMQ_FAR_NOSPLIT");
+  auto chunked = [&](long long blocks, int span, std::vector<std::vector<int4>>& g) {
+    for (long long p = 0; p < blocks; ++p) {
+      const int a = std::max(p_lo, ls[(size_t)(span * p)]);
+      const int b = std::min(p_hi, ls[(size_t)(span * p + span)]);
+      if (b <= a) continue;
+      // balanced chunks: fewest items of <= 32 rmax targets, sizes multiple of 32
+      const int nchunk = (b - a + 32 * rmax - 1) / (32 * rmax);
+      const int size = 32 * ((b - a + 32 * nchunk - 1) / (32 * nchunk));
+      for (int c = a; c < b; c += size) {
+        const int cnt = std::min(size, b - c);
+        // item.x: a level-(L-1) block containing the targets' ancestors
+        g[(size_t)((cnt + 31) / 32 - 1)].push_back(make_int4((int)(p * (span / 4)), c, cnt, 0));
+      }
     }
-  }
+  };
+  std::vector<std::vector<int4>> groups((size_t)rmax);
+  chunked(n_par, 4, groups);
   grouped(groups, far_items_h_, far_group_off_);
+  n_far_fine_ = (int)far_items_h_.size();
+  far_cgroup_off_.assign(16, n_far_fine_);
+  if (far_split_) {
+    std::vector<std::vector<int4>> cg((size_t)rmax);
+    chunked(n_par / 4, 16, cg);
+    std::vector<int4> citems;
+    grouped(cg, citems, far_cgroup_off_);
+    for (int& o : far_cgroup_off_) o += n_far_fine_;
+    far_items_h_.insert(far_items_h_.end(), citems.begin(), citems.end());
+    dfree(d_farc_);
+    d_farc_ = dalloc<double>((size_t)N_, "coarse far");
+  }
   // near items: one leaf each; R from the mean leaf occupancy (a typical leaf
   // in one item), then the smallest source split (1, 3 or 9 ways) that gives
   // the GPU enough warps
@@ -627,22 +649,35 @@ void DeviceOperator::far_near(const double* d_us, double* d_out, const int* perm
     imqk::launch_pair_reduce(d_chunks_, n_chunks_, d_contrib_off_, d_contrib_, d_pair_part_,
                              d_near_s_, nullptr, nullptr, s);
   }
-  if (far_end > far_begin) {
-    // fork: group launches on s + the aux streams, joined back into s
+  // fork: group launches on s + the aux streams, joined back into s
+  auto far_pass = [&](int b, int e, const int* goff, const double* near_part, int nslots,
+                      double* out, const int* pm, double* far_s, const double* far_add, int lmin,
+                      int lmax) {
+    if (e <= b) return;
     cudaStream_t ss[1 + kAuxStreams] = {s};
     cuda_check(cudaEventRecord(ev_fork_, s), "fork");
     for (int k = 0; k < kAuxStreams; ++k) {
       ss[k + 1] = aux_[k];
       cuda_check(cudaStreamWaitEvent(aux_[k], ev_fork_, 0), "fork wait");
     }
-    imqk::launch_m2p_far(P_, d_far_items_, far_group_off_.data(), far_begin, far_end, d_coef_,
-                         d_far_, ss, far_streams_,
-                         sym ? (near_pair_ ? d_near_s_ : d_part_) : nullptr, near_pair_ ? 1 : 5,
-                         d_out, perm);
+    imqk::launch_m2p_far(P_, d_far_items_, goff, b, e, d_coef_, far_s, ss, far_streams_,
+                         near_part, nslots, out, pm, far_add, lmin, lmax);
     for (int k = 0; k < kAuxStreams; ++k) {
       cuda_check(cudaEventRecord(ev_join_[k], aux_[k]), "join");
       cuda_check(cudaStreamWaitEvent(s, ev_join_[k], 0), "join wait");
     }
+  };
+  const double* near_part = sym ? (near_pair_ ? d_near_s_ : d_part_) : nullptr;
+  const int nslots = near_pair_ ? 1 : 5;
+  if (far_split_) {
+    // coarse pass (levels 1..L-2) into d_farc_, then the fine pass (L-1..L)
+    far_pass(std::max(far_begin, n_far_fine_), far_end, far_cgroup_off_.data(), nullptr, 0,
+             nullptr, nullptr, d_farc_, nullptr, 1, L_ - 2);
+    far_pass(far_begin, std::min(far_end, n_far_fine_), far_group_off_.data(), near_part, nslots,
+             d_out, perm, d_far_, d_farc_, L_ - 1, L_);
+  } else {
+    far_pass(far_begin, far_end, far_group_off_.data(), near_part, nslots, d_out, perm, d_far_,
+             nullptr, 1, L_);
   }
   if (near_sym_ || near_pair_) return;
   if (near_end > near_begin)

@@ -154,6 +154,10 @@ class DeviceOperator {
   int near_split_ = 1;
   bool near_sym_ = false;  // symmetric near-field evaluation (small leaves)
   bool near_pair_ = false; // chunk-pair symmetric near field (large leaves)
+  bool far_split_ = false; // far field in a coarse (levels 1..L-2) and a fine pass
+  int n_far_fine_ = 0;     // far items [0, n_far_fine_) fine, the rest coarse
+  std::vector<int> far_cgroup_off_;
+  double* d_farc_ = nullptr;  // coarse-pass far partial (sorted order)
   int n_pair_items_ = 0, n_chunks_ = 0;
   int4* d_pair_items_ = nullptr;
   double* d_pair_part_ = nullptr;
