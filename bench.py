@@ -357,7 +357,11 @@ def b200_arm(args):
 
     if rank == 0:
         fi, ni = op.items("far"), op.items("near")
-        groups = lambda it: len(set(((it[:, 2] + 31) // 32).tolist())) if len(it) else 0
+        def groups(it):  # launches = runs of equal points-per-lane (one per R group and pass)
+            if not len(it):
+                return 0
+            r = (it[:, 2] + 31) // 32
+            return 1 + int(np.count_nonzero(r[1:] != r[:-1]))
         mode = op.stats()["near_mode"]
         if mode == 1:    # symmetric per-leaf kernels, combined in the far epilogue
             near_launches = groups(ni)
