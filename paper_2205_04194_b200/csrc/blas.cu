@@ -201,19 +201,22 @@ __global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(1024)
       const int k = tid + e * T;
       if (k < n) acc = fma(wr[e], i <= j ? Vi[k] : wr[e], acc);
     }
+    // fixed-order tree reductions (warp, CTA, cluster): every CTA forms the
+    // same total; the serial per-thread sums they replace cost ~1 us per
+    // projection
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
     __syncthreads();
-    if (threadIdx.x == 0) {
-      double t = 0.0;
-      for (int k = 0; k < 32; ++k) t += red[k];
-      slot[i & 1] = t;
+    if (threadIdx.x < 32) {
+      double t = red[threadIdx.x];
+      for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+      if (threadIdx.x == 0) slot[i & 1] = t;
     }
     cl.sync();
-    if (threadIdx.x == 0) {
-      double t = 0.0;
-      for (int r = 0; r < kClusterCtas; ++r) t += *cl.map_shared_rank(&slot[i & 1], r);
-      bcast = t;
+    if (threadIdx.x < 32) {
+      double t = threadIdx.x < kClusterCtas ? *cl.map_shared_rank(&slot[i & 1], threadIdx.x) : 0.0;
+      for (int o = kClusterCtas / 2; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+      if (threadIdx.x == 0) bcast = t;
     }
     __syncthreads();
     const double tot = bcast;
