@@ -85,6 +85,7 @@ DeviceOperator::DeviceOperator(const double* xy_host, size_t n, double t, int M,
     cuda_check(cudaEventCreateWithFlags(&ev_join_[k], cudaEventDisableTiming), "event create");
   }
   cuda_check(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming), "event create");
+  cuda_check(cudaEventCreateWithFlags(&ev_last_, cudaEventDisableTiming), "event create");
   if (const char* e = getenv("IMQ_FAR_STREAMS"))  // tuning: far groups on 1..4 streams
     far_streams_ = std::max(1, std::min(1 + kAuxStreams, atoi(e)));
   cuda_check(cudaStreamCreateWithFlags(&near_stream_, cudaStreamNonBlocking), "stream create");
@@ -104,6 +105,7 @@ DeviceOperator::~DeviceOperator() { release(); }
 void DeviceOperator::release() {
   DeviceGuard g(device_);
   if (stream_) cudaStreamSynchronize(stream_);
+  if (ev_last_) cudaEventSynchronize(ev_last_);
   dfree(d_xs_); dfree(d_ys_); dfree(d_leaf_); dfree(d_perm_); dfree(d_leaf_start_);
   dfree(d_far_items_); dfree(d_near_items_);
   dfree(d_tr_off_); dfree(d_tr_idx_); dfree(d_tr_val_); dfree(d_binom_); dfree(d_m2m_);
@@ -127,6 +129,8 @@ void DeviceOperator::release() {
   }
   if (ev_fork_) cudaEventDestroy(ev_fork_);
   ev_fork_ = nullptr;
+  if (ev_last_) cudaEventDestroy(ev_last_);
+  ev_last_ = nullptr;
   if (near_stream_) cudaStreamDestroy(near_stream_);
   if (ev_near_fork_) cudaEventDestroy(ev_near_fork_);
   if (ev_near_done_) cudaEventDestroy(ev_near_done_);
@@ -469,6 +473,7 @@ void DeviceOperator::restrict_targets(int p_lo, int p_hi) {
   if (p_lo < 0 || p_hi > N_ || p_lo > p_hi)
     throw std::invalid_argument("restrict_targets: bad sorted-position range");
   cuda_check(cudaStreamSynchronize(stream_), "restrict");
+  cuda_check(cudaEventSynchronize(ev_last_), "restrict");  // work on other streams
   build_items(p_lo, p_hi);
   setup_sharded_moments(p_lo, p_hi);
 }
@@ -576,6 +581,7 @@ void DeviceOperator::setup_sharded_moments(int p_lo, int p_hi) {
 void DeviceOperator::moments_local(const double* d_us, cudaStream_t s) {
   std::lock_guard<std::mutex> lk(mtx_);
   DeviceGuard g(device_);
+  Ordered order(*this, s);
   if (!sharded()) {  // unsharded: the full moments, nothing to reduce
     moments(d_us, s);
     return;
@@ -624,6 +630,7 @@ void DeviceOperator::coarse_moments(double2** ptr, size_t* count) const {
 void DeviceOperator::moments_finish(cudaStream_t s) {
   std::lock_guard<std::mutex> lk(mtx_);
   DeviceGuard g(device_);
+  Ordered order(*this, s);
   if (!sharded()) return;  // moments_local already transformed everything
   imqk::launch_transform(P_, d_mu_, d_coef_, T_, s, 1, L_ - 2);
   imqk::launch_transform(P_, d_mu_, d_coef_, T_, s, L_ - 1, L_ - 1, d_need_par_,
@@ -711,6 +718,7 @@ void DeviceOperator::apply_sorted_locked(const double* d_us, double* d_out, cons
 void DeviceOperator::apply_sorted(const double* d_us, double* d_bs, cudaStream_t stream) {
   std::lock_guard<std::mutex> lk(mtx_);
   DeviceGuard g(device_);
+  Ordered o(*this, stream);
   apply_sorted_locked(d_us, d_bs, nullptr, stream);
   cuda_check(cudaGetLastError(), "apply_sorted launch");
 }
@@ -718,6 +726,7 @@ void DeviceOperator::apply_sorted(const double* d_us, double* d_bs, cudaStream_t
 void DeviceOperator::apply_device(const double* d_u, double* d_b, cudaStream_t stream) {
   std::lock_guard<std::mutex> lk(mtx_);
   DeviceGuard g(device_);
+  Ordered o(*this, stream);
   imqk::launch_gather(d_u, d_perm_, N_, d_us_, stream);
   apply_sorted_locked(d_us_, d_b, d_perm_, stream);
   cuda_check(cudaGetLastError(), "apply_device launch");
@@ -727,6 +736,7 @@ void DeviceOperator::apply_host(const double* u, double* b) {
   std::lock_guard<std::mutex> lk(mtx_);
   DeviceGuard g(device_);
   cudaStream_t s = stream_;
+  Ordered o(*this, s);
   cuda_check(cudaMemcpyAsync(d_u_, u, (size_t)N_ * sizeof(double), cudaMemcpyHostToDevice, s),
              "H2D u");
   imqk::launch_gather(d_u_, d_perm_, N_, d_us_, s);
@@ -821,6 +831,7 @@ SolveResult DeviceOperator::solve_host(const double* f, double tol, int max_iter
   std::lock_guard<std::mutex> lk(mtx_);
   DeviceGuard g(device_);
   cudaStream_t s = stream_;
+  Ordered order(*this, s);
   SolveResult rep;
   const auto t_enter = std::chrono::steady_clock::now();
   std::fill(c, c + n, 0.0);

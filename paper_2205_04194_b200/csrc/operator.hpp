@@ -77,16 +77,19 @@ class DeviceOperator {
   // the *_locked variants are the thread-safe entry points of the C ABI.
   void moments_locked(const double* d_us, cudaStream_t s) {
     std::lock_guard<std::mutex> lk(mtx_);
+    Ordered o(*this, s);
     moments(d_us, s);
   }
   void far_near_locked(const double* d_us, double* d_out, const int* perm, cudaStream_t s,
                        int fb, int fe, int nb, int ne) {
     std::lock_guard<std::mutex> lk(mtx_);
+    Ordered o(*this, s);
     far_near(d_us, d_out, perm, s, fb, fe, nb, ne);
   }
   void moments(const double* d_us, cudaStream_t s);  // P2M + M2M + transform
   // Sharded ranks: own + halo moments and own-only coarse partials; the caller
   // all-reduces coarse_moments() over ranks, then calls moments_finish().
+  // (Both lock and order themselves, like the *_locked entry points.)
   void moments_local(const double* d_us, cudaStream_t s);
   void coarse_moments(double2** ptr, size_t* count) const;
   void moments_finish(cudaStream_t s);
@@ -102,6 +105,18 @@ class DeviceOperator {
   const std::vector<int4>& near_items_host() const { return near_items_h_; }
 
  private:
+  // Device-side ordering of every entry point that touches the operator's
+  // internal buffers: each waits for the previous one's work (on whatever
+  // stream it ran) and marks its own end, so calls on different streams never
+  // overlap on the GPU.
+  struct Ordered {
+    DeviceOperator& op;
+    cudaStream_t s;
+    Ordered(DeviceOperator& o, cudaStream_t st) : op(o), s(st) {
+      imqh::cuda_check(cudaStreamWaitEvent(s, op.ev_last_, 0), "order wait");
+    }
+    ~Ordered() { cudaEventRecord(op.ev_last_, s); }
+  };
   void build(const double* xy_host);
   void build_items(int p_lo, int p_hi);
   void build_pair_items(int p_lo, int p_hi);
@@ -116,6 +131,7 @@ class DeviceOperator {
   cudaStream_t aux_[kAuxStreams] = {};
   int far_streams_ = 1 + kAuxStreams;
   cudaEvent_t ev_fork_ = nullptr;
+  cudaEvent_t ev_last_ = nullptr;  // end of the last enqueued entry point (Ordered)
   cudaStream_t near_stream_ = nullptr;  // chunk-pair near field, concurrent with far
   cudaEvent_t ev_near_fork_ = nullptr, ev_near_done_ = nullptr;
   cudaEvent_t ev_join_[kAuxStreams] = {};

@@ -366,3 +366,34 @@ def test_near_field_modes_vs_oracle(imq, oracle, case):
         ref = oracle.fast_matvec_rows(xy, t, m, L, u, rows)
         assert float(np.max(np.abs(b[rows] - ref)) / np.max(np.abs(ref))) <= TOL, case
     assert np.array_equal(op.apply(u), b)  # deterministic reductions
+
+
+@pytest.mark.parametrize("kind", ["pair", "sym_split"])
+def test_device_applies_on_different_streams_do_not_race(imq, kind):
+    """Entry points that use the operator's internal buffers are ordered on the
+    device: interleaved apply_device calls on two streams give the same
+    results as sequential ones."""
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(3)
+    if kind == "pair":
+        xy, t, m, L = rng.random(2 * 16384), 0.05, 12, 1
+    else:
+        xy, t, m, L = rng.random(2 * (1 << 20)), 0.02, 10, 6
+    n = xy.size // 2
+    op = imq.FastOperator(xy, t, m, L)
+    us = [torch.tensor(rng.uniform(-1, 1, n), device="cuda") for _ in range(2)]
+    want = []
+    for u in us:
+        b = torch.empty_like(u)
+        op.apply_device(u, b)
+        torch.cuda.synchronize()
+        want.append(b.clone())
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    outs = [torch.full_like(us[0], float("nan")) for _ in range(2)]
+    torch.cuda.synchronize()
+    for _ in range(4):
+        for k in range(2):
+            op.apply_device(us[k], outs[k], streams[k])
+    torch.cuda.synchronize()
+    for k in range(2):
+        assert torch.equal(outs[k], want[k])
