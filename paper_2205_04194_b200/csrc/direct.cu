@@ -164,27 +164,59 @@ __global__ void __launch_bounds__(kNearWarps * 32) k_p2p_near_sym(
   const int g = 1 << (P.L + 1);
   int li, lj;
   demorton(leaf, li, lj);
-  // self tile: forward sums only (cnt <= 32 R: whole leaf in this item)
-  for (int base = s0; base < s0 + cnt; base += 32) {
-    const int j = base + lane;
-    __syncwarp();
-    if (j < s0 + cnt) {
-      sxy[warp][lane] = make_double2(P.xs[j], P.ys[j]);
-      su[warp][lane] = u_s[j];
-    } else {
-      sxy[warp][lane] = make_double2(xi[0], yi[0]);
-      su[warp][lane] = 0.0;
-    }
-    __syncwarp();
-#pragma unroll 8
-    for (int k = 0; k < 32; ++k) {
-      const double2 sp = sxy[warp][k];
-      const double uk = su[warp][k];
+  // self block (cnt <= 32 R: the whole leaf is in this item's registers), each
+  // unordered pair once: source tile pt = the targets of slot pt.  Slots
+  // p < pt take a full rotation against the tile (forward into acc[p], the
+  // reverse sums rotate into lane j = target j of slot pt); slot pt itself
+  // takes a half rotation (k = 0: the pair (i, i), forward only; k = 1..15;
+  // k = 16 by lanes 0..15 only), its reverse sums realigned by 17 lanes.
+  const int ntile = (cnt + 31) / 32;
 #pragma unroll
-      for (int p = 0; p < R; ++p) {
-        const double dx = xi[p] - sp.x, dy = yi[p] - sp.y;
-        acc[p] = fma(uk, rsqrt_pos(fma(dx, dx, fma(dy, dy, t2))), acc[p]);
+  for (int pt = 0; pt < R; ++pt) {
+    if (pt >= ntile) break;
+    __syncwarp();
+    sxy[warp][lane] = make_double2(xi[pt], yi[pt]);  // padding: a valid point, u = 0
+    su[warp][lane] = ui[pt];
+    __syncwarp();
+    if (pt > 0) {
+      double racc = 0.0;
+#pragma unroll 8
+      for (int k = 0; k < 32; ++k) {
+        const int jj = (lane + k) & 31;
+        const double2 sp = sxy[warp][jj];
+        const double uk = su[warp][jj];
+        double r = 0.0;
+#pragma unroll
+        for (int p = 0; p < R; ++p) {
+          if (p < pt) {
+            const double dx = xi[p] - sp.x, dy = yi[p] - sp.y;
+            const double phi = rsqrt_pos(fma(dx, dx, fma(dy, dy, t2)));
+            acc[p] = fma(uk, phi, acc[p]);
+            r = fma(ui[p], phi, r);
+          }
+        }
+        racc += r;
+        racc = __shfl_sync(0xffffffffu, racc, (lane + 1) & 31);
       }
+      acc[pt] += racc;
+    }
+    {
+      const double dx0 = xi[pt] - xi[pt], dy0 = yi[pt] - yi[pt];
+      acc[pt] = fma(ui[pt], rsqrt_pos(fma(dx0, dx0, fma(dy0, dy0, t2))), acc[pt]);  // k = 0
+      double racc = 0.0;
+#pragma unroll 4
+      for (int k = 1; k <= 16; ++k) {
+        const int jj = (lane + k) & 31;
+        const double2 sp = sxy[warp][jj];
+        const double uk = (k < 16 || lane < 16) ? su[warp][jj] : 0.0;
+        const double ul = (k < 16 || lane < 16) ? ui[pt] : 0.0;
+        const double dx = xi[pt] - sp.x, dy = yi[pt] - sp.y;
+        const double phi = rsqrt_pos(fma(dx, dx, fma(dy, dy, t2)));
+        acc[pt] = fma(uk, phi, acc[pt]);
+        racc = fma(ul, phi, racc);
+        racc = __shfl_sync(0xffffffffu, racc, (lane + 1) & 31);
+      }
+      acc[pt] += __shfl_sync(0xffffffffu, racc, (lane + 15) & 31);
     }
   }
   // forward neighbours: forward + reverse sums over the concatenation of the
