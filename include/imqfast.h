@@ -187,6 +187,11 @@ IMQ_API int imq_ext_operator_moments_finish(const imq_operator* op, void* stream
  * computed from an operator's leaf_start (pure host function), and the
  * restriction of an operator's far/near evaluation to one such range. */
 IMQ_API int imq_ext_shard_bounds(const int* leaf_start, int levels, int world, int* bounds_out);
+/* Same cut rule, balanced by evaluation work instead of point count: per
+ * level-(L-1) block, far (target, block) pairs x (m^2 + 4m + 12) + near pairs
+ * x 6 ("balanced by work, P_far + P_near per leaf"). */
+IMQ_API int imq_ext_shard_bounds_work(const int* leaf_start, int levels, int m, int world,
+                                      int* bounds_out);
 IMQ_API int imq_ext_operator_restrict(const imq_operator* op, int sorted_lo, int sorted_hi);
 
 /* Measured FP64 FMA-pipe throughput (TFLOP/s) of the current device: the

@@ -207,6 +207,11 @@ class FastOperator:
         check(lib().imq_operator_levels(self._h, C.byref(o)))
         return o.value
 
+    @property
+    def order(self) -> int:
+        """Truncation order M (imq_ext_stats.m)."""
+        return int(self.stats()["m"])
+
     def apply(self, u) -> np.ndarray:
         """imq_operator_apply: host in, host out (fast_matvec, fastmv.cpp:184-217)."""
         u = _f64(u)

@@ -632,6 +632,20 @@ int imq_ext_shard_bounds(const int* leaf_start, int levels, int world, int* boun
   });
 }
 
+int imq_ext_shard_bounds_work(const int* leaf_start, int levels, int m, int world,
+                              int* bounds_out) {
+  if (!leaf_start || !bounds_out || levels < 1 || levels > 13 || world < 1 || m < 0)
+    return fail(IMQ_ERR_INVALID_ARG, "imq_ext_shard_bounds_work: bad argument");
+  return guard([&] {
+    const size_t n = ((size_t)1 << (2 * (levels + 1))) + 1;
+    std::vector<int> ls(leaf_start, leaf_start + n);
+    std::vector<int> b =
+        imqh::shard_bounds_weighted(ls, levels, world, imqh::parent_work(ls, levels, m));
+    std::copy(b.begin(), b.end(), bounds_out);
+    return IMQ_OK;
+  });
+}
+
 int imq_ext_operator_restrict(const imq_operator* op, int sorted_lo, int sorted_hi) {
   if (!op) return fail(IMQ_ERR_INVALID_ARG, "imq_ext_operator_restrict: null argument");
   return guard([&] {

@@ -284,6 +284,57 @@ __global__ void __launch_bounds__(kNearWarps * 32) k_p2p_near_sym(
   }
 }
 
+// Sharded symmetric near field: a rank evaluates the pairs {C, B} of its own
+// leaves C (k_p2p_near_sym), which leaves, for an own leaf B whose backward
+// neighbour C in direction d belongs to another rank, slot 1 + d unwritten.
+// This kernel fills exactly those: items {b_start, b_cnt | d << 16, c_start,
+// c_cnt}, part[(1 + d) N + j] = sum_{i in C} u_i phi(x_j, x_i) for j in B.
+__global__ void __launch_bounds__(kNearWarps * 32) k_p2p_pull(
+    const TreeParams P, const int4* __restrict__ items, int n_items,
+    const double* __restrict__ u_s, double* __restrict__ part) {
+  constexpr int R = kNearMaxR;
+  __shared__ double2 sxy[kNearWarps][32];
+  __shared__ double su[kNearWarps][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int it = blockIdx.x * kNearWarps + warp;
+  if (it >= n_items) return;
+  const int4 item = items[it];
+  const int b0 = item.x, nb = item.y & 0xffff, dir = item.y >> 16, c0 = item.z, nc = item.w;
+  double xi[R], yi[R], acc[R];
+#pragma unroll
+  for (int p = 0; p < R; ++p) {
+    const int q = lane + 32 * p < nb ? b0 + lane + 32 * p : b0;
+    xi[p] = P.xs[q];
+    yi[p] = P.ys[q];
+    acc[p] = 0.0;
+  }
+  const double t2 = P.t2;
+  for (int base = 0; base < nc; base += 32) {
+    __syncwarp();
+    if (base + lane < nc) {
+      sxy[warp][lane] = make_double2(P.xs[c0 + base + lane], P.ys[c0 + base + lane]);
+      su[warp][lane] = u_s[c0 + base + lane];
+    } else {
+      sxy[warp][lane] = make_double2(xi[0], yi[0]);
+      su[warp][lane] = 0.0;
+    }
+    __syncwarp();
+#pragma unroll 8
+    for (int k = 0; k < 32; ++k) {
+      const double2 sp = sxy[warp][k];
+      const double uk = su[warp][k];
+#pragma unroll
+      for (int p = 0; p < R; ++p) {
+        const double dx = xi[p] - sp.x, dy = yi[p] - sp.y;
+        acc[p] = fma(uk, rsqrt_pos(fma(dx, dx, fma(dy, dy, t2))), acc[p]);
+      }
+    }
+  }
+#pragma unroll
+  for (int p = 0; p < R; ++p)
+    if (lane + 32 * p < nb) part[(size_t)(1 + dir) * P.N + b0 + lane + 32 * p] = acc[p];
+}
+
 // Symmetric near field for large leaves: items are unordered pairs of leaf
 // chunks (<= 32 R points each) {A, B} -- A's chunk with itself, with the later
 // chunks of its own leaf, and with every chunk of its four forward neighbour
@@ -474,6 +525,13 @@ void launch_p2p_pair(const TreeParams& P, const int4* items, int n_items, const 
   if (n_items)
     k_p2p_pair<kPairR><<<(unsigned)((n_items + kNearWarps - 1) / kNearWarps), kNearWarps * 32, 0,
                          s>>>(P, items, n_items, u_s, part);
+}
+
+void launch_p2p_pull(const TreeParams& P, const int4* items, int n_items, const double* u_s,
+                     double* part, cudaStream_t s) {
+  if (n_items)
+    k_p2p_pull<<<(unsigned)((n_items + kNearWarps - 1) / kNearWarps), kNearWarps * 32, 0, s>>>(
+        P, items, n_items, u_s, part);
 }
 
 void launch_pair_reduce(const int2* chunks, int n_chunks, const int* contrib_off,

@@ -111,6 +111,10 @@ void launch_p2p_near_sym(const TreeParams& P, const int4* items, const int* grou
 constexpr int kNearChunk = 128;
 void launch_p2p_pair(const TreeParams& P, const int4* items, int n_items, const double* u_s,
                      double* part, cudaStream_t s);
+// Sharded symmetric near field: slots of own leaves whose backward neighbour
+// belongs to another rank (items {b_start, b_cnt | dir << 16, c_start, c_cnt}).
+void launch_p2p_pull(const TreeParams& P, const int4* items, int n_items, const double* u_s,
+                     double* part, cudaStream_t s);
 void launch_pair_reduce(const int2* chunks, int n_chunks, const int* contrib_off,
                         const int* contrib, const double* part, double* out,
                         const double* far_s, const int* perm, cudaStream_t s);

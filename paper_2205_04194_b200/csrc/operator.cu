@@ -115,7 +115,7 @@ void DeviceOperator::release() {
   dfree(d_part_);
   dfree(d_need_par_); dfree(d_local_leaves_); dfree(d_pack_a_); dfree(d_pack_c_); dfree(d_own_lvl_);
   dfree(d_pair_items_); dfree(d_pair_part_); dfree(d_chunks_); dfree(d_contrib_off_);
-  dfree(d_contrib_); dfree(d_near_s_); dfree(d_farc_);
+  dfree(d_contrib_); dfree(d_near_s_); dfree(d_farc_); dfree(d_pull_items_);
   if (solve_pin_) cudaFreeHost(solve_pin_);
   solve_pin_ = nullptr;
   solve_pin_bytes_ = 0;
@@ -364,8 +364,13 @@ void DeviceOperator::build_items(int p_lo, int p_hi) {
   int max_leaf = 0;
   for (long long q = 0; q < n_leaves; ++q)
     max_leaf = std::max(max_leaf, ls[(size_t)q + 1] - ls[(size_t)q]);
-  near_sym_ = p_lo == 0 && p_hi == N_ && near_split_ == 1 &&
+  // unsharded: when the per-leaf items fill the GPU (else the chunk-pair
+  // path); sharded ranges: whenever the leaves fit one item (boundary pairs
+  // are completed by pull items below)
+  const bool full = p_lo == 0 && p_hi == N_;
+  near_sym_ = (full ? near_split_ == 1 : true) &&
               max_leaf <= 32 * imqk::near_max_points_per_lane() && !getenv("IMQ_NEAR_NOSYM");
+  if (near_sym_) near_split_ = 1;
   if (near_sym_) nrmax = imqk::near_max_points_per_lane();
   std::vector<std::vector<int4>> ngroups((size_t)nrmax);
   for (long long q = 0; q < n_leaves; ++q) {
@@ -376,6 +381,33 @@ void DeviceOperator::build_items(int p_lo, int p_hi) {
         ngroups[(size_t)((cnt + 31) / 32 - 1)].push_back(make_int4(
             (int)q, c, cnt, near_split_ == 1 ? 15 : (near_split_ == 3 ? 16 + r : 32 + r)));
     }
+  }
+  // pull items (sharded symmetric mode): own leaf B, direction d, backward
+  // neighbour C (non-empty) outside [p_lo, p_hi)
+  std::vector<int4> pull;
+  if (near_sym_ && !full) {
+    const int g = 1 << (L_ + 1);
+    for (long long q = 0; q < n_leaves; ++q) {
+      const int a = ls[(size_t)q], b = ls[(size_t)q + 1];
+      if (b <= a || a < p_lo || b > p_hi) continue;
+      int li, lj;
+      imqdev::demorton((uint32_t)q, li, lj);
+      for (int dir = 0; dir < 4; ++dir) {
+        const int ci = li - (dir == 0 ? 0 : 1), cj = lj - (dir == 0 ? 1 : dir - 2);
+        if (ci < 0 || cj < 0 || cj > g - 1) continue;
+        const uint32_t qc = imqdev::morton((uint32_t)ci, (uint32_t)cj);
+        const int c0 = ls[qc], c1 = ls[(size_t)qc + 1];
+        if (c1 <= c0 || (c0 >= p_lo && c1 <= p_hi)) continue;
+        pull.push_back(make_int4(a, (b - a) | (dir << 16), c0, c1 - c0));
+      }
+    }
+  }
+  dfree(d_pull_items_);
+  n_pull_ = (int)pull.size();
+  if (n_pull_) {
+    d_pull_items_ = dalloc<int4>(pull.size(), "pull items");
+    cuda_check(cudaMemcpy(d_pull_items_, pull.data(), pull.size() * sizeof(int4),
+                          cudaMemcpyHostToDevice), "H2D pull items");
   }
   build_pair_items(p_lo, p_hi);
   const int nslots = near_sym_ ? 5 : (near_pair_ ? 1 : near_split_);
@@ -493,6 +525,87 @@ std::vector<int> shard_bounds(const std::vector<int>& ls, int L, int world) {
     // choose the closer of the two parent boundaries around `want`
     int lo = ls[(size_t)(4 * p)], hi = p < n_par ? ls[(size_t)(4 * (p + 1))] : n;
     b[(size_t)r] = (want - lo <= hi - want) ? lo : hi;
+    if (b[(size_t)r] < b[(size_t)r - 1]) b[(size_t)r] = b[(size_t)r - 1];
+  }
+  return b;
+}
+
+// Per level-(L-1) block evaluation work, from the tree alone: far (target,
+// source block) pairs x (M^2 + 4M + 12) DFMA-equivalents + near pairs x 6
+// (symmetric evaluation), the counts exactly as pair_counts() forms them.
+std::vector<double> parent_work(const std::vector<int>& ls, int L, int M) {
+  auto count = [&](int l, int i, int j) -> long long {
+    const uint32_t q = imqdev::morton((uint32_t)i, (uint32_t)j);
+    const int sh = 2 * (L - l);
+    return (long long)ls[(size_t)(q + 1) << sh] - ls[(size_t)q << sh];
+  };
+  auto list_count = [&](int l, int i, int j) {
+    const int grid = 1 << (l + 1);
+    int lo_i = 0, hi_i = grid - 1, lo_j = 0, hi_j = grid - 1;
+    if (l >= 2) {
+      lo_i = std::max(0, 2 * (i / 2 - 1)); hi_i = std::min(grid - 1, 2 * (i / 2 + 1) + 1);
+      lo_j = std::max(0, 2 * (j / 2 - 1)); hi_j = std::min(grid - 1, 2 * (j / 2 + 1) + 1);
+    }
+    int ns = 0;
+    for (int qi = lo_i; qi <= hi_i; ++qi)
+      for (int qj = lo_j; qj <= hi_j; ++qj)
+        if (std::max(std::abs(qi - i), std::abs(qj - j)) >= 2 && count(l, qi, qj) > 0) ++ns;
+    return ns;
+  };
+  // shared list sizes of levels 1..L-1, per block (Morton order)
+  std::vector<std::vector<int>> ns((size_t)L);
+  for (int l = 1; l < L; ++l) {
+    const int grid = 1 << (l + 1);
+    ns[(size_t)l].assign((size_t)grid * grid, 0);
+    for (int i = 0; i < grid; ++i)
+      for (int j = 0; j < grid; ++j)
+        if (count(l, i, j) > 0) ns[(size_t)l][imqdev::morton(i, j)] = list_count(l, i, j);
+  }
+  const double c_far = (double)M * M + 4.0 * M + 12.0, c_near = 6.0;
+  const int gL = 1 << (L + 1);
+  const long long n_par = 1ll << (2 * L);
+  std::vector<double> w((size_t)n_par, 0.0);
+  for (long long p = 0; p < n_par; ++p) {
+    const long long np = (long long)ls[(size_t)(4 * p + 4)] - ls[(size_t)(4 * p)];
+    if (!np) continue;
+    double shared = 0.0;
+    for (int l = 1; l < L; ++l) shared += ns[(size_t)l][(size_t)(p >> (2 * (L - 1 - l)))];
+    double far = shared * (double)np, near = 0.0;
+    for (int c = 0; c < 4; ++c) {
+      const uint32_t q = (uint32_t)(4 * p + c);
+      const long long nc = (long long)ls[(size_t)q + 1] - ls[q];
+      if (!nc) continue;
+      int i, j;
+      imqdev::demorton(q, i, j);
+      far += (double)nc * list_count(L, i, j);
+      long long nn = 0;
+      for (int qi = std::max(0, i - 1); qi <= std::min(gL - 1, i + 1); ++qi)
+        for (int qj = std::max(0, j - 1); qj <= std::min(gL - 1, j + 1); ++qj)
+          nn += count(L, qi, qj);
+      near += (double)nc * (double)nn;
+    }
+    w[(size_t)p] = c_far * far + c_near * near;
+  }
+  return w;
+}
+
+// Bounds balanced by a per-parent weight (cuts at level-(L-1) boundaries).
+std::vector<int> shard_bounds_weighted(const std::vector<int>& ls, int L, int world,
+                                       const std::vector<double>& w) {
+  if (world < 1) throw std::invalid_argument("shard_bounds: world must be >= 1");
+  const long long n_par = 1ll << (2 * L);
+  std::vector<double> cum((size_t)n_par + 1, 0.0);
+  for (long long p = 0; p < n_par; ++p) cum[(size_t)p + 1] = cum[(size_t)p] + w[(size_t)p];
+  const int n = ls.back();
+  std::vector<int> b((size_t)world + 1, n);
+  b[0] = 0;
+  long long p = 0;
+  for (int r = 1; r < world; ++r) {
+    const double want = cum[(size_t)n_par] * r / world;
+    while (p < n_par && cum[(size_t)p + 1] <= want) ++p;
+    const long long cut = (want - cum[(size_t)p] <= cum[(size_t)std::min(p + 1, n_par)] - want)
+                              ? p : std::min(p + 1, n_par);
+    b[(size_t)r] = ls[(size_t)(4 * cut)];
     if (b[(size_t)r] < b[(size_t)r - 1]) b[(size_t)r] = b[(size_t)r - 1];
   }
   return b;
@@ -648,9 +761,11 @@ void DeviceOperator::far_near(const double* d_us, double* d_out, const int* perm
   near_begin = std::max(0, near_begin);
   near_end = std::min(near_end, n_near_);
   const bool sym = (near_sym_ || near_pair_) && near_end > near_begin;
-  if (sym && near_sym_)  // symmetric near field first; the far epilogue combines and scatters
+  if (sym && near_sym_) {  // symmetric near field first; the far epilogue combines and scatters
     imqk::launch_p2p_near_sym(P_, d_near_items_, near_group_off_.data(), near_begin, near_end,
                               d_us, d_part_, s);
+    imqk::launch_p2p_pull(P_, d_pull_items_, n_pull_, d_us, d_part_, s);
+  }
   if (sym && near_pair_) {
     imqk::launch_p2p_pair(P_, d_pair_items_, n_pair_items_, d_us, d_pair_part_, s);
     imqk::launch_pair_reduce(d_chunks_, n_chunks_, d_contrib_off_, d_contrib_, d_pair_part_,

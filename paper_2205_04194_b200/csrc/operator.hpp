@@ -38,6 +38,9 @@ struct PairCounts {
 };
 
 std::vector<int> shard_bounds(const std::vector<int>& leaf_start, int L, int world);
+std::vector<double> parent_work(const std::vector<int>& leaf_start, int L, int M);
+std::vector<int> shard_bounds_weighted(const std::vector<int>& leaf_start, int L, int world,
+                                       const std::vector<double>& w);
 
 class DeviceOperator {
  public:
@@ -171,6 +174,8 @@ class DeviceOperator {
   bool near_sym_ = false;  // symmetric near-field evaluation (small leaves)
   bool near_pair_ = false; // chunk-pair symmetric near field (large leaves)
   bool far_split_ = false; // far field in a coarse (levels 1..L-2) and a fine pass
+  int4* d_pull_items_ = nullptr;  // sharded symmetric near field: boundary slots
+  int n_pull_ = 0;
   int n_far_fine_ = 0;     // far items [0, n_far_fine_) fine, the rest coarse
   std::vector<int> far_cgroup_off_;
   double* d_farc_ = nullptr;  // coarse-pass far partial (sorted order)

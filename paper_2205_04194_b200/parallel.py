@@ -24,14 +24,18 @@ import numpy as np
 from .capi import check, lib
 
 
-def shard_bounds(leaf_start, levels: int, world: int) -> np.ndarray:
-    """world+1 sorted-position bounds, balanced, aligned to level-(L-1) blocks."""
+def shard_bounds(leaf_start, levels: int, world: int, order: int | None = None) -> np.ndarray:
+    """world+1 sorted-position bounds aligned to level-(L-1) blocks, balanced by
+    point count, or by evaluation work when the expansion order is given."""
     ls = np.ascontiguousarray(leaf_start, dtype=np.int32)
     if ls.size != (1 << (2 * (levels + 1))) + 1:
         raise ValueError("leaf_start has the wrong length for `levels`")
     out = np.empty(world + 1, dtype=np.int32)
-    check(lib().imq_ext_shard_bounds(ls.ctypes.data_as(C.POINTER(C.c_int)), levels, world,
-                                     out.ctypes.data_as(C.POINTER(C.c_int))))
+    lp, op = ls.ctypes.data_as(C.POINTER(C.c_int)), out.ctypes.data_as(C.POINTER(C.c_int))
+    if order is None:
+        check(lib().imq_ext_shard_bounds(lp, levels, world, op))
+    else:
+        check(lib().imq_ext_shard_bounds_work(lp, levels, order, world, op))
     return out
 
 
@@ -57,7 +61,7 @@ class ShardedOperator:
         import torch
         self.op = op
         self.rank, self.world = rank, world
-        self.bounds = shard_bounds(op.leaf_start(), op.levels, world)
+        self.bounds = shard_bounds(op.leaf_start(), op.levels, world, op.order)
         self.lo, self.hi = int(self.bounds[rank]), int(self.bounds[rank + 1])
         check(lib().imq_ext_operator_restrict(op.handle, self.lo, self.hi))
         self.perm = op.permutation()

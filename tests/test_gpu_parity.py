@@ -261,6 +261,9 @@ def test_sharded_application_emulated(imq, world):
         full.apply_device(u, b_ref)
         torch.cuda.synchronize()
         ranks = [ShardedOperator(imq.FastOperator(xy, t, m, L), r, world) for r in range(world)]
+        if xy is not None and full.stats()["near_mode"] == 1:
+            # the ranks run the symmetric near field too (boundary slots pulled)
+            assert all(sh.op.stats()["near_mode"] == 1 for sh in ranks)
         for sh in ranks:
             sh.moments(u, reduce=False)
         torch.cuda.synchronize()

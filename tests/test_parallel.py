@@ -96,3 +96,68 @@ def test_shard_bounds_aligned_and_balanced(imq, oracle, world):
         assert np.all(np.diff(b) >= 0)
         biggest = int(np.max(np.diff(ls[::4])))
         assert np.max(np.abs(np.diff(b) - 20000 / world)) <= biggest   # balanced to a block
+
+
+def _morton(i, j):
+    out = 0
+    for b in range(16):
+        out |= ((i >> b) & 1) << (2 * b + 1)
+        out |= ((j >> b) & 1) << (2 * b)
+    return out
+
+
+def _parent_work(ls, L, M):
+    """Independent restatement of the sharding work model: per level-(L-1)
+    block, far (target, non-empty list block) pairs x (M^2+4M+12) + near
+    pairs x 6 (interaction lists as partition.cpp:56-83)."""
+    def count(l, i, j):
+        q, sh = _morton(i, j), 2 * (L - l)
+        return int(ls[(q + 1) << sh] - ls[q << sh])
+
+    def nlist(l, i, j):
+        g = 1 << (l + 1)
+        if l == 1:
+            cand = [(a, b) for a in range(g) for b in range(g)]
+        else:
+            pi, pj = i // 2, j // 2
+            cand = [(a, b) for a in range(max(0, 2 * pi - 2), min(g, 2 * pi + 4))
+                    for b in range(max(0, 2 * pj - 2), min(g, 2 * pj + 4))]
+        return sum(1 for a, b in cand if max(abs(a - i), abs(b - j)) >= 2 and count(l, a, b) > 0)
+
+    gL = 1 << (L + 1)
+    w = np.zeros(1 << (2 * L))
+    for p in range(1 << (2 * L)):
+        far = near = 0
+        for c in range(4):
+            q = 4 * p + c
+            nc = int(ls[q + 1] - ls[q])
+            if not nc:
+                continue
+            i = j = 0
+            for b in range(16):
+                i |= ((q >> (2 * b + 1)) & 1) << b
+                j |= ((q >> (2 * b)) & 1) << b
+            f = nlist(L, i, j) + sum(nlist(l, i >> (L - l), j >> (L - l)) for l in range(1, L))
+            far += nc * f
+            near += nc * sum(count(L, a, b) for a in range(max(0, i - 1), min(gL, i + 2))
+                             for b in range(max(0, j - 1), min(gL, j + 2)))
+        w[p] = (M * M + 4 * M + 12) * far + 6 * near
+    return w
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_shard_bounds_balanced_by_work(imq, oracle, world):
+    from paper_2205_04194_b200 import inputs
+    from paper_2205_04194_b200.parallel import shard_bounds
+    L, M = 4, 12
+    for xy in (inputs.uniform_points(20000, 0), inputs.gaussian_mixture(20000, 1)):
+        _, ls = sorted_tree(oracle, xy, L)
+        b = shard_bounds(ls, L, world, order=M)
+        parents = ls[::4]
+        assert b[0] == 0 and b[-1] == 20000 and np.all(np.diff(b) >= 0)
+        assert all(x in set(parents.tolist()) for x in b.tolist())
+        w = _parent_work(ls, L, M)
+        cum = np.concatenate([[0.0], np.cumsum(w)])
+        at = np.searchsorted(parents, b, side="left")     # parent index of each cut
+        share = np.diff(cum[at])
+        assert np.max(np.abs(share - cum[-1] / world)) <= np.max(w) + 1e-6
