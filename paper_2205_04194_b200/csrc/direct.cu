@@ -19,7 +19,6 @@ namespace {
 
 constexpr int kNearWarps = 4;
 constexpr int kNearMaxR = 4;  // a near work item holds <= 32 * kNearMaxR targets of one leaf
-constexpr int kPairR = 4;     // chunk size 32 * kPairR of the chunk-pair near field
 
 // Warp per near work item: <= 32 R targets of one leaf, R per lane.  Every
 // source point staged in the warp's shared-memory tile is read back once per
@@ -354,8 +353,8 @@ __global__ void __launch_bounds__(kNearWarps * 32) k_p2p_pair(
   const int4 item = items[it];
   const int a0 = item.x, na = item.y, b0 = item.z, nb = item.w;
   const bool self = a0 == b0;
-  double* fwd = part + (size_t)it * (64 * R);
-  double* rev = fwd + 32 * R;
+  double* fwd = part + (size_t)it * (2 * kNearChunk);  // rows: forward, then reverse
+  double* rev = fwd + kNearChunk;
   double xi[R], yi[R], ui[R], acc[R];
 #pragma unroll
   for (int p = 0; p < R; ++p) {
@@ -520,11 +519,20 @@ void launch_p2p_near_sym(const TreeParams& P, const int4* items, const int* grou
   }
 }
 
-void launch_p2p_pair(const TreeParams& P, const int4* items, int n_items, const double* u_s,
-                     double* part, cudaStream_t s) {
-  if (n_items)
-    k_p2p_pair<kPairR><<<(unsigned)((n_items + kNearWarps - 1) / kNearWarps), kNearWarps * 32, 0,
-                         s>>>(P, items, n_items, u_s, part);
+void launch_p2p_pair(const TreeParams& P, const int4* items, const int* group_off,
+                     const double* u_s, double* part, cudaStream_t s) {
+  for (int R = kPairR; R >= 1; --R) {
+    const int lo = group_off[R - 1], n = group_off[R] - lo;
+    if (n <= 0) continue;
+    const unsigned grid = (unsigned)((n + kNearWarps - 1) / kNearWarps);
+    double* pp = part + (size_t)lo * 2 * kNearChunk;
+    switch (R) {
+      case 1: k_p2p_pair<1><<<grid, kNearWarps * 32, 0, s>>>(P, items + lo, n, u_s, pp); break;
+      case 2: k_p2p_pair<2><<<grid, kNearWarps * 32, 0, s>>>(P, items + lo, n, u_s, pp); break;
+      case 3: k_p2p_pair<3><<<grid, kNearWarps * 32, 0, s>>>(P, items + lo, n, u_s, pp); break;
+      default: k_p2p_pair<4><<<grid, kNearWarps * 32, 0, s>>>(P, items + lo, n, u_s, pp); break;
+    }
+  }
 }
 
 void launch_p2p_pull(const TreeParams& P, const int4* items, int n_items, const double* u_s,

@@ -108,9 +108,10 @@ void launch_p2p_near_sym(const TreeParams& P, const int4* items, const int* grou
 // b_start, b_cnt} (chunks <= 128 points), part = n_items x 256 doubles; the
 // reduction adds each chunk's rows (contrib CSR over chunks): out[q] = near
 // (far_s == nullptr) or out[perm ? perm[q] : q] = far_s[q] + near.
-constexpr int kNearChunk = 128;
-void launch_p2p_pair(const TreeParams& P, const int4* items, int n_items, const double* u_s,
-                     double* part, cudaStream_t s);
+constexpr int kNearChunk = 128;  // = 32 * kPairR
+constexpr int kPairR = 4;  // chunk = 32 * kPairR points; items grouped by R = 1..kPairR
+void launch_p2p_pair(const TreeParams& P, const int4* items, const int* group_off,
+                     const double* u_s, double* part, cudaStream_t s);
 // Sharded symmetric near field: slots of own leaves whose backward neighbour
 // belongs to another rank (items {b_start, b_cnt | dir << 16, c_start, c_cnt}).
 void launch_p2p_pull(const TreeParams& P, const int4* items, int n_items, const double* u_s,

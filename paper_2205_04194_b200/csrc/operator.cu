@@ -451,15 +451,8 @@ void DeviceOperator::build_pair_items(int p_lo, int p_hi) {
       chunks.push_back(make_int2(c, std::min(CS, ls[(size_t)q + 1] - c)));
   }
   leaf_chunk0[(size_t)n_leaves] = (int)chunks.size();
-  std::vector<int4> items;
-  std::vector<std::vector<int>> contrib(chunks.size());
-  auto add = [&](int a, int b) {
-    const int i = (int)items.size();
-    items.push_back(make_int4(chunks[(size_t)a].x, chunks[(size_t)a].y, chunks[(size_t)b].x,
-                              chunks[(size_t)b].y));
-    contrib[(size_t)a].push_back(i * 2 * CS);
-    if (a != b) contrib[(size_t)b].push_back(i * 2 * CS + CS);
-  };
+  std::vector<int2> pairs;  // (target chunk a, source chunk b)
+  auto add = [&](int a, int b) { pairs.push_back(make_int2(a, b)); };
   for (long long q = 0; q < n_leaves; ++q) {
     int li, lj;
     imqdev::demorton((uint32_t)q, li, lj);
@@ -472,7 +465,25 @@ void DeviceOperator::build_pair_items(int p_lo, int p_hi) {
         for (int b = leaf_chunk0[qb]; b < leaf_chunk0[(size_t)qb + 1]; ++b) add(a, b);
       }
     }
-    if ((double)items.size() * 2 * CS * sizeof(double) > 2.0e9) return;  // too large: plain path
+    if ((double)pairs.size() * 2 * CS * sizeof(double) > 2.0e9) return;  // too large: plain path
+  }
+  // group by targets per lane R = ceil(|a| / 32) (one kernel specialisation
+  // per group, so small chunks do not idle 3/4 of an R = 4 item); the order
+  // inside a group, and with it every chunk's contribution order, is fixed
+  auto rof = [&](const int2& pr) { return (chunks[(size_t)pr.x].y + 31) / 32; };
+  std::stable_sort(pairs.begin(), pairs.end(),
+                   [&](const int2& x, const int2& y) { return rof(x) < rof(y); });
+  pair_group_off_.assign(imqk::kPairR + 1, 0);
+  for (const int2& pr : pairs) ++pair_group_off_[(size_t)rof(pr)];
+  for (int r = 1; r <= imqk::kPairR; ++r) pair_group_off_[(size_t)r] += pair_group_off_[(size_t)r - 1];
+  std::vector<int4> items;
+  std::vector<std::vector<int>> contrib(chunks.size());
+  for (const int2& pr : pairs) {
+    const int i = (int)items.size(), a = pr.x, b = pr.y;
+    items.push_back(make_int4(chunks[(size_t)a].x, chunks[(size_t)a].y, chunks[(size_t)b].x,
+                              chunks[(size_t)b].y));
+    contrib[(size_t)a].push_back(i * 2 * CS);
+    if (a != b) contrib[(size_t)b].push_back(i * 2 * CS + CS);
   }
   std::vector<int> off(chunks.size() + 1, 0), flat;
   for (size_t c = 0; c < chunks.size(); ++c) {
@@ -767,7 +778,7 @@ void DeviceOperator::far_near(const double* d_us, double* d_out, const int* perm
     imqk::launch_p2p_pull(P_, d_pull_items_, n_pull_, d_us, d_part_, s);
   }
   if (sym && near_pair_) {
-    imqk::launch_p2p_pair(P_, d_pair_items_, n_pair_items_, d_us, d_pair_part_, s);
+    imqk::launch_p2p_pair(P_, d_pair_items_, pair_group_off_.data(), d_us, d_pair_part_, s);
     imqk::launch_pair_reduce(d_chunks_, n_chunks_, d_contrib_off_, d_contrib_, d_pair_part_,
                              d_near_s_, nullptr, nullptr, s);
   }
@@ -817,7 +828,8 @@ void DeviceOperator::apply_sorted_locked(const double* d_us, double* d_out, cons
     // and the far field; the pair reduction adds far + near and unsorts
     cuda_check(cudaEventRecord(ev_near_fork_, s), "near fork");
     cuda_check(cudaStreamWaitEvent(near_stream_, ev_near_fork_, 0), "near fork wait");
-    imqk::launch_p2p_pair(P_, d_pair_items_, n_pair_items_, d_us, d_pair_part_, near_stream_);
+    imqk::launch_p2p_pair(P_, d_pair_items_, pair_group_off_.data(), d_us, d_pair_part_,
+                          near_stream_);
     cuda_check(cudaEventRecord(ev_near_done_, near_stream_), "near done");
     moments(d_us, s);
     far_near(d_us, d_out, perm, s, 0, n_far_, 0, 0);  // far field only -> d_far_

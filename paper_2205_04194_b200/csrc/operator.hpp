@@ -174,6 +174,7 @@ class DeviceOperator {
   bool near_sym_ = false;  // symmetric near-field evaluation (small leaves)
   bool near_pair_ = false; // chunk-pair symmetric near field (large leaves)
   bool far_split_ = false; // far field in a coarse (levels 1..L-2) and a fine pass
+  std::vector<int> pair_group_off_;  // chunk-pair items grouped by R = 1..kPairR
   int4* d_pull_items_ = nullptr;  // sharded symmetric near field: boundary slots
   int n_pull_ = 0;
   int n_far_fine_ = 0;     // far items [0, n_far_fine_) fine, the rest coarse
