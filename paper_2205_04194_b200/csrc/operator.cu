@@ -297,7 +297,9 @@ void DeviceOperator::build_items(int p_lo, int p_hi) {
   constexpr double kWarpsWanted = 148.0 * 64;
   const double nt = (double)(p_hi - p_lo);
   const int rfit = (int)std::max(1.0, std::floor(nt / (32.0 * kWarpsWanted)));
-  const int rmax = imqk::m2p_specialised(M_) ? std::min(rfit, imqk::far_max_points_per_lane()) : 2;
+  int rmax = imqk::m2p_specialised(M_) ? std::min(rfit, imqk::far_max_points_per_lane()) : 2;
+  if (const char* e = getenv("IMQ_FAR_RMAX"))  // tuning
+    rmax = std::max(1, std::min(imqk::far_max_points_per_lane(), atoi(e)));
   // Level split (L >= 4): the lists of levels 1..L-2 are shared by every
   // target of a level-(L-2) block, so those levels run as a separate "coarse"
   // pass whose items span whole grandparents (fewer idle lanes), and the
