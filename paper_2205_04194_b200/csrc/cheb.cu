@@ -1,0 +1,185 @@
+// cheb.cu -- the far field of the coarse levels through Chebyshev
+// interpolation on the target boxes.
+//
+// For a target box X at level l the reference adds, for every point of X, the
+// same list of source blocks (partition.cpp:56-72; fastmv.cpp:201-212).  That
+// sum F_X(x) = sum_{B in list_l(X)} F_B(x) is a smooth function on X (every
+// source block sits >= 1.5 cells away), so it is evaluated with the
+// reference's own M2P at n x n Chebyshev nodes of X (k_m2p_far on node
+// "targets", operator.cu), turned into a tensor Chebyshev series of degree
+// n-1, pushed down the levels (the restriction of a degree-(n-1) series to a
+// child box is again exactly such a series), and summed at every target of
+// the level-lc boxes.  With n = 20 the interpolation error of one box's field
+// is <= ~1e-13 of its maximum (tests vs the oracle).
+//
+// Layouts: per box (levels 1..lc, all boxes, level-major, Morton inside a
+// level) 400 node values / coefficients, index [box][i * 20 + j], i the x
+// index and j the y index; x_i = c_x + (cell/2) cos(pi (i + 1/2) / 20).
+#include "imq_device.cuh"
+#include "imq_kernels.hpp"
+
+namespace imqk {
+
+namespace {
+
+using namespace imqdev;
+constexpr int NC = kChebN;
+constexpr int NN = NC * NC;
+
+__constant__ double c_T[NN];      // T[k * NC + i] = cos(k theta_i), theta_i = pi (i + 1/2) / NC
+__constant__ double c_S[2][NN];   // child restriction, [half][k' * NC + k]
+
+__global__ void k_cheb_nodes(const TreeParams P, int l, long long box_base, double* __restrict__ nx,
+                             double* __restrict__ ny) {
+  const long long nb = 1ll << (2 * (l + 1));
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nb * NN) return;
+  const uint32_t q = (uint32_t)(t / NN);
+  const int r = (int)(t % NN), i = r / NC, j = r % NC;
+  int bi, bj;
+  demorton(q, bi, bj);
+  const double h = 0.5 * P.cell[l];
+  nx[(box_base + q) * NN + r] = block_center(P.ox, bi, P.cell[l]) + h * c_T[NC + i];
+  ny[(box_base + q) * NN + r] = block_center(P.oy, bj, P.cell[l]) + h * c_T[NC + j];
+}
+
+// One CTA per box of level l (boxes listed in `boxes`): node values ->
+// Chebyshev coefficients, plus the parent's series restricted to this box.
+__global__ void __launch_bounds__(NN) k_cheb_coef(int l, const int* __restrict__ boxes,
+                                                  long long base_l, long long base_parent,
+                                                  const double* __restrict__ vals,
+                                                  double* __restrict__ coef) {
+  __shared__ double a[NN], b[NN];
+  const uint32_t q = (uint32_t)boxes[blockIdx.x];
+  const int r = threadIdx.x, k = r / NC, m = r % NC;
+  const double* v = vals + (base_l + q) * NN;
+  a[r] = v[r];
+  __syncthreads();
+  // b[i][m] = sum_j v[i][j] T[m][j]
+  {
+    double s = 0.0;
+    for (int j = 0; j < NC; ++j) s = fma(a[k * NC + j], c_T[m * NC + j], s);
+    b[r] = s;  // (k plays i here)
+  }
+  __syncthreads();
+  // c[k][m] = (2/n)^2 w_k w_m sum_i T[k][i] b[i][m]
+  double c = 0.0;
+  for (int i = 0; i < NC; ++i) c = fma(c_T[k * NC + i], b[i * NC + m], c);
+  c *= (2.0 / NC) * (2.0 / NC) * (k == 0 ? 0.5 : 1.0) * (m == 0 ? 0.5 : 1.0);
+  if (l > 1) {
+    // parent series restricted to this quadrant: S_x C_p S_y^T
+    const double* cp = coef + (base_parent + (q >> 2)) * NN;
+    const double* sx = c_S[(q >> 1) & 1];
+    const double* sy = c_S[q & 1];
+    __syncthreads();
+    a[r] = cp[r];
+    __syncthreads();
+    {
+      double s = 0.0;  // b[k][m'] = sum_j Cp[k][j] Sy[m'][j]
+      for (int j = 0; j < NC; ++j) s = fma(a[k * NC + j], sy[m * NC + j], s);
+      b[r] = s;
+    }
+    __syncthreads();
+    double s = 0.0;  // c[k'][m'] += sum_k Sx[k'][k] b[k][m']
+    for (int kk = 0; kk < NC; ++kk) s = fma(sx[k * NC + kk], b[kk * NC + m], s);
+    c += s;
+  }
+  coef[(base_l + q) * NN + r] = c;
+}
+
+// Warp per item {box q at level lc, first sorted target, count <= 32 R}:
+// out[p] = sum_{k,m} C[k][m] T_k(x^) T_m(y^) at each target.
+constexpr int kEvalWarps = 4, kEvalR = 4;
+__global__ void __launch_bounds__(kEvalWarps * 32) k_cheb_eval(const TreeParams P, int lc,
+                                                               const int4* __restrict__ items,
+                                                               int n_items, long long base_lc,
+                                                               const double* __restrict__ coef,
+                                                               double* __restrict__ out) {
+  __shared__ __align__(16) double cs[kEvalWarps][NN];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int it = blockIdx.x * kEvalWarps + warp;
+  if (it >= n_items) return;
+  const int4 item = items[it];
+  const uint32_t q = (uint32_t)item.x;
+  const int s0 = item.y, cnt = item.z;
+  const double* c = coef + (base_lc + q) * NN;
+  for (int r = lane; r < NN; r += 32) cs[warp][r] = c[r];
+  __syncwarp();
+  int bi, bj;
+  demorton(q, bi, bj);
+  const double cx = block_center(P.ox, bi, P.cell[lc]), cy = block_center(P.oy, bj, P.cell[lc]);
+  const double inv = 2.0 / P.cell[lc];
+  double xh[kEvalR], ty[kEvalR][NC], acc[kEvalR];
+#pragma unroll
+  for (int p = 0; p < kEvalR; ++p) {
+    const int idx = lane + 32 * p < cnt ? s0 + lane + 32 * p : s0;
+    xh[p] = (P.xs[idx] - cx) * inv;
+    const double yh = (P.ys[idx] - cy) * inv;
+    ty[p][0] = 1.0;
+    ty[p][1] = yh;
+#pragma unroll
+    for (int m = 2; m < NC; ++m) ty[p][m] = fma(2.0 * yh, ty[p][m - 1], -ty[p][m - 2]);
+    acc[p] = 0.0;
+  }
+  double tx0[kEvalR], tx1[kEvalR];
+#pragma unroll
+  for (int p = 0; p < kEvalR; ++p) {
+    tx0[p] = 1.0;
+    tx1[p] = xh[p];
+  }
+#pragma unroll 2
+  for (int k = 0; k < NC; ++k) {
+    double s[kEvalR];
+#pragma unroll
+    for (int p = 0; p < kEvalR; ++p) s[p] = 0.0;
+#pragma unroll
+    for (int m = 0; m < NC; m += 2) {
+      const double2 cc = *reinterpret_cast<const double2*>(&cs[warp][k * NC + m]);
+#pragma unroll
+      for (int p = 0; p < kEvalR; ++p) s[p] = fma(cc.y, ty[p][m + 1], fma(cc.x, ty[p][m], s[p]));
+    }
+#pragma unroll
+    for (int p = 0; p < kEvalR; ++p) {
+      const double tk = k == 0 ? 1.0 : (k == 1 ? xh[p] : fma(2.0 * xh[p], tx1[p], -tx0[p]));
+      if (k >= 2) {
+        tx0[p] = tx1[p];
+        tx1[p] = tk;
+      }
+      acc[p] = fma(tk, s[p], acc[p]);
+    }
+  }
+#pragma unroll
+  for (int p = 0; p < kEvalR; ++p)
+    if (lane + 32 * p < cnt) out[s0 + lane + 32 * p] = acc[p];
+}
+
+}  // namespace
+
+void cheb_set_tables(const double* T, const double* S_left, const double* S_right) {
+  cudaMemcpyToSymbol(c_T, T, NN * sizeof(double));
+  cudaMemcpyToSymbol(c_S, S_left, NN * sizeof(double), 0);
+  cudaMemcpyToSymbol(c_S, S_right, NN * sizeof(double), NN * sizeof(double));
+}
+
+void launch_cheb_nodes(const TreeParams& P, int l, long long box_base, double* nx, double* ny,
+                       cudaStream_t s) {
+  const long long n = (1ll << (2 * (l + 1))) * NN;
+  k_cheb_nodes<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(P, l, box_base, nx, ny);
+}
+
+void launch_cheb_coef(int l, const int* boxes, int n_boxes, long long base_l,
+                      long long base_parent, const double* vals, double* coef, cudaStream_t s) {
+  if (n_boxes)
+    k_cheb_coef<<<(unsigned)n_boxes, NN, 0, s>>>(l, boxes, base_l, base_parent, vals, coef);
+}
+
+void launch_cheb_eval(const TreeParams& P, int lc, const int4* items, int n_items,
+                      long long base_lc, const double* coef, double* out, cudaStream_t s) {
+  if (n_items)
+    k_cheb_eval<<<(unsigned)((n_items + kEvalWarps - 1) / kEvalWarps), kEvalWarps * 32, 0, s>>>(
+        P, lc, items, n_items, base_lc, coef, out);
+}
+
+int cheb_eval_points_per_item() { return 32 * kEvalR; }
+
+}  // namespace imqk

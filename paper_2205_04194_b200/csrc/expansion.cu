@@ -765,7 +765,9 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_m2p_far(const TreeParams P
   const int4 item = items[it];
   const uint32_t par = (uint32_t)item.x;
   const int s0 = item.y, cnt = item.z;
-  const int n = build_far_list(P, par, s0, cnt, list, lane, O.lmin, O.lmax);
+  const int lev = item.w;  // > 0: this item's level only (Chebyshev node items)
+  const int n = build_far_list(P, par, s0, cnt, list, lane, lev > 0 ? lev : O.lmin,
+                               lev > 0 ? lev : O.lmax);
   Targets<R> T;
   load_targets<R>(P, s0, cnt, lane, T);
   const int L = P.L;
@@ -842,7 +844,9 @@ __global__ void __launch_bounds__(WARPS * 32) k_m2p_far_generic(const TreeParams
   const uint32_t par = (uint32_t)item.x;
   const int s0 = item.y, cnt = item.z;
   uint32_t* list = lists[warp];
-  const int n = build_far_list(P, par, s0, cnt, list, lane, O.lmin, O.lmax);
+  const int lev = item.w;
+  const int n = build_far_list(P, par, s0, cnt, list, lane, lev > 0 ? lev : O.lmin,
+                               lev > 0 ? lev : O.lmax);
   for (int p0 = lane; p0 < cnt; p0 += 32) {
     const int p = s0 + p0;
     const double x = P.xs[p], y = P.ys[p];

@@ -89,6 +89,17 @@ void launch_m2p_far(const TreeParams& P, const int4* items, const int* group_off
                     double* out = nullptr, const int* perm = nullptr,
                     const double* far_add = nullptr, int lmin = 1, int lmax = 0);
 bool m2p_specialised(int M);
+
+// ---- coarse far field by Chebyshev interpolation (cheb.cu)
+constexpr int kChebN = 20;  // nodes per dimension (degree kChebN - 1)
+void cheb_set_tables(const double* T, const double* S_left, const double* S_right);
+void launch_cheb_nodes(const TreeParams& P, int l, long long box_base, double* nx, double* ny,
+                       cudaStream_t s);
+void launch_cheb_coef(int l, const int* boxes, int n_boxes, long long base_l,
+                      long long base_parent, const double* vals, double* coef, cudaStream_t s);
+void launch_cheb_eval(const TreeParams& P, int lc, const int4* items, int n_items,
+                      long long base_lc, const double* coef, double* out, cudaStream_t s);
+int cheb_eval_points_per_item();
 int far_max_points_per_lane();
 
 // ---- direct interactions (direct.cu)

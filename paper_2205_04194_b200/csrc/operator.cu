@@ -116,6 +116,8 @@ void DeviceOperator::release() {
   dfree(d_need_par_); dfree(d_local_leaves_); dfree(d_pack_a_); dfree(d_pack_c_); dfree(d_own_lvl_);
   dfree(d_pair_items_); dfree(d_pair_part_); dfree(d_chunks_); dfree(d_contrib_off_);
   dfree(d_contrib_); dfree(d_near_s_); dfree(d_farc_); dfree(d_pull_items_);
+  dfree(d_cheb_items_); dfree(d_cboxes_); dfree(d_ceval_items_);
+  dfree(d_cnx_); dfree(d_cny_); dfree(d_cnleaf_); dfree(d_cval_); dfree(d_ccoef_);
   if (solve_pin_) cudaFreeHost(solve_pin_);
   solve_pin_ = nullptr;
   solve_pin_bytes_ = 0;
@@ -215,6 +217,10 @@ void DeviceOperator::build(const double* xy_host) {
       while (w < 8 && mean > 64.0 * w * 1.5) w *= 2;
       P_.p2m_wpl = w;
     }
+    P_.xs = d_xs_;
+    P_.ys = d_ys_;
+    P_.leaf = d_leaf_;
+    P_.leaf_start = d_leaf_start_;
     // ---- work lists (all targets)
     leaf_start_h_ = std::move(ls);
     build_items(0, N_);
@@ -261,10 +267,6 @@ void DeviceOperator::build(const double* xy_host) {
     d_far_ = dalloc<double>((size_t)n, "far");
     d_b_ = dalloc<double>((size_t)n, "b");
 
-    P_.xs = d_xs_;
-    P_.ys = d_ys_;
-    P_.leaf = d_leaf_;
-    P_.leaf_start = d_leaf_start_;
     cuda_check(cudaStreamSynchronize(s), "operator build");
   } catch (...) {
     dfree(d_xy); dfree(d_keys); dfree(d_idx); dfree(d_tmp); dfree(d_part);
@@ -335,6 +337,7 @@ void DeviceOperator::build_items(int p_lo, int p_hi) {
     dfree(d_farc_);
     d_farc_ = dalloc<double>((size_t)N_, "coarse far");
   }
+  build_cheb(p_lo, p_hi);
   // near items: one leaf each; R from the mean leaf occupancy (a typical leaf
   // in one item), then the smallest source split (1, 3 or 9 ways) that gives
   // the GPU enough warps
@@ -510,6 +513,119 @@ void DeviceOperator::build_pair_items(int p_lo, int p_hi) {
   cuda_check(cudaMemcpy(d_contrib_, flat.data(), flat.size() * sizeof(int),
                         cudaMemcpyHostToDevice), "H2D contrib");
   near_pair_ = true;
+}
+
+// Coarse far field by Chebyshev interpolation (cheb.cu): for the levels
+// 1..lc = L-2 of the coarse pass, each non-empty box evaluates its list at
+// kChebN^2 nodes instead of at all of its points; used when the boxes of
+// level lc hold on average >= 1.5x as many targets as nodes.
+void DeviceOperator::build_cheb(int p_lo, int p_hi) {
+  constexpr int NC = imqk::kChebN, NN = NC * NC;
+  cheb_ = false;
+  dfree(d_cheb_items_); dfree(d_cboxes_); dfree(d_ceval_items_);
+  n_cheb_items_ = n_ceval_ = 0;
+  if (!far_split_ || getenv("IMQ_FAR_NOCHEB") || !imqk::m2p_specialised(M_)) return;
+  const int lc = L_ - 2;
+  const std::vector<int>& ls = leaf_start_h_;
+  auto own = [&](int l, long long q) {  // targets of block q at level l inside [p_lo, p_hi)
+    const int sh = 2 * (L_ - l);
+    const int a = std::max(p_lo, ls[(size_t)(q << sh)]);
+    const int b = std::min(p_hi, ls[(size_t)((q + 1) << sh)]);
+    return std::max(0, b - a);
+  };
+  long long nonempty = 0, tot = 0;
+  for (long long q = 0; q < (1ll << (2 * (lc + 1))); ++q) {
+    const int c = own(lc, q);
+    if (c > 0) ++nonempty, tot += c;
+  }
+  if (!nonempty || (double)tot < 1.5 * NN * (double)nonempty) return;
+  // node geometry (all boxes of levels 1..lc), tables
+  cheb_base_.assign((size_t)lc + 1, 0);
+  long long nb = 0;
+  for (int l = 1; l <= lc; ++l) {
+    cheb_base_[(size_t)l] = nb;
+    nb += 1ll << (2 * (l + 1));
+  }
+  if (cheb_nodes_ != (size_t)nb * NN) {
+    dfree(d_cnx_); dfree(d_cny_); dfree(d_cnleaf_); dfree(d_cval_); dfree(d_ccoef_);
+    cheb_nodes_ = (size_t)nb * NN;
+    d_cnx_ = dalloc<double>(cheb_nodes_, "cheb nodes");
+    d_cny_ = dalloc<double>(cheb_nodes_, "cheb nodes");
+    d_cnleaf_ = dalloc<uint32_t>(cheb_nodes_, "cheb node keys");
+    d_cval_ = dalloc<double>(cheb_nodes_, "cheb values");
+    d_ccoef_ = dalloc<double>(cheb_nodes_, "cheb coefficients");
+    cuda_check(cudaMemset(d_cnleaf_, 0, cheb_nodes_ * sizeof(uint32_t)), "cheb keys");
+    std::vector<double> T(NN), SL(NN), SR(NN);
+    const long double pi = 3.141592653589793238462643383279502884L;
+    for (int k = 0; k < NC; ++k)
+      for (int i = 0; i < NC; ++i) T[(size_t)k * NC + i] = (double)cosl(k * pi * (i + 0.5L) / NC);
+    for (int kp = 0; kp < NC; ++kp)
+      for (int k = 0; k < NC; ++k) {
+        long double sl = 0, sr = 0;
+        for (int i = 0; i < NC; ++i) {
+          const long double u = cosl(pi * (i + 0.5L) / NC), w = cosl(kp * pi * (i + 0.5L) / NC);
+          sl += w * cosl(k * acosl((u - 1) / 2));
+          sr += w * cosl(k * acosl((u + 1) / 2));
+        }
+        const long double f = (2.0L / NC) * (kp == 0 ? 0.5L : 1.0L);
+        SL[(size_t)kp * NC + k] = (double)(f * sl);
+        SR[(size_t)kp * NC + k] = (double)(f * sr);
+      }
+    imqk::cheb_set_tables(T.data(), SL.data(), SR.data());
+    for (int l = 1; l <= lc; ++l)
+      imqk::launch_cheb_nodes(P_, l, cheb_base_[(size_t)l], d_cnx_, d_cny_, stream_);
+    cuda_check(cudaStreamSynchronize(stream_), "cheb nodes");
+  }
+  Pn_ = P_;
+  Pn_.xs = d_cnx_;
+  Pn_.ys = d_cny_;
+  Pn_.leaf = d_cnleaf_;
+  Pn_.N = (int)cheb_nodes_;
+  // node items (level in item.w), coefficient box lists, evaluation items
+  std::vector<std::vector<int4>> g((size_t)imqk::far_max_points_per_lane());
+  std::vector<int> boxes;
+  cbox_off_.assign((size_t)lc + 2, 0);
+  for (int l = 1; l <= lc; ++l) {
+    cbox_off_[(size_t)l] = (int)boxes.size();
+    for (long long q = 0; q < (1ll << (2 * (l + 1))); ++q) {
+      if (!own(l, q)) continue;
+      boxes.push_back((int)q);
+      const int par = (int)(q << (2 * (L_ - 1 - l)));
+      const int start = (int)((cheb_base_[(size_t)l] + q) * NN);
+      for (int c = 0; c < NN; c += 224) {
+        const int cnt = std::min(224, NN - c);
+        g[(size_t)((cnt + 31) / 32 - 1)].push_back(make_int4(par, start + c, cnt, l));
+      }
+    }
+  }
+  cbox_off_[(size_t)lc + 1] = (int)boxes.size();
+  std::vector<int4> citems;
+  cheb_group_off_.assign(16, 0);
+  for (size_t r = 0; r < g.size(); ++r) {
+    citems.insert(citems.end(), g[r].begin(), g[r].end());
+    cheb_group_off_[r + 1] = (int)citems.size();
+  }
+  for (size_t r = g.size() + 1; r < 16; ++r) cheb_group_off_[r] = (int)citems.size();
+  std::vector<int4> ev;
+  const int per = imqk::cheb_eval_points_per_item();
+  for (long long q = 0; q < (1ll << (2 * (lc + 1))); ++q) {
+    const int sh = 2 * (L_ - lc);
+    const int a = std::max(p_lo, ls[(size_t)(q << sh)]), b = std::min(p_hi, ls[(size_t)((q + 1) << sh)]);
+    for (int c = a; c < b; c += per) ev.push_back(make_int4((int)q, c, std::min(per, b - c), 0));
+  }
+  n_cheb_items_ = (int)citems.size();
+  n_ceval_ = (int)ev.size();
+  d_cheb_items_ = dalloc<int4>(citems.size(), "cheb items");
+  d_cboxes_ = dalloc<int>(boxes.size(), "cheb boxes");
+  d_ceval_items_ = dalloc<int4>(ev.size(), "cheb eval items");
+  cuda_check(cudaMemcpy(d_cheb_items_, citems.data(), citems.size() * sizeof(int4),
+                        cudaMemcpyHostToDevice), "H2D cheb items");
+  cuda_check(cudaMemcpy(d_cboxes_, boxes.data(), boxes.size() * sizeof(int),
+                        cudaMemcpyHostToDevice), "H2D cheb boxes");
+  cuda_check(cudaMemcpy(d_ceval_items_, ev.data(), ev.size() * sizeof(int4),
+                        cudaMemcpyHostToDevice), "H2D cheb eval");
+  cheb_lc_ = lc;
+  cheb_ = true;
 }
 
 void DeviceOperator::restrict_targets(int p_lo, int p_hi) {
@@ -787,7 +903,8 @@ void DeviceOperator::far_near(const double* d_us, double* d_out, const int* perm
   // fork: group launches on s + the aux streams, joined back into s
   auto far_pass = [&](int b, int e, const int* goff, const double* near_part, int nslots,
                       double* out, const int* pm, double* far_s, const double* far_add, int lmin,
-                      int lmax) {
+                      int lmax, const imqk::TreeParams* Pp = nullptr,
+                      const int4* its = nullptr) {
     if (e <= b) return;
     cudaStream_t ss[1 + kAuxStreams] = {s};
     cuda_check(cudaEventRecord(ev_fork_, s), "fork");
@@ -795,8 +912,8 @@ void DeviceOperator::far_near(const double* d_us, double* d_out, const int* perm
       ss[k + 1] = aux_[k];
       cuda_check(cudaStreamWaitEvent(aux_[k], ev_fork_, 0), "fork wait");
     }
-    imqk::launch_m2p_far(P_, d_far_items_, goff, b, e, d_coef_, far_s, ss, far_streams_,
-                         near_part, nslots, out, pm, far_add, lmin, lmax);
+    imqk::launch_m2p_far(Pp ? *Pp : P_, its ? its : d_far_items_, goff, b, e, d_coef_, far_s, ss,
+                         far_streams_, near_part, nslots, out, pm, far_add, lmin, lmax);
     for (int k = 0; k < kAuxStreams; ++k) {
       cuda_check(cudaEventRecord(ev_join_[k], aux_[k]), "join");
       cuda_check(cudaStreamWaitEvent(s, ev_join_[k], 0), "join wait");
@@ -806,8 +923,22 @@ void DeviceOperator::far_near(const double* d_us, double* d_out, const int* perm
   const int nslots = near_pair_ ? 1 : 5;
   if (far_split_) {
     // coarse pass (levels 1..L-2) into d_farc_, then the fine pass (L-1..L)
-    far_pass(std::max(far_begin, n_far_fine_), far_end, far_cgroup_off_.data(), nullptr, 0,
-             nullptr, nullptr, d_farc_, nullptr, 1, L_ - 2);
+    if (cheb_ && far_end > n_far_fine_) {
+      // list fields at the Chebyshev nodes of every box, series per level
+      // (parent restricted + own), summed at the targets of the level-lc boxes
+      far_pass(0, n_cheb_items_, cheb_group_off_.data(), nullptr, 0, nullptr, nullptr, d_cval_,
+               nullptr, 1, cheb_lc_, &Pn_, d_cheb_items_);
+      for (int l = 1; l <= cheb_lc_; ++l)
+        imqk::launch_cheb_coef(l, d_cboxes_ + cbox_off_[(size_t)l],
+                               cbox_off_[(size_t)l + 1] - cbox_off_[(size_t)l],
+                               cheb_base_[(size_t)l], l > 1 ? cheb_base_[(size_t)l - 1] : 0,
+                               d_cval_, d_ccoef_, s);
+      imqk::launch_cheb_eval(P_, cheb_lc_, d_ceval_items_, n_ceval_, cheb_base_[(size_t)cheb_lc_],
+                             d_ccoef_, d_farc_, s);
+    } else {
+      far_pass(std::max(far_begin, n_far_fine_), far_end, far_cgroup_off_.data(), nullptr, 0,
+               nullptr, nullptr, d_farc_, nullptr, 1, L_ - 2);
+    }
     far_pass(far_begin, std::min(far_end, n_far_fine_), far_group_off_.data(), near_part, nslots,
              d_out, perm, d_far_, d_farc_, L_ - 1, L_);
   } else {

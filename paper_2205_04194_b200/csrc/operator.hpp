@@ -123,6 +123,7 @@ class DeviceOperator {
   void build(const double* xy_host);
   void build_items(int p_lo, int p_hi);
   void build_pair_items(int p_lo, int p_hi);
+  void build_cheb(int p_lo, int p_hi);
   void setup_sharded_moments(int p_lo, int p_hi);
   void release();
   void apply_sorted_locked(const double* d_us, double* d_bs, const int* perm,
@@ -175,6 +176,17 @@ class DeviceOperator {
   bool near_pair_ = false; // chunk-pair symmetric near field (large leaves)
   bool far_split_ = false; // far field in a coarse (levels 1..L-2) and a fine pass
   std::vector<int> pair_group_off_;  // chunk-pair items grouped by R = 1..kPairR
+  // coarse far field by Chebyshev interpolation (build_cheb, cheb.cu)
+  bool cheb_ = false;
+  int cheb_lc_ = 0, n_cheb_items_ = 0, n_ceval_ = 0;
+  size_t cheb_nodes_ = 0;
+  std::vector<long long> cheb_base_;   // first box of level l in the node arrays
+  std::vector<int> cheb_group_off_, cbox_off_;
+  imqk::TreeParams Pn_{};              // P_ with the node coordinates as "points"
+  double *d_cnx_ = nullptr, *d_cny_ = nullptr, *d_cval_ = nullptr, *d_ccoef_ = nullptr;
+  uint32_t* d_cnleaf_ = nullptr;
+  int4 *d_cheb_items_ = nullptr, *d_ceval_items_ = nullptr;
+  int* d_cboxes_ = nullptr;
   int4* d_pull_items_ = nullptr;  // sharded symmetric near field: boundary slots
   int n_pull_ = 0;
   int n_far_fine_ = 0;     // far items [0, n_far_fine_) fine, the rest coarse
