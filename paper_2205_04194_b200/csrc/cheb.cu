@@ -49,39 +49,44 @@ __global__ void __launch_bounds__(NN) k_cheb_coef(int l, const int* __restrict__
                                                   long long base_l, long long base_parent,
                                                   const double* __restrict__ vals,
                                                   double* __restrict__ coef) {
-  __shared__ double a[NN], b[NN];
+  // (the tables are staged in shared memory: per-thread indices differ, and
+  // constant memory serialises non-uniform addresses)
+  __shared__ double a[NN], b[NN], T[NN], Sx[NN], Sy[NN];
   const uint32_t q = (uint32_t)boxes[blockIdx.x];
   const int r = threadIdx.x, k = r / NC, m = r % NC;
   const double* v = vals + (base_l + q) * NN;
   a[r] = v[r];
+  T[r] = c_T[r];
+  if (l > 1) {
+    Sx[r] = c_S[(q >> 1) & 1][r];
+    Sy[r] = c_S[q & 1][r];
+  }
   __syncthreads();
   // b[i][m] = sum_j v[i][j] T[m][j]
   {
     double s = 0.0;
-    for (int j = 0; j < NC; ++j) s = fma(a[k * NC + j], c_T[m * NC + j], s);
+    for (int j = 0; j < NC; ++j) s = fma(a[k * NC + j], T[m * NC + j], s);
     b[r] = s;  // (k plays i here)
   }
   __syncthreads();
   // c[k][m] = (2/n)^2 w_k w_m sum_i T[k][i] b[i][m]
   double c = 0.0;
-  for (int i = 0; i < NC; ++i) c = fma(c_T[k * NC + i], b[i * NC + m], c);
+  for (int i = 0; i < NC; ++i) c = fma(T[k * NC + i], b[i * NC + m], c);
   c *= (2.0 / NC) * (2.0 / NC) * (k == 0 ? 0.5 : 1.0) * (m == 0 ? 0.5 : 1.0);
   if (l > 1) {
     // parent series restricted to this quadrant: S_x C_p S_y^T
     const double* cp = coef + (base_parent + (q >> 2)) * NN;
-    const double* sx = c_S[(q >> 1) & 1];
-    const double* sy = c_S[q & 1];
     __syncthreads();
     a[r] = cp[r];
     __syncthreads();
     {
       double s = 0.0;  // b[k][m'] = sum_j Cp[k][j] Sy[m'][j]
-      for (int j = 0; j < NC; ++j) s = fma(a[k * NC + j], sy[m * NC + j], s);
+      for (int j = 0; j < NC; ++j) s = fma(a[k * NC + j], Sy[m * NC + j], s);
       b[r] = s;
     }
     __syncthreads();
     double s = 0.0;  // c[k'][m'] += sum_k Sx[k'][k] b[k][m']
-    for (int kk = 0; kk < NC; ++kk) s = fma(sx[k * NC + kk], b[kk * NC + m], s);
+    for (int kk = 0; kk < NC; ++kk) s = fma(Sx[k * NC + kk], b[kk * NC + m], s);
     c += s;
   }
   coef[(base_l + q) * NN + r] = c;
