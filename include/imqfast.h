@@ -147,6 +147,9 @@ typedef struct {
   long long far_items, near_items;
   int near_mode; /* near-field evaluation: 0 = per target (split sources, sharded ranges),
                     1 = symmetric per leaf (leaves <= 128), 2 = symmetric chunk pairs */
+  double far_pairs_direct; /* (target, block) pairs evaluated directly */
+  double cheb_node_pairs;  /* (Chebyshev node, block) pairs of the coarse levels */
+  int cheb_levels;         /* levels 1..cheb_levels evaluated through Chebyshev nodes (0: none) */
 } imq_ext_stats;
 IMQ_API int imq_ext_operator_stats(const imq_operator* op, imq_ext_stats* out);
 

@@ -511,6 +511,9 @@ int imq_ext_operator_stats(const imq_operator* op, imq_ext_stats* out) {
     out->far_items = c.far_items;
     out->near_items = c.near_items;
     out->near_mode = c.near_mode;
+    out->far_pairs_direct = c.far_pairs_direct;
+    out->cheb_node_pairs = c.cheb_node_pairs;
+    out->cheb_levels = c.cheb_levels;
     return IMQ_OK;
   });
 }

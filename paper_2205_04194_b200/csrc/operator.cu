@@ -1028,6 +1028,7 @@ PairCounts DeviceOperator::pair_counts() {
     counts_.far_items = n_far_;
     counts_.near_items = n_near_;
     counts_.near_mode = near_pair_ ? 2 : (near_sym_ ? 1 : 0);
+    fill_eval_counts();
     return counts_;
   }
   std::vector<int> ls;
@@ -1039,6 +1040,8 @@ PairCounts DeviceOperator::pair_counts() {
     return (long long)ls[(size_t)(q + 1) << sh] - ls[(size_t)q << sh];
   };
   double far = 0, near = 0;
+  far_by_level_.assign((size_t)L + 1, 0.0);
+  lists_by_level_.assign((size_t)L + 1, 0.0);
   for (int l = 1; l <= L; ++l) {
     const int grid = 1 << (l + 1);
     for (int i = 0; i < grid; ++i)
@@ -1055,6 +1058,8 @@ PairCounts DeviceOperator::pair_counts() {
           for (int qj = lo_j; qj <= hi_j; ++qj)
             if (std::max(std::abs(qi - i), std::abs(qj - j)) >= 2 && count(l, qi, qj) > 0) ++ns;
         far += (double)nt * (double)ns;
+        far_by_level_[(size_t)l] += (double)nt * (double)ns;
+        lists_by_level_[(size_t)l] += (double)ns;
         if (l == L) {
           long long nn = 0;
           for (int qi = std::max(0, i - 1); qi <= std::min(grid - 1, i + 1); ++qi)
@@ -1070,7 +1075,22 @@ PairCounts DeviceOperator::pair_counts() {
   counts_.far_items = n_far_;
   counts_.near_items = n_near_;
   counts_.near_mode = near_pair_ ? 2 : (near_sym_ ? 1 : 0);
+  fill_eval_counts();
   return counts_;
+}
+
+// Pairs the kernels actually evaluate: direct (target, block) pairs of the
+// levels not covered by the Chebyshev pass, and (node, block) pairs.
+void DeviceOperator::fill_eval_counts() {
+  const int lc = cheb_ ? cheb_lc_ : 0;
+  double direct = 0, nodes = 0;
+  for (int l = 1; l <= L_ && l < (int)far_by_level_.size(); ++l) {
+    if (l <= lc) nodes += lists_by_level_[(size_t)l] * imqk::kChebN * imqk::kChebN;
+    else direct += far_by_level_[(size_t)l];
+  }
+  counts_.far_pairs_direct = direct;
+  counts_.cheb_node_pairs = nodes;
+  counts_.cheb_levels = lc;
 }
 
 // ------------------------------------------------------------------ GMRES --

@@ -35,6 +35,9 @@ struct PairCounts {
   double far_pairs = 0, near_pairs = 0;  // exact, from the built tree
   int64_t far_items = 0, near_items = 0;
   int near_mode = 0;  // 0 plain (split sources), 1 symmetric per leaf, 2 chunk pairs
+  double far_pairs_direct = 0;  // (target, block) pairs evaluated directly
+  double cheb_node_pairs = 0;   // (Chebyshev node, block) pairs
+  int cheb_levels = 0;          // levels 1..cheb_levels through the Chebyshev pass
 };
 
 std::vector<int> shard_bounds(const std::vector<int>& leaf_start, int L, int world);
@@ -124,6 +127,8 @@ class DeviceOperator {
   void build_items(int p_lo, int p_hi);
   void build_pair_items(int p_lo, int p_hi);
   void build_cheb(int p_lo, int p_hi);
+  void fill_eval_counts();
+  std::vector<double> far_by_level_, lists_by_level_;
   void setup_sharded_moments(int p_lo, int p_hi);
   void release();
   void apply_sorted_locked(const double* d_us, double* d_bs, const int* perm,
