@@ -662,6 +662,9 @@ std::vector<int> shard_bounds(const std::vector<int>& ls, int L, int world) {
 // Per level-(L-1) block evaluation work, from the tree alone: far (target,
 // source block) pairs x (M^2 + 4M + 12) DFMA-equivalents + near pairs x 6
 // (symmetric evaluation), the counts exactly as pair_counts() forms them.
+// For L >= 4 the levels 1..L-2 go through the Chebyshev nodes (build_cheb):
+// a box's list then costs min(1, 400 / its targets) per target, plus the
+// series evaluation (~1.4 pairs per target).
 std::vector<double> parent_work(const std::vector<int>& ls, int L, int M) {
   auto count = [&](int l, int i, int j) -> long long {
     const uint32_t q = imqdev::morton((uint32_t)i, (uint32_t)j);
@@ -698,7 +701,17 @@ std::vector<double> parent_work(const std::vector<int>& ls, int L, int M) {
     const long long np = (long long)ls[(size_t)(4 * p + 4)] - ls[(size_t)(4 * p)];
     if (!np) continue;
     double shared = 0.0;
-    for (int l = 1; l < L; ++l) shared += ns[(size_t)l][(size_t)(p >> (2 * (L - 1 - l)))];
+    for (int l = 1; l < L; ++l) {
+      const long long a = p >> (2 * (L - 1 - l));
+      double wl = 1.0;
+      if (L >= 4 && l <= L - 2) {
+        const int sh = 2 * (L - l);
+        const double na = (double)ls[(size_t)((a + 1) << sh)] - ls[(size_t)(a << sh)];
+        wl = std::min(1.0, (double)(imqk::kChebN * imqk::kChebN) / na);
+      }
+      shared += wl * ns[(size_t)l][(size_t)a];
+    }
+    if (L >= 4) shared += 1.4;
     double far = shared * (double)np, near = 0.0;
     for (int c = 0; c < 4; ++c) {
       const uint32_t q = (uint32_t)(4 * p + c);

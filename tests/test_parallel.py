@@ -109,7 +109,8 @@ def _morton(i, j):
 def _parent_work(ls, L, M):
     """Independent restatement of the sharding work model: per level-(L-1)
     block, far (target, non-empty list block) pairs x (M^2+4M+12) + near
-    pairs x 6 (interaction lists as partition.cpp:56-83)."""
+    pairs x 6 (interaction lists as partition.cpp:56-83); coarse levels
+    weighted by the Chebyshev node share."""
     def count(l, i, j):
         q, sh = _morton(i, j), 2 * (L - l)
         return int(ls[(q + 1) << sh] - ls[q << sh])
@@ -137,7 +138,12 @@ def _parent_work(ls, L, M):
             for b in range(16):
                 i |= ((q >> (2 * b + 1)) & 1) << b
                 j |= ((q >> (2 * b)) & 1) << b
-            f = nlist(L, i, j) + sum(nlist(l, i >> (L - l), j >> (L - l)) for l in range(1, L))
+            f = nlist(L, i, j)
+            for l in range(1, L):  # levels 1..L-2 through 20x20 Chebyshev nodes when L >= 4
+                il, jl = i >> (L - l), j >> (L - l)
+                wl = min(1.0, 400.0 / count(l, il, jl)) if (L >= 4 and l <= L - 2) else 1.0
+                f += wl * nlist(l, il, jl)
+            f += 1.4 if L >= 4 else 0.0
             far += nc * f
             near += nc * sum(count(L, a, b) for a in range(max(0, i - 1), min(gL, i + 2))
                              for b in range(max(0, j - 1), min(gL, j + 2)))
