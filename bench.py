@@ -13,7 +13,8 @@ coefficients) exceed the 126 MB L2, so no flush is needed between steps.
 N > 1 GPUs (torchrun): every rank holds the Morton-sorted points and the full
 source vector, forms the moments, and evaluates the far + near field of its own
 contiguous Morton range of targets (paper_2205_04194_b200/parallel.py, cut at
-level-(L-1) blocks); no collective on the data path.  The target points are
+level-(L-1) blocks); the one data-path collective is an all-reduce (NCCL) of
+the coarse-level (1..L-2) moments, 28 MB at config 4.  The target points are
 sharded, the work per rank shrinks with N ("strong" scaling).
 value = N points / max-over-ranks time.
 
@@ -323,7 +324,10 @@ def b200_arm(args):
     mom_ms = e0.elapsed_time(e1)
     peak_tf, _ = P.api.fp64_peak(8192)
     far_flops = st["far_pairs"] * f_pair(M) * share  # this rank's targets
-    achieved = far_flops / (far_ms * 1e-3) / 1e12
+    survey_achieved = far_flops / (far_ms * 1e-3) / 1e12
+    exec_flops = ((st["far_pairs_direct"] + st["cheb_node_pairs"]) * share
+                  * 2 * (M * M + 4 * M + 12))
+    achieved = exec_flops / (far_ms * 1e-3) / 1e12
     traffic = None
     prof = os.path.join(ROOT, "profiles", "far_kernel_ncu.json")
     if os.path.exists(prof):
@@ -344,6 +348,29 @@ def b200_arm(args):
             gs = time.perf_counter() - t0
         cr = r.cycle_residuals
         gm = {"config": "cfg2: N=65536 uniform, c=0.05, p=12, L=auto(2), GMRES(50), x0=0",
+              "tol": 1e-8, "max_iter": args.gmres_iters, "iterations": r.iterations,
+              "time_s": gs, "ms_per_iteration": gs * 1e3 / max(1, r.iterations),
+              "final_relative_residual": r.final_relative_residual,
+              "converged": r.converged,
+              "cycle_residuals_head": cr[:6], "cycle_residuals_tail": cr[-3:]}
+
+    if world > 1 and not args.no_gmres:
+        # the same solve sharded over the ranks (dist_solve.py): all-gather of the
+        # Krylov vector, coarse-moment all-reduce per matvec, CGS2 all-reduces
+        from paper_2205_04194_b200.dist_solve import ShardedSolver
+        xy2 = inputs.uniform_points(65536, 0)
+        f2 = inputs.cfg2_rhs(xy2)
+        with P.FastOperator(xy2, 0.05, 12, 0) as op2:
+            ss = ShardedSolver(ShardedOperator(op2, rank, world))
+            barrier()
+            t0 = time.perf_counter()
+            r = ss.solve(f2, 1e-8, args.gmres_iters, 50, ortho="cgs2")
+            gs = torch.tensor([time.perf_counter() - t0], device="cuda", dtype=torch.float64)
+            dist.all_reduce(gs, op=dist.ReduceOp.MAX)
+            gs = float(gs.item())
+        cr = r.cycle_residuals
+        gm = {"config": f"cfg2: N=65536 uniform, c=0.05, p=12, L=auto(2), GMRES(50), x0=0, "
+                        f"vectors sharded {world}-way, CGS2 with all-reduced inner products",
               "tol": 1e-8, "max_iter": args.gmres_iters, "iterations": r.iterations,
               "time_s": gs, "ms_per_iteration": gs * 1e3 / max(1, r.iterations),
               "final_relative_residual": r.final_relative_residual,
@@ -399,26 +426,30 @@ def b200_arm(args):
                             "sharded ext API, pinned host buffers"},
             "roofline": {"bound": "fp64",
                          "kernel": "k_m2p_far (M2P far field: direct for the fine levels, at "
-                                   "Chebyshev nodes for levels 1..%d)" % st["cheb_levels"],
+                                   "Chebyshev nodes for levels 1..%d) + k_cheb_*" % st["cheb_levels"],
                          "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
                          "frac": achieved / peak_tf, "traffic": traffic,
+                         "traffic_unit": "DRAM bytes per product over the far-field launches "
+                                         "(profiles/far_kernel_ncu.json)",
                          "peak_source": "measured live: DFMA probe (imq_ext_fp64_peak); "
                                         "MEASURED_PEAKS.json has no FP64 entry",
-                         "flops_per_launch": far_flops,
-                         "flop_model": "SURVEY 8(d): P_far x (4K+6Ke+6(M+1)+12)"
+                         "flops_per_launch": exec_flops,
+                         "flop_model": "evaluated (target or Chebyshev node, source block) pairs "
+                                       "x 2(M^2+4M+12) flop (complex-Horner M2P, DESIGN.md s4)"
                                        + ("" if world == 1 else " x rank-0 target share"),
-                         "executed_flops_per_pair": 2 * (M * M + 4 * M + 12),
                          "evaluated_pairs": {"direct": st["far_pairs_direct"] * share,
                                              "cheb_nodes": st["cheb_node_pairs"] * share,
                                              "algorithmic_P_far": st["far_pairs"] * share},
-                         "executed_frac": (st["far_pairs_direct"] + st["cheb_node_pairs"]) * share
-                                          * 2 * (M * M + 4 * M + 12)
-                                          / (far_ms * 1e-3) / 1e12 / peak_tf,
-                         "note": "achieved = SURVEY flops for all P_far pairs / far time; the "
-                                 "coarse levels evaluate the reference M2P only at Chebyshev "
-                                 "nodes (cheb_nodes pairs), so achieved exceeds the pipe peak; "
-                                 "executed_frac is the hardware DFMA-pipe figure (far_ms also "
-                                 "holds the small series/evaluation kernels)",
+                         "survey_model": {"achieved": survey_achieved,
+                                          "frac": survey_achieved / peak_tf,
+                                          "flops": far_flops,
+                                          "model": "SURVEY 8(d): P_far x (4K+6Ke+6(M+1)+12) for "
+                                                   "every reference (target, block) pair",
+                                          "note": "the reference-algorithm work the far field "
+                                                  "replaces; exceeds the pipe peak because the "
+                                                  "Horner form needs ~0.55x the flops per pair "
+                                                  "and levels 1..L-2 are evaluated only at "
+                                                  "Chebyshev nodes"},
                          "far_ms": far_ms, "near_ms": near_ms, "moments_ms": mom_ms,
                          "far_share_of_step": far_ms / ms if world == 1 else None},
             "cpu_baseline": cpu,
