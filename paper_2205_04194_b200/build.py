@@ -16,8 +16,9 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-OBJ = os.path.join(HERE, "build_obj")
-LIB = os.path.join(HERE, "libimqfast.so")
+_TAG = os.environ.get("IMQ_BUILD_TAG", "")  # development variants: build_obj_<tag>, libimqfast_<tag>.so
+OBJ = os.path.join(HERE, "build_obj" + (f"_{_TAG}" if _TAG else ""))
+LIB = os.path.join(HERE, f"libimqfast_{_TAG}.so" if _TAG else "libimqfast.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-ffp-contract=off,-fvisibility=hidden",

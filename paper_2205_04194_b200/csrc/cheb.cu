@@ -9,12 +9,12 @@
 // "targets", operator.cu), turned into a tensor Chebyshev series of degree
 // n-1, pushed down the levels (the restriction of a degree-(n-1) series to a
 // child box is again exactly such a series), and summed at every target of
-// the level-lc boxes.  With n = 20 the interpolation error of one box's field
-// is <= ~1e-13 of its maximum (tests vs the oracle).
+// the level-lc boxes.  With n = kChebN = 18 the interpolation error of one
+// box's field is <= ~1e-13 of its maximum (tests vs the oracle).
 //
 // Layouts: per box (levels 1..lc, all boxes, level-major, Morton inside a
-// level) 400 node values / coefficients, index [box][i * 20 + j], i the x
-// index and j the y index; x_i = c_x + (cell/2) cos(pi (i + 1/2) / 20).
+// level) n^2 node values / coefficients, index [box][i * n + j], i the x
+// index and j the y index; x_i = c_x + (cell/2) cos(pi (i + 1/2) / n).
 #include "imq_device.cuh"
 #include "imq_kernels.hpp"
 

@@ -91,7 +91,10 @@ void launch_m2p_far(const TreeParams& P, const int4* items, const int* group_off
 bool m2p_specialised(int M);
 
 // ---- coarse far field by Chebyshev interpolation (cheb.cu)
-constexpr int kChebN = 20;  // nodes per dimension (degree kChebN - 1)
+#ifndef IMQ_CHEB_N
+#define IMQ_CHEB_N 18
+#endif
+constexpr int kChebN = IMQ_CHEB_N;  // nodes per dimension (degree kChebN - 1), even
 void cheb_set_tables(const double* T, const double* S_left, const double* S_right);
 void launch_cheb_nodes(const TreeParams& P, int l, long long box_base, double* nx, double* ny,
                        cudaStream_t s);

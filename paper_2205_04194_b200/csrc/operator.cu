@@ -592,8 +592,12 @@ void DeviceOperator::build_cheb(int p_lo, int p_hi) {
       boxes.push_back((int)q);
       const int par = (int)(q << (2 * (L_ - 1 - l)));
       const int start = (int)((cheb_base_[(size_t)l] + q) * NN);
-      for (int c = 0; c < NN; c += 224) {
-        const int cnt = std::min(224, NN - c);
+      // node chunks of <= 32 * kFarMaxR, balanced (400 -> 224 + 176, 256 -> 256)
+      constexpr int kMaxChunk = 256;
+      constexpr int kChunks = (NN + kMaxChunk - 1) / kMaxChunk;
+      constexpr int kChunk = ((NN + kChunks - 1) / kChunks + 31) / 32 * 32;
+      for (int c = 0; c < NN; c += kChunk) {
+        const int cnt = std::min(kChunk, NN - c);
         g[(size_t)((cnt + 31) / 32 - 1)].push_back(make_int4(par, start + c, cnt, l));
       }
     }
