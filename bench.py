@@ -405,7 +405,7 @@ def b200_arm(args):
             r = (fi[:, 2] + 31) // 32
             drop = np.nonzero(r[1:] < r[:-1])[0]
             fine = fi[:int(drop[0]) + 1] if len(drop) else fi
-            far_launches = groups(fine) + 2 + st["cheb_levels"] + 1
+            far_launches = groups(fine) + 2 + st["cheb_levels"] + 1 + 2 * st["cheb_ring"]
         launches_per_step = 1 + 1 + L + far_launches + near_launches
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -426,7 +426,9 @@ def b200_arm(args):
                             "sharded ext API, pinned host buffers"},
             "roofline": {"bound": "fp64",
                          "kernel": "k_m2p_far (M2P far field: direct for the fine levels, at "
-                                   "Chebyshev nodes for levels 1..%d) + k_cheb_*" % st["cheb_levels"],
+                                   "Chebyshev nodes for levels 1..%d%s) + k_cheb_*"
+                                   % (st["cheb_levels"], " and the level-%d ring" % (L - 1)
+                                      if st["cheb_ring"] else ""),
                          "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
                          "frac": achieved / peak_tf, "traffic": traffic,
                          "traffic_unit": "DRAM bytes per product over the far-field launches "

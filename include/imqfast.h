@@ -150,6 +150,7 @@ typedef struct {
   double far_pairs_direct; /* (target, block) pairs evaluated directly */
   double cheb_node_pairs;  /* (Chebyshev node, block) pairs of the coarse levels */
   int cheb_levels;         /* levels 1..cheb_levels evaluated through Chebyshev nodes (0: none) */
+  int cheb_ring;           /* 1: the level-(L-1) ring also goes through the level-(L-2) nodes */
 } imq_ext_stats;
 IMQ_API int imq_ext_operator_stats(const imq_operator* op, imq_ext_stats* out);
 

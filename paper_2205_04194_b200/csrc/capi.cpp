@@ -514,6 +514,7 @@ int imq_ext_operator_stats(const imq_operator* op, imq_ext_stats* out) {
     out->far_pairs_direct = c.far_pairs_direct;
     out->cheb_node_pairs = c.cheb_node_pairs;
     out->cheb_levels = c.cheb_levels;
+    out->cheb_ring = c.cheb_ring;
     return IMQ_OK;
   });
 }

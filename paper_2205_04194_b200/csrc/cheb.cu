@@ -28,6 +28,10 @@ constexpr int NN = NC * NC;
 
 __constant__ double c_T[NN];      // T[k * NC + i] = cos(k theta_i), theta_i = pi (i + 1/2) / NC
 __constant__ double c_S[2][NN];   // child restriction, [half][k' * NC + k]
+constexpr int NR = kChebNR;       // ring nodes per dimension on the level-(L-2) boxes
+constexpr int NRR = NR * NR;
+__constant__ double c_TR[NRR];       // cos(k theta_i), theta_i = pi (i + 1/2) / NR
+__constant__ double c_B[2][NC * NR];  // ring values -> child coefficients, [half][k' * NR + i]
 
 __global__ void k_cheb_nodes(const TreeParams P, int l, long long box_base, double* __restrict__ nx,
                              double* __restrict__ ny) {
@@ -41,6 +45,69 @@ __global__ void k_cheb_nodes(const TreeParams P, int l, long long box_base, doub
   const double h = 0.5 * P.cell[l];
   nx[(box_base + q) * NN + r] = block_center(P.ox, bi, P.cell[l]) + h * c_T[NC + i];
   ny[(box_base + q) * NN + r] = block_center(P.oy, bj, P.cell[l]) + h * c_T[NC + j];
+}
+
+// Ring nodes: NR x NR Chebyshev nodes of every box of level l, [box][i * NR + j].
+__global__ void k_cheb_nodes_ring(const TreeParams P, int l, double* __restrict__ nx,
+                                  double* __restrict__ ny) {
+  const long long nb = 1ll << (2 * (l + 1));
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nb * NRR) return;
+  const uint32_t q = (uint32_t)(t / NRR);
+  const int r = (int)(t % NRR), i = r / NR, j = r % NR;
+  int bi, bj;
+  demorton(q, bi, bj);
+  const double h = 0.5 * P.cell[l];
+  nx[t] = block_center(P.ox, bi, P.cell[l]) + h * c_TR[NR + i];
+  ny[t] = block_center(P.oy, bj, P.cell[l]) + h * c_TR[NR + j];
+}
+
+// One CTA per level-(L-2) box A (listed in `boxes`): for each child c of A
+// (Morton 4A + 2 hx + hy), the degree-(NC-1) series on c of
+//   ring field of A:  B_hx V_A B_hy^T   (V_A: NR x NR node values)
+//   series of A:      S_hx C_A S_hy^T   (C_A: NC x NC coefficients)
+// coef_c[c] = their sum; the level-(L-1) series evaluated at the targets.
+__global__ void __launch_bounds__(NN) k_cheb_ring_coef(const int* __restrict__ boxes,
+                                                       long long base_a,
+                                                       const double* __restrict__ coef_a,
+                                                       const double* __restrict__ ring_vals,
+                                                       double* __restrict__ coef_c) {
+  __shared__ double V[NRR], W[2][NR * NC], U[2][NN], Ca[NN], B[2][NC * NR], S[2][NN];
+  const uint32_t a = (uint32_t)boxes[blockIdx.x];
+  const int r = threadIdx.x;
+  for (int o = r; o < NRR; o += NN) V[o] = ring_vals[(size_t)a * NRR + o];
+  for (int o = r; o < 2 * NC * NR; o += NN) (&B[0][0])[o] = (&c_B[0][0])[o];
+  Ca[r] = coef_a[(size_t)(base_a + a) * NN + r];
+  S[0][r] = c_S[0][r];
+  S[1][r] = c_S[1][r];
+  __syncthreads();
+  // W[h][i][m'] = sum_j V[i][j] B[h][m'][j];  U[h][k][m'] = sum_j Ca[k][j] S[h][m'][j]
+  for (int o = r; o < 2 * NR * NC; o += NN) {
+    const int h = o / (NR * NC), i = (o / NC) % NR, m = o % NC;
+    double acc = 0.0;
+#pragma unroll 4
+    for (int j = 0; j < NR; ++j) acc = fma(V[i * NR + j], B[h][m * NR + j], acc);
+    W[h][i * NC + m] = acc;
+  }
+  for (int o = r; o < 2 * NN; o += NN) {
+    const int h = o / NN, k = (o / NC) % NC, m = o % NC;
+    double acc = 0.0;
+#pragma unroll 6
+    for (int j = 0; j < NC; ++j) acc = fma(Ca[k * NC + j], S[h][m * NC + j], acc);
+    U[h][k * NC + m] = acc;
+  }
+  __syncthreads();
+  const int k = r / NC, m = r % NC;
+#pragma unroll 1
+  for (int c = 0; c < 4; ++c) {
+    const int hx = c >> 1, hy = c & 1;
+    double acc = 0.0;
+#pragma unroll 4
+    for (int i = 0; i < NR; ++i) acc = fma(B[hx][k * NR + i], W[hy][i * NC + m], acc);
+#pragma unroll 6
+    for (int kk = 0; kk < NC; ++kk) acc = fma(S[hx][k * NC + kk], U[hy][kk * NC + m], acc);
+    coef_c[(size_t)(4 * a + c) * NN + r] = acc;
+  }
 }
 
 // One CTA per box of level l (boxes listed in `boxes`): node values ->
@@ -164,6 +231,24 @@ void cheb_set_tables(const double* T, const double* S_left, const double* S_righ
   cudaMemcpyToSymbol(c_T, T, NN * sizeof(double));
   cudaMemcpyToSymbol(c_S, S_left, NN * sizeof(double), 0);
   cudaMemcpyToSymbol(c_S, S_right, NN * sizeof(double), NN * sizeof(double));
+}
+
+void cheb_set_ring_tables(const double* T_nr, const double* B_left, const double* B_right) {
+  cudaMemcpyToSymbol(c_TR, T_nr, NRR * sizeof(double));
+  cudaMemcpyToSymbol(c_B, B_left, NC * NR * sizeof(double), 0);
+  cudaMemcpyToSymbol(c_B, B_right, NC * NR * sizeof(double), NC * NR * sizeof(double));
+}
+
+void launch_cheb_nodes_ring(const TreeParams& P, int l, double* nx, double* ny, cudaStream_t s) {
+  const long long n = (1ll << (2 * (l + 1))) * NRR;
+  k_cheb_nodes_ring<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(P, l, nx, ny);
+}
+
+void launch_cheb_ring_coef(const int* boxes, int n_boxes, long long base_a,
+                           const double* coef_a, const double* ring_vals, double* coef_c,
+                           cudaStream_t s) {
+  if (n_boxes)
+    k_cheb_ring_coef<<<(unsigned)n_boxes, NN, 0, s>>>(boxes, base_a, coef_a, ring_vals, coef_c);
 }
 
 void launch_cheb_nodes(const TreeParams& P, int l, long long box_base, double* nx, double* ny,

@@ -430,8 +430,13 @@ constexpr int kFarMaxR = 8;    // a far work item holds <= 32 * kFarMaxR targets
 // at levels 1..L-1 of the (shared) ancestor lists, then the level-L union over
 // the children of the parent's 3x3 neighbourhood that some present leaf needs.
 // Entries are (level << 28 | block) in the reference's list order.
+// ring (level L-1 only): 0 = the whole list; 1 = without the "ring" of the
+// level-(L-2) ancestor A (the children of A's 3x3 neighbourhood at Chebyshev
+// distance >= 2 from all four children of A -- the outer ring of the 6x6
+// candidate square, common to the lists of all of A's descendants); 2 = the
+// ring only (Chebyshev-node items of A, cheb.cu).
 __device__ int build_far_list(const TreeParams& P, uint32_t par, int s, int cnt, uint32_t* list,
-                              int lane, int lmin, int lmax) {
+                              int lane, int lmin, int lmax, int ring = 0) {
   const int L = P.L;
   const int e = s + cnt;
   bool present = false;
@@ -470,6 +475,11 @@ __device__ int build_far_list(const TreeParams& P, uint32_t par, int s, int cnt,
         const int qi = lo_i + c / wj, qj = lo_j + c % wj;
         if (l < L) {
           keep = max(abs(qi - ai), abs(qj - aj)) >= 2;
+          if (ring && l == L - 1) {
+            const int ri = qi - 2 * (ai >> 1), rj = qj - 2 * (aj >> 1);
+            const bool in_ring = ri == -2 || ri == 3 || rj == -2 || rj == 3;
+            keep = ring == 2 ? in_ring : (keep && !in_ring);
+          }
         } else {
           int pi, pj;
           demorton(par, pi, pj);
@@ -720,6 +730,7 @@ struct FarOut {
   const int* perm;
   const double* far_add;  // or nullptr
   int lmin, lmax;
+  int ring;  // build_far_list ring mode of items without a level tag
 };
 
 __device__ __forceinline__ void far_store(const TreeParams& P, const FarOut& O, int q,
@@ -765,9 +776,10 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_m2p_far(const TreeParams P
   const int4 item = items[it];
   const uint32_t par = (uint32_t)item.x;
   const int s0 = item.y, cnt = item.z;
-  const int lev = item.w;  // > 0: this item's level only (Chebyshev node items)
+  // item.w > 0: Chebyshev node item of level (w & 0xff) only, ring mode w >> 8
+  const int lev = item.w & 0xff, ring = lev > 0 ? (item.w >> 8) : O.ring;
   const int n = build_far_list(P, par, s0, cnt, list, lane, lev > 0 ? lev : O.lmin,
-                               lev > 0 ? lev : O.lmax);
+                               lev > 0 ? lev : O.lmax, ring);
   Targets<R> T;
   load_targets<R>(P, s0, cnt, lane, T);
   const int L = P.L;
@@ -844,9 +856,9 @@ __global__ void __launch_bounds__(WARPS * 32) k_m2p_far_generic(const TreeParams
   const uint32_t par = (uint32_t)item.x;
   const int s0 = item.y, cnt = item.z;
   uint32_t* list = lists[warp];
-  const int lev = item.w;
+  const int lev = item.w & 0xff, ring = lev > 0 ? (item.w >> 8) : O.ring;
   const int n = build_far_list(P, par, s0, cnt, list, lane, lev > 0 ? lev : O.lmin,
-                               lev > 0 ? lev : O.lmax);
+                               lev > 0 ? lev : O.lmax, ring);
   for (int p0 = lane; p0 < cnt; p0 += 32) {
     const int p = s0 + p0;
     const double x = P.xs[p], y = P.ys[p];
@@ -1023,11 +1035,11 @@ void launch_scatter_rows(const double* src, const int* idx, int n, int width, do
 void launch_m2p_far(const TreeParams& P, const int4* items, const int* group_off, int begin,
                     int end, const double2* coef, double* far_s_ptr, const cudaStream_t* streams,
                     int nstreams, const double* near_part, int nslots, double* out,
-                    const int* perm, const double* far_add, int lmin, int lmax) {
+                    const int* perm, const double* far_add, int lmin, int lmax, int ring) {
   if (end <= begin) return;
   if (lmin < 1) lmin = 1;
   if (lmax < 1 || lmax > P.L) lmax = P.L;
-  const FarOut far_s{far_s_ptr, near_part, nslots, out, perm, far_add, lmin, lmax};
+  const FarOut far_s{far_s_ptr, near_part, nslots, out, perm, far_add, lmin, lmax, ring};
   cudaStream_t s = streams[0];
   int launched = 0;
   if (!m2p_specialised(P.M)) {

@@ -87,7 +87,8 @@ void launch_m2p_far(const TreeParams& P, const int4* items, const int* group_off
                     int end, const double2* coef, double* far_s, const cudaStream_t* streams,
                     int nstreams, const double* near_part = nullptr, int nslots = 0,
                     double* out = nullptr, const int* perm = nullptr,
-                    const double* far_add = nullptr, int lmin = 1, int lmax = 0);
+                    const double* far_add = nullptr, int lmin = 1, int lmax = 0,
+                    int ring = 0);
 bool m2p_specialised(int M);
 
 // ---- coarse far field by Chebyshev interpolation (cheb.cu)
@@ -95,7 +96,24 @@ bool m2p_specialised(int M);
 #define IMQ_CHEB_N 18
 #endif
 constexpr int kChebN = IMQ_CHEB_N;  // nodes per dimension (degree kChebN - 1), even
+// The ring of level L-1 (build_far_list) is interpolated on the level-(L-2)
+// boxes at kChebNR^2 nodes (its block centres sit 2.5 half-widths from the box
+// centre instead of 4), then restricted to the level-(L-1) boxes at kChebN.
+#ifndef IMQ_CHEB_NR
+#define IMQ_CHEB_NR 26
+#endif
+constexpr int kChebNR = IMQ_CHEB_NR;
 void cheb_set_tables(const double* T, const double* S_left, const double* S_right);
+// B[half][k' * NR + i]: ring node values on a level-(L-2) box (NR x NR nodes)
+// -> degree-(NC-1) coefficients on its child half (interpolation at the
+// child's NC nodes of the degree-(NR-1) interpolant).
+void cheb_set_ring_tables(const double* T_nr, const double* B_left, const double* B_right);
+void launch_cheb_nodes_ring(const TreeParams& P, int l, double* nx, double* ny, cudaStream_t s);
+// One CTA per listed level-(L-2) box A: coef_c[child] = B V_A B^T (ring) +
+// S C_A S^T (series of A restricted), for the four children of A.
+void launch_cheb_ring_coef(const int* boxes, int n_boxes, long long base_a,
+                           const double* coef_a, const double* ring_vals, double* coef_c,
+                           cudaStream_t s);
 void launch_cheb_nodes(const TreeParams& P, int l, long long box_base, double* nx, double* ny,
                        cudaStream_t s);
 void launch_cheb_coef(int l, const int* boxes, int n_boxes, long long base_l,

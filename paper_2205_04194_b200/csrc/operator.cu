@@ -118,6 +118,8 @@ void DeviceOperator::release() {
   dfree(d_contrib_); dfree(d_near_s_); dfree(d_farc_); dfree(d_pull_items_);
   dfree(d_cheb_items_); dfree(d_cboxes_); dfree(d_ceval_items_);
   dfree(d_cnx_); dfree(d_cny_); dfree(d_cnleaf_); dfree(d_cval_); dfree(d_ccoef_);
+  dfree(d_rnx_); dfree(d_rny_); dfree(d_rnleaf_); dfree(d_rval_); dfree(d_rcoef_);
+  dfree(d_ring_items_); dfree(d_rboxes_);
   if (solve_pin_) cudaFreeHost(solve_pin_);
   solve_pin_ = nullptr;
   solve_pin_bytes_ = 0;
@@ -522,8 +524,10 @@ void DeviceOperator::build_pair_items(int p_lo, int p_hi) {
 void DeviceOperator::build_cheb(int p_lo, int p_hi) {
   constexpr int NC = imqk::kChebN, NN = NC * NC;
   cheb_ = false;
+  ring_ = false;
   dfree(d_cheb_items_); dfree(d_cboxes_); dfree(d_ceval_items_);
-  n_cheb_items_ = n_ceval_ = 0;
+  dfree(d_ring_items_); dfree(d_rboxes_);
+  n_cheb_items_ = n_ceval_ = n_ring_items_ = n_ring_boxes_ = 0;
   if (!far_split_ || getenv("IMQ_FAR_NOCHEB") || !imqk::m2p_specialised(M_)) return;
   const int lc = L_ - 2;
   const std::vector<int>& ls = leaf_start_h_;
@@ -610,12 +614,93 @@ void DeviceOperator::build_cheb(int p_lo, int p_hi) {
     cheb_group_off_[r + 1] = (int)citems.size();
   }
   for (size_t r = g.size() + 1; r < 16; ++r) cheb_group_off_[r] = (int)citems.size();
+  // the level-(L-1) ring through NR x NR nodes of the level-lc boxes, when
+  // those boxes hold on average >= 1.25x as many targets as ring nodes
+  constexpr int NR = imqk::kChebNR, NRR = NR * NR;
+  ring_ = !getenv("IMQ_FAR_NORING") && (double)tot >= 1.25 * NRR * (double)nonempty;
+  std::vector<int4> ritems;
+  std::vector<int> rboxes;
+  ring_group_off_.assign(16, 0);
+  if (ring_) {
+    const long long nbl = 1ll << (2 * (lc + 1));
+    if (ring_nodes_ != (size_t)nbl * NRR) {
+      dfree(d_rnx_); dfree(d_rny_); dfree(d_rnleaf_); dfree(d_rval_); dfree(d_rcoef_);
+      ring_nodes_ = (size_t)nbl * NRR;
+      d_rnx_ = dalloc<double>(ring_nodes_, "ring nodes");
+      d_rny_ = dalloc<double>(ring_nodes_, "ring nodes");
+      d_rnleaf_ = dalloc<uint32_t>(ring_nodes_, "ring node keys");
+      d_rval_ = dalloc<double>(ring_nodes_, "ring values");
+      d_rcoef_ = dalloc<double>((size_t)(4 * nbl) * NN, "ring child coefficients");
+      cuda_check(cudaMemset(d_rnleaf_, 0, ring_nodes_ * sizeof(uint32_t)), "ring keys");
+      const long double pi = 3.141592653589793238462643383279502884L;
+      std::vector<double> TR((size_t)NRR), B[2];
+      for (int k = 0; k < NR; ++k)
+        for (int i = 0; i < NR; ++i) TR[(size_t)k * NR + i] = (double)cosl(k * pi * (i + 0.5L) / NR);
+      // B[h][k'][i] = (2/NC) w_k' sum_i' T_k'(u_i') l_i((u_i' -/+ 1) / 2), l_i the
+      // Lagrange basis of the NR parent nodes, l_i(y) = (2/NR) sum_k w_k T_k(x_i) T_k(y)
+      for (int h = 0; h < 2; ++h) {
+        B[h].assign((size_t)NC * NR, 0.0);
+        for (int kp = 0; kp < NC; ++kp)
+          for (int i = 0; i < NR; ++i) {
+            const long double xi = cosl(pi * (i + 0.5L) / NR);
+            long double acc = 0;
+            for (int ip = 0; ip < NC; ++ip) {
+              const long double u = cosl(pi * (ip + 0.5L) / NC);
+              const long double y = h == 0 ? (u - 1) / 2 : (u + 1) / 2;
+              long double li = 0;
+              for (int k = 0; k < NR; ++k)
+                li += (k == 0 ? 0.5L : 1.0L) * cosl(k * acosl(xi)) * cosl(k * acosl(y));
+              acc += cosl(kp * pi * (ip + 0.5L) / NC) * (2.0L / NR) * li;
+            }
+            B[h][(size_t)kp * NR + i] = (double)((2.0L / NC) * (kp == 0 ? 0.5L : 1.0L) * acc);
+          }
+      }
+      imqk::cheb_set_ring_tables(TR.data(), B[0].data(), B[1].data());
+      imqk::launch_cheb_nodes_ring(P_, lc, d_rnx_, d_rny_, stream_);
+      cuda_check(cudaStreamSynchronize(stream_), "ring nodes");
+    }
+    Pr_ = P_;
+    Pr_.xs = d_rnx_;
+    Pr_.ys = d_rny_;
+    Pr_.leaf = d_rnleaf_;
+    Pr_.N = (int)ring_nodes_;
+    constexpr int kChunks = (NRR + 255) / 256;
+    constexpr int kChunk = ((NRR + kChunks - 1) / kChunks + 31) / 32 * 32;
+    std::vector<std::vector<int4>> rg((size_t)imqk::far_max_points_per_lane());
+    for (int k = cbox_off_[(size_t)lc]; k < cbox_off_[(size_t)lc + 1]; ++k) {
+      const int q = boxes[(size_t)k];
+      rboxes.push_back(q);
+      for (int c = 0; c < NRR; c += kChunk) {
+        const int cnt = std::min(kChunk, NRR - c);
+        rg[(size_t)((cnt + 31) / 32 - 1)].push_back(
+            make_int4(q << 2, (int)((long long)q * NRR + c), cnt, (L_ - 1) | (2 << 8)));
+      }
+    }
+    for (size_t r = 0; r < rg.size(); ++r) {
+      ritems.insert(ritems.end(), rg[r].begin(), rg[r].end());
+      ring_group_off_[r + 1] = (int)ritems.size();
+    }
+    for (size_t r = rg.size() + 1; r < 16; ++r) ring_group_off_[r] = (int)ritems.size();
+  }
+  // evaluation items: targets of the level-lc boxes, or with the ring of the
+  // level-(L-1) boxes (their series carries the ring's field)
   std::vector<int4> ev;
   const int per = imqk::cheb_eval_points_per_item();
-  for (long long q = 0; q < (1ll << (2 * (lc + 1))); ++q) {
-    const int sh = 2 * (L_ - lc);
+  const int le = ring_ ? L_ - 1 : lc;
+  for (long long q = 0; q < (1ll << (2 * (le + 1))); ++q) {
+    const int sh = 2 * (L_ - le);
     const int a = std::max(p_lo, ls[(size_t)(q << sh)]), b = std::min(p_hi, ls[(size_t)((q + 1) << sh)]);
     for (int c = a; c < b; c += per) ev.push_back(make_int4((int)q, c, std::min(per, b - c), 0));
+  }
+  n_ring_items_ = (int)ritems.size();
+  n_ring_boxes_ = (int)rboxes.size();
+  if (ring_) {
+    d_ring_items_ = dalloc<int4>(ritems.size(), "ring items");
+    d_rboxes_ = dalloc<int>(rboxes.size(), "ring boxes");
+    cuda_check(cudaMemcpy(d_ring_items_, ritems.data(), ritems.size() * sizeof(int4),
+                          cudaMemcpyHostToDevice), "H2D ring items");
+    cuda_check(cudaMemcpy(d_rboxes_, rboxes.data(), rboxes.size() * sizeof(int),
+                          cudaMemcpyHostToDevice), "H2D ring boxes");
   }
   n_cheb_items_ = (int)citems.size();
   n_ceval_ = (int)ev.size();
@@ -713,7 +798,21 @@ std::vector<double> parent_work(const std::vector<int>& ls, int L, int M) {
         const double na = (double)ls[(size_t)((a + 1) << sh)] - ls[(size_t)(a << sh)];
         wl = std::min(1.0, (double)(imqk::kChebN * imqk::kChebN) / na);
       }
-      shared += wl * ns[(size_t)l][(size_t)a];
+      double nl = ns[(size_t)l][(size_t)a];
+      if (L >= 4 && l == L - 1) {  // the ring goes through the level-(L-2) box's nodes
+        int ai, aj;
+        imqdev::demorton((uint32_t)(p >> 2), ai, aj);
+        const int g1 = 1 << L;
+        double nr = 0;
+        for (int qi = std::max(0, 2 * ai - 2); qi <= std::min(g1 - 1, 2 * ai + 3); ++qi)
+          for (int qj = std::max(0, 2 * aj - 2); qj <= std::min(g1 - 1, 2 * aj + 3); ++qj) {
+            const int ri = qi - 2 * ai, rj = qj - 2 * aj;
+            if ((ri == -2 || ri == 3 || rj == -2 || rj == 3) && count(L - 1, qi, qj) > 0) nr += 1;
+          }
+        const double na = (double)ls[(size_t)((p >> 2) + 1) << 4] - ls[(size_t)(p >> 2) << 4];
+        nl += nr * (std::min(1.0, (double)(imqk::kChebNR * imqk::kChebNR) / na) - 1.0);
+      }
+      shared += wl * nl;
     }
     if (L >= 4) shared += 1.4;
     double far = shared * (double)np, near = 0.0;
@@ -921,7 +1020,7 @@ void DeviceOperator::far_near(const double* d_us, double* d_out, const int* perm
   auto far_pass = [&](int b, int e, const int* goff, const double* near_part, int nslots,
                       double* out, const int* pm, double* far_s, const double* far_add, int lmin,
                       int lmax, const imqk::TreeParams* Pp = nullptr,
-                      const int4* its = nullptr) {
+                      const int4* its = nullptr, int ring = 0) {
     if (e <= b) return;
     cudaStream_t ss[1 + kAuxStreams] = {s};
     cuda_check(cudaEventRecord(ev_fork_, s), "fork");
@@ -930,7 +1029,7 @@ void DeviceOperator::far_near(const double* d_us, double* d_out, const int* perm
       cuda_check(cudaStreamWaitEvent(aux_[k], ev_fork_, 0), "fork wait");
     }
     imqk::launch_m2p_far(Pp ? *Pp : P_, its ? its : d_far_items_, goff, b, e, d_coef_, far_s, ss,
-                         far_streams_, near_part, nslots, out, pm, far_add, lmin, lmax);
+                         far_streams_, near_part, nslots, out, pm, far_add, lmin, lmax, ring);
     for (int k = 0; k < kAuxStreams; ++k) {
       cuda_check(cudaEventRecord(ev_join_[k], aux_[k]), "join");
       cuda_check(cudaStreamWaitEvent(s, ev_join_[k], 0), "join wait");
@@ -940,24 +1039,35 @@ void DeviceOperator::far_near(const double* d_us, double* d_out, const int* perm
   const int nslots = near_pair_ ? 1 : 5;
   if (far_split_) {
     // coarse pass (levels 1..L-2) into d_farc_, then the fine pass (L-1..L)
-    if (cheb_ && far_end > n_far_fine_) {
+    const bool cheb_run = cheb_ && far_end > n_far_fine_;
+    if (cheb_run) {
       // list fields at the Chebyshev nodes of every box, series per level
       // (parent restricted + own), summed at the targets of the level-lc boxes
       far_pass(0, n_cheb_items_, cheb_group_off_.data(), nullptr, 0, nullptr, nullptr, d_cval_,
                nullptr, 1, cheb_lc_, &Pn_, d_cheb_items_);
+      if (ring_)  // the level-(L-1) ring at the NR x NR nodes of the level-lc boxes
+        far_pass(0, n_ring_items_, ring_group_off_.data(), nullptr, 0, nullptr, nullptr, d_rval_,
+                 nullptr, L_ - 1, L_ - 1, &Pr_, d_ring_items_);
       for (int l = 1; l <= cheb_lc_; ++l)
         imqk::launch_cheb_coef(l, d_cboxes_ + cbox_off_[(size_t)l],
                                cbox_off_[(size_t)l + 1] - cbox_off_[(size_t)l],
                                cheb_base_[(size_t)l], l > 1 ? cheb_base_[(size_t)l - 1] : 0,
                                d_cval_, d_ccoef_, s);
-      imqk::launch_cheb_eval(P_, cheb_lc_, d_ceval_items_, n_ceval_, cheb_base_[(size_t)cheb_lc_],
-                             d_ccoef_, d_farc_, s);
+      if (ring_) {
+        imqk::launch_cheb_ring_coef(d_rboxes_, n_ring_boxes_, cheb_base_[(size_t)cheb_lc_],
+                                    d_ccoef_, d_rval_, d_rcoef_, s);
+        imqk::launch_cheb_eval(P_, L_ - 1, d_ceval_items_, n_ceval_, 0, d_rcoef_, d_farc_, s);
+      } else {
+        imqk::launch_cheb_eval(P_, cheb_lc_, d_ceval_items_, n_ceval_,
+                               cheb_base_[(size_t)cheb_lc_], d_ccoef_, d_farc_, s);
+      }
     } else {
       far_pass(std::max(far_begin, n_far_fine_), far_end, far_cgroup_off_.data(), nullptr, 0,
                nullptr, nullptr, d_farc_, nullptr, 1, L_ - 2);
     }
     far_pass(far_begin, std::min(far_end, n_far_fine_), far_group_off_.data(), near_part, nslots,
-             d_out, perm, d_far_, d_farc_, L_ - 1, L_);
+             d_out, perm, d_far_, d_farc_, L_ - 1, L_, nullptr, nullptr,
+             cheb_run && ring_ ? 1 : 0);
   } else {
     far_pass(far_begin, far_end, far_group_off_.data(), near_part, nslots, d_out, perm, d_far_,
              nullptr, 1, L_);
@@ -1058,6 +1168,20 @@ PairCounts DeviceOperator::pair_counts() {
   };
   double far = 0, near = 0;
   far_by_level_.assign((size_t)L + 1, 0.0);
+  ring_direct_ = ring_lists_ = 0;
+  if (L >= 3) {  // ring lists of the non-empty level-(L-2) boxes (node pairs / NR^2)
+    const int ga = 1 << (L - 1), g1 = 1 << L;
+    for (int ai = 0; ai < ga; ++ai)
+      for (int aj = 0; aj < ga; ++aj) {
+        if (!count(L - 2, ai, aj)) continue;
+        for (int qi = std::max(0, 2 * ai - 2); qi <= std::min(g1 - 1, 2 * ai + 3); ++qi)
+          for (int qj = std::max(0, 2 * aj - 2); qj <= std::min(g1 - 1, 2 * aj + 3); ++qj) {
+            const int ri = qi - 2 * ai, rj = qj - 2 * aj;
+            if ((ri == -2 || ri == 3 || rj == -2 || rj == 3) && count(L - 1, qi, qj) > 0)
+              ring_lists_ += 1;
+          }
+      }
+  }
   lists_by_level_.assign((size_t)L + 1, 0.0);
   for (int l = 1; l <= L; ++l) {
     const int grid = 1 << (l + 1);
@@ -1077,6 +1201,16 @@ PairCounts DeviceOperator::pair_counts() {
         far += (double)nt * (double)ns;
         far_by_level_[(size_t)l] += (double)nt * (double)ns;
         lists_by_level_[(size_t)l] += (double)ns;
+        if (l == L - 1 && L >= 3) {  // the ring of the level-(L-2) parent
+          const int pi = i >> 1, pj = j >> 1;
+          long long nr = 0;
+          for (int qi = lo_i; qi <= hi_i; ++qi)
+            for (int qj = lo_j; qj <= hi_j; ++qj) {
+              const int ri = qi - 2 * pi, rj = qj - 2 * pj;
+              if ((ri == -2 || ri == 3 || rj == -2 || rj == 3) && count(l, qi, qj) > 0) ++nr;
+            }
+          ring_direct_ += (double)nt * (double)nr;
+        }
         if (l == L) {
           long long nn = 0;
           for (int qi = std::max(0, i - 1); qi <= std::min(grid - 1, i + 1); ++qi)
@@ -1105,9 +1239,14 @@ void DeviceOperator::fill_eval_counts() {
     if (l <= lc) nodes += lists_by_level_[(size_t)l] * imqk::kChebN * imqk::kChebN;
     else direct += far_by_level_[(size_t)l];
   }
+  if (cheb_ && ring_) {
+    direct -= ring_direct_;
+    nodes += ring_lists_ * imqk::kChebNR * imqk::kChebNR;
+  }
   counts_.far_pairs_direct = direct;
   counts_.cheb_node_pairs = nodes;
   counts_.cheb_levels = lc;
+  counts_.cheb_ring = cheb_ && ring_ ? 1 : 0;
 }
 
 // ------------------------------------------------------------------ GMRES --

@@ -36,8 +36,9 @@ struct PairCounts {
   int64_t far_items = 0, near_items = 0;
   int near_mode = 0;  // 0 plain (split sources), 1 symmetric per leaf, 2 chunk pairs
   double far_pairs_direct = 0;  // (target, block) pairs evaluated directly
-  double cheb_node_pairs = 0;   // (Chebyshev node, block) pairs
+  double cheb_node_pairs = 0;   // (Chebyshev node, block) pairs (incl. the level-(L-1) ring)
   int cheb_levels = 0;          // levels 1..cheb_levels through the Chebyshev pass
+  int cheb_ring = 0;            // level-(L-1) ring through the level-(L-2) nodes
 };
 
 std::vector<int> shard_bounds(const std::vector<int>& leaf_start, int L, int world);
@@ -129,6 +130,7 @@ class DeviceOperator {
   void build_cheb(int p_lo, int p_hi);
   void fill_eval_counts();
   std::vector<double> far_by_level_, lists_by_level_;
+  double ring_direct_ = 0, ring_lists_ = 0;  // level-(L-1) ring: target pairs, lists of L-2 boxes
   void setup_sharded_moments(int p_lo, int p_hi);
   void release();
   void apply_sorted_locked(const double* d_us, double* d_bs, const int* perm,
@@ -192,6 +194,16 @@ class DeviceOperator {
   uint32_t* d_cnleaf_ = nullptr;
   int4 *d_cheb_items_ = nullptr, *d_ceval_items_ = nullptr;
   int* d_cboxes_ = nullptr;
+  // level-(L-1) ring through the level-(L-2) boxes' NR x NR nodes (build_cheb)
+  bool ring_ = false;
+  int n_ring_items_ = 0, n_ring_boxes_ = 0;
+  size_t ring_nodes_ = 0;
+  std::vector<int> ring_group_off_;
+  imqk::TreeParams Pr_{};
+  double *d_rnx_ = nullptr, *d_rny_ = nullptr, *d_rval_ = nullptr, *d_rcoef_ = nullptr;
+  uint32_t* d_rnleaf_ = nullptr;
+  int4* d_ring_items_ = nullptr;
+  int* d_rboxes_ = nullptr;
   int4* d_pull_items_ = nullptr;  // sharded symmetric near field: boundary slots
   int n_pull_ = 0;
   int n_far_fine_ = 0;     // far items [0, n_far_fine_) fine, the rest coarse
