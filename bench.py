@@ -405,7 +405,7 @@ def b200_arm(args):
             r = (fi[:, 2] + 31) // 32
             drop = np.nonzero(r[1:] < r[:-1])[0]
             fine = fi[:int(drop[0]) + 1] if len(drop) else fi
-            far_launches = groups(fine) + 2 + st["cheb_levels"] + 1 + 2 * st["cheb_ring"]
+            far_launches = groups(fine) + 2 + st["cheb_levels"] + 1 + st["cheb_ring"] * (2 + st["cheb_levels"])
         launches_per_step = 1 + 1 + L + far_launches + near_launches
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,

@@ -48,8 +48,8 @@ __global__ void k_cheb_nodes(const TreeParams P, int l, long long box_base, doub
 }
 
 // Ring nodes: NR x NR Chebyshev nodes of every box of level l, [box][i * NR + j].
-__global__ void k_cheb_nodes_ring(const TreeParams P, int l, double* __restrict__ nx,
-                                  double* __restrict__ ny) {
+__global__ void k_cheb_nodes_ring(const TreeParams P, int l, long long box_base,
+                                  double* __restrict__ nx, double* __restrict__ ny) {
   const long long nb = 1ll << (2 * (l + 1));
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= nb * NRR) return;
@@ -58,15 +58,16 @@ __global__ void k_cheb_nodes_ring(const TreeParams P, int l, double* __restrict_
   int bi, bj;
   demorton(q, bi, bj);
   const double h = 0.5 * P.cell[l];
-  nx[t] = block_center(P.ox, bi, P.cell[l]) + h * c_TR[NR + i];
-  ny[t] = block_center(P.oy, bj, P.cell[l]) + h * c_TR[NR + j];
+  nx[box_base * NRR + t] = block_center(P.ox, bi, P.cell[l]) + h * c_TR[NR + i];
+  ny[box_base * NRR + t] = block_center(P.oy, bj, P.cell[l]) + h * c_TR[NR + j];
 }
 
-// One CTA per level-(L-2) box A (listed in `boxes`): for each child c of A
+// One CTA per box A of level l - 1 (listed in `boxes`): for each child c of A
 // (Morton 4A + 2 hx + hy), the degree-(NC-1) series on c of
-//   ring field of A:  B_hx V_A B_hy^T   (V_A: NR x NR node values)
-//   series of A:      S_hx C_A S_hy^T   (C_A: NC x NC coefficients)
-// coef_c[c] = their sum; the level-(L-1) series evaluated at the targets.
+//   level-l ring field of A:  B_hx V_A B_hy^T   (V_A: NR x NR node values)
+//   series of A:              S_hx C_A S_hy^T   (C_A: NC x NC coefficients)
+// coef_c[c] = their sum (k_cheb_coef then adds c's own list at level l < L-1;
+// at level L-1 it is the series evaluated at the targets).
 __global__ void __launch_bounds__(NN) k_cheb_ring_coef(const int* __restrict__ boxes,
                                                        long long base_a,
                                                        const double* __restrict__ coef_a,
@@ -111,7 +112,9 @@ __global__ void __launch_bounds__(NN) k_cheb_ring_coef(const int* __restrict__ b
 }
 
 // One CTA per box of level l (boxes listed in `boxes`): node values ->
-// Chebyshev coefficients, plus the parent's series restricted to this box.
+// Chebyshev coefficients, plus the parent's series restricted to this box;
+// base_parent < 0: plus what coef already holds for the box instead (the
+// parent's restricted series and ring, k_cheb_ring_coef).
 __global__ void __launch_bounds__(NN) k_cheb_coef(int l, const int* __restrict__ boxes,
                                                   long long base_l, long long base_parent,
                                                   const double* __restrict__ vals,
@@ -124,7 +127,8 @@ __global__ void __launch_bounds__(NN) k_cheb_coef(int l, const int* __restrict__
   const double* v = vals + (base_l + q) * NN;
   a[r] = v[r];
   T[r] = c_T[r];
-  if (l > 1) {
+  const bool restrict_parent = l > 1 && base_parent >= 0;
+  if (restrict_parent) {
     Sx[r] = c_S[(q >> 1) & 1][r];
     Sy[r] = c_S[q & 1][r];
   }
@@ -140,7 +144,8 @@ __global__ void __launch_bounds__(NN) k_cheb_coef(int l, const int* __restrict__
   double c = 0.0;
   for (int i = 0; i < NC; ++i) c = fma(T[k * NC + i], b[i * NC + m], c);
   c *= (2.0 / NC) * (2.0 / NC) * (k == 0 ? 0.5 : 1.0) * (m == 0 ? 0.5 : 1.0);
-  if (l > 1) {
+  if (base_parent < 0) c += coef[(base_l + q) * NN + r];
+  if (restrict_parent) {
     // parent series restricted to this quadrant: S_x C_p S_y^T
     const double* cp = coef + (base_parent + (q >> 2)) * NN;
     __syncthreads();
@@ -239,9 +244,10 @@ void cheb_set_ring_tables(const double* T_nr, const double* B_left, const double
   cudaMemcpyToSymbol(c_B, B_right, NC * NR * sizeof(double), NC * NR * sizeof(double));
 }
 
-void launch_cheb_nodes_ring(const TreeParams& P, int l, double* nx, double* ny, cudaStream_t s) {
+void launch_cheb_nodes_ring(const TreeParams& P, int l, long long box_base, double* nx, double* ny,
+                            cudaStream_t s) {
   const long long n = (1ll << (2 * (l + 1))) * NRR;
-  k_cheb_nodes_ring<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(P, l, nx, ny);
+  k_cheb_nodes_ring<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(P, l, box_base, nx, ny);
 }
 
 void launch_cheb_ring_coef(const int* boxes, int n_boxes, long long base_a,

@@ -430,11 +430,11 @@ constexpr int kFarMaxR = 8;    // a far work item holds <= 32 * kFarMaxR targets
 // at levels 1..L-1 of the (shared) ancestor lists, then the level-L union over
 // the children of the parent's 3x3 neighbourhood that some present leaf needs.
 // Entries are (level << 28 | block) in the reference's list order.
-// ring (level L-1 only): 0 = the whole list; 1 = without the "ring" of the
-// level-(L-2) ancestor A (the children of A's 3x3 neighbourhood at Chebyshev
+// ring (levels 2..L-1): 0 = the whole list; 1 = without the "ring" of the
+// level-(l-1) ancestor A (the children of A's 3x3 neighbourhood at Chebyshev
 // distance >= 2 from all four children of A -- the outer ring of the 6x6
-// candidate square, common to the lists of all of A's descendants); 2 = the
-// ring only (Chebyshev-node items of A, cheb.cu).
+// candidate square, common to the level-l lists of all of A's descendants);
+// 2 = the ring only (Chebyshev-node items of A, cheb.cu).
 __device__ int build_far_list(const TreeParams& P, uint32_t par, int s, int cnt, uint32_t* list,
                               int lane, int lmin, int lmax, int ring = 0) {
   const int L = P.L;
@@ -475,7 +475,7 @@ __device__ int build_far_list(const TreeParams& P, uint32_t par, int s, int cnt,
         const int qi = lo_i + c / wj, qj = lo_j + c % wj;
         if (l < L) {
           keep = max(abs(qi - ai), abs(qj - aj)) >= 2;
-          if (ring && l == L - 1) {
+          if (ring && l >= 2) {
             const int ri = qi - 2 * (ai >> 1), rj = qj - 2 * (aj >> 1);
             const bool in_ring = ri == -2 || ri == 3 || rj == -2 || rj == 3;
             keep = ring == 2 ? in_ring : (keep && !in_ring);

@@ -108,7 +108,8 @@ void cheb_set_tables(const double* T, const double* S_left, const double* S_righ
 // -> degree-(NC-1) coefficients on its child half (interpolation at the
 // child's NC nodes of the degree-(NR-1) interpolant).
 void cheb_set_ring_tables(const double* T_nr, const double* B_left, const double* B_right);
-void launch_cheb_nodes_ring(const TreeParams& P, int l, double* nx, double* ny, cudaStream_t s);
+void launch_cheb_nodes_ring(const TreeParams& P, int l, long long box_base, double* nx, double* ny,
+                            cudaStream_t s);
 // One CTA per listed level-(L-2) box A: coef_c[child] = B V_A B^T (ring) +
 // S C_A S^T (series of A restricted), for the four children of A.
 void launch_cheb_ring_coef(const int* boxes, int n_boxes, long long base_a,

@@ -119,7 +119,7 @@ void DeviceOperator::release() {
   dfree(d_cheb_items_); dfree(d_cboxes_); dfree(d_ceval_items_);
   dfree(d_cnx_); dfree(d_cny_); dfree(d_cnleaf_); dfree(d_cval_); dfree(d_ccoef_);
   dfree(d_rnx_); dfree(d_rny_); dfree(d_rnleaf_); dfree(d_rval_); dfree(d_rcoef_);
-  dfree(d_ring_items_); dfree(d_rboxes_);
+  dfree(d_ring_items_);
   if (solve_pin_) cudaFreeHost(solve_pin_);
   solve_pin_ = nullptr;
   solve_pin_bytes_ = 0;
@@ -526,8 +526,8 @@ void DeviceOperator::build_cheb(int p_lo, int p_hi) {
   cheb_ = false;
   ring_ = false;
   dfree(d_cheb_items_); dfree(d_cboxes_); dfree(d_ceval_items_);
-  dfree(d_ring_items_); dfree(d_rboxes_);
-  n_cheb_items_ = n_ceval_ = n_ring_items_ = n_ring_boxes_ = 0;
+  dfree(d_ring_items_);
+  n_cheb_items_ = n_ceval_ = n_ring_items_ = 0;
   if (!far_split_ || getenv("IMQ_FAR_NOCHEB") || !imqk::m2p_specialised(M_)) return;
   const int lc = L_ - 2;
   const std::vector<int>& ls = leaf_start_h_;
@@ -543,6 +543,23 @@ void DeviceOperator::build_cheb(int p_lo, int p_hi) {
     if (c > 0) ++nonempty, tot += c;
   }
   if (!nonempty || (double)tot < 1.5 * NN * (double)nonempty) return;
+  // The rings (build_far_list mode 2): the level-l ring of a level-(l-1) box
+  // A, l = 2..L-1, through NR x NR nodes of A, when the level-lc boxes hold on
+  // average >= 1.25x as many targets as ring nodes (coarser levels always
+  // gain: A's four children would evaluate the ring at 4 NC^2 nodes).
+  constexpr int NR = imqk::kChebNR, NRR = NR * NR;
+  ring_ = !getenv("IMQ_FAR_NORING") && (double)tot >= 1.25 * NRR * (double)nonempty;
+  // Rings of levels ring_l0_..L-1 only: the level-l ring is interpolated on a
+  // level-(l-1) box A of half-width h only where t >= tau h, i.e. where the
+  // lifted singularities of the ring's expansions sit >= tau h off the real
+  // plane (coarse boxes with t << h need more nodes at high orders).
+  {
+    const char* e = getenv("IMQ_RING_TAU");
+    const double tau = e ? atof(e) : 1.0;
+    ring_l0_ = L_;
+    for (int l = L_ - 1; l >= 2 && P_.t >= tau * 0.5 * P_.cell[l - 1]; --l) ring_l0_ = l;
+    if (ring_l0_ > L_ - 1) ring_ = false;
+  }
   // node geometry (all boxes of levels 1..lc), tables
   cheb_base_.assign((size_t)lc + 1, 0);
   long long nb = 0;
@@ -585,52 +602,15 @@ void DeviceOperator::build_cheb(int p_lo, int p_hi) {
   Pn_.ys = d_cny_;
   Pn_.leaf = d_cnleaf_;
   Pn_.N = (int)cheb_nodes_;
-  // node items (level in item.w), coefficient box lists, evaluation items
-  std::vector<std::vector<int4>> g((size_t)imqk::far_max_points_per_lane());
-  std::vector<int> boxes;
-  cbox_off_.assign((size_t)lc + 2, 0);
-  for (int l = 1; l <= lc; ++l) {
-    cbox_off_[(size_t)l] = (int)boxes.size();
-    for (long long q = 0; q < (1ll << (2 * (l + 1))); ++q) {
-      if (!own(l, q)) continue;
-      boxes.push_back((int)q);
-      const int par = (int)(q << (2 * (L_ - 1 - l)));
-      const int start = (int)((cheb_base_[(size_t)l] + q) * NN);
-      // node chunks of <= 32 * kFarMaxR, balanced (400 -> 224 + 176, 256 -> 256)
-      constexpr int kMaxChunk = 256;
-      constexpr int kChunks = (NN + kMaxChunk - 1) / kMaxChunk;
-      constexpr int kChunk = ((NN + kChunks - 1) / kChunks + 31) / 32 * 32;
-      for (int c = 0; c < NN; c += kChunk) {
-        const int cnt = std::min(kChunk, NN - c);
-        g[(size_t)((cnt + 31) / 32 - 1)].push_back(make_int4(par, start + c, cnt, l));
-      }
-    }
-  }
-  cbox_off_[(size_t)lc + 1] = (int)boxes.size();
-  std::vector<int4> citems;
-  cheb_group_off_.assign(16, 0);
-  for (size_t r = 0; r < g.size(); ++r) {
-    citems.insert(citems.end(), g[r].begin(), g[r].end());
-    cheb_group_off_[r + 1] = (int)citems.size();
-  }
-  for (size_t r = g.size() + 1; r < 16; ++r) cheb_group_off_[r] = (int)citems.size();
-  // the level-(L-1) ring through NR x NR nodes of the level-lc boxes, when
-  // those boxes hold on average >= 1.25x as many targets as ring nodes
-  constexpr int NR = imqk::kChebNR, NRR = NR * NR;
-  ring_ = !getenv("IMQ_FAR_NORING") && (double)tot >= 1.25 * NRR * (double)nonempty;
-  std::vector<int4> ritems;
-  std::vector<int> rboxes;
-  ring_group_off_.assign(16, 0);
-  if (ring_) {
-    const long long nbl = 1ll << (2 * (lc + 1));
-    if (ring_nodes_ != (size_t)nbl * NRR) {
+  if (ring_) {  // ring nodes of every box of levels 1..lc (rings of levels 2..L-1)
+    if (ring_nodes_ != (size_t)nb * NRR) {
       dfree(d_rnx_); dfree(d_rny_); dfree(d_rnleaf_); dfree(d_rval_); dfree(d_rcoef_);
-      ring_nodes_ = (size_t)nbl * NRR;
+      ring_nodes_ = (size_t)nb * NRR;
       d_rnx_ = dalloc<double>(ring_nodes_, "ring nodes");
       d_rny_ = dalloc<double>(ring_nodes_, "ring nodes");
       d_rnleaf_ = dalloc<uint32_t>(ring_nodes_, "ring node keys");
       d_rval_ = dalloc<double>(ring_nodes_, "ring values");
-      d_rcoef_ = dalloc<double>((size_t)(4 * nbl) * NN, "ring child coefficients");
+      d_rcoef_ = dalloc<double>((size_t)(1ll << (2 * (lc + 2))) * NN, "ring child coefficients");
       cuda_check(cudaMemset(d_rnleaf_, 0, ring_nodes_ * sizeof(uint32_t)), "ring keys");
       const long double pi = 3.141592653589793238462643383279502884L;
       std::vector<double> TR((size_t)NRR), B[2];
@@ -656,7 +636,8 @@ void DeviceOperator::build_cheb(int p_lo, int p_hi) {
           }
       }
       imqk::cheb_set_ring_tables(TR.data(), B[0].data(), B[1].data());
-      imqk::launch_cheb_nodes_ring(P_, lc, d_rnx_, d_rny_, stream_);
+      for (int l = 1; l <= lc; ++l)
+        imqk::launch_cheb_nodes_ring(P_, l, cheb_base_[(size_t)l], d_rnx_, d_rny_, stream_);
       cuda_check(cudaStreamSynchronize(stream_), "ring nodes");
     }
     Pr_ = P_;
@@ -664,26 +645,51 @@ void DeviceOperator::build_cheb(int p_lo, int p_hi) {
     Pr_.ys = d_rny_;
     Pr_.leaf = d_rnleaf_;
     Pr_.N = (int)ring_nodes_;
-    constexpr int kChunks = (NRR + 255) / 256;
-    constexpr int kChunk = ((NRR + kChunks - 1) / kChunks + 31) / 32 * 32;
-    std::vector<std::vector<int4>> rg((size_t)imqk::far_max_points_per_lane());
-    for (int k = cbox_off_[(size_t)lc]; k < cbox_off_[(size_t)lc + 1]; ++k) {
-      const int q = boxes[(size_t)k];
-      rboxes.push_back(q);
-      for (int c = 0; c < NRR; c += kChunk) {
-        const int cnt = std::min(kChunk, NRR - c);
-        rg[(size_t)((cnt + 31) / 32 - 1)].push_back(
-            make_int4(q << 2, (int)((long long)q * NRR + c), cnt, (L_ - 1) | (2 << 8)));
-      }
-    }
-    for (size_t r = 0; r < rg.size(); ++r) {
-      ritems.insert(ritems.end(), rg[r].begin(), rg[r].end());
-      ring_group_off_[r + 1] = (int)ritems.size();
-    }
-    for (size_t r = rg.size() + 1; r < 16; ++r) ring_group_off_[r] = (int)ritems.size();
   }
-  // evaluation items: targets of the level-lc boxes, or with the ring of the
-  // level-(L-1) boxes (their series carries the ring's field)
+  // node items (level | list mode << 8 in item.w), coefficient box lists
+  // (own non-empty boxes per level), evaluation items
+  std::vector<std::vector<int4>> g((size_t)imqk::far_max_points_per_lane());
+  std::vector<std::vector<int4>> rg((size_t)imqk::far_max_points_per_lane());
+  std::vector<int> boxes;
+  cbox_off_.assign((size_t)lc + 2, 0);
+  // node chunks of <= 32 * kFarMaxR, balanced (324 -> 192 + 132, 676 -> 256 + 256 + 164)
+  auto chunks = [](std::vector<std::vector<int4>>& grp, int par, long long start, int nn, int w) {
+    const int nch = (nn + 255) / 256, ch = ((nn + nch - 1) / nch + 31) / 32 * 32;
+    for (int c = 0; c < nn; c += ch) {
+      const int cnt = std::min(ch, nn - c);
+      grp[(size_t)((cnt + 31) / 32 - 1)].push_back(make_int4(par, (int)(start + c), cnt, w));
+    }
+  };
+  for (int l = 1; l <= lc; ++l) {
+    cbox_off_[(size_t)l] = (int)boxes.size();
+    for (long long q = 0; q < (1ll << (2 * (l + 1))); ++q) {
+      if (!own(l, q)) continue;
+      boxes.push_back((int)q);
+      // own list of q at level l (without the ring of its parent when rings are on)
+      chunks(g, (int)(q << (2 * (L_ - 1 - l))), (cheb_base_[(size_t)l] + q) * NN, NN,
+             l | ((ring_ && l >= ring_l0_ ? 1 : 0) << 8));
+      // the level-(l+1) ring of q at q's ring nodes
+      if (ring_ && l + 1 >= ring_l0_)
+        chunks(rg, (int)((4 * q) << (2 * (L_ - 2 - l))), (cheb_base_[(size_t)l] + q) * NRR, NRR,
+               (l + 1) | (2 << 8));
+    }
+  }
+  cbox_off_[(size_t)lc + 1] = (int)boxes.size();
+  std::vector<int4> citems, ritems;
+  cheb_group_off_.assign(16, 0);
+  ring_group_off_.assign(16, 0);
+  for (size_t r = 0; r < g.size(); ++r) {
+    citems.insert(citems.end(), g[r].begin(), g[r].end());
+    cheb_group_off_[r + 1] = (int)citems.size();
+    ritems.insert(ritems.end(), rg[r].begin(), rg[r].end());
+    ring_group_off_[r + 1] = (int)ritems.size();
+  }
+  for (size_t r = g.size() + 1; r < 16; ++r) {
+    cheb_group_off_[r] = (int)citems.size();
+    ring_group_off_[r] = (int)ritems.size();
+  }
+  // evaluation items: targets of the level-lc boxes, or with the rings of the
+  // level-(L-1) boxes (their series carries the level-(L-1) ring's field)
   std::vector<int4> ev;
   const int per = imqk::cheb_eval_points_per_item();
   const int le = ring_ ? L_ - 1 : lc;
@@ -693,14 +699,10 @@ void DeviceOperator::build_cheb(int p_lo, int p_hi) {
     for (int c = a; c < b; c += per) ev.push_back(make_int4((int)q, c, std::min(per, b - c), 0));
   }
   n_ring_items_ = (int)ritems.size();
-  n_ring_boxes_ = (int)rboxes.size();
-  if (ring_) {
+  if (ring_ && n_ring_items_) {
     d_ring_items_ = dalloc<int4>(ritems.size(), "ring items");
-    d_rboxes_ = dalloc<int>(rboxes.size(), "ring boxes");
     cuda_check(cudaMemcpy(d_ring_items_, ritems.data(), ritems.size() * sizeof(int4),
                           cudaMemcpyHostToDevice), "H2D ring items");
-    cuda_check(cudaMemcpy(d_rboxes_, rboxes.data(), rboxes.size() * sizeof(int),
-                          cudaMemcpyHostToDevice), "H2D ring boxes");
   }
   n_cheb_items_ = (int)citems.size();
   n_ceval_ = (int)ev.size();
@@ -798,21 +800,23 @@ std::vector<double> parent_work(const std::vector<int>& ls, int L, int M) {
         const double na = (double)ls[(size_t)((a + 1) << sh)] - ls[(size_t)(a << sh)];
         wl = std::min(1.0, (double)(imqk::kChebN * imqk::kChebN) / na);
       }
-      double nl = ns[(size_t)l][(size_t)a];
-      if (L >= 4 && l == L - 1) {  // the ring goes through the level-(L-2) box's nodes
+      double nl = wl * ns[(size_t)l][(size_t)a];
+      if (L >= 4 && l >= 2) {  // the level-l ring goes through the level-(l-1) box's nodes
+        const long long pa = a >> 2;
         int ai, aj;
-        imqdev::demorton((uint32_t)(p >> 2), ai, aj);
-        const int g1 = 1 << L;
+        imqdev::demorton((uint32_t)pa, ai, aj);
+        const int g1 = 1 << (l + 1);
         double nr = 0;
         for (int qi = std::max(0, 2 * ai - 2); qi <= std::min(g1 - 1, 2 * ai + 3); ++qi)
           for (int qj = std::max(0, 2 * aj - 2); qj <= std::min(g1 - 1, 2 * aj + 3); ++qj) {
             const int ri = qi - 2 * ai, rj = qj - 2 * aj;
-            if ((ri == -2 || ri == 3 || rj == -2 || rj == 3) && count(L - 1, qi, qj) > 0) nr += 1;
+            if ((ri == -2 || ri == 3 || rj == -2 || rj == 3) && count(l, qi, qj) > 0) nr += 1;
           }
-        const double na = (double)ls[(size_t)((p >> 2) + 1) << 4] - ls[(size_t)(p >> 2) << 4];
-        nl += nr * (std::min(1.0, (double)(imqk::kChebNR * imqk::kChebNR) / na) - 1.0);
+        const int sh = 2 * (L - l + 1);
+        const double na = (double)ls[(size_t)(pa + 1) << sh] - ls[(size_t)pa << sh];
+        nl += nr * (std::min(1.0, (double)(imqk::kChebNR * imqk::kChebNR) / na) - wl);
       }
-      shared += wl * nl;
+      shared += nl;
     }
     if (L >= 4) shared += 1.4;
     double far = shared * (double)np, near = 0.0;
@@ -1045,17 +1049,32 @@ void DeviceOperator::far_near(const double* d_us, double* d_out, const int* perm
       // (parent restricted + own), summed at the targets of the level-lc boxes
       far_pass(0, n_cheb_items_, cheb_group_off_.data(), nullptr, 0, nullptr, nullptr, d_cval_,
                nullptr, 1, cheb_lc_, &Pn_, d_cheb_items_);
-      if (ring_)  // the level-(L-1) ring at the NR x NR nodes of the level-lc boxes
+      if (ring_)  // the level-(l+1) rings at the NR x NR nodes of the level-l boxes
         far_pass(0, n_ring_items_, ring_group_off_.data(), nullptr, 0, nullptr, nullptr, d_rval_,
-                 nullptr, L_ - 1, L_ - 1, &Pr_, d_ring_items_);
-      for (int l = 1; l <= cheb_lc_; ++l)
-        imqk::launch_cheb_coef(l, d_cboxes_ + cbox_off_[(size_t)l],
-                               cbox_off_[(size_t)l + 1] - cbox_off_[(size_t)l],
-                               cheb_base_[(size_t)l], l > 1 ? cheb_base_[(size_t)l - 1] : 0,
-                               d_cval_, d_ccoef_, s);
+                 nullptr, 2, L_ - 1, &Pr_, d_ring_items_);
+      constexpr long long NN = imqk::kChebN * imqk::kChebN, NRR = imqk::kChebNR * imqk::kChebNR;
+      for (int l = 1; l <= cheb_lc_; ++l) {
+        const int* bx = d_cboxes_ + cbox_off_[(size_t)l];
+        const int nbx = cbox_off_[(size_t)l + 1] - cbox_off_[(size_t)l];
+        if (ring_ && l >= ring_l0_) {
+          // parent series restricted + parent's level-l ring -> this level; then + own list
+          const int* pbx = d_cboxes_ + cbox_off_[(size_t)l - 1];
+          const int npb = cbox_off_[(size_t)l] - cbox_off_[(size_t)l - 1];
+          imqk::launch_cheb_ring_coef(pbx, npb, cheb_base_[(size_t)l - 1], d_ccoef_,
+                                      d_rval_ + cheb_base_[(size_t)l - 1] * NRR,
+                                      d_ccoef_ + cheb_base_[(size_t)l] * NN, s);
+          imqk::launch_cheb_coef(l, bx, nbx, cheb_base_[(size_t)l], -1, d_cval_, d_ccoef_, s);
+        } else {
+          imqk::launch_cheb_coef(l, bx, nbx, cheb_base_[(size_t)l],
+                                 l > 1 ? cheb_base_[(size_t)l - 1] : 0, d_cval_, d_ccoef_, s);
+        }
+      }
       if (ring_) {
-        imqk::launch_cheb_ring_coef(d_rboxes_, n_ring_boxes_, cheb_base_[(size_t)cheb_lc_],
-                                    d_ccoef_, d_rval_, d_rcoef_, s);
+        const int lc = cheb_lc_;
+        imqk::launch_cheb_ring_coef(d_cboxes_ + cbox_off_[(size_t)lc],
+                                    cbox_off_[(size_t)lc + 1] - cbox_off_[(size_t)lc],
+                                    cheb_base_[(size_t)lc], d_ccoef_,
+                                    d_rval_ + cheb_base_[(size_t)lc] * NRR, d_rcoef_, s);
         imqk::launch_cheb_eval(P_, L_ - 1, d_ceval_items_, n_ceval_, 0, d_rcoef_, d_farc_, s);
       } else {
         imqk::launch_cheb_eval(P_, cheb_lc_, d_ceval_items_, n_ceval_,
@@ -1168,19 +1187,25 @@ PairCounts DeviceOperator::pair_counts() {
   };
   double far = 0, near = 0;
   far_by_level_.assign((size_t)L + 1, 0.0);
-  ring_direct_ = ring_lists_ = 0;
-  if (L >= 3) {  // ring lists of the non-empty level-(L-2) boxes (node pairs / NR^2)
-    const int ga = 1 << (L - 1), g1 = 1 << L;
-    for (int ai = 0; ai < ga; ++ai)
-      for (int aj = 0; aj < ga; ++aj) {
-        if (!count(L - 2, ai, aj)) continue;
-        for (int qi = std::max(0, 2 * ai - 2); qi <= std::min(g1 - 1, 2 * ai + 3); ++qi)
-          for (int qj = std::max(0, 2 * aj - 2); qj <= std::min(g1 - 1, 2 * aj + 3); ++qj) {
-            const int ri = qi - 2 * ai, rj = qj - 2 * aj;
-            if ((ri == -2 || ri == 3 || rj == -2 || rj == 3) && count(L - 1, qi, qj) > 0)
-              ring_lists_ += 1;
-          }
+  ring_direct_ = 0;
+  ring_child_by_level_.assign((size_t)L + 1, 0.0);
+  ring_par_by_level_.assign((size_t)L + 1, 0.0);
+  // number of non-empty level-l ring blocks of the level-(l-1) box (ai, aj)
+  auto ring_count = [&](int l, int ai, int aj) {
+    const int g1 = 1 << (l + 1);
+    long long nr = 0;
+    for (int qi = std::max(0, 2 * ai - 2); qi <= std::min(g1 - 1, 2 * ai + 3); ++qi)
+      for (int qj = std::max(0, 2 * aj - 2); qj <= std::min(g1 - 1, 2 * aj + 3); ++qj) {
+        const int ri = qi - 2 * ai, rj = qj - 2 * aj;
+        if ((ri == -2 || ri == 3 || rj == -2 || rj == 3) && count(l, qi, qj) > 0) ++nr;
       }
+    return nr;
+  };
+  for (int l = 2; l < L; ++l) {
+    const int ga = 1 << l;
+    for (int ai = 0; ai < ga; ++ai)
+      for (int aj = 0; aj < ga; ++aj)
+        if (count(l - 1, ai, aj)) ring_par_by_level_[(size_t)l] += (double)ring_count(l, ai, aj);
   }
   lists_by_level_.assign((size_t)L + 1, 0.0);
   for (int l = 1; l <= L; ++l) {
@@ -1201,15 +1226,10 @@ PairCounts DeviceOperator::pair_counts() {
         far += (double)nt * (double)ns;
         far_by_level_[(size_t)l] += (double)nt * (double)ns;
         lists_by_level_[(size_t)l] += (double)ns;
-        if (l == L - 1 && L >= 3) {  // the ring of the level-(L-2) parent
-          const int pi = i >> 1, pj = j >> 1;
-          long long nr = 0;
-          for (int qi = lo_i; qi <= hi_i; ++qi)
-            for (int qj = lo_j; qj <= hi_j; ++qj) {
-              const int ri = qi - 2 * pi, rj = qj - 2 * pj;
-              if ((ri == -2 || ri == 3 || rj == -2 || rj == 3) && count(l, qi, qj) > 0) ++nr;
-            }
-          ring_direct_ += (double)nt * (double)nr;
+        if (l >= 2 && l < L) {  // the level-l ring of the parent
+          const long long nr = ring_count(l, i >> 1, j >> 1);
+          ring_child_by_level_[(size_t)l] += (double)nr;
+          if (l == L - 1) ring_direct_ += (double)nt * (double)nr;
         }
         if (l == L) {
           long long nn = 0;
@@ -1234,15 +1254,18 @@ PairCounts DeviceOperator::pair_counts() {
 // levels not covered by the Chebyshev pass, and (node, block) pairs.
 void DeviceOperator::fill_eval_counts() {
   const int lc = cheb_ ? cheb_lc_ : 0;
+  const bool rings = cheb_ && ring_ && ring_par_by_level_.size() == far_by_level_.size();
+  constexpr double NN = imqk::kChebN * imqk::kChebN, NRR = imqk::kChebNR * imqk::kChebNR;
   double direct = 0, nodes = 0;
   for (int l = 1; l <= L_ && l < (int)far_by_level_.size(); ++l) {
-    if (l <= lc) nodes += lists_by_level_[(size_t)l] * imqk::kChebN * imqk::kChebN;
-    else direct += far_by_level_[(size_t)l];
+    if (l <= lc)
+      nodes += (lists_by_level_[(size_t)l] -
+                (rings && l >= ring_l0_ ? ring_child_by_level_[(size_t)l] : 0.0)) * NN;
+    else
+      direct += far_by_level_[(size_t)l];
+    if (rings && l >= ring_l0_ && l < L_) nodes += ring_par_by_level_[(size_t)l] * NRR;
   }
-  if (cheb_ && ring_) {
-    direct -= ring_direct_;
-    nodes += ring_lists_ * imqk::kChebNR * imqk::kChebNR;
-  }
+  if (rings) direct -= ring_direct_;
   counts_.far_pairs_direct = direct;
   counts_.cheb_node_pairs = nodes;
   counts_.cheb_levels = lc;

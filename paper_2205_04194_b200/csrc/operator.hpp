@@ -130,7 +130,10 @@ class DeviceOperator {
   void build_cheb(int p_lo, int p_hi);
   void fill_eval_counts();
   std::vector<double> far_by_level_, lists_by_level_;
-  double ring_direct_ = 0, ring_lists_ = 0;  // level-(L-1) ring: target pairs, lists of L-2 boxes
+  // rings: level-(L-1) ring (target, block) pairs; per level l, ring entries of
+  // the level-l lists (summed over non-empty boxes) and of the level-(l-1) boxes
+  double ring_direct_ = 0;
+  std::vector<double> ring_child_by_level_, ring_par_by_level_;
   void setup_sharded_moments(int p_lo, int p_hi);
   void release();
   void apply_sorted_locked(const double* d_us, double* d_bs, const int* perm,
@@ -196,14 +199,14 @@ class DeviceOperator {
   int* d_cboxes_ = nullptr;
   // level-(L-1) ring through the level-(L-2) boxes' NR x NR nodes (build_cheb)
   bool ring_ = false;
-  int n_ring_items_ = 0, n_ring_boxes_ = 0;
+  int ring_l0_ = 0;  // rings of levels ring_l0_..L-1
+  int n_ring_items_ = 0;
   size_t ring_nodes_ = 0;
   std::vector<int> ring_group_off_;
   imqk::TreeParams Pr_{};
   double *d_rnx_ = nullptr, *d_rny_ = nullptr, *d_rval_ = nullptr, *d_rcoef_ = nullptr;
   uint32_t* d_rnleaf_ = nullptr;
   int4* d_ring_items_ = nullptr;
-  int* d_rboxes_ = nullptr;
   int4* d_pull_items_ = nullptr;  // sharded symmetric near field: boundary slots
   int n_pull_ = 0;
   int n_far_fine_ = 0;     // far items [0, n_far_fine_) fine, the rest coarse

@@ -12,7 +12,8 @@ rng = np.random.default_rng(0)
 cases = []
 n = 1 << 22
 xy = inputs.uniform_points(n, 0)
-for p, c in ((4, 0.001), (8, 1e-5), (12, 0.1), (16, 0.01), (20, 1.0), (20, 40.0)):
+for p, c in ((4, 0.001), (8, 1e-5), (12, 0.1), (16, 0.01), (20, 1.0), (20, 40.0),
+             (20, 0.01), (16, 0.003), (20, 0.001), (16, 1e-5)):
     cases.append((f"uniform 4M L7 p={p} c={c}", xy, c, p, 7))
 cases.append(("cfg4 16M L8 p=16 c=0.01", inputs.uniform_points(1 << 24, 0), 0.01, 16, 8))
 g = inputs.gaussian_mixture(1 << 20, 1)
