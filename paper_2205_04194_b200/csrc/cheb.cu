@@ -12,9 +12,14 @@
 // the level-lc boxes.  With n = kChebN = 18 the interpolation error of one
 // box's field is <= ~1e-13 of its maximum (tests vs the oracle).
 //
+// (tables in global memory: the kernels index them per thread, which the
+// constant cache would serialise)
 // Layouts: per box (levels 1..lc, all boxes, level-major, Morton inside a
 // level) n^2 node values / coefficients, index [box][i * n + j], i the x
 // index and j the y index; x_i = c_x + (cell/2) cos(pi (i + 1/2) / n).
+#include <algorithm>
+#include <cstdlib>
+
 #include "imq_device.cuh"
 #include "imq_kernels.hpp"
 
@@ -26,12 +31,12 @@ using namespace imqdev;
 constexpr int NC = kChebN;
 constexpr int NN = NC * NC;
 
-__constant__ double c_T[NN];      // T[k * NC + i] = cos(k theta_i), theta_i = pi (i + 1/2) / NC
-__constant__ double c_S[2][NN];   // child restriction, [half][k' * NC + k]
+__device__ double c_T[NN];        // T[k * NC + i] = cos(k theta_i), theta_i = pi (i + 1/2) / NC
+__device__ double c_S[2][NN];     // child restriction, [half][k' * NC + k]
 constexpr int NR = kChebNR;       // ring nodes per dimension on the level-(L-2) boxes
 constexpr int NRR = NR * NR;
-__constant__ double c_TR[NRR];       // cos(k theta_i), theta_i = pi (i + 1/2) / NR
-__constant__ double c_B[2][NC * NR];  // ring values -> child coefficients, [half][k' * NR + i]
+__device__ double c_TR[NRR];         // cos(k theta_i), theta_i = pi (i + 1/2) / NR
+__device__ double c_B[2][NC * NR];    // ring values -> child coefficients, [half][k' * NR + i]
 
 __global__ void k_cheb_nodes(const TreeParams P, int l, long long box_base, double* __restrict__ nx,
                              double* __restrict__ ny) {
@@ -69,45 +74,79 @@ __global__ void k_cheb_nodes_ring(const TreeParams P, int l, long long box_base,
 // coef_c[c] = their sum (k_cheb_coef then adds c's own list at level l < L-1;
 // at level L-1 it is the series evaluated at the targets).
 __global__ void __launch_bounds__(NN) k_cheb_ring_coef(const int* __restrict__ boxes,
-                                                       long long base_a,
+                                                       int n_boxes, long long base_a,
                                                        const double* __restrict__ coef_a,
                                                        const double* __restrict__ ring_vals,
                                                        double* __restrict__ coef_c) {
-  __shared__ double V[NRR], W[2][NR * NC], U[2][NN], Ca[NN], B[2][NC * NR], S[2][NN];
-  const uint32_t a = (uint32_t)boxes[blockIdx.x];
+  static_assert(NR % 2 == 0 && NC % 2 == 0, "paired (LDS.128) loads");
+  // transposed intermediates (contraction index contiguous): Wt[h][m'][i] =
+  // sum_j V[i][j] B[h][m'][j], Ut[h][m'][k] = sum_j Ca[k][j] S[h][m'][j]
+  __shared__ __align__(16) double V[NRR], Wt[2][NC * NR], Ut[2][NN], Ca[NN], B[2][NC * NR],
+      S[2][NN];
   const int r = threadIdx.x;
-  for (int o = r; o < NRR; o += NN) V[o] = ring_vals[(size_t)a * NRR + o];
   for (int o = r; o < 2 * NC * NR; o += NN) (&B[0][0])[o] = (&c_B[0][0])[o];
-  Ca[r] = coef_a[(size_t)(base_a + a) * NN + r];
   S[0][r] = c_S[0][r];
   S[1][r] = c_S[1][r];
+  // persistent over the listed boxes: the tables are staged once per CTA
+  for (int bx = blockIdx.x; bx < n_boxes; bx += gridDim.x) {
+  const uint32_t a = (uint32_t)boxes[bx];
+  __syncthreads();  // previous box done with V, Ca, Wt, Ut
+  for (int o = r; o < NRR; o += NN) V[o] = ring_vals[(size_t)a * NRR + o];
+  Ca[r] = coef_a[(size_t)(base_a + a) * NN + r];
   __syncthreads();
-  // W[h][i][m'] = sum_j V[i][j] B[h][m'][j];  U[h][k][m'] = sum_j Ca[k][j] S[h][m'][j]
-  for (int o = r; o < 2 * NR * NC; o += NN) {
-    const int h = o / (NR * NC), i = (o / NC) % NR, m = o % NC;
-    double acc = 0.0;
-#pragma unroll 4
-    for (int j = 0; j < NR; ++j) acc = fma(V[i * NR + j], B[h][m * NR + j], acc);
-    W[h][i * NC + m] = acc;
+  auto ld2 = [](const double* p) { return *reinterpret_cast<const double2*>(p); };
+  for (int o = r; o < NR * NC; o += NN) {  // both halves per (i, m')
+    const int i = o / NC, m = o % NC;
+    double w0 = 0.0, w1 = 0.0;
+#pragma unroll
+    for (int j = 0; j < NR; j += 2) {
+      const double2 v = ld2(&V[i * NR + j]), b0 = ld2(&B[0][m * NR + j]), b1 = ld2(&B[1][m * NR + j]);
+      w0 = fma(v.y, b0.y, fma(v.x, b0.x, w0));
+      w1 = fma(v.y, b1.y, fma(v.x, b1.x, w1));
+    }
+    Wt[0][m * NR + i] = w0;
+    Wt[1][m * NR + i] = w1;
   }
-  for (int o = r; o < 2 * NN; o += NN) {
-    const int h = o / NN, k = (o / NC) % NC, m = o % NC;
-    double acc = 0.0;
-#pragma unroll 6
-    for (int j = 0; j < NC; ++j) acc = fma(Ca[k * NC + j], S[h][m * NC + j], acc);
-    U[h][k * NC + m] = acc;
+  {
+    const int k = r / NC, m = r % NC;
+    double u0 = 0.0, u1 = 0.0;
+#pragma unroll
+    for (int j = 0; j < NC; j += 2) {
+      const double2 cv = ld2(&Ca[k * NC + j]), s0 = ld2(&S[0][m * NC + j]), s1 = ld2(&S[1][m * NC + j]);
+      u0 = fma(cv.y, s0.y, fma(cv.x, s0.x, u0));
+      u1 = fma(cv.y, s1.y, fma(cv.x, s1.x, u1));
+    }
+    Ut[0][m * NC + k] = u0;
+    Ut[1][m * NC + k] = u1;
   }
   __syncthreads();
+  // the four children (hx, hy) of (k', m'): sum_i B[hx][k'][i] Wt[hy][m'][i]
+  //                                       + sum_k S[hx][k'][k] Ut[hy][m'][k]
   const int k = r / NC, m = r % NC;
-#pragma unroll 1
-  for (int c = 0; c < 4; ++c) {
-    const int hx = c >> 1, hy = c & 1;
-    double acc = 0.0;
-#pragma unroll 4
-    for (int i = 0; i < NR; ++i) acc = fma(B[hx][k * NR + i], W[hy][i * NC + m], acc);
-#pragma unroll 6
-    for (int kk = 0; kk < NC; ++kk) acc = fma(S[hx][k * NC + kk], U[hy][kk * NC + m], acc);
-    coef_c[(size_t)(4 * a + c) * NN + r] = acc;
+  double c00 = 0.0, c01 = 0.0, c10 = 0.0, c11 = 0.0;
+#pragma unroll
+  for (int i = 0; i < NR; i += 2) {
+    const double2 b0 = ld2(&B[0][k * NR + i]), b1 = ld2(&B[1][k * NR + i]);
+    const double2 w0 = ld2(&Wt[0][m * NR + i]), w1 = ld2(&Wt[1][m * NR + i]);
+    c00 = fma(b0.y, w0.y, fma(b0.x, w0.x, c00));
+    c01 = fma(b0.y, w1.y, fma(b0.x, w1.x, c01));
+    c10 = fma(b1.y, w0.y, fma(b1.x, w0.x, c10));
+    c11 = fma(b1.y, w1.y, fma(b1.x, w1.x, c11));
+  }
+#pragma unroll
+  for (int kk = 0; kk < NC; kk += 2) {
+    const double2 s0 = ld2(&S[0][k * NC + kk]), s1 = ld2(&S[1][k * NC + kk]);
+    const double2 u0 = ld2(&Ut[0][m * NC + kk]), u1 = ld2(&Ut[1][m * NC + kk]);
+    c00 = fma(s0.y, u0.y, fma(s0.x, u0.x, c00));
+    c01 = fma(s0.y, u1.y, fma(s0.x, u1.x, c01));
+    c10 = fma(s1.y, u0.y, fma(s1.x, u0.x, c10));
+    c11 = fma(s1.y, u1.y, fma(s1.x, u1.x, c11));
+  }
+  double* out = coef_c + (size_t)(4 * a) * NN + r;  // child 2 hx + hy
+  out[0] = c00;
+  out[NN] = c01;
+  out[2 * NN] = c10;
+  out[3 * NN] = c11;
   }
 }
 
@@ -230,7 +269,113 @@ __global__ void __launch_bounds__(kEvalWarps * 32) k_cheb_eval(const TreeParams 
     if (lane + 32 * p < cnt) out[s0 + lane + 32 * p] = acc[p];
 }
 
+// Same evaluation on the FP64 tensor cores (mma.sync m8n8k4 f64): per group
+// of 8 targets, Z = Ty C^T ([8 x m] x [m x k], m padded to 4 KS, k to 8 NT)
+// with the coefficient fragments held in registers for the whole item (no
+// shared-memory traffic in the loop), then out = sum_k Z[., k] T_k(x^).
+// Fragments (PTX m8n8k4 .f64): A (row) lane -> [lane/4][lane%4], B (col)
+// lane -> [lane%4][lane/4], C/D lane -> [lane/4][2 (lane%4) + {0,1}].
+// Chebyshev values by the step identities T_{n+4} = 2 T_4 T_n - T_{n-4} and
+// T_{n+8} = 2 T_8 T_n - T_{n-8}, so a lane forms only the degrees it holds.
+constexpr int kMmaKS = (NC + 3) / 4, kMmaNT = (NC + 7) / 8, kMmaWarps = 4;
+__device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+__global__ void __launch_bounds__(kMmaWarps * 32) k_cheb_eval_mma(
+    const TreeParams P, int lc, const int4* __restrict__ items, int n_items, long long base_lc,
+    const double* __restrict__ coef, double* __restrict__ out) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int it = blockIdx.x * kMmaWarps + warp;
+  if (it >= n_items) return;
+  const int4 item = items[it];
+  const uint32_t q = (uint32_t)item.x;
+  const int s0 = item.y, cnt = item.z;
+  const double* c = coef + (base_lc + q) * NN;
+  const int r = lane >> 2, j = lane & 3;
+  double b[kMmaNT][kMmaKS];
+#pragma unroll
+  for (int nt = 0; nt < kMmaNT; ++nt)
+#pragma unroll
+    for (int s = 0; s < kMmaKS; ++s) {
+      const int m = 4 * s + j, k = 8 * nt + r;
+      b[nt][s] = (m < NC && k < NC) ? __ldg(&c[k * NC + m]) : 0.0;
+    }
+  int bi, bj;
+  demorton(q, bi, bj);
+  const double cx = block_center(P.ox, bi, P.cell[lc]), cy = block_center(P.oy, bj, P.cell[lc]);
+  const double inv = 2.0 / P.cell[lc];
+  // coordinates one group ahead (the loop is otherwise bound by load latency)
+  double xn = P.xs[s0 + min(r, cnt - 1)], yn = P.ys[s0 + min(r, cnt - 1)];
+  for (int g = 0; g < cnt; g += 8) {
+    const int t = g + r;
+    const double xh = (xn - cx) * inv, yh = (yn - cy) * inv;
+    if (g + 8 < cnt) {
+      const int nidx = s0 + min(t + 8, cnt - 1);
+      xn = P.xs[nidx];
+      yn = P.ys[nidx];
+    }
+    // A: T_{4s+j}(y)
+    double a[kMmaKS];
+    {
+      const double y2 = 2.0 * yh;
+      const double t2 = fma(y2, yh, -1.0), t3 = fma(y2, t2, -yh), t4 = fma(y2, t3, -t2);
+      const double tj = j == 0 ? 1.0 : (j == 1 ? yh : (j == 2 ? t2 : t3));
+      const double tm = j == 0 ? t4 : (j == 1 ? t3 : (j == 2 ? t2 : yh));  // T_{4-j}
+      const double t4x2 = 2.0 * t4;
+      a[0] = tj;
+      if (kMmaKS > 1) a[1] = fma(t4x2, tj, -tm);
+#pragma unroll
+      for (int s = 2; s < kMmaKS; ++s) a[s] = fma(t4x2, a[s - 1], -a[s - 2]);
+    }
+    double d[kMmaNT][2];
+#pragma unroll
+    for (int nt = 0; nt < kMmaNT; ++nt) {
+      d[nt][0] = d[nt][1] = 0.0;
+#pragma unroll
+      for (int s = 0; s < kMmaKS; ++s) dmma_884(d[nt][0], d[nt][1], a[s], b[nt][s]);
+    }
+    // T_{8nt + 2j + e}(x), e = 0, 1
+    double v;
+    {
+      const double x2 = 2.0 * xh;
+      double T[9];
+      T[0] = 1.0;
+      T[1] = xh;
+#pragma unroll
+      for (int k = 2; k <= 8; ++k) T[k] = fma(x2, T[k - 1], -T[k - 2]);
+      const double u0 = j == 0 ? T[0] : (j == 1 ? T[2] : (j == 2 ? T[4] : T[6]));
+      const double u1 = j == 0 ? T[1] : (j == 1 ? T[3] : (j == 2 ? T[5] : T[7]));
+      const double w0 = j == 0 ? T[8] : (j == 1 ? T[6] : (j == 2 ? T[4] : T[2]));  // T_{8-k0}
+      const double w1 = j == 0 ? T[7] : (j == 1 ? T[5] : (j == 2 ? T[3] : T[1]));  // T_{8-k1}
+      const double t8x2 = 2.0 * T[8];
+      double p0 = u0, p1 = u1, q0 = w0, q1 = w1;  // T_{k+8(nt-1)} roles
+      v = d[0][0] * u0 + d[0][1] * u1;
+#pragma unroll
+      for (int nt = 1; nt < kMmaNT; ++nt) {
+        const double n0 = fma(t8x2, p0, -q0), n1 = fma(t8x2, p1, -q1);
+        v = fma(d[nt][0], n0, v);
+        v = fma(d[nt][1], n1, v);
+        q0 = p0;
+        q1 = p1;
+        p0 = n0;
+        p1 = n1;
+      }
+    }
+    v += __shfl_xor_sync(0xffffffffu, v, 1);
+    v += __shfl_xor_sync(0xffffffffu, v, 2);
+    if (j == 0 && t < cnt) out[s0 + t] = v;
+  }
+}
+
 }  // namespace
+
+// IMQ_CHEB_EVAL_FMA=1: the CUDA-core evaluation (comparison / development)
+static bool eval_fma() {
+  static const bool v = getenv("IMQ_CHEB_EVAL_FMA") != nullptr;
+  return v;
+}
 
 void cheb_set_tables(const double* T, const double* S_left, const double* S_right) {
   cudaMemcpyToSymbol(c_T, T, NN * sizeof(double));
@@ -253,8 +398,13 @@ void launch_cheb_nodes_ring(const TreeParams& P, int l, long long box_base, doub
 void launch_cheb_ring_coef(const int* boxes, int n_boxes, long long base_a,
                            const double* coef_a, const double* ring_vals, double* coef_c,
                            cudaStream_t s) {
-  if (n_boxes)
-    k_cheb_ring_coef<<<(unsigned)n_boxes, NN, 0, s>>>(boxes, base_a, coef_a, ring_vals, coef_c);
+  if (n_boxes) {
+    static int sms = 0;
+    if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const int grid = std::min(n_boxes, 4 * std::max(sms, 1));
+    k_cheb_ring_coef<<<(unsigned)grid, NN, 0, s>>>(boxes, n_boxes, base_a, coef_a, ring_vals,
+                                                   coef_c);
+  }
 }
 
 void launch_cheb_nodes(const TreeParams& P, int l, long long box_base, double* nx, double* ny,
@@ -271,11 +421,14 @@ void launch_cheb_coef(int l, const int* boxes, int n_boxes, long long base_l,
 
 void launch_cheb_eval(const TreeParams& P, int lc, const int4* items, int n_items,
                       long long base_lc, const double* coef, double* out, cudaStream_t s) {
-  if (n_items)
+  if (n_items && !eval_fma())
+    k_cheb_eval_mma<<<(unsigned)((n_items + kMmaWarps - 1) / kMmaWarps), kMmaWarps * 32, 0, s>>>(
+        P, lc, items, n_items, base_lc, coef, out);
+  else if (n_items)
     k_cheb_eval<<<(unsigned)((n_items + kEvalWarps - 1) / kEvalWarps), kEvalWarps * 32, 0, s>>>(
         P, lc, items, n_items, base_lc, coef, out);
 }
 
-int cheb_eval_points_per_item() { return 32 * kEvalR; }
+int cheb_eval_points_per_item() { return eval_fma() ? 32 * kEvalR : 1024; }
 
 }  // namespace imqk

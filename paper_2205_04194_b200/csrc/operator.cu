@@ -80,8 +80,14 @@ DeviceOperator::DeviceOperator(const double* xy_host, size_t n, double t, int M,
   M_ = M;
   t_ = t;
   cuda_check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "stream create");
+  int prio_lo = 0, prio_hi = 0;
+  cuda_check(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi), "priority range");
+  cuda_check(cudaStreamCreateWithPriority(&hp_stream_, cudaStreamNonBlocking, prio_hi),
+             "stream create");
+  cuda_check(cudaEventCreateWithFlags(&ev_hp_done_, cudaEventDisableTiming), "event create");
   for (int k = 0; k < kAuxStreams; ++k) {
-    cuda_check(cudaStreamCreateWithFlags(&aux_[k], cudaStreamNonBlocking), "stream create");
+    cuda_check(cudaStreamCreateWithPriority(&aux_[k], cudaStreamNonBlocking, prio_hi),
+               "stream create");
     cuda_check(cudaEventCreateWithFlags(&ev_join_[k], cudaEventDisableTiming), "event create");
   }
   cuda_check(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming), "event create");
@@ -136,6 +142,10 @@ void DeviceOperator::release() {
   if (ev_last_) cudaEventDestroy(ev_last_);
   ev_last_ = nullptr;
   if (near_stream_) cudaStreamDestroy(near_stream_);
+  if (hp_stream_) cudaStreamDestroy(hp_stream_);
+  if (ev_hp_done_) cudaEventDestroy(ev_hp_done_);
+  hp_stream_ = nullptr;
+  ev_hp_done_ = nullptr;
   if (ev_near_fork_) cudaEventDestroy(ev_near_fork_);
   if (ev_near_done_) cudaEventDestroy(ev_near_done_);
   near_stream_ = nullptr;
@@ -1004,13 +1014,13 @@ void DeviceOperator::moments_finish(cudaStream_t s) {
 
 void DeviceOperator::far_near(const double* d_us, double* d_out, const int* perm,
                               cudaStream_t s, int far_begin, int far_end, int near_begin,
-                              int near_end) {
+                              int near_end, bool near_launched) {
   far_begin = std::max(0, far_begin);
   far_end = std::min(far_end, n_far_);
   near_begin = std::max(0, near_begin);
   near_end = std::min(near_end, n_near_);
   const bool sym = (near_sym_ || near_pair_) && near_end > near_begin;
-  if (sym && near_sym_) {  // symmetric near field first; the far epilogue combines and scatters
+  if (sym && near_sym_ && !near_launched) {  // symmetric near field first; the far epilogue combines
     imqk::launch_p2p_near_sym(P_, d_near_items_, near_group_off_.data(), near_begin, near_end,
                               d_us, d_part_, s);
     imqk::launch_p2p_pull(P_, d_pull_items_, n_pull_, d_us, d_part_, s);
@@ -1084,10 +1094,12 @@ void DeviceOperator::far_near(const double* d_us, double* d_out, const int* perm
       far_pass(std::max(far_begin, n_far_fine_), far_end, far_cgroup_off_.data(), nullptr, 0,
                nullptr, nullptr, d_farc_, nullptr, 1, L_ - 2);
     }
+    if (near_launched && sym) cuda_check(cudaStreamWaitEvent(s, ev_near_done_, 0), "near join");
     far_pass(far_begin, std::min(far_end, n_far_fine_), far_group_off_.data(), near_part, nslots,
              d_out, perm, d_far_, d_farc_, L_ - 1, L_, nullptr, nullptr,
              cheb_run && ring_ ? 1 : 0);
   } else {
+    if (near_launched && sym) cuda_check(cudaStreamWaitEvent(s, ev_near_done_, 0), "near join");
     far_pass(far_begin, far_end, far_group_off_.data(), near_part, nslots, d_out, perm, d_far_,
              nullptr, 1, L_);
   }
@@ -1115,6 +1127,26 @@ void DeviceOperator::apply_sorted_locked(const double* d_us, double* d_out, cons
     cuda_check(cudaStreamWaitEvent(s, ev_near_done_, 0), "near join");
     imqk::launch_pair_reduce(d_chunks_, n_chunks_, d_contrib_off_, d_contrib_, d_pair_part_, d_out,
                              d_far_, perm, s);
+    return;
+  }
+  if (near_sym_ && n_near_ > 0 && n_far_ > 0 && !sharded()) {
+    // symmetric near field on its own stream, concurrent with the moments and
+    // the coarse / node passes (which leave FP64 issue slots free); the fine
+    // pass, whose epilogue adds the near slots, waits for it
+    cuda_check(cudaEventRecord(ev_near_fork_, s), "near fork");
+    cuda_check(cudaStreamWaitEvent(near_stream_, ev_near_fork_, 0), "near fork wait");
+    imqk::launch_p2p_near_sym(P_, d_near_items_, near_group_off_.data(), 0, n_near_, d_us,
+                              d_part_, near_stream_);
+    imqk::launch_p2p_pull(P_, d_pull_items_, n_pull_, d_us, d_part_, near_stream_);
+    cuda_check(cudaEventRecord(ev_near_done_, near_stream_), "near done");
+    // the critical path (moments -> node passes -> fine pass) on a
+    // high-priority stream, so its blocks are scheduled ahead of pending near
+    // blocks; the near field fills the SMs it leaves idle
+    cuda_check(cudaStreamWaitEvent(hp_stream_, ev_near_fork_, 0), "hp fork wait");
+    moments(d_us, hp_stream_);
+    far_near(d_us, d_out, perm, hp_stream_, 0, n_far_, 0, n_near_, true);
+    cuda_check(cudaEventRecord(ev_hp_done_, hp_stream_), "hp done");
+    cuda_check(cudaStreamWaitEvent(s, ev_hp_done_, 0), "hp join");
     return;
   }
   moments(d_us, s);

@@ -101,8 +101,11 @@ class DeviceOperator {
   void coarse_moments(double2** ptr, size_t* count) const;
   void moments_finish(cudaStream_t s);
   bool sharded() const;
+  // near_launched: the symmetric near field already runs on near_stream_
+  // (apply_sorted_locked); the pass that reads its slots waits for ev_near_done_.
   void far_near(const double* d_us, double* d_out, const int* perm, cudaStream_t s,
-                int far_begin, int far_end, int near_begin, int near_end);
+                int far_begin, int far_end, int near_begin, int near_end,
+                bool near_launched = false);
   double2* coef_ptr() const { return d_coef_; }
   const int* perm_ptr() const { return d_perm_; }
   size_t coef_count() const { return coef_count_; }
@@ -148,6 +151,8 @@ class DeviceOperator {
   cudaEvent_t ev_last_ = nullptr;  // end of the last enqueued entry point (Ordered)
   cudaStream_t near_stream_ = nullptr;  // chunk-pair near field, concurrent with far
   cudaEvent_t ev_near_fork_ = nullptr, ev_near_done_ = nullptr;
+  cudaStream_t hp_stream_ = nullptr;  // high-priority critical path (near field overlapped)
+  cudaEvent_t ev_hp_done_ = nullptr;
   cudaEvent_t ev_join_[kAuxStreams] = {};
   int N_ = 0, M_ = 0, K_ = 0, Ke_ = 0, L_ = 0, pending_levels_ = 0;
   double t_ = 0.0;

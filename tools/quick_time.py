@@ -24,9 +24,9 @@ for _ in range(2): op.apply_device(u, b, s)
 s.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record(s)
-for _ in range(3): op.apply_device(u, b, s)
+for _ in range(10): op.apply_device(u, b, s)
 e1.record(s); s.synchronize()
-ms = e0.elapsed_time(e1) / 3
+ms = e0.elapsed_time(e1) / 10
 print(f"apply {ms:.3f} ms  -> {n/ms*1e3/1e6:.1f} Mpts/s", flush=True)
 nf = len(op.items("far")); nn = len(op.items("near"))
 e0.record(s); op.moments(us, s); e1.record(s); s.synchronize(); print(f"moments {e0.elapsed_time(e1):.3f} ms")
