@@ -100,7 +100,7 @@ constexpr int kChebN = IMQ_CHEB_N;  // nodes per dimension (degree kChebN - 1), 
 // boxes at kChebNR^2 nodes (its block centres sit 2.5 half-widths from the box
 // centre instead of 4), then restricted to the level-(L-1) boxes at kChebN.
 #ifndef IMQ_CHEB_NR
-#define IMQ_CHEB_NR 26
+#define IMQ_CHEB_NR 20
 #endif
 constexpr int kChebNR = IMQ_CHEB_NR;
 void cheb_set_tables(const double* T, const double* S_left, const double* S_right);
