@@ -253,10 +253,15 @@ def test_sharded_application_emulated(imq, world):
     torch = pytest.importorskip("torch")
     from paper_2205_04194_b200 import inputs
     from paper_2205_04194_b200.parallel import ShardedOperator
-    n, t, m, L = 1 << 18, 0.01, 12, 5
-    for xy in (inputs.uniform_points(n, 3), inputs.gaussian_mixture(n, 1)):
+    n, m, L = 1 << 18, 12, 5
+    # t = 0.01: Chebyshev coarse levels, no rings (t < h); t = 0.05: the
+    # level-(L-1) ring through the level-(L-2) boxes' nodes is on
+    for xy, t in ((inputs.uniform_points(n, 3), 0.01), (inputs.gaussian_mixture(n, 1), 0.01),
+                  (inputs.uniform_points(n, 3), 0.05)):
         u = torch.tensor(inputs.random_vector(n, 7), device="cuda")
         full = imq.FastOperator(xy, t, m, L)
+        if t == 0.05:
+            assert full.stats()["cheb_ring"] == 1, full.stats()
         b_ref = torch.empty_like(u)
         full.apply_device(u, b_ref)
         torch.cuda.synchronize()
