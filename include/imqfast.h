@@ -175,6 +175,12 @@ IMQ_API int imq_ext_operator_far_near(const imq_operator* op, const double* d_us
 /* u (original order) -> Morton order. */
 IMQ_API int imq_ext_operator_gather(const imq_operator* op, const double* d_u, double* d_us,
                                     void* stream);
+/* Starts the near field of the Morton-ordered d_us on the operator's own
+ * stream (ordered after `stream`), so that it overlaps the moments; the next
+ * imq_ext_operator_far_near on this operator uses it (d_us must stay valid
+ * and unchanged until then).  No-op unless the near field is the symmetric
+ * per-leaf kind (imq_ext_stats.near_mode == 1). */
+IMQ_API int imq_ext_operator_near_begin(const imq_operator* op, const double* d_us, void* stream);
 /* Sharded moments (after imq_ext_operator_restrict): own + halo fine levels and
  * own-only coarse partial moments; all-reduce (sum) the coarse region returned
  * by imq_ext_operator_coarse_moments over the ranks, then moments_finish.

@@ -293,6 +293,11 @@ class FastOperator:
     def gather(self, d_u, d_us, stream=None) -> None:
         check(lib().imq_ext_operator_gather(self._h, _addr(d_u), _addr(d_us), _stream(stream)))
 
+    def near_begin(self, d_us, stream=None) -> None:
+        """Start the near field of d_us early (overlaps the moments); the next
+        far_near uses it."""
+        check(lib().imq_ext_operator_near_begin(self._h, _addr(d_us), _stream(stream)))
+
     def moments_local(self, d_us, stream=None) -> None:
         check(lib().imq_ext_operator_moments_local(self._h, _addr(d_us), _stream(stream)))
 

@@ -89,6 +89,7 @@ _SIGS = {
     "imq_ext_operator_far_near": (C.c_int, [_vp, _vp, _vp, C.c_int, C.c_int, C.c_int, C.c_int,
                                             C.c_int, _vp]),
     "imq_ext_operator_gather": (C.c_int, [_vp, _vp, _vp, _vp]),
+    "imq_ext_operator_near_begin": (C.c_int, [_vp, _vp, _vp]),
     "imq_ext_operator_moments_local": (C.c_int, [_vp, _vp, _vp]),
     "imq_ext_operator_coarse_moments": (C.c_int, [_vp, C.POINTER(_vp), C.POINTER(C.c_size_t)]),
     "imq_ext_operator_moments_finish": (C.c_int, [_vp, _vp]),

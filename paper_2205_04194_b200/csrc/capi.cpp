@@ -558,6 +558,15 @@ int imq_ext_operator_gather(const imq_operator* op, const double* d_u, double* d
   });
 }
 
+int imq_ext_operator_near_begin(const imq_operator* op, const double* d_us, void* stream) {
+  if (!op || !d_us) return fail(IMQ_ERR_INVALID_ARG, "imq_ext_operator_near_begin: null argument");
+  return guard([&] {
+    op->op->near_begin(d_us, static_cast<cudaStream_t>(stream));
+    imqh::cuda_check(cudaGetLastError(), "near_begin launch");
+    return IMQ_OK;
+  });
+}
+
 int imq_ext_operator_moments_local(const imq_operator* op, const double* d_us, void* stream) {
   if (!op || !d_us) return fail(IMQ_ERR_INVALID_ARG, "imq_ext_operator_moments_local: null argument");
   return guard([&] {

@@ -974,23 +974,35 @@ void DeviceOperator::moments_local(const double* d_us, cudaStream_t s) {
     throw cuda_error("cublasDgemm (M2M, level L-1) failed");
   imqk::launch_scatter_rows(d_pack_c_, d_need_par_, nneed, 2 * Ke_,
                             reinterpret_cast<double*>(d_mu_ + P_.mu_off[L_ - 1]), s);
-  // own-only level L-1 -> coarse levels (partial sums, reduced by the caller)
-  cuda_check(cudaMemsetAsync(d_own_lvl_, 0, (size_t)npar * Ke_ * sizeof(double2), s), "memset");
-  if (par_hi_ > par_lo_)
-    cuda_check(cudaMemcpyAsync(d_own_lvl_ + (size_t)par_lo_ * Ke_,
-                               d_mu_ + P_.mu_off[L_ - 1] + (size_t)par_lo_ * Ke_,
-                               (size_t)(par_hi_ - par_lo_) * Ke_ * sizeof(double2),
-                               cudaMemcpyDeviceToDevice, s),
-               "own level copy");
+  // own-only level L-1 -> coarse levels (partial sums, reduced by the caller).
+  // The coarse region is zeroed and only the parents above the own range are
+  // translated (a contiguous Morton range per level): the all-reduce then
+  // sums exactly the own-only partials.
+  (void)npar;
+  cuda_check(cudaMemsetAsync(d_mu_ + P_.mu_off[1], 0,
+                             (size_t)(P_.mu_off[L_ - 1] - P_.mu_off[1]) * sizeof(double2), s),
+             "coarse memset");
+  if (par_hi_ <= par_lo_) return;
+  long long a0 = par_lo_ >> 2, a1 = ((long long)par_hi_ + 3) >> 2;  // level-(L-2) parents
+  // level L-1 input rows of those parents: own blocks, zero for the others
+  cuda_check(cudaMemsetAsync(d_own_lvl_ + (size_t)(4 * a0) * Ke_, 0,
+                             (size_t)(4 * (a1 - a0)) * Ke_ * sizeof(double2), s),
+             "memset");
+  cuda_check(cudaMemcpyAsync(d_own_lvl_ + (size_t)par_lo_ * Ke_,
+                             d_mu_ + P_.mu_off[L_ - 1] + (size_t)par_lo_ * Ke_,
+                             (size_t)(par_hi_ - par_lo_) * Ke_ * sizeof(double2),
+                             cudaMemcpyDeviceToDevice, s),
+             "own level copy");
   for (int l = L_ - 2; l >= 1; --l) {
-    const int parents = 1 << (2 * (l + 1));
     const double* A = l == L_ - 2 ? reinterpret_cast<const double*>(d_own_lvl_)
                                   : reinterpret_cast<const double*>(d_mu_ + P_.mu_off[l + 1]);
-    if (cublasDgemm(blas_, CUBLAS_OP_N, CUBLAS_OP_N, 2 * Ke_, parents, 8 * Ke_, &one,
-                    d_m2m_ + msz * (size_t)(l - 1), 2 * Ke_, A, 8 * Ke_, &zero,
-                    reinterpret_cast<double*>(d_mu_ + P_.mu_off[l]), 2 * Ke_) !=
-        CUBLAS_STATUS_SUCCESS)
+    if (cublasDgemm(blas_, CUBLAS_OP_N, CUBLAS_OP_N, 2 * Ke_, (int)(a1 - a0), 8 * Ke_, &one,
+                    d_m2m_ + msz * (size_t)(l - 1), 2 * Ke_, A + (size_t)a0 * 8 * Ke_, 8 * Ke_,
+                    &zero, reinterpret_cast<double*>(d_mu_ + P_.mu_off[l]) + (size_t)a0 * 2 * Ke_,
+                    2 * Ke_) != CUBLAS_STATUS_SUCCESS)
       throw cuda_error("cublasDgemm (M2M, coarse) failed");
+    a0 >>= 2;
+    a1 = (a1 + 3) >> 2;
   }
 }
 
@@ -1151,6 +1163,20 @@ void DeviceOperator::apply_sorted_locked(const double* d_us, double* d_out, cons
   }
   moments(d_us, s);
   far_near(d_us, d_out, perm, s, 0, n_far_, 0, n_near_);
+}
+
+void DeviceOperator::near_begin(const double* d_us, cudaStream_t s) {
+  std::lock_guard<std::mutex> lk(mtx_);
+  DeviceGuard g(device_);
+  Ordered o(*this, s);
+  if (!near_sym_ || n_near_ == 0) return;
+  cuda_check(cudaEventRecord(ev_near_fork_, s), "near fork");
+  cuda_check(cudaStreamWaitEvent(near_stream_, ev_near_fork_, 0), "near fork wait");
+  imqk::launch_p2p_near_sym(P_, d_near_items_, near_group_off_.data(), 0, n_near_, d_us, d_part_,
+                            near_stream_);
+  imqk::launch_p2p_pull(P_, d_pull_items_, n_pull_, d_us, d_part_, near_stream_);
+  cuda_check(cudaEventRecord(ev_near_done_, near_stream_), "near done");
+  near_pending_ = true;
 }
 
 void DeviceOperator::apply_sorted(const double* d_us, double* d_bs, cudaStream_t stream) {

@@ -91,8 +91,18 @@ class DeviceOperator {
                        int fb, int fe, int nb, int ne) {
     std::lock_guard<std::mutex> lk(mtx_);
     Ordered o(*this, s);
-    far_near(d_us, d_out, perm, s, fb, fe, nb, ne);
+    const bool pending = near_pending_;
+    near_pending_ = false;
+    far_near(d_us, d_out, perm, s, fb, fe, nb, ne, pending);
+    // later work on s is ordered after the near field even if this call did
+    // not read it (a far-only range)
+    if (pending) cuda_check(cudaStreamWaitEvent(s, ev_near_done_, 0), "near join");
   }
+  // Starts the symmetric near field of d_us on the operator's near stream
+  // (after the work queued on s); the next far_near_locked consumes it
+  // instead of launching its own.  No-op unless the near field is symmetric
+  // per leaf.  (Sharded ranks: overlaps the near field with the moments.)
+  void near_begin(const double* d_us, cudaStream_t s);
   void moments(const double* d_us, cudaStream_t s);  // P2M + M2M + transform
   // Sharded ranks: own + halo moments and own-only coarse partials; the caller
   // all-reduces coarse_moments() over ranks, then calls moments_finish().
@@ -152,6 +162,7 @@ class DeviceOperator {
   cudaStream_t near_stream_ = nullptr;  // chunk-pair near field, concurrent with far
   cudaEvent_t ev_near_fork_ = nullptr, ev_near_done_ = nullptr;
   cudaStream_t hp_stream_ = nullptr;  // high-priority critical path (near field overlapped)
+  bool near_pending_ = false;          // near_begin ran; far_near_locked waits for it
   cudaEvent_t ev_hp_done_ = nullptr;
   cudaEvent_t ev_join_[kAuxStreams] = {};
   int N_ = 0, M_ = 0, K_ = 0, Ke_ = 0, L_ = 0, pending_levels_ = 0;

@@ -74,6 +74,7 @@ class ShardedOperator:
         """Gather u, local + coarse-partial moments, coarse all-reduce, transform."""
         import torch.distributed as dist
         self.op.gather(d_u, self.d_us, stream)
+        self.op.near_begin(self.d_us, stream)  # near field overlaps the moments + all-reduce
         self.op.moments_local(self.d_us, stream)
         if reduce and self.coarse is not None and self.world > 1:
             dist.all_reduce(self.coarse, group=group)
