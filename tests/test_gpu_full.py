@@ -66,6 +66,35 @@ def test_config5_sweep_sampled(imq, oracle):
         op.close()
 
 
+@pytest.mark.parametrize("case", ["strip", "clustered_wide_t", "uniform_all_rings"])
+def test_chebyshev_and_ring_paths_vs_oracle(imq, oracle, case):
+    """Large inputs that switch on the Chebyshev coarse pass and the rings in
+    different places: a thin strip (most boxes empty, full ones crowded), a
+    clustered set with t large enough that every level 2..L-1 has a ring,
+    and a uniform set with rings from level 3 on.  Sampled rows vs the
+    oracle's reference-order rows (<= 1e-10, expected ~1e-14)."""
+    from paper_2205_04194_b200 import inputs
+    n = 1 << 20
+    rng = np.random.default_rng(11)
+    if case == "strip":
+        xy = np.stack([rng.random(n), 0.3 + 0.01 * rng.random(n)], 1).reshape(-1)
+        t, m, L = 0.05, 12, 6
+    elif case == "clustered_wide_t":
+        xy = inputs.gaussian_mixture(n, 1)
+        t, m, L = 0.2, 10, 6
+    else:
+        xy = inputs.uniform_points(n, 5)
+        t, m, L = 0.03, 14, 6
+    u = inputs.random_vector(n, 9)
+    op, b, rows, ref, err = sampled_check(imq, oracle, xy, t, m, L, u, 1024, seed=3)
+    st = op.stats()
+    if case != "strip":
+        assert st["cheb_levels"] > 0 and st["cheb_ring"] == 1, st
+    assert err <= 1e-10, (case, err)
+    assert err <= 1e-12, (case, err)  # the interpolation keeps ~1e-14 in practice
+    op.close()
+
+
 def test_dense_262144(imq, oracle):
     """Config 5's direct O(N^2) reference point at N = 262,144."""
     from paper_2205_04194_b200 import inputs
