@@ -435,8 +435,12 @@ constexpr int kFarMaxR = 8;    // a far work item holds <= 32 * kFarMaxR targets
 // distance >= 2 from all four children of A -- the outer ring of the 6x6
 // candidate square, common to the level-l lists of all of A's descendants);
 // 2 = the ring only (Chebyshev-node items of A, cheb.cu).
+// lsplit (level L): 0 = the union over the item's present children; 1 = only
+// its part in the outer ring of the level-(L-1) block X (needed by all of X's
+// children: the fine pass); 2 = only the inner part (per-leaf items of the
+// partial pass, each the leaf's own 7 of X's 12 inner-ring leaves).
 __device__ int build_far_list(const TreeParams& P, uint32_t par, int s, int cnt, uint32_t* list,
-                              int lane, int lmin, int lmax, int ring = 0) {
+                              int lane, int lmin, int lmax, int ring = 0, int lsplit = 0) {
   const int L = P.L;
   const int e = s + cnt;
   bool present = false;
@@ -487,6 +491,11 @@ __device__ int build_far_list(const TreeParams& P, uint32_t par, int s, int cnt,
             if (!((pmask >> ch) & 1)) continue;
             const int ci = 2 * pi + (ch >> 1), cj = 2 * pj + (ch & 1);
             if (max(abs(qi - ci), abs(qj - cj)) >= 2) keep = true;
+          }
+          if (lsplit) {
+            const int ri = qi - 2 * pi, rj = qj - 2 * pj;
+            const bool outer = ri == -2 || ri == 3 || rj == -2 || rj == 3;
+            keep = keep && (lsplit == 1 ? outer : !outer);
           }
         }
         q = morton(qi, qj);
@@ -730,7 +739,8 @@ struct FarOut {
   const int* perm;
   const double* far_add;  // or nullptr
   int lmin, lmax;
-  int ring;  // build_far_list ring mode of items without a level tag
+  int ring;    // build_far_list ring mode of items without a level tag
+  int lsplit;  // build_far_list level-L split of items without a level tag
 };
 
 __device__ __forceinline__ void far_store(const TreeParams& P, const FarOut& O, int q,
@@ -776,10 +786,13 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_m2p_far(const TreeParams P
   const int4 item = items[it];
   const uint32_t par = (uint32_t)item.x;
   const int s0 = item.y, cnt = item.z;
-  // item.w > 0: Chebyshev node item of level (w & 0xff) only, ring mode w >> 8
-  const int lev = item.w & 0xff, ring = lev > 0 ? (item.w >> 8) : O.ring;
+  // item.w > 0: item of level (w & 0xff) only (Chebyshev node / ring items,
+  // partial-pass leaves), ring mode (w >> 8) & 15, level-L split w >> 12
+  const int lev = item.w & 0xff;
+  const int ring = lev > 0 ? (item.w >> 8) & 15 : O.ring;
+  const int lsplit = lev > 0 ? (item.w >> 12) & 15 : O.lsplit;
   const int n = build_far_list(P, par, s0, cnt, list, lane, lev > 0 ? lev : O.lmin,
-                               lev > 0 ? lev : O.lmax, ring);
+                               lev > 0 ? lev : O.lmax, ring, lsplit);
   Targets<R> T;
   load_targets<R>(P, s0, cnt, lane, T);
   const int L = P.L;
@@ -856,9 +869,11 @@ __global__ void __launch_bounds__(WARPS * 32) k_m2p_far_generic(const TreeParams
   const uint32_t par = (uint32_t)item.x;
   const int s0 = item.y, cnt = item.z;
   uint32_t* list = lists[warp];
-  const int lev = item.w & 0xff, ring = lev > 0 ? (item.w >> 8) : O.ring;
+  const int lev = item.w & 0xff;
+  const int ring = lev > 0 ? (item.w >> 8) & 15 : O.ring;
+  const int lsplit = lev > 0 ? (item.w >> 12) & 15 : O.lsplit;
   const int n = build_far_list(P, par, s0, cnt, list, lane, lev > 0 ? lev : O.lmin,
-                               lev > 0 ? lev : O.lmax, ring);
+                               lev > 0 ? lev : O.lmax, ring, lsplit);
   for (int p0 = lane; p0 < cnt; p0 += 32) {
     const int p = s0 + p0;
     const double x = P.xs[p], y = P.ys[p];
@@ -1035,11 +1050,12 @@ void launch_scatter_rows(const double* src, const int* idx, int n, int width, do
 void launch_m2p_far(const TreeParams& P, const int4* items, const int* group_off, int begin,
                     int end, const double2* coef, double* far_s_ptr, const cudaStream_t* streams,
                     int nstreams, const double* near_part, int nslots, double* out,
-                    const int* perm, const double* far_add, int lmin, int lmax, int ring) {
+                    const int* perm, const double* far_add, int lmin, int lmax, int ring,
+                    int lsplit) {
   if (end <= begin) return;
   if (lmin < 1) lmin = 1;
   if (lmax < 1 || lmax > P.L) lmax = P.L;
-  const FarOut far_s{far_s_ptr, near_part, nslots, out, perm, far_add, lmin, lmax, ring};
+  const FarOut far_s{far_s_ptr, near_part, nslots, out, perm, far_add, lmin, lmax, ring, lsplit};
   cudaStream_t s = streams[0];
   int launched = 0;
   if (!m2p_specialised(P.M)) {

@@ -88,7 +88,7 @@ void launch_m2p_far(const TreeParams& P, const int4* items, const int* group_off
                     int nstreams, const double* near_part = nullptr, int nslots = 0,
                     double* out = nullptr, const int* perm = nullptr,
                     const double* far_add = nullptr, int lmin = 1, int lmax = 0,
-                    int ring = 0);
+                    int ring = 0, int lsplit = 0);
 bool m2p_specialised(int M);
 
 // ---- coarse far field by Chebyshev interpolation (cheb.cu)

@@ -125,7 +125,7 @@ void DeviceOperator::release() {
   dfree(d_cheb_items_); dfree(d_cboxes_); dfree(d_ceval_items_);
   dfree(d_cnx_); dfree(d_cny_); dfree(d_cnleaf_); dfree(d_cval_); dfree(d_ccoef_);
   dfree(d_rnx_); dfree(d_rny_); dfree(d_rnleaf_); dfree(d_rval_); dfree(d_rcoef_);
-  dfree(d_ring_items_);
+  dfree(d_ring_items_); dfree(d_lpart_items_);
   if (solve_pin_) cudaFreeHost(solve_pin_);
   solve_pin_ = nullptr;
   solve_pin_bytes_ = 0;
@@ -348,6 +348,34 @@ void DeviceOperator::build_items(int p_lo, int p_hi) {
     far_items_h_.insert(far_items_h_.end(), citems.begin(), citems.end());
     dfree(d_farc_);
     d_farc_ = dalloc<double>((size_t)N_, "coarse far");
+  }
+  // Partial pass (L >= 4): the fine items keep only the outer ring of X at
+  // level L (needed by all four leaves of X), and per-leaf items evaluate the
+  // rest of each leaf's level-L list (7 of X's 12 inner-ring leaves), adding
+  // into the coarse partial before the fine pass (build_far_list lsplit).
+  dfree(d_lpart_items_);
+  n_lpart_items_ = 0;
+  lpart_group_off_.assign(16, 0);
+  if (far_split_ && !getenv("IMQ_FAR_NOLSPLIT")) {
+    std::vector<std::vector<int4>> pg((size_t)rmax);
+    for (long long q = 0; q < n_leaves; ++q) {
+      const int a = std::max(p_lo, ls[(size_t)q]), b = std::min(p_hi, ls[(size_t)q + 1]);
+      if (b <= a) continue;
+      const int nchunk = (b - a + 32 * rmax - 1) / (32 * rmax);
+      const int size = 32 * ((b - a + 32 * nchunk - 1) / (32 * nchunk));
+      for (int c = a; c < b; c += size) {
+        const int cnt = std::min(size, b - c);
+        pg[(size_t)((cnt + 31) / 32 - 1)].push_back(make_int4((int)(q >> 2), c, cnt, L_ | (2 << 12)));
+      }
+    }
+    std::vector<int4> pitems;
+    grouped(pg, pitems, lpart_group_off_);
+    n_lpart_items_ = (int)pitems.size();
+    if (n_lpart_items_) {
+      d_lpart_items_ = dalloc<int4>(pitems.size(), "partial items");
+      cuda_check(cudaMemcpy(d_lpart_items_, pitems.data(), pitems.size() * sizeof(int4),
+                            cudaMemcpyHostToDevice), "H2D partial items");
+    }
   }
   build_cheb(p_lo, p_hi);
   // near items: one leaf each; R from the mean leaf occupancy (a typical leaf
@@ -1046,7 +1074,7 @@ void DeviceOperator::far_near(const double* d_us, double* d_out, const int* perm
   auto far_pass = [&](int b, int e, const int* goff, const double* near_part, int nslots,
                       double* out, const int* pm, double* far_s, const double* far_add, int lmin,
                       int lmax, const imqk::TreeParams* Pp = nullptr,
-                      const int4* its = nullptr, int ring = 0) {
+                      const int4* its = nullptr, int ring = 0, int lsplit = 0) {
     if (e <= b) return;
     cudaStream_t ss[1 + kAuxStreams] = {s};
     cuda_check(cudaEventRecord(ev_fork_, s), "fork");
@@ -1055,7 +1083,8 @@ void DeviceOperator::far_near(const double* d_us, double* d_out, const int* perm
       cuda_check(cudaStreamWaitEvent(aux_[k], ev_fork_, 0), "fork wait");
     }
     imqk::launch_m2p_far(Pp ? *Pp : P_, its ? its : d_far_items_, goff, b, e, d_coef_, far_s, ss,
-                         far_streams_, near_part, nslots, out, pm, far_add, lmin, lmax, ring);
+                         far_streams_, near_part, nslots, out, pm, far_add, lmin, lmax, ring,
+                         lsplit);
     for (int k = 0; k < kAuxStreams; ++k) {
       cuda_check(cudaEventRecord(ev_join_[k], aux_[k]), "join");
       cuda_check(cudaStreamWaitEvent(s, ev_join_[k], 0), "join wait");
@@ -1106,10 +1135,16 @@ void DeviceOperator::far_near(const double* d_us, double* d_out, const int* perm
       far_pass(std::max(far_begin, n_far_fine_), far_end, far_cgroup_off_.data(), nullptr, 0,
                nullptr, nullptr, d_farc_, nullptr, 1, L_ - 2);
     }
+    // the partial pass (whole fine range only): inner-ring leaves of level L
+    // per leaf, accumulated into the coarse partial
+    const bool lsplit = n_lpart_items_ > 0 && far_begin == 0 && far_end >= n_far_fine_;
+    if (lsplit)
+      far_pass(0, n_lpart_items_, lpart_group_off_.data(), nullptr, 0, nullptr, nullptr, d_farc_,
+               d_farc_, L_, L_, nullptr, d_lpart_items_);
     if (near_launched && sym) cuda_check(cudaStreamWaitEvent(s, ev_near_done_, 0), "near join");
     far_pass(far_begin, std::min(far_end, n_far_fine_), far_group_off_.data(), near_part, nslots,
              d_out, perm, d_far_, d_farc_, L_ - 1, L_, nullptr, nullptr,
-             cheb_run && ring_ ? 1 : 0);
+             cheb_run && ring_ ? 1 : 0, lsplit ? 1 : 0);
   } else {
     if (near_launched && sym) cuda_check(cudaStreamWaitEvent(s, ev_near_done_, 0), "near join");
     far_pass(far_begin, far_end, far_group_off_.data(), near_part, nslots, d_out, perm, d_far_,

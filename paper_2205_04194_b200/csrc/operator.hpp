@@ -226,6 +226,10 @@ class DeviceOperator {
   int4* d_pull_items_ = nullptr;  // sharded symmetric near field: boundary slots
   int n_pull_ = 0;
   int n_far_fine_ = 0;     // far items [0, n_far_fine_) fine, the rest coarse
+  // partial pass (far_split_): per-leaf items for the inner ring of level L
+  int n_lpart_items_ = 0;
+  std::vector<int> lpart_group_off_;
+  int4* d_lpart_items_ = nullptr;
   std::vector<int> far_cgroup_off_;
   double* d_farc_ = nullptr;  // coarse-pass far partial (sorted order)
   int n_pair_items_ = 0, n_chunks_ = 0;
