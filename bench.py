@@ -383,30 +383,9 @@ def b200_arm(args):
         cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
 
     if rank == 0:
-        fi, ni = op.items("far"), op.items("near")
-        def groups(it):  # launches = runs of equal points-per-lane (one per R group and pass)
-            if not len(it):
-                return 0
-            r = (it[:, 2] + 31) // 32
-            return 1 + int(np.count_nonzero(r[1:] != r[:-1]))
-        mode = op.stats()["near_mode"]
-        if mode == 1:    # symmetric per-leaf kernels, combined in the far epilogue
-            near_launches = groups(ni)
-        elif mode == 2:  # chunk-pair kernel + its reduction
-            near_launches = 2
-        else:            # per-target kernels (+ combine when the sources are split)
-            near_launches = groups(ni) + int(len(ni) > 0 and (ni[:, 3] != 15).any())
-        # ours per step: gather, leaf P2M, L transforms, far groups, near kernels;
-        # the L-1 M2M DGEMMs are cuBLAS (not counted).  With the Chebyshev
-        # coarse pass the coarse items are not launched: 2 node groups, one
-        # coefficient launch per coarse level and one evaluation launch instead.
-        far_launches = groups(fi)
-        if st["cheb_levels"] and len(fi):
-            r = (fi[:, 2] + 31) // 32
-            drop = np.nonzero(r[1:] < r[:-1])[0]
-            fine = fi[:int(drop[0]) + 1] if len(drop) else fi
-            far_launches = groups(fine) + 2 + st["cheb_levels"] + 1 + st["cheb_ring"] * (2 + st["cheb_levels"])
-        launches_per_step = 1 + 1 + L + far_launches + near_launches
+        # this library's kernel launches per product, counted by the library
+        # from its work-item groups; cuBLAS M2M not included
+        launches_per_step = int(op.stats()["kernel_launches"])
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,

@@ -515,6 +515,7 @@ int imq_ext_operator_stats(const imq_operator* op, imq_ext_stats* out) {
     out->cheb_node_pairs = c.cheb_node_pairs;
     out->cheb_levels = c.cheb_levels;
     out->cheb_ring = c.cheb_ring;
+    out->kernel_launches = c.kernel_launches;
     return IMQ_OK;
   });
 }

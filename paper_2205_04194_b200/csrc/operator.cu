@@ -1345,6 +1345,37 @@ PairCounts DeviceOperator::pair_counts() {
 
 // Pairs the kernels actually evaluate: direct (target, block) pairs of the
 // levels not covered by the Chebyshev pass, and (node, block) pairs.
+// This library's kernel launches in one apply_device (cuBLAS M2M excluded).
+int DeviceOperator::kernel_launches_per_apply() const {
+  auto groups = [](const std::vector<int>& off) {
+    int g = 0;
+    for (size_t r = 1; r < off.size(); ++r) g += off[r] > off[r - 1];
+    return g;
+  };
+  int n = 1 + 1 + L_;  // gather, leaf P2M, transform per level
+  if (M_ > 30) n += L_ - 1;  // custom M2M kernel instead of the DGEMMs
+  if (near_sym_) n += groups(near_group_off_) + (n_pull_ > 0);
+  else if (near_pair_) n += groups(pair_group_off_) + 1;
+  else n += groups(near_group_off_) + (near_split_ > 1);
+  if (far_split_) {
+    std::vector<int> fine(far_group_off_);
+    for (int& o : fine) o = std::min(o, n_far_fine_);
+    n += groups(fine) + groups(lpart_group_off_);
+    if (cheb_) {
+      n += groups(cheb_group_off_) + cheb_lc_ + 1;  // node groups, coefficients, evaluation
+      if (ring_) {
+        n += groups(ring_group_off_) + 1;  // ring node groups, level-(L-1) ring coefficients
+        for (int l = std::max(2, ring_l0_); l <= cheb_lc_; ++l) ++n;  // coarse ring coefficients
+      }
+    } else {
+      n += groups(far_cgroup_off_);
+    }
+  } else {
+    n += groups(far_group_off_);
+  }
+  return n;
+}
+
 void DeviceOperator::fill_eval_counts() {
   const int lc = cheb_ ? cheb_lc_ : 0;
   const bool rings = cheb_ && ring_ && ring_par_by_level_.size() == far_by_level_.size();
@@ -1363,6 +1394,7 @@ void DeviceOperator::fill_eval_counts() {
   counts_.cheb_node_pairs = nodes;
   counts_.cheb_levels = lc;
   counts_.cheb_ring = cheb_ && ring_ ? 1 : 0;
+  counts_.kernel_launches = kernel_launches_per_apply();
 }
 
 // ------------------------------------------------------------------ GMRES --

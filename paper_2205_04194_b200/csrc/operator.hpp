@@ -39,6 +39,7 @@ struct PairCounts {
   double cheb_node_pairs = 0;   // (Chebyshev node, block) pairs (incl. the level-(L-1) ring)
   int cheb_levels = 0;          // levels 1..cheb_levels through the Chebyshev pass
   int cheb_ring = 0;            // level-(L-1) ring through the level-(L-2) nodes
+  int kernel_launches = 0;      // this library's kernels per apply_device
 };
 
 std::vector<int> shard_bounds(const std::vector<int>& leaf_start, int L, int world);
@@ -141,6 +142,7 @@ class DeviceOperator {
   void build_items(int p_lo, int p_hi);
   void build_pair_items(int p_lo, int p_hi);
   void build_cheb(int p_lo, int p_hi);
+  int kernel_launches_per_apply() const;
   void fill_eval_counts();
   std::vector<double> far_by_level_, lists_by_level_;
   // rings: level-(L-1) ring (target, block) pairs; per level l, ring entries of
