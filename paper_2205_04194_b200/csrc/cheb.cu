@@ -369,6 +369,92 @@ __global__ void __launch_bounds__(kMmaWarps * 32) k_cheb_eval_mma(
   }
 }
 
+// The ring coefficients on the FP64 tensor cores.  A's series is first folded
+// into the ring values (exact: its degree NC-1 <= NR-1 is reproduced by the
+// NR-node interpolant),  V' = V + TT C_A TT^T  (TT[i][k] = T_k(x_i)),  then
+// for each child  c = B_hx V' B_hy^T.  Every product is a 24 x 24 x 20
+// zero-padded GEMM of m8n8k4 DMMA tiles (fragments from shared memory); the
+// zero padding of the staged matrices makes the padded outputs exactly 0.
+constexpr int kRcWarps = 4, kRcP = 24;  // padded leading dimension
+static_assert(NR <= 20 && NC <= 20, "k-steps of 4 up to 20");
+template <bool TA, bool TB>
+__device__ __forceinline__ void rc_tile(const double* A, const double* Bm, int tm, int tn,
+                                        int lane, double& d0, double& d1) {
+  const int r = lane >> 2, c = lane & 3;
+#pragma unroll
+  for (int s = 0; s < 5; ++s) {
+    const int k = 4 * s + c;
+    // A[m][k] (TA: stored transposed, A[k][m]);  B[k][n] (TB: stored as B[n][k])
+    const double a = TA ? A[k * kRcP + tm * 8 + r] : A[(tm * 8 + r) * kRcP + k];
+    const double b = TB ? Bm[(tn * 8 + r) * kRcP + k] : Bm[k * kRcP + tn * 8 + r];
+    dmma_884(d0, d1, a, b);
+  }
+}
+__global__ void __launch_bounds__(kRcWarps * 32) k_cheb_ring_coef_mma(
+    const int* __restrict__ boxes, int n_boxes, long long base_a, const double* __restrict__ coef_a,
+    const double* __restrict__ ring_vals, double* __restrict__ coef_c) {
+  constexpr int S = kRcP * kRcP;
+  __shared__ __align__(16) double TT[S], B[2][S], Ca[S], P[S], V[S], W[2][S];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nt = kRcWarps * 32;
+  for (int o = threadIdx.x; o < S; o += nt) {
+    const int i = o / kRcP, k = o % kRcP;
+    TT[o] = (i < NR && k < NC) ? c_TR[k * NR + i] : 0.0;          // [i][k]
+    B[0][o] = (i < NC && k < NR) ? c_B[0][i * NR + k] : 0.0;      // [k'][i]
+    B[1][o] = (i < NC && k < NR) ? c_B[1][i * NR + k] : 0.0;
+    Ca[o] = P[o] = V[o] = W[0][o] = W[1][o] = 0.0;
+  }
+  const int r = lane >> 2, cc = lane & 3;
+  for (int bx = blockIdx.x; bx < n_boxes; bx += gridDim.x) {
+    const uint32_t a = (uint32_t)boxes[bx];
+    __syncthreads();  // tables / previous box done
+    for (int o = threadIdx.x; o < NRR; o += nt) V[(o / NR) * kRcP + o % NR] = ring_vals[(size_t)a * NRR + o];
+    for (int o = threadIdx.x; o < NN; o += nt)
+      Ca[(o / NC) * kRcP + o % NC] = coef_a[(size_t)(base_a + a) * NN + o];
+    __syncthreads();
+    // P[k][j] = sum_m Ca[k][m] TT[j][m]   (B operand = TT stored transposed)
+    for (int t = warp; t < 9; t += kRcWarps) {
+      const int tm = t / 3, tn = t % 3;
+      double d0 = 0.0, d1 = 0.0;
+      rc_tile<false, true>(Ca, TT, tm, tn, lane, d0, d1);
+      P[(tm * 8 + r) * kRcP + tn * 8 + 2 * cc] = d0;
+      P[(tm * 8 + r) * kRcP + tn * 8 + 2 * cc + 1] = d1;
+    }
+    __syncthreads();
+    // V'[i][j] = V[i][j] + sum_k TT[i][k] P[k][j]
+    for (int t = warp; t < 9; t += kRcWarps) {
+      const int tm = t / 3, tn = t % 3;
+      double* v = &V[(tm * 8 + r) * kRcP + tn * 8 + 2 * cc];
+      double d0 = v[0], d1 = v[1];
+      rc_tile<false, false>(TT, P, tm, tn, lane, d0, d1);
+      __syncwarp();
+      v[0] = d0;
+      v[1] = d1;
+    }
+    __syncthreads();
+    // W[h][i][m'] = sum_j V'[i][j] B[h][m'][j]
+    for (int t = warp; t < 18; t += kRcWarps) {
+      const int h = t / 9, tm = (t % 9) / 3, tn = t % 3;
+      double d0 = 0.0, d1 = 0.0;
+      rc_tile<false, true>(V, B[h], tm, tn, lane, d0, d1);
+      W[h][(tm * 8 + r) * kRcP + tn * 8 + 2 * cc] = d0;
+      W[h][(tm * 8 + r) * kRcP + tn * 8 + 2 * cc + 1] = d1;
+    }
+    __syncthreads();
+    // child (hx, hy): c[k'][m'] = sum_i B[hx][k'][i] W[hy][i][m']
+    for (int t = warp; t < 36; t += kRcWarps) {
+      const int ch = t / 9, tm = (t % 9) / 3, tn = t % 3;
+      double d0 = 0.0, d1 = 0.0;
+      rc_tile<false, false>(B[ch >> 1], W[ch & 1], tm, tn, lane, d0, d1);
+      const int k = tm * 8 + r, m = tn * 8 + 2 * cc;
+      double* out = coef_c + (size_t)(4 * a + ch) * NN + k * NC;
+      if (k < NC) {
+        if (m < NC) out[m] = d0;
+        if (m + 1 < NC) out[m + 1] = d1;
+      }
+    }
+  }
+}
+
 }  // namespace
 
 // IMQ_CHEB_EVAL_FMA=1: the CUDA-core evaluation (comparison / development)
@@ -401,9 +487,15 @@ void launch_cheb_ring_coef(const int* boxes, int n_boxes, long long base_a,
   if (n_boxes) {
     static int sms = 0;
     if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    const int grid = std::min(n_boxes, 4 * std::max(sms, 1));
-    k_cheb_ring_coef<<<(unsigned)grid, NN, 0, s>>>(boxes, n_boxes, base_a, coef_a, ring_vals,
-                                                   coef_c);
+    if (eval_fma()) {
+      const int grid = std::min(n_boxes, 4 * std::max(sms, 1));
+      k_cheb_ring_coef<<<(unsigned)grid, NN, 0, s>>>(boxes, n_boxes, base_a, coef_a, ring_vals,
+                                                     coef_c);
+    } else {
+      const int grid = std::min(n_boxes, 8 * std::max(sms, 1));
+      k_cheb_ring_coef_mma<<<(unsigned)grid, kRcWarps * 32, 0, s>>>(boxes, n_boxes, base_a, coef_a,
+                                                                    ring_vals, coef_c);
+    }
   }
 }
 
