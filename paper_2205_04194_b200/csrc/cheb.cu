@@ -279,7 +279,7 @@ __global__ void __launch_bounds__(kEvalWarps * 32) k_cheb_eval(const TreeParams 
 // T_{n+8} = 2 T_8 T_n - T_{n-8}, so a lane forms only the degrees it holds.
 constexpr int kMmaKS = (NC + 3) / 4, kMmaNT = (NC + 7) / 8, kMmaWarps = 4;
 __device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
                : "+d"(d0), "+d"(d1)
                : "d"(a), "d"(b));
 }
@@ -306,16 +306,8 @@ __global__ void __launch_bounds__(kMmaWarps * 32) k_cheb_eval_mma(
   demorton(q, bi, bj);
   const double cx = block_center(P.ox, bi, P.cell[lc]), cy = block_center(P.oy, bj, P.cell[lc]);
   const double inv = 2.0 / P.cell[lc];
-  // coordinates one group ahead (the loop is otherwise bound by load latency)
-  double xn = P.xs[s0 + min(r, cnt - 1)], yn = P.ys[s0 + min(r, cnt - 1)];
-  for (int g = 0; g < cnt; g += 8) {
-    const int t = g + r;
-    const double xh = (xn - cx) * inv, yh = (yn - cy) * inv;
-    if (g + 8 < cnt) {
-      const int nidx = s0 + min(t + 8, cnt - 1);
-      xn = P.xs[nidx];
-      yn = P.ys[nidx];
-    }
+  // one group of 8 targets (lane row r): sum_{k,m} C[k][m] T_k(x^) T_m(y^)
+  auto group = [&](double xh, double yh) {
     // A: T_{4s+j}(y)
     double a[kMmaKS];
     {
@@ -337,35 +329,42 @@ __global__ void __launch_bounds__(kMmaWarps * 32) k_cheb_eval_mma(
       for (int s = 0; s < kMmaKS; ++s) dmma_884(d[nt][0], d[nt][1], a[s], b[nt][s]);
     }
     // T_{8nt + 2j + e}(x), e = 0, 1
-    double v;
-    {
-      const double x2 = 2.0 * xh;
-      double T[9];
-      T[0] = 1.0;
-      T[1] = xh;
+    const double x2 = 2.0 * xh;
+    double T[9];
+    T[0] = 1.0;
+    T[1] = xh;
 #pragma unroll
-      for (int k = 2; k <= 8; ++k) T[k] = fma(x2, T[k - 1], -T[k - 2]);
-      const double u0 = j == 0 ? T[0] : (j == 1 ? T[2] : (j == 2 ? T[4] : T[6]));
-      const double u1 = j == 0 ? T[1] : (j == 1 ? T[3] : (j == 2 ? T[5] : T[7]));
-      const double w0 = j == 0 ? T[8] : (j == 1 ? T[6] : (j == 2 ? T[4] : T[2]));  // T_{8-k0}
-      const double w1 = j == 0 ? T[7] : (j == 1 ? T[5] : (j == 2 ? T[3] : T[1]));  // T_{8-k1}
-      const double t8x2 = 2.0 * T[8];
-      double p0 = u0, p1 = u1, q0 = w0, q1 = w1;  // T_{k+8(nt-1)} roles
-      v = d[0][0] * u0 + d[0][1] * u1;
+    for (int k = 2; k <= 8; ++k) T[k] = fma(x2, T[k - 1], -T[k - 2]);
+    const double u0 = j == 0 ? T[0] : (j == 1 ? T[2] : (j == 2 ? T[4] : T[6]));
+    const double u1 = j == 0 ? T[1] : (j == 1 ? T[3] : (j == 2 ? T[5] : T[7]));
+    const double w0 = j == 0 ? T[8] : (j == 1 ? T[6] : (j == 2 ? T[4] : T[2]));  // T_{8-k0}
+    const double w1 = j == 0 ? T[7] : (j == 1 ? T[5] : (j == 2 ? T[3] : T[1]));  // T_{8-k1}
+    const double t8x2 = 2.0 * T[8];
+    double p0 = u0, p1 = u1, q0 = w0, q1 = w1;  // T_{k+8(nt-1)} roles
+    double v = d[0][0] * u0 + d[0][1] * u1;
 #pragma unroll
-      for (int nt = 1; nt < kMmaNT; ++nt) {
-        const double n0 = fma(t8x2, p0, -q0), n1 = fma(t8x2, p1, -q1);
-        v = fma(d[nt][0], n0, v);
-        v = fma(d[nt][1], n1, v);
-        q0 = p0;
-        q1 = p1;
-        p0 = n0;
-        p1 = n1;
-      }
+    for (int nt = 1; nt < kMmaNT; ++nt) {
+      const double n0 = fma(t8x2, p0, -q0), n1 = fma(t8x2, p1, -q1);
+      v = fma(d[nt][0], n0, v);
+      v = fma(d[nt][1], n1, v);
+      q0 = p0;
+      q1 = p1;
+      p0 = n0;
+      p1 = n1;
     }
     v += __shfl_xor_sync(0xffffffffu, v, 1);
     v += __shfl_xor_sync(0xffffffffu, v, 2);
-    if (j == 0 && t < cnt) out[s0 + t] = v;
+    return v;
+  };
+  // two independent groups per trip (ILP across the DMMA chains); targets
+  // past cnt repeat the last one and are not stored
+  for (int g = 0; g < cnt; g += 16) {
+    const int t0 = g + r, t1 = g + 8 + r;
+    const int i0 = s0 + min(t0, cnt - 1), i1 = s0 + min(t1, cnt - 1);
+    const double v0 = group((P.xs[i0] - cx) * inv, (P.ys[i0] - cy) * inv);
+    const double v1 = group((P.xs[i1] - cx) * inv, (P.ys[i1] - cy) * inv);
+    if (j == 0 && t0 < cnt) out[s0 + t0] = v0;
+    if (j == 0 && t1 < cnt) out[s0 + t1] = v1;
   }
 }
 
