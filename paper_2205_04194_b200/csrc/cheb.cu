@@ -277,7 +277,10 @@ __global__ void __launch_bounds__(kEvalWarps * 32) k_cheb_eval(const TreeParams 
 // lane -> [lane%4][lane/4], C/D lane -> [lane/4][2 (lane%4) + {0,1}].
 // Chebyshev values by the step identities T_{n+4} = 2 T_4 T_n - T_{n-4} and
 // T_{n+8} = 2 T_8 T_n - T_{n-8}, so a lane forms only the degrees it holds.
-constexpr int kMmaKS = (NC + 3) / 4, kMmaNT = (NC + 7) / 8, kMmaWarps = 4;
+// x-degrees k >= 8 NT (the last NC % 8) are summed with plain FMAs instead of
+// a third, mostly padded DMMA tile (10 instead of 15 DMMA per 8 targets).
+constexpr int kMmaKS = (NC + 3) / 4, kMmaNT = NC / 8, kMmaRem = NC % 8, kMmaWarps = 4;
+static_assert(kMmaRem == 0 || kMmaNT == 2, "remainder degrees 16..NC-1");
 __device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
                : "+d"(d0), "+d"(d1)
@@ -301,6 +304,14 @@ __global__ void __launch_bounds__(kMmaWarps * 32) k_cheb_eval_mma(
     for (int s = 0; s < kMmaKS; ++s) {
       const int m = 4 * s + j, k = 8 * nt + r;
       b[nt][s] = (m < NC && k < NC) ? __ldg(&c[k * NC + m]) : 0.0;
+    }
+  double cr[kMmaRem > 0 ? kMmaRem : 1][kMmaKS];  // C[16 + e][4 s + j]
+#pragma unroll
+  for (int e = 0; e < kMmaRem; ++e)
+#pragma unroll
+    for (int s = 0; s < kMmaKS; ++s) {
+      const int m = 4 * s + j;
+      cr[e][s] = m < NC ? __ldg(&c[(8 * kMmaNT + e) * NC + m]) : 0.0;
     }
   int bi, bj;
   demorton(q, bi, bj);
@@ -351,6 +362,16 @@ __global__ void __launch_bounds__(kMmaWarps * 32) k_cheb_eval_mma(
       q1 = p1;
       p0 = n0;
       p1 = n1;
+    }
+    // remainder degrees 16 + e: this lane's part of sum_m C[16+e][m] T_m(y),
+    // times T_{16+e}(x) = 2 T_8 T_{8+e} - T_e  (summed over the row's lanes below)
+#pragma unroll
+    for (int e = 0; e < kMmaRem; ++e) {
+      double z = 0.0;
+#pragma unroll
+      for (int s = 0; s < kMmaKS; ++s) z = fma(cr[e][s], a[s], z);
+      const double t8e = fma(t8x2, T[e], -T[8 - e]);
+      v = fma(z, fma(t8x2, t8e, -T[e]), v);
     }
     v += __shfl_xor_sync(0xffffffffu, v, 1);
     v += __shfl_xor_sync(0xffffffffu, v, 2);
@@ -484,8 +505,9 @@ void launch_cheb_ring_coef(const int* boxes, int n_boxes, long long base_a,
                            const double* coef_a, const double* ring_vals, double* coef_c,
                            cudaStream_t s) {
   if (n_boxes) {
-    static int sms = 0;
-    if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (eval_fma()) {
       const int grid = std::min(n_boxes, 4 * std::max(sms, 1));
       k_cheb_ring_coef<<<(unsigned)grid, NN, 0, s>>>(boxes, n_boxes, base_a, coef_a, ring_vals,
