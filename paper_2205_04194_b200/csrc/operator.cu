@@ -593,7 +593,7 @@ void DeviceOperator::build_cheb(int p_lo, int p_hi) {
   // plane (coarse boxes with t << h need more nodes at high orders).
   {
     const char* e = getenv("IMQ_RING_TAU");
-    const double tau = e ? atof(e) : 1.0;
+    const double tau = e ? atof(e) : 1.25;
     ring_l0_ = L_;
     for (int l = L_ - 1; l >= 2 && P_.t >= tau * 0.5 * P_.cell[l - 1]; --l) ring_l0_ = l;
     if (ring_l0_ > L_ - 1) ring_ = false;

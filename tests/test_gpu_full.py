@@ -1,6 +1,8 @@
 """Full-size configurations on the GPU: the product at BASELINE.json sizes is
 checked against the oracle on sampled rows (same per-row arithmetic as the
 reference, ora_fast_matvec_rows) and through size-independent properties."""
+import os
+
 import numpy as np
 import pytest
 
@@ -93,6 +95,20 @@ def test_chebyshev_and_ring_paths_vs_oracle(imq, oracle, case):
     assert err <= 1e-10, (case, err)
     assert err <= 1e-12, (case, err)  # the interpolation keeps ~1e-14 in practice
     op.close()
+
+
+def test_randomised_geometries_vs_oracle(imq, oracle):
+    """tools/stress_paths.py at a fixed seed: random point sets (strips,
+    annuli, clusters, duplicates), shapes, orders and levels through the
+    Chebyshev / ring / finest-split paths; sampled rows vs the oracle."""
+    import subprocess
+    import sys
+    from conftest import ROOT
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "stress_paths.py"), "11", "12"],
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-2000:]
+    worst = float(r.stdout.strip().splitlines()[-1].split()[-1])
+    assert worst <= 1e-12, r.stdout
 
 
 def test_dense_262144(imq, oracle):
