@@ -173,7 +173,9 @@ IMQ_API int imq_ext_operator_items(const imq_operator* op, int which, int* items
 IMQ_API int imq_ext_operator_far_near(const imq_operator* op, const double* d_us, double* d_bs,
                               int far_begin, int far_end, int near_begin, int near_end,
                               int scatter, void* stream);
-/* u (original order) -> Morton order. */
+/* u (original order) -> Morton order.  After imq_ext_operator_restrict only
+ * the positions of the rank's own and halo leaves are written (everything
+ * its moments and near field read). */
 IMQ_API int imq_ext_operator_gather(const imq_operator* op, const double* d_u, double* d_us,
                                     void* stream);
 /* Starts the near field of the Morton-ordered d_us on the operator's own

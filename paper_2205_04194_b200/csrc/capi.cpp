@@ -552,8 +552,7 @@ int imq_ext_operator_gather(const imq_operator* op, const double* d_u, double* d
                             void* stream) {
   if (!op || !d_u || !d_us) return fail(IMQ_ERR_INVALID_ARG, "imq_ext_operator_gather: null argument");
   return guard([&] {
-    imqk::launch_gather(d_u, op->op->perm_ptr(), op->op->size(), d_us,
-                        static_cast<cudaStream_t>(stream));
+    op->op->gather(d_u, d_us, static_cast<cudaStream_t>(stream));
     imqh::cuda_check(cudaGetLastError(), "gather launch");
     return IMQ_OK;
   });

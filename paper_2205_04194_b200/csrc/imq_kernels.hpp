@@ -56,6 +56,9 @@ void launch_leaf_start(const uint32_t* keys_sorted, long long n, long long n_lea
                        int* leaf_start, cudaStream_t s);
 void launch_gather(const double* src, const int* perm, long long n, double* dst,
                    cudaStream_t s);
+// Only the sorted positions of the listed leaves.
+void launch_gather_leaves(const double* src, const int* perm, const int* leaf_start,
+                          const int* leaves, int n_leaves, double* dst, cudaStream_t s);
 void launch_scatter(const double* src, const int* perm, long long n, double* dst,
                     cudaStream_t s);
 size_t sort_temp_bytes(long long n, int bits);

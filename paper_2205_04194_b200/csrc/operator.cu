@@ -931,6 +931,17 @@ void DeviceOperator::moments(const double* d_us, cudaStream_t s) {
 // ---------------------------------------------------------------------------
 bool DeviceOperator::sharded() const { return !need_par_h_.empty(); }
 
+void DeviceOperator::gather(const double* d_u, double* d_us, cudaStream_t s) {
+  std::lock_guard<std::mutex> lk(mtx_);
+  DeviceGuard g(device_);
+  Ordered o(*this, s);
+  if (sharded())
+    imqk::launch_gather_leaves(d_u, d_perm_, d_leaf_start_, d_local_leaves_,
+                               (int)local_leaves_h_.size(), d_us, s);
+  else
+    imqk::launch_gather(d_u, d_perm_, N_, d_us, s);
+}
+
 void DeviceOperator::setup_sharded_moments(int p_lo, int p_hi) {
   dfree(d_need_par_); dfree(d_local_leaves_); dfree(d_pack_a_); dfree(d_pack_c_); dfree(d_own_lvl_);
   need_par_h_.clear();

@@ -112,6 +112,9 @@ class DeviceOperator {
   void coarse_moments(double2** ptr, size_t* count) const;
   void moments_finish(cudaStream_t s);
   bool sharded() const;
+  // u (original order) -> Morton order; a sharded (restricted) operator
+  // writes only the positions of its own and halo leaves (all it reads).
+  void gather(const double* d_u, double* d_us, cudaStream_t s);
   // near_launched: the symmetric near field already runs on near_stream_
   // (apply_sorted_locked); the pass that reads its slots waits for ev_near_done_.
   void far_near(const double* d_us, double* d_out, const int* perm, cudaStream_t s,

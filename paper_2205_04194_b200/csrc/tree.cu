@@ -119,6 +119,18 @@ __global__ void __launch_bounds__(kThreads) k_gather(const double* __restrict__ 
   long long p = blockIdx.x * (long long)kThreads + threadIdx.x;
   if (p < n) dst[p] = src[perm[p]];
 }
+// Warp per listed leaf: dst[p] = src[perm[p]] for the leaf's sorted positions.
+__global__ void __launch_bounds__(kThreads) k_gather_leaves(const double* __restrict__ src,
+                                                            const int* __restrict__ perm,
+                                                            const int* __restrict__ leaf_start,
+                                                            const int* __restrict__ leaves,
+                                                            int n_leaves, double* __restrict__ dst) {
+  const int w = (int)((blockIdx.x * (long long)kThreads + threadIdx.x) >> 5), lane = threadIdx.x & 31;
+  if (w >= n_leaves) return;
+  const int q = leaves[w];
+  const int e = leaf_start[q + 1];
+  for (int p = leaf_start[q] + lane; p < e; p += 32) dst[p] = src[perm[p]];
+}
 __global__ void __launch_bounds__(kThreads) k_scatter(const double* __restrict__ src,
                                                       const int* __restrict__ perm, long long n,
                                                       double* __restrict__ dst) {
@@ -154,6 +166,12 @@ void launch_leaf_start(const uint32_t* keys_sorted, long long n, long long n_lea
 void launch_gather(const double* src, const int* perm, long long n, double* dst,
                    cudaStream_t s) {
   k_gather<<<nblk(n), kThreads, 0, s>>>(src, perm, n, dst);
+}
+void launch_gather_leaves(const double* src, const int* perm, const int* leaf_start,
+                          const int* leaves, int n_leaves, double* dst, cudaStream_t s) {
+  if (n_leaves > 0)
+    k_gather_leaves<<<nblk(32ll * n_leaves), kThreads, 0, s>>>(src, perm, leaf_start, leaves,
+                                                                 n_leaves, dst);
 }
 void launch_scatter(const double* src, const int* perm, long long n, double* dst,
                     cudaStream_t s) {
