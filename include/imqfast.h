@@ -152,6 +152,7 @@ typedef struct {
   int cheb_levels;         /* levels 1..cheb_levels evaluated through Chebyshev nodes (0: none) */
   int cheb_ring;           /* 1: the level-(L-1) ring also goes through the level-(L-2) nodes */
   int kernel_launches;     /* this library's kernel launches per imq_ext_operator_apply_device */
+  int cheb_xring;          /* 1: the level-L outer rings go through the level-(L-1) nodes */
 } imq_ext_stats;
 IMQ_API int imq_ext_operator_stats(const imq_operator* op, imq_ext_stats* out);
 

@@ -43,7 +43,7 @@ class imq_ext_stats(C.Structure):
                 ("far_items", C.c_longlong), ("near_items", C.c_longlong),
                 ("near_mode", C.c_int), ("far_pairs_direct", C.c_double),
                 ("cheb_node_pairs", C.c_double), ("cheb_levels", C.c_int), ("cheb_ring", C.c_int),
-                ("kernel_launches", C.c_int)]
+                ("kernel_launches", C.c_int), ("cheb_xring", C.c_int)]
 
 
 VERIFY_CB = C.CFUNCTYPE(None, C.c_char_p, C.c_int, C.c_double, C.c_void_p)

@@ -516,6 +516,7 @@ int imq_ext_operator_stats(const imq_operator* op, imq_ext_stats* out) {
     out->cheb_levels = c.cheb_levels;
     out->cheb_ring = c.cheb_ring;
     out->kernel_launches = c.kernel_launches;
+    out->cheb_xring = c.cheb_xring;
     return IMQ_OK;
   });
 }

@@ -37,6 +37,10 @@ constexpr int NR = kChebNR;       // ring nodes per dimension on the level-(L-2)
 constexpr int NRR = NR * NR;
 __device__ double c_TR[NRR];         // cos(k theta_i), theta_i = pi (i + 1/2) / NR
 __device__ double c_B[2][NC * NR];    // ring values -> child coefficients, [half][k' * NR + i]
+constexpr int NX = kChebNX;
+constexpr int NXX = NX * NX;
+static_assert(NX <= NC, "the X-ring series is added into the level-(L-1) series");
+__device__ double c_TX[NXX];         // cos(k theta_i), theta_i = pi (i + 1/2) / NX
 
 __global__ void k_cheb_nodes(const TreeParams P, int l, long long box_base, double* __restrict__ nx,
                              double* __restrict__ ny) {
@@ -65,6 +69,56 @@ __global__ void k_cheb_nodes_ring(const TreeParams P, int l, long long box_base,
   const double h = 0.5 * P.cell[l];
   nx[box_base * NRR + t] = block_center(P.ox, bi, P.cell[l]) + h * c_TR[NR + i];
   ny[box_base * NRR + t] = block_center(P.oy, bj, P.cell[l]) + h * c_TR[NR + j];
+}
+
+// X-ring nodes: NX x NX Chebyshev nodes of every box of level l, [box][i * NX + j].
+__global__ void k_cheb_nodes_x(const TreeParams P, int l, double* __restrict__ nx,
+                               double* __restrict__ ny) {
+  const long long nb = 1ll << (2 * (l + 1));
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nb * NXX) return;
+  const uint32_t q = (uint32_t)(t / NXX);
+  const int r = (int)(t % NXX), i = r / NX, j = r % NX;
+  int bi, bj;
+  demorton(q, bi, bj);
+  const double h = 0.5 * P.cell[l];
+  nx[t] = block_center(P.ox, bi, P.cell[l]) + h * c_TX[NX + i];
+  ny[t] = block_center(P.oy, bj, P.cell[l]) + h * c_TX[NX + j];
+}
+
+// Warp-per-box DCT of the X-ring node values, added into the box's level-(L-1)
+// series: coef[X][k][m] += (2/NX)^2 w_k w_m sum_{i,j} T_k(x_i) T_m(y_j) V[i][j].
+constexpr int kXcWarps = 4;
+__global__ void __launch_bounds__(kXcWarps * 32) k_cheb_xring_coef(const int* __restrict__ boxes,
+                                                                  int n_boxes,
+                                                                  const double* __restrict__ vals,
+                                                                  double* __restrict__ coef) {
+  __shared__ double T[NXX];
+  __shared__ double V[kXcWarps][NXX], Bm[kXcWarps][NXX];
+  for (int o = threadIdx.x; o < NXX; o += kXcWarps * 32) T[o] = c_TX[o];
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int bx = blockIdx.x * kXcWarps + warp;
+  if (bx >= n_boxes) return;
+  const uint32_t x = (uint32_t)boxes[bx];
+  const double* v = vals + (size_t)x * NXX;
+  for (int o = lane; o < NXX; o += 32) V[warp][o] = v[o];
+  __syncwarp();
+  for (int o = lane; o < NXX; o += 32) {  // Bm[i][m] = sum_j V[i][j] T[m][j]
+    const int i = o / NX, m = o % NX;
+    double s = 0.0;
+    for (int j = 0; j < NX; ++j) s = fma(V[warp][i * NX + j], T[m * NX + j], s);
+    Bm[warp][o] = s;
+  }
+  __syncwarp();
+  double* c = coef + (size_t)x * NN;
+  for (int o = lane; o < NXX; o += 32) {
+    const int k = o / NX, m = o % NX;
+    double s = 0.0;
+    for (int i = 0; i < NX; ++i) s = fma(T[k * NX + i], Bm[warp][i * NX + m], s);
+    s *= (2.0 / NX) * (2.0 / NX) * (k == 0 ? 0.5 : 1.0) * (m == 0 ? 0.5 : 1.0);
+    c[k * NC + m] += s;
+  }
 }
 
 // One CTA per box A of level l - 1 (listed in `boxes`): for each child c of A
@@ -493,6 +547,22 @@ void cheb_set_ring_tables(const double* T_nr, const double* B_left, const double
   cudaMemcpyToSymbol(c_TR, T_nr, NRR * sizeof(double));
   cudaMemcpyToSymbol(c_B, B_left, NC * NR * sizeof(double), 0);
   cudaMemcpyToSymbol(c_B, B_right, NC * NR * sizeof(double), NC * NR * sizeof(double));
+}
+
+void cheb_set_x_tables(const double* T_nx) {
+  cudaMemcpyToSymbol(c_TX, T_nx, NXX * sizeof(double));
+}
+
+void launch_cheb_nodes_x(const TreeParams& P, int l, double* nx, double* ny, cudaStream_t s) {
+  const long long n = (1ll << (2 * (l + 1))) * NXX;
+  k_cheb_nodes_x<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(P, l, nx, ny);
+}
+
+void launch_cheb_xring_coef(const int* boxes, int n_boxes, const double* vals, double* coef,
+                            cudaStream_t s) {
+  if (n_boxes)
+    k_cheb_xring_coef<<<(unsigned)((n_boxes + kXcWarps - 1) / kXcWarps), kXcWarps * 32, 0, s>>>(
+        boxes, n_boxes, vals, coef);
 }
 
 void launch_cheb_nodes_ring(const TreeParams& P, int l, long long box_base, double* nx, double* ny,

@@ -438,7 +438,8 @@ constexpr int kFarMaxR = 8;    // a far work item holds <= 32 * kFarMaxR targets
 // lsplit (level L): 0 = the union over the item's present children; 1 = only
 // its part in the outer ring of the level-(L-1) block X (needed by all of X's
 // children: the fine pass); 2 = only the inner part (per-leaf items of the
-// partial pass, each the leaf's own 7 of X's 12 inner-ring leaves).
+// partial pass, each the leaf's own 7 of X's 12 inner-ring leaves); 4 = the
+// outer ring of X for items whose targets are Chebyshev nodes of X.
 __device__ int build_far_list(const TreeParams& P, uint32_t par, int s, int cnt, uint32_t* list,
                               int lane, int lmin, int lmax, int ring = 0, int lsplit = 0) {
   const int L = P.L;
@@ -495,7 +496,8 @@ __device__ int build_far_list(const TreeParams& P, uint32_t par, int s, int cnt,
           if (lsplit) {
             const int ri = qi - 2 * pi, rj = qj - 2 * pj;
             const bool outer = ri == -2 || ri == 3 || rj == -2 || rj == 3;
-            keep = keep && (lsplit == 1 ? outer : !outer);
+            // 4: the outer ring whatever the item's targets (Chebyshev nodes of X)
+            keep = lsplit == 4 ? outer : (keep && (lsplit == 1 ? outer : !outer));
           }
         }
         q = morton(qi, qj);

@@ -106,6 +106,18 @@ constexpr int kChebN = IMQ_CHEB_N;  // nodes per dimension (degree kChebN - 1), 
 #define IMQ_CHEB_NR 20
 #endif
 constexpr int kChebNR = IMQ_CHEB_NR;
+// The level-L outer ring of a level-(L-1) box X through NX x NX nodes of X,
+// added into X's series (used where t >= tau_x h_X).
+#ifndef IMQ_CHEB_NX
+#define IMQ_CHEB_NX 14
+#endif
+constexpr int kChebNX = IMQ_CHEB_NX;
+void cheb_set_x_tables(const double* T_nx);
+void launch_cheb_nodes_x(const TreeParams& P, int l, double* nx, double* ny, cudaStream_t s);
+// coef[X] (NC x NC, x-degree major) += the NX x NX Chebyshev coefficients of
+// the node values of each listed box X.
+void launch_cheb_xring_coef(const int* boxes, int n_boxes, const double* vals, double* coef,
+                            cudaStream_t s);
 void cheb_set_tables(const double* T, const double* S_left, const double* S_right);
 // B[half][k' * NR + i]: ring node values on a level-(L-2) box (NR x NR nodes)
 // -> degree-(NC-1) coefficients on its child half (interpolation at the

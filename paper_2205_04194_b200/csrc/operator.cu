@@ -126,6 +126,8 @@ void DeviceOperator::release() {
   dfree(d_cnx_); dfree(d_cny_); dfree(d_cnleaf_); dfree(d_cval_); dfree(d_ccoef_);
   dfree(d_rnx_); dfree(d_rny_); dfree(d_rnleaf_); dfree(d_rval_); dfree(d_rcoef_);
   dfree(d_ring_items_); dfree(d_lpart_items_);
+  dfree(d_xnx_); dfree(d_xny_); dfree(d_xnleaf_); dfree(d_xval_); dfree(d_xring_items_);
+  dfree(d_xboxes_);
   if (solve_pin_) cudaFreeHost(solve_pin_);
   solve_pin_ = nullptr;
   solve_pin_bytes_ = 0;
@@ -565,7 +567,9 @@ void DeviceOperator::build_cheb(int p_lo, int p_hi) {
   ring_ = false;
   dfree(d_cheb_items_); dfree(d_cboxes_); dfree(d_ceval_items_);
   dfree(d_ring_items_);
-  n_cheb_items_ = n_ceval_ = n_ring_items_ = 0;
+  dfree(d_xring_items_); dfree(d_xboxes_);
+  xring_ = false;
+  n_cheb_items_ = n_ceval_ = n_ring_items_ = n_xring_items_ = n_xboxes_ = 0;
   if (!far_split_ || getenv("IMQ_FAR_NOCHEB") || !imqk::m2p_specialised(M_)) return;
   const int lc = L_ - 2;
   const std::vector<int>& ls = leaf_start_h_;
@@ -741,6 +745,71 @@ void DeviceOperator::build_cheb(int p_lo, int p_hi) {
     d_ring_items_ = dalloc<int4>(ritems.size(), "ring items");
     cuda_check(cudaMemcpy(d_ring_items_, ritems.data(), ritems.size() * sizeof(int4),
                           cudaMemcpyHostToDevice), "H2D ring items");
+  }
+  // The level-L outer ring of each level-(L-1) box X (20 leaves needed by all
+  // of X's targets) through NX x NX nodes of X, added into X's series, where
+  // the lifted singularities sit >= tau_x h_X off the real plane (NX = 14
+  // needs t / h_X >= ~5 for ~1e-13) and X holds enough targets.
+  if (ring_) {
+    constexpr int NX = imqk::kChebNX, NXX = NX * NX;
+    const char* e = getenv("IMQ_XRING_TAU");
+    const double taux = e ? atof(e) : 5.0;
+    long long nx_ne = 0, nx_tot = 0;
+    for (long long q = 0; q < (1ll << (2 * L_)); ++q) {
+      const int c = own(L_ - 1, q);
+      if (c > 0) ++nx_ne, nx_tot += c;
+    }
+    xring_ = !getenv("IMQ_FAR_NOXRING") && nx_ne > 0 &&
+             P_.t >= taux * 0.5 * P_.cell[L_ - 1] &&
+             (double)nx_tot >= 1.25 * NXX * (double)nx_ne;
+    if (xring_) {
+      const long long nbx = 1ll << (2 * L_);
+      if (xring_nodes_ != (size_t)nbx * NXX) {
+        dfree(d_xnx_); dfree(d_xny_); dfree(d_xnleaf_); dfree(d_xval_);
+        xring_nodes_ = (size_t)nbx * NXX;
+        d_xnx_ = dalloc<double>(xring_nodes_, "x-ring nodes");
+        d_xny_ = dalloc<double>(xring_nodes_, "x-ring nodes");
+        d_xnleaf_ = dalloc<uint32_t>(xring_nodes_, "x-ring node keys");
+        d_xval_ = dalloc<double>(xring_nodes_, "x-ring values");
+        cuda_check(cudaMemset(d_xnleaf_, 0, xring_nodes_ * sizeof(uint32_t)), "x-ring keys");
+        const long double pi = 3.141592653589793238462643383279502884L;
+        std::vector<double> TX((size_t)NXX);
+        for (int k = 0; k < NX; ++k)
+          for (int i = 0; i < NX; ++i) TX[(size_t)k * NX + i] = (double)cosl(k * pi * (i + 0.5L) / NX);
+        imqk::cheb_set_x_tables(TX.data());
+        imqk::launch_cheb_nodes_x(P_, L_ - 1, d_xnx_, d_xny_, stream_);
+        cuda_check(cudaStreamSynchronize(stream_), "x-ring nodes");
+      }
+      Px_ = P_;
+      Px_.xs = d_xnx_;
+      Px_.ys = d_xny_;
+      Px_.leaf = d_xnleaf_;
+      Px_.N = (int)xring_nodes_;
+      std::vector<std::vector<int4>> xg((size_t)imqk::far_max_points_per_lane());
+      std::vector<int> xboxes;
+      for (long long q = 0; q < nbx; ++q) {
+        if (!own(L_ - 1, q)) continue;
+        xboxes.push_back((int)q);
+        chunks(xg, (int)q, q * NXX, NXX, L_ | (4 << 12));
+      }
+      std::vector<int4> xitems;
+      xring_group_off_.assign(16, 0);
+      for (size_t r = 0; r < xg.size(); ++r) {
+        xitems.insert(xitems.end(), xg[r].begin(), xg[r].end());
+        xring_group_off_[r + 1] = (int)xitems.size();
+      }
+      for (size_t r = xg.size() + 1; r < 16; ++r) xring_group_off_[r] = (int)xitems.size();
+      n_xring_items_ = (int)xitems.size();
+      n_xboxes_ = (int)xboxes.size();
+      d_xring_items_ = dalloc<int4>(std::max<size_t>(1, xitems.size()), "x-ring items");
+      d_xboxes_ = dalloc<int>(std::max<size_t>(1, xboxes.size()), "x-ring boxes");
+      if (n_xring_items_)
+        cuda_check(cudaMemcpy(d_xring_items_, xitems.data(), xitems.size() * sizeof(int4),
+                              cudaMemcpyHostToDevice), "H2D x-ring items");
+      if (n_xboxes_)
+        cuda_check(cudaMemcpy(d_xboxes_, xboxes.data(), xboxes.size() * sizeof(int),
+                              cudaMemcpyHostToDevice), "H2D x-ring boxes");
+    }
   }
   n_cheb_items_ = (int)citems.size();
   n_ceval_ = (int)ev.size();
@@ -1106,6 +1175,9 @@ void DeviceOperator::far_near(const double* d_us, double* d_out, const int* perm
   if (far_split_) {
     // coarse pass (levels 1..L-2) into d_farc_, then the fine pass (L-1..L)
     const bool cheb_run = cheb_ && far_end > n_far_fine_;
+    // the partial pass (whole fine range only) and, with it, the X-ring
+    const bool lsplit = n_lpart_items_ > 0 && far_begin == 0 && far_end >= n_far_fine_;
+    const bool xr = cheb_run && xring_ && lsplit;
     if (cheb_run) {
       // list fields at the Chebyshev nodes of every box, series per level
       // (parent restricted + own), summed at the targets of the level-lc boxes
@@ -1114,6 +1186,9 @@ void DeviceOperator::far_near(const double* d_us, double* d_out, const int* perm
       if (ring_)  // the level-(l+1) rings at the NR x NR nodes of the level-l boxes
         far_pass(0, n_ring_items_, ring_group_off_.data(), nullptr, 0, nullptr, nullptr, d_rval_,
                  nullptr, 2, L_ - 1, &Pr_, d_ring_items_);
+      if (xr)  // the level-L outer rings at the NX x NX nodes of the level-(L-1) boxes
+        far_pass(0, n_xring_items_, xring_group_off_.data(), nullptr, 0, nullptr, nullptr,
+                 d_xval_, nullptr, L_, L_, &Px_, d_xring_items_);
       constexpr long long NN = imqk::kChebN * imqk::kChebN, NRR = imqk::kChebNR * imqk::kChebNR;
       for (int l = 1; l <= cheb_lc_; ++l) {
         const int* bx = d_cboxes_ + cbox_off_[(size_t)l];
@@ -1137,6 +1212,7 @@ void DeviceOperator::far_near(const double* d_us, double* d_out, const int* perm
                                     cbox_off_[(size_t)lc + 1] - cbox_off_[(size_t)lc],
                                     cheb_base_[(size_t)lc], d_ccoef_,
                                     d_rval_ + cheb_base_[(size_t)lc] * NRR, d_rcoef_, s);
+        if (xr) imqk::launch_cheb_xring_coef(d_xboxes_, n_xboxes_, d_xval_, d_rcoef_, s);
         imqk::launch_cheb_eval(P_, L_ - 1, d_ceval_items_, n_ceval_, 0, d_rcoef_, d_farc_, s);
       } else {
         imqk::launch_cheb_eval(P_, cheb_lc_, d_ceval_items_, n_ceval_,
@@ -1146,15 +1222,15 @@ void DeviceOperator::far_near(const double* d_us, double* d_out, const int* perm
       far_pass(std::max(far_begin, n_far_fine_), far_end, far_cgroup_off_.data(), nullptr, 0,
                nullptr, nullptr, d_farc_, nullptr, 1, L_ - 2);
     }
-    // the partial pass (whole fine range only): inner-ring leaves of level L
-    // per leaf, accumulated into the coarse partial
-    const bool lsplit = n_lpart_items_ > 0 && far_begin == 0 && far_end >= n_far_fine_;
+    // the partial pass: inner-ring leaves of level L per leaf, accumulated
+    // into the coarse partial
     if (lsplit)
       far_pass(0, n_lpart_items_, lpart_group_off_.data(), nullptr, 0, nullptr, nullptr, d_farc_,
                d_farc_, L_, L_, nullptr, d_lpart_items_);
     if (near_launched && sym) cuda_check(cudaStreamWaitEvent(s, ev_near_done_, 0), "near join");
+    // with the X-ring the fine pass keeps only the level-(L-1) inner blocks
     far_pass(far_begin, std::min(far_end, n_far_fine_), far_group_off_.data(), near_part, nslots,
-             d_out, perm, d_far_, d_farc_, L_ - 1, L_, nullptr, nullptr,
+             d_out, perm, d_far_, d_farc_, L_ - 1, xr ? L_ - 1 : L_, nullptr, nullptr,
              cheb_run && ring_ ? 1 : 0, lsplit ? 1 : 0);
   } else {
     if (near_launched && sym) cuda_check(cudaStreamWaitEvent(s, ev_near_done_, 0), "near join");
@@ -1311,6 +1387,13 @@ PairCounts DeviceOperator::pair_counts() {
       for (int aj = 0; aj < ga; ++aj)
         if (count(l - 1, ai, aj)) ring_par_by_level_[(size_t)l] += (double)ring_count(l, ai, aj);
   }
+  xring_direct_ = xring_lists_ = 0;
+  if (L >= 3) {  // level-L outer rings of the level-(L-1) boxes
+    const int ga = 1 << L;
+    for (int ai = 0; ai < ga; ++ai)
+      for (int aj = 0; aj < ga; ++aj)
+        if (count(L - 1, ai, aj)) xring_lists_ += (double)ring_count(L, ai, aj);
+  }
   lists_by_level_.assign((size_t)L + 1, 0.0);
   for (int l = 1; l <= L; ++l) {
     const int grid = 1 << (l + 1);
@@ -1335,6 +1418,7 @@ PairCounts DeviceOperator::pair_counts() {
           ring_child_by_level_[(size_t)l] += (double)nr;
           if (l == L - 1) ring_direct_ += (double)nt * (double)nr;
         }
+        if (l == L && L >= 3) xring_direct_ += (double)nt * (double)ring_count(L, i >> 1, j >> 1);
         if (l == L) {
           long long nn = 0;
           for (int qi = std::max(0, i - 1); qi <= std::min(grid - 1, i + 1); ++qi)
@@ -1376,6 +1460,7 @@ int DeviceOperator::kernel_launches_per_apply() const {
       n += groups(cheb_group_off_) + cheb_lc_ + 1;  // node groups, coefficients, evaluation
       if (ring_) {
         n += groups(ring_group_off_) + 1;  // ring node groups, level-(L-1) ring coefficients
+        if (xring_) n += groups(xring_group_off_) + 1;  // X-ring node groups, coefficients
         for (int l = std::max(2, ring_l0_); l <= cheb_lc_; ++l) ++n;  // coarse ring coefficients
       }
     } else {
@@ -1401,11 +1486,16 @@ void DeviceOperator::fill_eval_counts() {
     if (rings && l >= ring_l0_ && l < L_) nodes += ring_par_by_level_[(size_t)l] * NRR;
   }
   if (rings) direct -= ring_direct_;
+  if (rings && xring_ && n_lpart_items_ > 0) {
+    direct -= xring_direct_;
+    nodes += xring_lists_ * imqk::kChebNX * imqk::kChebNX;
+  }
   counts_.far_pairs_direct = direct;
   counts_.cheb_node_pairs = nodes;
   counts_.cheb_levels = lc;
   counts_.cheb_ring = cheb_ && ring_ ? 1 : 0;
   counts_.kernel_launches = kernel_launches_per_apply();
+  counts_.cheb_xring = cheb_ && ring_ && xring_ && n_lpart_items_ > 0 ? 1 : 0;
 }
 
 // ------------------------------------------------------------------ GMRES --

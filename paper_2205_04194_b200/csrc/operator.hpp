@@ -40,6 +40,7 @@ struct PairCounts {
   int cheb_levels = 0;          // levels 1..cheb_levels through the Chebyshev pass
   int cheb_ring = 0;            // level-(L-1) ring through the level-(L-2) nodes
   int kernel_launches = 0;      // this library's kernels per apply_device
+  int cheb_xring = 0;           // level-L outer rings through the level-(L-1) nodes
 };
 
 std::vector<int> shard_bounds(const std::vector<int>& leaf_start, int L, int world);
@@ -151,6 +152,7 @@ class DeviceOperator {
   // rings: level-(L-1) ring (target, block) pairs; per level l, ring entries of
   // the level-l lists (summed over non-empty boxes) and of the level-(l-1) boxes
   double ring_direct_ = 0;
+  double xring_direct_ = 0, xring_lists_ = 0;  // level-L outer rings: target pairs, X lists
   std::vector<double> ring_child_by_level_, ring_par_by_level_;
   void setup_sharded_moments(int p_lo, int p_hi);
   void release();
@@ -221,6 +223,16 @@ class DeviceOperator {
   // level-(L-1) ring through the level-(L-2) boxes' NR x NR nodes (build_cheb)
   bool ring_ = false;
   int ring_l0_ = 0;  // rings of levels ring_l0_..L-1
+  // the level-L outer ring through NX x NX nodes of the level-(L-1) boxes
+  bool xring_ = false;
+  int n_xring_items_ = 0, n_xboxes_ = 0;
+  size_t xring_nodes_ = 0;
+  std::vector<int> xring_group_off_;
+  imqk::TreeParams Px_{};
+  double *d_xnx_ = nullptr, *d_xny_ = nullptr, *d_xval_ = nullptr;
+  uint32_t* d_xnleaf_ = nullptr;
+  int4* d_xring_items_ = nullptr;
+  int* d_xboxes_ = nullptr;
   int n_ring_items_ = 0;
   size_t ring_nodes_ = 0;
   std::vector<int> ring_group_off_;

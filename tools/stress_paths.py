@@ -56,6 +56,7 @@ for c in range(ncase):
         extra = f"  (no rings: {float(np.max(np.abs(b2[rows] - ref)) / np.max(np.abs(ref))):.2e})"
         op2.close()
     print(f"{c:2d} {kind:8s} n={n:8d} L={L} m={m:2d} t={t:.2e}  cheb={st['cheb_levels']} "
-          f"ring={st['cheb_ring']} near={st['near_mode']}  dev {err:.2e}{extra}", flush=True)
+          f"ring={st['cheb_ring']} xring={st['cheb_xring']} near={st['near_mode']}  dev {err:.2e}{extra}",
+          flush=True)
     op.close()
 print(f"worst {worst:.2e}")
