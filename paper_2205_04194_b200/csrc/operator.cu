@@ -790,7 +790,7 @@ void DeviceOperator::build_cheb(int p_lo, int p_hi) {
       for (long long q = 0; q < nbx; ++q) {
         if (!own(L_ - 1, q)) continue;
         xboxes.push_back((int)q);
-        chunks(xg, (int)q, q * NXX, NXX, L_ | (4 << 12));
+        chunks(xg, (int)q, q * NXX, NXX, 0);  // levels / modes from the launch (far_near)
       }
       std::vector<int4> xitems;
       xring_group_off_.assign(16, 0);
@@ -1186,9 +1186,10 @@ void DeviceOperator::far_near(const double* d_us, double* d_out, const int* perm
       if (ring_)  // the level-(l+1) rings at the NR x NR nodes of the level-l boxes
         far_pass(0, n_ring_items_, ring_group_off_.data(), nullptr, 0, nullptr, nullptr, d_rval_,
                  nullptr, 2, L_ - 1, &Pr_, d_ring_items_);
-      if (xr)  // the level-L outer rings at the NX x NX nodes of the level-(L-1) boxes
+      if (xr)  // at the NX x NX nodes of each level-(L-1) box X: its level-(L-1)
+               // inner blocks (ring mode 1) and its level-L outer ring (lsplit 4)
         far_pass(0, n_xring_items_, xring_group_off_.data(), nullptr, 0, nullptr, nullptr,
-                 d_xval_, nullptr, L_, L_, &Px_, d_xring_items_);
+                 d_xval_, nullptr, L_ - 1, L_, &Px_, d_xring_items_, 1, 4);
       constexpr long long NN = imqk::kChebN * imqk::kChebN, NRR = imqk::kChebNR * imqk::kChebNR;
       for (int l = 1; l <= cheb_lc_; ++l) {
         const int* bx = d_cboxes_ + cbox_off_[(size_t)l];
@@ -1222,16 +1223,23 @@ void DeviceOperator::far_near(const double* d_us, double* d_out, const int* perm
       far_pass(std::max(far_begin, n_far_fine_), far_end, far_cgroup_off_.data(), nullptr, 0,
                nullptr, nullptr, d_farc_, nullptr, 1, L_ - 2);
     }
-    // the partial pass: inner-ring leaves of level L per leaf, accumulated
-    // into the coarse partial
-    if (lsplit)
-      far_pass(0, n_lpart_items_, lpart_group_off_.data(), nullptr, 0, nullptr, nullptr, d_farc_,
+    if (xr) {
+      // everything but the level-L inner ring went through the series: the
+      // per-leaf partial pass is the last far pass and combines far + near
+      if (near_launched && sym) cuda_check(cudaStreamWaitEvent(s, ev_near_done_, 0), "near join");
+      far_pass(0, n_lpart_items_, lpart_group_off_.data(), near_part, nslots, d_out, perm, d_far_,
                d_farc_, L_, L_, nullptr, d_lpart_items_);
-    if (near_launched && sym) cuda_check(cudaStreamWaitEvent(s, ev_near_done_, 0), "near join");
-    // with the X-ring the fine pass keeps only the level-(L-1) inner blocks
-    far_pass(far_begin, std::min(far_end, n_far_fine_), far_group_off_.data(), near_part, nslots,
-             d_out, perm, d_far_, d_farc_, L_ - 1, xr ? L_ - 1 : L_, nullptr, nullptr,
-             cheb_run && ring_ ? 1 : 0, lsplit ? 1 : 0);
+    } else {
+      // the partial pass: inner-ring leaves of level L per leaf, accumulated
+      // into the coarse partial
+      if (lsplit)
+        far_pass(0, n_lpart_items_, lpart_group_off_.data(), nullptr, 0, nullptr, nullptr, d_farc_,
+                 d_farc_, L_, L_, nullptr, d_lpart_items_);
+      if (near_launched && sym) cuda_check(cudaStreamWaitEvent(s, ev_near_done_, 0), "near join");
+      far_pass(far_begin, std::min(far_end, n_far_fine_), far_group_off_.data(), near_part, nslots,
+               d_out, perm, d_far_, d_farc_, L_ - 1, L_, nullptr, nullptr,
+               cheb_run && ring_ ? 1 : 0, lsplit ? 1 : 0);
+    }
   } else {
     if (near_launched && sym) cuda_check(cudaStreamWaitEvent(s, ev_near_done_, 0), "near join");
     far_pass(far_begin, far_end, far_group_off_.data(), near_part, nslots, d_out, perm, d_far_,
@@ -1455,7 +1463,8 @@ int DeviceOperator::kernel_launches_per_apply() const {
   if (far_split_) {
     std::vector<int> fine(far_group_off_);
     for (int& o : fine) o = std::min(o, n_far_fine_);
-    n += groups(fine) + groups(lpart_group_off_);
+    n += (cheb_ && ring_ && xring_ && n_lpart_items_ > 0 ? 0 : groups(fine)) +
+         groups(lpart_group_off_);
     if (cheb_) {
       n += groups(cheb_group_off_) + cheb_lc_ + 1;  // node groups, coefficients, evaluation
       if (ring_) {
@@ -1487,8 +1496,10 @@ void DeviceOperator::fill_eval_counts() {
   }
   if (rings) direct -= ring_direct_;
   if (rings && xring_ && n_lpart_items_ > 0) {
-    direct -= xring_direct_;
-    nodes += xring_lists_ * imqk::kChebNX * imqk::kChebNX;
+    // X nodes: level-L outer rings and the level-(L-1) inner lists
+    const double inner_lm1 = lists_by_level_[(size_t)L_ - 1] - ring_child_by_level_[(size_t)L_ - 1];
+    direct -= xring_direct_ + (far_by_level_[(size_t)L_ - 1] - ring_direct_);
+    nodes += (xring_lists_ + inner_lm1) * imqk::kChebNX * imqk::kChebNX;
   }
   counts_.far_pairs_direct = direct;
   counts_.cheb_node_pairs = nodes;
