@@ -255,13 +255,16 @@ def test_sharded_application_emulated(imq, world):
     from paper_2205_04194_b200.parallel import ShardedOperator
     n, m, L = 1 << 18, 12, 5
     # t = 0.01: Chebyshev coarse levels, no rings (t < h); t = 0.05: the
-    # level-(L-1) ring through the level-(L-2) boxes' nodes is on
+    # level-(L-1) ring through the level-(L-2) boxes' nodes is on; t = 0.2:
+    # also the X-ring (the fine pass is gone, the partial pass combines)
     for xy, t in ((inputs.uniform_points(n, 3), 0.01), (inputs.gaussian_mixture(n, 1), 0.01),
-                  (inputs.uniform_points(n, 3), 0.05)):
+                  (inputs.uniform_points(n, 3), 0.05), (inputs.uniform_points(n, 3), 0.2)):
         u = torch.tensor(inputs.random_vector(n, 7), device="cuda")
         full = imq.FastOperator(xy, t, m, L)
-        if t == 0.05:
+        if t >= 0.05:
             assert full.stats()["cheb_ring"] == 1, full.stats()
+        if t >= 0.2:  # t >= 5 h of the level-(L-1) boxes: the X-ring too
+            assert full.stats()["cheb_xring"] == 1, full.stats()
         b_ref = torch.empty_like(u)
         full.apply_device(u, b_ref)
         torch.cuda.synchronize()
