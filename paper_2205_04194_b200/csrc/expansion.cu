@@ -168,11 +168,26 @@ __global__ void __launch_bounds__(32 * (WPL > 4 ? WPL : 4), WPL == 1 ? 4 : 1) k_
   for (int k = 0; k < NM; ++k)
 #pragma unroll
     for (int i = 0; i < NI; ++i) ar[k][i] = ai[k][i] = 0.0;
+  // the next point's coordinates and weight are loaded one trip ahead (the
+  // loop is otherwise bound by their load latency)
+  constexpr int kStep = WPL * (32 / G);
+  int p = s + grp + sub * (32 / G);
+  double nx = 0.0, ny = 0.0, nu = 0.0;
+  if (p < e) {
+    nx = P.xs[p];
+    ny = P.ys[p];
+    nu = u_s[p];
+  }
 #pragma unroll 1
-  for (int p = s + grp + sub * (32 / G); p < e; p += WPL * (32 / G)) {
-    const double ex = P.xs[p] - zx, ey = P.ys[p] - zy;
+  for (; p < e; p += kStep) {
+    const double ex = nx - zx, ey = ny - zy, uu = nu;
+    if (p + kStep < e) {
+      nx = P.xs[p + kStep];
+      ny = P.ys[p + kStep];
+      nu = u_s[p + kStep];
+    }
     const double e2 = fma(ex, ex, ey * ey);
-    double pr = u_s[p], pi = 0.0, br = ex, bi = ey;
+    double pr = uu, pi = 0.0, br = ex, bi = ey;
 #pragma unroll
     for (int b = 0; b < LOGG; ++b) {
       if ((g >> b) & 1) {
