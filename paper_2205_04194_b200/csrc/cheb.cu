@@ -433,11 +433,22 @@ __global__ void __launch_bounds__(kMmaWarps * 32) k_cheb_eval_mma(
   };
   // two independent groups per trip (ILP across the DMMA chains); targets
   // past cnt repeat the last one and are not stored
+  // coordinates one trip ahead
+  double x0 = P.xs[s0 + min(r, cnt - 1)], y0 = P.ys[s0 + min(r, cnt - 1)];
+  double x1 = P.xs[s0 + min(8 + r, cnt - 1)], y1 = P.ys[s0 + min(8 + r, cnt - 1)];
   for (int g = 0; g < cnt; g += 16) {
     const int t0 = g + r, t1 = g + 8 + r;
-    const int i0 = s0 + min(t0, cnt - 1), i1 = s0 + min(t1, cnt - 1);
-    const double v0 = group((P.xs[i0] - cx) * inv, (P.ys[i0] - cy) * inv);
-    const double v1 = group((P.xs[i1] - cx) * inv, (P.ys[i1] - cy) * inv);
+    const double a0 = (x0 - cx) * inv, b0 = (y0 - cy) * inv;
+    const double a1 = (x1 - cx) * inv, b1 = (y1 - cy) * inv;
+    if (g + 16 < cnt) {
+      const int n0 = s0 + min(t0 + 16, cnt - 1), n1 = s0 + min(t1 + 16, cnt - 1);
+      x0 = P.xs[n0];
+      y0 = P.ys[n0];
+      x1 = P.xs[n1];
+      y1 = P.ys[n1];
+    }
+    const double v0 = group(a0, b0);
+    const double v1 = group(a1, b1);
     if (j == 0 && t0 < cnt) out[s0 + t0] = v0;
     if (j == 0 && t1 < cnt) out[s0 + t1] = v1;
   }
