@@ -12,6 +12,13 @@
 // the level-lc boxes.  With n = kChebN = 18 the interpolation error of one
 // box's field is <= ~1e-13 of its maximum (tests vs the oracle).
 //
+// Rings: the part of a level-l list common to all four
+// children of a level-(l-1) box A is evaluated once at NR x NR nodes of A and
+// restricted into each child's series (k_cheb_ring_coef_mma); where t is
+// large against the level-(L-1) boxes X, X's shared lists go through NX x NX
+// nodes of X (k_cheb_xring_coef).  The series is evaluated at the targets on
+// the FP64 tensor cores (k_cheb_eval_mma).
+//
 // (tables in global memory: the kernels index them per thread, which the
 // constant cache would serialise)
 // Layouts: per box (levels 1..lc, all boxes, level-major, Morton inside a
