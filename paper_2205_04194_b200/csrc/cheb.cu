@@ -40,10 +40,13 @@ constexpr int NN = NC * NC;
 
 __device__ double c_T[NN];        // T[k * NC + i] = cos(k theta_i), theta_i = pi (i + 1/2) / NC
 __device__ double c_S[2][NN];     // child restriction, [half][k' * NC + k]
-constexpr int NR = kChebNR;       // ring nodes per dimension on the level-(L-2) boxes
+constexpr int NR = kChebNR;       // ring nodes per dimension (the larger variant)
 constexpr int NRR = NR * NR;
-__device__ double c_TR[NRR];         // cos(k theta_i), theta_i = pi (i + 1/2) / NR
-__device__ double c_B[2][NC * NR];    // ring values -> child coefficients, [half][k' * NR + i]
+static_assert(kChebNR2 <= kChebNR, "variant 1 is the smaller ring");
+// per ring variant v (nr = kRingNr[v]): cos(k theta_i) at [k * nr + i], and
+// ring values -> child coefficients at [half][k' * nr + i]
+__device__ double c_TR[2][NRR];
+__device__ double c_B[2][2][NC * NR];
 constexpr int NX = kChebNX;
 constexpr int NXX = NX * NX;
 static_assert(NX <= NC, "the X-ring series is added into the level-(L-1) series");
@@ -63,19 +66,20 @@ __global__ void k_cheb_nodes(const TreeParams P, int l, long long box_base, doub
   ny[(box_base + q) * NN + r] = block_center(P.oy, bj, P.cell[l]) + h * c_T[NC + j];
 }
 
-// Ring nodes: NR x NR Chebyshev nodes of every box of level l, [box][i * NR + j].
-__global__ void k_cheb_nodes_ring(const TreeParams P, int l, long long box_base,
+// Ring nodes: nr x nr Chebyshev nodes of every box of level l, [box][i * nr + j].
+__global__ void k_cheb_nodes_ring(const TreeParams P, int l, int v, long long node_base,
                                   double* __restrict__ nx, double* __restrict__ ny) {
+  const int nr = v ? kChebNR2 : kChebNR, nrr = nr * nr;
   const long long nb = 1ll << (2 * (l + 1));
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= nb * NRR) return;
-  const uint32_t q = (uint32_t)(t / NRR);
-  const int r = (int)(t % NRR), i = r / NR, j = r % NR;
+  if (t >= nb * nrr) return;
+  const uint32_t q = (uint32_t)(t / nrr);
+  const int r = (int)(t % nrr), i = r / nr, j = r % nr;
   int bi, bj;
   demorton(q, bi, bj);
   const double h = 0.5 * P.cell[l];
-  nx[box_base * NRR + t] = block_center(P.ox, bi, P.cell[l]) + h * c_TR[NR + i];
-  ny[box_base * NRR + t] = block_center(P.oy, bj, P.cell[l]) + h * c_TR[NR + j];
+  nx[node_base + t] = block_center(P.ox, bi, P.cell[l]) + h * c_TR[v][nr + i];
+  ny[node_base + t] = block_center(P.oy, bj, P.cell[l]) + h * c_TR[v][nr + j];
 }
 
 // X-ring nodes: NX x NX Chebyshev nodes of every box of level l, [box][i * NX + j].
@@ -125,89 +129,6 @@ __global__ void __launch_bounds__(kXcWarps * 32) k_cheb_xring_coef(const int* __
     for (int i = 0; i < NX; ++i) s = fma(T[k * NX + i], Bm[warp][i * NX + m], s);
     s *= (2.0 / NX) * (2.0 / NX) * (k == 0 ? 0.5 : 1.0) * (m == 0 ? 0.5 : 1.0);
     c[k * NC + m] += s;
-  }
-}
-
-// One CTA per box A of level l - 1 (listed in `boxes`): for each child c of A
-// (Morton 4A + 2 hx + hy), the degree-(NC-1) series on c of
-//   level-l ring field of A:  B_hx V_A B_hy^T   (V_A: NR x NR node values)
-//   series of A:              S_hx C_A S_hy^T   (C_A: NC x NC coefficients)
-// coef_c[c] = their sum (k_cheb_coef then adds c's own list at level l < L-1;
-// at level L-1 it is the series evaluated at the targets).
-__global__ void __launch_bounds__(NN) k_cheb_ring_coef(const int* __restrict__ boxes,
-                                                       int n_boxes, long long base_a,
-                                                       const double* __restrict__ coef_a,
-                                                       const double* __restrict__ ring_vals,
-                                                       double* __restrict__ coef_c) {
-  static_assert(NR % 2 == 0 && NC % 2 == 0, "paired (LDS.128) loads");
-  // transposed intermediates (contraction index contiguous): Wt[h][m'][i] =
-  // sum_j V[i][j] B[h][m'][j], Ut[h][m'][k] = sum_j Ca[k][j] S[h][m'][j]
-  __shared__ __align__(16) double V[NRR], Wt[2][NC * NR], Ut[2][NN], Ca[NN], B[2][NC * NR],
-      S[2][NN];
-  const int r = threadIdx.x;
-  for (int o = r; o < 2 * NC * NR; o += NN) (&B[0][0])[o] = (&c_B[0][0])[o];
-  S[0][r] = c_S[0][r];
-  S[1][r] = c_S[1][r];
-  // persistent over the listed boxes: the tables are staged once per CTA
-  for (int bx = blockIdx.x; bx < n_boxes; bx += gridDim.x) {
-  const uint32_t a = (uint32_t)boxes[bx];
-  __syncthreads();  // previous box done with V, Ca, Wt, Ut
-  for (int o = r; o < NRR; o += NN) V[o] = ring_vals[(size_t)a * NRR + o];
-  Ca[r] = coef_a[(size_t)(base_a + a) * NN + r];
-  __syncthreads();
-  auto ld2 = [](const double* p) { return *reinterpret_cast<const double2*>(p); };
-  for (int o = r; o < NR * NC; o += NN) {  // both halves per (i, m')
-    const int i = o / NC, m = o % NC;
-    double w0 = 0.0, w1 = 0.0;
-#pragma unroll
-    for (int j = 0; j < NR; j += 2) {
-      const double2 v = ld2(&V[i * NR + j]), b0 = ld2(&B[0][m * NR + j]), b1 = ld2(&B[1][m * NR + j]);
-      w0 = fma(v.y, b0.y, fma(v.x, b0.x, w0));
-      w1 = fma(v.y, b1.y, fma(v.x, b1.x, w1));
-    }
-    Wt[0][m * NR + i] = w0;
-    Wt[1][m * NR + i] = w1;
-  }
-  {
-    const int k = r / NC, m = r % NC;
-    double u0 = 0.0, u1 = 0.0;
-#pragma unroll
-    for (int j = 0; j < NC; j += 2) {
-      const double2 cv = ld2(&Ca[k * NC + j]), s0 = ld2(&S[0][m * NC + j]), s1 = ld2(&S[1][m * NC + j]);
-      u0 = fma(cv.y, s0.y, fma(cv.x, s0.x, u0));
-      u1 = fma(cv.y, s1.y, fma(cv.x, s1.x, u1));
-    }
-    Ut[0][m * NC + k] = u0;
-    Ut[1][m * NC + k] = u1;
-  }
-  __syncthreads();
-  // the four children (hx, hy) of (k', m'): sum_i B[hx][k'][i] Wt[hy][m'][i]
-  //                                       + sum_k S[hx][k'][k] Ut[hy][m'][k]
-  const int k = r / NC, m = r % NC;
-  double c00 = 0.0, c01 = 0.0, c10 = 0.0, c11 = 0.0;
-#pragma unroll
-  for (int i = 0; i < NR; i += 2) {
-    const double2 b0 = ld2(&B[0][k * NR + i]), b1 = ld2(&B[1][k * NR + i]);
-    const double2 w0 = ld2(&Wt[0][m * NR + i]), w1 = ld2(&Wt[1][m * NR + i]);
-    c00 = fma(b0.y, w0.y, fma(b0.x, w0.x, c00));
-    c01 = fma(b0.y, w1.y, fma(b0.x, w1.x, c01));
-    c10 = fma(b1.y, w0.y, fma(b1.x, w0.x, c10));
-    c11 = fma(b1.y, w1.y, fma(b1.x, w1.x, c11));
-  }
-#pragma unroll
-  for (int kk = 0; kk < NC; kk += 2) {
-    const double2 s0 = ld2(&S[0][k * NC + kk]), s1 = ld2(&S[1][k * NC + kk]);
-    const double2 u0 = ld2(&Ut[0][m * NC + kk]), u1 = ld2(&Ut[1][m * NC + kk]);
-    c00 = fma(s0.y, u0.y, fma(s0.x, u0.x, c00));
-    c01 = fma(s0.y, u1.y, fma(s0.x, u1.x, c01));
-    c10 = fma(s1.y, u0.y, fma(s1.x, u0.x, c10));
-    c11 = fma(s1.y, u1.y, fma(s1.x, u1.x, c11));
-  }
-  double* out = coef_c + (size_t)(4 * a) * NN + r;  // child 2 hx + hy
-  out[0] = c00;
-  out[NN] = c01;
-  out[2 * NN] = c10;
-  out[3 * NN] = c11;
   }
 }
 
@@ -483,23 +404,26 @@ __device__ __forceinline__ void rc_tile(const double* A, const double* Bm, int t
   }
 }
 __global__ void __launch_bounds__(kRcWarps * 32) k_cheb_ring_coef_mma(
-    const int* __restrict__ boxes, int n_boxes, long long base_a, const double* __restrict__ coef_a,
-    const double* __restrict__ ring_vals, double* __restrict__ coef_c) {
+    int v, const int* __restrict__ boxes, int n_boxes, long long base_a,
+    const double* __restrict__ coef_a, const double* __restrict__ ring_vals,
+    double* __restrict__ coef_c) {
   constexpr int S = kRcP * kRcP;
   __shared__ __align__(16) double TT[S], B[2][S], Ca[S], P[S], V[S], W[2][S];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nt = kRcWarps * 32;
+  const int nr = v ? kChebNR2 : kChebNR, nrr = nr * nr;  // ring variant
   for (int o = threadIdx.x; o < S; o += nt) {
     const int i = o / kRcP, k = o % kRcP;
-    TT[o] = (i < NR && k < NC) ? c_TR[k * NR + i] : 0.0;          // [i][k]
-    B[0][o] = (i < NC && k < NR) ? c_B[0][i * NR + k] : 0.0;      // [k'][i]
-    B[1][o] = (i < NC && k < NR) ? c_B[1][i * NR + k] : 0.0;
+    TT[o] = (i < nr && k < NC) ? c_TR[v][k * nr + i] : 0.0;          // [i][k]
+    B[0][o] = (i < NC && k < nr) ? c_B[v][0][i * nr + k] : 0.0;      // [k'][i]
+    B[1][o] = (i < NC && k < nr) ? c_B[v][1][i * nr + k] : 0.0;
     Ca[o] = P[o] = V[o] = W[0][o] = W[1][o] = 0.0;
   }
   const int r = lane >> 2, cc = lane & 3;
   for (int bx = blockIdx.x; bx < n_boxes; bx += gridDim.x) {
     const uint32_t a = (uint32_t)boxes[bx];
     __syncthreads();  // tables / previous box done
-    for (int o = threadIdx.x; o < NRR; o += nt) V[(o / NR) * kRcP + o % NR] = ring_vals[(size_t)a * NRR + o];
+    for (int o = threadIdx.x; o < nrr; o += nt)
+      V[(o / nr) * kRcP + o % nr] = ring_vals[(size_t)a * nrr + o];
     for (int o = threadIdx.x; o < NN; o += nt)
       Ca[(o / NC) * kRcP + o % NC] = coef_a[(size_t)(base_a + a) * NN + o];
     __syncthreads();
@@ -561,10 +485,12 @@ void cheb_set_tables(const double* T, const double* S_left, const double* S_righ
   cudaMemcpyToSymbol(c_S, S_right, NN * sizeof(double), NN * sizeof(double));
 }
 
-void cheb_set_ring_tables(const double* T_nr, const double* B_left, const double* B_right) {
-  cudaMemcpyToSymbol(c_TR, T_nr, NRR * sizeof(double));
-  cudaMemcpyToSymbol(c_B, B_left, NC * NR * sizeof(double), 0);
-  cudaMemcpyToSymbol(c_B, B_right, NC * NR * sizeof(double), NC * NR * sizeof(double));
+void cheb_set_ring_tables(int v, const double* T_nr, const double* B_left, const double* B_right) {
+  const int nr = kRingNr[v];
+  cudaMemcpyToSymbol(c_TR, T_nr, (size_t)nr * nr * sizeof(double), (size_t)v * NRR * sizeof(double));
+  const size_t bsz = (size_t)NC * NR * sizeof(double);
+  cudaMemcpyToSymbol(c_B, B_left, (size_t)NC * nr * sizeof(double), ((size_t)v * 2 + 0) * bsz);
+  cudaMemcpyToSymbol(c_B, B_right, (size_t)NC * nr * sizeof(double), ((size_t)v * 2 + 1) * bsz);
 }
 
 void cheb_set_x_tables(const double* T_nx) {
@@ -583,28 +509,22 @@ void launch_cheb_xring_coef(const int* boxes, int n_boxes, const double* vals, d
         boxes, n_boxes, vals, coef);
 }
 
-void launch_cheb_nodes_ring(const TreeParams& P, int l, long long box_base, double* nx, double* ny,
-                            cudaStream_t s) {
-  const long long n = (1ll << (2 * (l + 1))) * NRR;
-  k_cheb_nodes_ring<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(P, l, box_base, nx, ny);
+void launch_cheb_nodes_ring(const TreeParams& P, int l, int v, long long node_base, double* nx,
+                            double* ny, cudaStream_t s) {
+  const long long n = (1ll << (2 * (l + 1))) * kRingNr[v] * kRingNr[v];
+  k_cheb_nodes_ring<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(P, l, v, node_base, nx, ny);
 }
 
-void launch_cheb_ring_coef(const int* boxes, int n_boxes, long long base_a,
+void launch_cheb_ring_coef(int v, const int* boxes, int n_boxes, long long base_a,
                            const double* coef_a, const double* ring_vals, double* coef_c,
                            cudaStream_t s) {
   if (n_boxes) {
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (eval_fma()) {
-      const int grid = std::min(n_boxes, 4 * std::max(sms, 1));
-      k_cheb_ring_coef<<<(unsigned)grid, NN, 0, s>>>(boxes, n_boxes, base_a, coef_a, ring_vals,
-                                                     coef_c);
-    } else {
-      const int grid = std::min(n_boxes, 8 * std::max(sms, 1));
-      k_cheb_ring_coef_mma<<<(unsigned)grid, kRcWarps * 32, 0, s>>>(boxes, n_boxes, base_a, coef_a,
-                                                                    ring_vals, coef_c);
-    }
+    const int grid = std::min(n_boxes, 8 * std::max(sms, 1));
+    k_cheb_ring_coef_mma<<<(unsigned)grid, kRcWarps * 32, 0, s>>>(v, boxes, n_boxes, base_a, coef_a,
+                                                                  ring_vals, coef_c);
   }
 }
 

@@ -106,6 +106,12 @@ constexpr int kChebN = IMQ_CHEB_N;  // nodes per dimension (degree kChebN - 1), 
 #define IMQ_CHEB_NR 20
 #endif
 constexpr int kChebNR = IMQ_CHEB_NR;
+// Rings whose parent boxes have t >= 2.5 h use fewer nodes (variant 1).
+#ifndef IMQ_CHEB_NR2
+#define IMQ_CHEB_NR2 18
+#endif
+constexpr int kChebNR2 = IMQ_CHEB_NR2;
+constexpr int kRingNr[2] = {kChebNR, kChebNR2};
 // The level-L outer ring of a level-(L-1) box X through NX x NX nodes of X,
 // added into X's series (used where t >= tau_x h_X).
 #ifndef IMQ_CHEB_NX
@@ -119,15 +125,17 @@ void launch_cheb_nodes_x(const TreeParams& P, int l, double* nx, double* ny, cud
 void launch_cheb_xring_coef(const int* boxes, int n_boxes, const double* vals, double* coef,
                             cudaStream_t s);
 void cheb_set_tables(const double* T, const double* S_left, const double* S_right);
-// B[half][k' * NR + i]: ring node values on a level-(L-2) box (NR x NR nodes)
-// -> degree-(NC-1) coefficients on its child half (interpolation at the
-// child's NC nodes of the degree-(NR-1) interpolant).
-void cheb_set_ring_tables(const double* T_nr, const double* B_left, const double* B_right);
-void launch_cheb_nodes_ring(const TreeParams& P, int l, long long box_base, double* nx, double* ny,
-                            cudaStream_t s);
-// One CTA per listed level-(L-2) box A: coef_c[child] = B V_A B^T (ring) +
-// S C_A S^T (series of A restricted), for the four children of A.
-void launch_cheb_ring_coef(const int* boxes, int n_boxes, long long base_a,
+// Ring variant v (nr = kRingNr[v] nodes per dimension): T_nr[k * nr + i],
+// B[half][k' * nr + i]: ring node values on a box A (nr x nr nodes) ->
+// degree-(NC-1) coefficients on its child half (interpolation at the child's
+// NC nodes of the degree-(nr-1) interpolant).
+void cheb_set_ring_tables(int v, const double* T_nr, const double* B_left, const double* B_right);
+// nr x nr nodes of every box of level l, written from node index node_base.
+void launch_cheb_nodes_ring(const TreeParams& P, int l, int v, long long node_base, double* nx,
+                            double* ny, cudaStream_t s);
+// One CTA per listed box A: coef_c[child] = B V_A B^T (ring, values at
+// ring_vals + a * nr^2) + S C_A S^T (series of A restricted), four children.
+void launch_cheb_ring_coef(int v, const int* boxes, int n_boxes, long long base_a,
                            const double* coef_a, const double* ring_vals, double* coef_c,
                            cudaStream_t s);
 void launch_cheb_nodes(const TreeParams& P, int l, long long box_base, double* nx, double* ny,

@@ -645,9 +645,21 @@ void DeviceOperator::build_cheb(int p_lo, int p_hi) {
   Pn_.leaf = d_cnleaf_;
   Pn_.N = (int)cheb_nodes_;
   if (ring_) {  // ring nodes of every box of levels 1..lc (rings of levels 2..L-1)
-    if (ring_nodes_ != (size_t)nb * NRR) {
+    // per parent level a: ring variant (fewer nodes where t >= 2.5 h_a, the
+    // singularities sitting further off the real plane) and node offset
+    const char* e2 = getenv("IMQ_RING2_TAU");
+    const double tau2 = e2 ? atof(e2) : 2.5;
+    ring_v_.assign((size_t)lc + 1, 0);
+    ring_nbase_.assign((size_t)lc + 2, 0);
+    for (int a = 1; a <= lc; ++a) {
+      ring_v_[(size_t)a] = P_.t >= tau2 * 0.5 * P_.cell[a] ? 1 : 0;
+      const long long nr = imqk::kRingNr[ring_v_[(size_t)a]];
+      ring_nbase_[(size_t)a + 1] = ring_nbase_[(size_t)a] + (1ll << (2 * (a + 1))) * nr * nr;
+    }
+    const size_t want = (size_t)ring_nbase_[(size_t)lc + 1];
+    if (ring_nodes_ != want) {
       dfree(d_rnx_); dfree(d_rny_); dfree(d_rnleaf_); dfree(d_rval_); dfree(d_rcoef_);
-      ring_nodes_ = (size_t)nb * NRR;
+      ring_nodes_ = want;
       d_rnx_ = dalloc<double>(ring_nodes_, "ring nodes");
       d_rny_ = dalloc<double>(ring_nodes_, "ring nodes");
       d_rnleaf_ = dalloc<uint32_t>(ring_nodes_, "ring node keys");
@@ -655,31 +667,35 @@ void DeviceOperator::build_cheb(int p_lo, int p_hi) {
       d_rcoef_ = dalloc<double>((size_t)(1ll << (2 * (lc + 2))) * NN, "ring child coefficients");
       cuda_check(cudaMemset(d_rnleaf_, 0, ring_nodes_ * sizeof(uint32_t)), "ring keys");
       const long double pi = 3.141592653589793238462643383279502884L;
-      std::vector<double> TR((size_t)NRR), B[2];
-      for (int k = 0; k < NR; ++k)
-        for (int i = 0; i < NR; ++i) TR[(size_t)k * NR + i] = (double)cosl(k * pi * (i + 0.5L) / NR);
-      // B[h][k'][i] = (2/NC) w_k' sum_i' T_k'(u_i') l_i((u_i' -/+ 1) / 2), l_i the
-      // Lagrange basis of the NR parent nodes, l_i(y) = (2/NR) sum_k w_k T_k(x_i) T_k(y)
-      for (int h = 0; h < 2; ++h) {
-        B[h].assign((size_t)NC * NR, 0.0);
-        for (int kp = 0; kp < NC; ++kp)
-          for (int i = 0; i < NR; ++i) {
-            const long double xi = cosl(pi * (i + 0.5L) / NR);
-            long double acc = 0;
-            for (int ip = 0; ip < NC; ++ip) {
-              const long double u = cosl(pi * (ip + 0.5L) / NC);
-              const long double y = h == 0 ? (u - 1) / 2 : (u + 1) / 2;
-              long double li = 0;
-              for (int k = 0; k < NR; ++k)
-                li += (k == 0 ? 0.5L : 1.0L) * cosl(k * acosl(xi)) * cosl(k * acosl(y));
-              acc += cosl(kp * pi * (ip + 0.5L) / NC) * (2.0L / NR) * li;
+      for (int v = 0; v < 2; ++v) {
+        const int nr = imqk::kRingNr[v];
+        std::vector<double> TR((size_t)nr * nr), B[2];
+        for (int k = 0; k < nr; ++k)
+          for (int i = 0; i < nr; ++i) TR[(size_t)k * nr + i] = (double)cosl(k * pi * (i + 0.5L) / nr);
+        // B[h][k'][i] = (2/NC) w_k' sum_i' T_k'(u_i') l_i((u_i' -/+ 1) / 2), l_i the
+        // Lagrange basis of the nr parent nodes, l_i(y) = (2/nr) sum_k w_k T_k(x_i) T_k(y)
+        for (int h = 0; h < 2; ++h) {
+          B[h].assign((size_t)NC * nr, 0.0);
+          for (int kp = 0; kp < NC; ++kp)
+            for (int i = 0; i < nr; ++i) {
+              const long double xi = cosl(pi * (i + 0.5L) / nr);
+              long double acc = 0;
+              for (int ip = 0; ip < NC; ++ip) {
+                const long double u = cosl(pi * (ip + 0.5L) / NC);
+                const long double y = h == 0 ? (u - 1) / 2 : (u + 1) / 2;
+                long double li = 0;
+                for (int k = 0; k < nr; ++k)
+                  li += (k == 0 ? 0.5L : 1.0L) * cosl(k * acosl(xi)) * cosl(k * acosl(y));
+                acc += cosl(kp * pi * (ip + 0.5L) / NC) * (2.0L / nr) * li;
+              }
+              B[h][(size_t)kp * nr + i] = (double)((2.0L / NC) * (kp == 0 ? 0.5L : 1.0L) * acc);
             }
-            B[h][(size_t)kp * NR + i] = (double)((2.0L / NC) * (kp == 0 ? 0.5L : 1.0L) * acc);
-          }
+        }
+        imqk::cheb_set_ring_tables(v, TR.data(), B[0].data(), B[1].data());
       }
-      imqk::cheb_set_ring_tables(TR.data(), B[0].data(), B[1].data());
       for (int l = 1; l <= lc; ++l)
-        imqk::launch_cheb_nodes_ring(P_, l, cheb_base_[(size_t)l], d_rnx_, d_rny_, stream_);
+        imqk::launch_cheb_nodes_ring(P_, l, ring_v_[(size_t)l], ring_nbase_[(size_t)l], d_rnx_,
+                                     d_rny_, stream_);
       cuda_check(cudaStreamSynchronize(stream_), "ring nodes");
     }
     Pr_ = P_;
@@ -712,7 +728,10 @@ void DeviceOperator::build_cheb(int p_lo, int p_hi) {
              l | ((ring_ && l >= ring_l0_ ? 1 : 0) << 8));
       // the level-(l+1) ring of q at q's ring nodes
       if (ring_ && l + 1 >= ring_l0_)
-        chunks(rg, (int)((4 * q) << (2 * (L_ - 2 - l))), (cheb_base_[(size_t)l] + q) * NRR, NRR,
+        chunks(rg, (int)((4 * q) << (2 * (L_ - 2 - l))),
+               ring_nbase_[(size_t)l] + q * imqk::kRingNr[ring_v_[(size_t)l]] *
+                                            imqk::kRingNr[ring_v_[(size_t)l]],
+               imqk::kRingNr[ring_v_[(size_t)l]] * imqk::kRingNr[ring_v_[(size_t)l]],
                (l + 1) | (2 << 8));
     }
   }
@@ -1198,8 +1217,8 @@ void DeviceOperator::far_near(const double* d_us, double* d_out, const int* perm
           // parent series restricted + parent's level-l ring -> this level; then + own list
           const int* pbx = d_cboxes_ + cbox_off_[(size_t)l - 1];
           const int npb = cbox_off_[(size_t)l] - cbox_off_[(size_t)l - 1];
-          imqk::launch_cheb_ring_coef(pbx, npb, cheb_base_[(size_t)l - 1], d_ccoef_,
-                                      d_rval_ + cheb_base_[(size_t)l - 1] * NRR,
+          imqk::launch_cheb_ring_coef(ring_v_[(size_t)l - 1], pbx, npb, cheb_base_[(size_t)l - 1],
+                                      d_ccoef_, d_rval_ + ring_nbase_[(size_t)l - 1],
                                       d_ccoef_ + cheb_base_[(size_t)l] * NN, s);
           imqk::launch_cheb_coef(l, bx, nbx, cheb_base_[(size_t)l], -1, d_cval_, d_ccoef_, s);
         } else {
@@ -1209,10 +1228,10 @@ void DeviceOperator::far_near(const double* d_us, double* d_out, const int* perm
       }
       if (ring_) {
         const int lc = cheb_lc_;
-        imqk::launch_cheb_ring_coef(d_cboxes_ + cbox_off_[(size_t)lc],
+        imqk::launch_cheb_ring_coef(ring_v_[(size_t)lc], d_cboxes_ + cbox_off_[(size_t)lc],
                                     cbox_off_[(size_t)lc + 1] - cbox_off_[(size_t)lc],
                                     cheb_base_[(size_t)lc], d_ccoef_,
-                                    d_rval_ + cheb_base_[(size_t)lc] * NRR, d_rcoef_, s);
+                                    d_rval_ + ring_nbase_[(size_t)lc], d_rcoef_, s);
         if (xr) imqk::launch_cheb_xring_coef(d_xboxes_, n_xboxes_, d_xval_, d_rcoef_, s);
         imqk::launch_cheb_eval(P_, L_ - 1, d_ceval_items_, n_ceval_, 0, d_rcoef_, d_farc_, s);
       } else {
@@ -1492,7 +1511,10 @@ void DeviceOperator::fill_eval_counts() {
                 (rings && l >= ring_l0_ ? ring_child_by_level_[(size_t)l] : 0.0)) * NN;
     else
       direct += far_by_level_[(size_t)l];
-    if (rings && l >= ring_l0_ && l < L_) nodes += ring_par_by_level_[(size_t)l] * NRR;
+    if (rings && l >= ring_l0_ && l < L_ && (size_t)l - 1 < ring_v_.size()) {
+      const double nr = imqk::kRingNr[ring_v_[(size_t)l - 1]];
+      nodes += ring_par_by_level_[(size_t)l] * nr * nr;
+    }
   }
   if (rings) direct -= ring_direct_;
   if (rings && xring_ && n_lpart_items_ > 0) {

@@ -223,6 +223,8 @@ class DeviceOperator {
   // level-(L-1) ring through the level-(L-2) boxes' NR x NR nodes (build_cheb)
   bool ring_ = false;
   int ring_l0_ = 0;  // rings of levels ring_l0_..L-1
+  std::vector<int> ring_v_;            // ring variant per parent level (kRingNr)
+  std::vector<long long> ring_nbase_;  // first ring node of each parent level
   // the level-L outer ring through NX x NX nodes of the level-(L-1) boxes
   bool xring_ = false;
   int n_xring_items_ = 0, n_xboxes_ = 0;
