@@ -115,7 +115,7 @@ constexpr int kRingNr[2] = {kChebNR, kChebNR2};
 // The level-L outer ring of a level-(L-1) box X through NX x NX nodes of X,
 // added into X's series (used where t >= tau_x h_X).
 #ifndef IMQ_CHEB_NX
-#define IMQ_CHEB_NX 14
+#define IMQ_CHEB_NX 12
 #endif
 constexpr int kChebNX = IMQ_CHEB_NX;
 void cheb_set_x_tables(const double* T_nx);

@@ -39,6 +39,11 @@ for c in range(ncase):
     m = int(rng.choice([4, 6, 8, 10, 12, 14, 16, 18, 20]))
     t = float(10 ** rng.uniform(-4, 0))
     L = int(rng.integers(4, 8))
+    if os.environ.get("STRESS_XGATE"):  # t just above the X-ring gate: t / h_X in [5, 5.4]
+        m = int(rng.choice([12, 16, 20]))
+        pts = xy.reshape(-1, 2)
+        side = float(max(np.ptp(pts[:, 0]), np.ptp(pts[:, 1])))
+        t = float(rng.uniform(5.0, 5.4) * side / 2 ** (L + 1))
     u = inputs.random_vector(n, 100 + c)
     op = P.FastOperator(xy, t, m, L)
     st = op.stats()
