@@ -108,7 +108,7 @@ constexpr int kChebN = IMQ_CHEB_N;  // nodes per dimension (degree kChebN - 1), 
 constexpr int kChebNR = IMQ_CHEB_NR;
 // Rings whose parent boxes have t >= 2.5 h use fewer nodes (variant 1).
 #ifndef IMQ_CHEB_NR2
-#define IMQ_CHEB_NR2 18
+#define IMQ_CHEB_NR2 16
 #endif
 constexpr int kChebNR2 = IMQ_CHEB_NR2;
 constexpr int kRingNr[2] = {kChebNR, kChebNR2};
