@@ -51,6 +51,9 @@ constexpr int NX = kChebNX;
 constexpr int NXX = NX * NX;
 static_assert(NX <= NC, "the X-ring series is added into the level-(L-1) series");
 __device__ double c_TX[NXX];         // cos(k theta_i), theta_i = pi (i + 1/2) / NX
+constexpr int NI = kChebNI;          // own inner lists of the levels with t >= 2.5 h
+static_assert(NI <= NC, "the inner-list series is added into the level series");
+__device__ double c_TI[NI * NI];
 
 __global__ void k_cheb_nodes(const TreeParams P, int l, long long box_base, double* __restrict__ nx,
                              double* __restrict__ ny) {
@@ -82,52 +85,60 @@ __global__ void k_cheb_nodes_ring(const TreeParams P, int l, int v, long long no
   ny[node_base + t] = block_center(P.oy, bj, P.cell[l]) + h * c_TR[v][nr + j];
 }
 
-// X-ring nodes: NX x NX Chebyshev nodes of every box of level l, [box][i * NX + j].
-__global__ void k_cheb_nodes_x(const TreeParams P, int l, double* __restrict__ nx,
-                               double* __restrict__ ny) {
+// N x N Chebyshev nodes of every box of level l, [box][i * N + j], written
+// from node index node_base (W = 0: X-ring nodes, NX; W = 1: inner-list
+// nodes, NI).
+template <int W>
+__global__ void k_cheb_nodes_n(const TreeParams P, int l, long long node_base,
+                               double* __restrict__ nx, double* __restrict__ ny) {
+  constexpr int N = W ? NI : NX, NNn = N * N;
+  const double* T = W ? c_TI : c_TX;
   const long long nb = 1ll << (2 * (l + 1));
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= nb * NXX) return;
-  const uint32_t q = (uint32_t)(t / NXX);
-  const int r = (int)(t % NXX), i = r / NX, j = r % NX;
+  if (t >= nb * NNn) return;
+  const uint32_t q = (uint32_t)(t / NNn);
+  const int r = (int)(t % NNn), i = r / N, j = r % N;
   int bi, bj;
   demorton(q, bi, bj);
   const double h = 0.5 * P.cell[l];
-  nx[t] = block_center(P.ox, bi, P.cell[l]) + h * c_TX[NX + i];
-  ny[t] = block_center(P.oy, bj, P.cell[l]) + h * c_TX[NX + j];
+  nx[node_base + t] = block_center(P.ox, bi, P.cell[l]) + h * T[N + i];
+  ny[node_base + t] = block_center(P.oy, bj, P.cell[l]) + h * T[N + j];
 }
 
-// Warp-per-box DCT of the X-ring node values, added into the box's level-(L-1)
-// series: coef[X][k][m] += (2/NX)^2 w_k w_m sum_{i,j} T_k(x_i) T_m(y_j) V[i][j].
+// Warp-per-box DCT of N x N node values, added into the box's degree-(NC-1)
+// series: coef[X][k][m] += (2/N)^2 w_k w_m sum_{i,j} T_k(x_i) T_m(y_j) V[i][j]
+// (W = 0: the X-ring, N = NX; W = 1: a level's own inner lists, N = NI).
 constexpr int kXcWarps = 4;
-__global__ void __launch_bounds__(kXcWarps * 32) k_cheb_xring_coef(const int* __restrict__ boxes,
-                                                                  int n_boxes,
-                                                                  const double* __restrict__ vals,
-                                                                  double* __restrict__ coef) {
-  __shared__ double T[NXX];
-  __shared__ double V[kXcWarps][NXX], Bm[kXcWarps][NXX];
-  for (int o = threadIdx.x; o < NXX; o += kXcWarps * 32) T[o] = c_TX[o];
+template <int W>
+__global__ void __launch_bounds__(kXcWarps * 32) k_cheb_dct_add(const int* __restrict__ boxes,
+                                                               int n_boxes,
+                                                               const double* __restrict__ vals,
+                                                               double* __restrict__ coef) {
+  constexpr int N = W ? NI : NX, NNn = N * N;
+  __shared__ double T[NNn];
+  __shared__ double V[kXcWarps][NNn], Bm[kXcWarps][NNn];
+  for (int o = threadIdx.x; o < NNn; o += kXcWarps * 32) T[o] = W ? c_TI[o] : c_TX[o];
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int bx = blockIdx.x * kXcWarps + warp;
   if (bx >= n_boxes) return;
   const uint32_t x = (uint32_t)boxes[bx];
-  const double* v = vals + (size_t)x * NXX;
-  for (int o = lane; o < NXX; o += 32) V[warp][o] = v[o];
+  const double* v = vals + (size_t)x * NNn;
+  for (int o = lane; o < NNn; o += 32) V[warp][o] = v[o];
   __syncwarp();
-  for (int o = lane; o < NXX; o += 32) {  // Bm[i][m] = sum_j V[i][j] T[m][j]
-    const int i = o / NX, m = o % NX;
+  for (int o = lane; o < NNn; o += 32) {  // Bm[i][m] = sum_j V[i][j] T[m][j]
+    const int i = o / N, m = o % N;
     double s = 0.0;
-    for (int j = 0; j < NX; ++j) s = fma(V[warp][i * NX + j], T[m * NX + j], s);
+    for (int j = 0; j < N; ++j) s = fma(V[warp][i * N + j], T[m * N + j], s);
     Bm[warp][o] = s;
   }
   __syncwarp();
   double* c = coef + (size_t)x * NN;
-  for (int o = lane; o < NXX; o += 32) {
-    const int k = o / NX, m = o % NX;
+  for (int o = lane; o < NNn; o += 32) {
+    const int k = o / N, m = o % N;
     double s = 0.0;
-    for (int i = 0; i < NX; ++i) s = fma(T[k * NX + i], Bm[warp][i * NX + m], s);
-    s *= (2.0 / NX) * (2.0 / NX) * (k == 0 ? 0.5 : 1.0) * (m == 0 ? 0.5 : 1.0);
+    for (int i = 0; i < N; ++i) s = fma(T[k * N + i], Bm[warp][i * N + m], s);
+    s *= (2.0 / N) * (2.0 / N) * (k == 0 ? 0.5 : 1.0) * (m == 0 ? 0.5 : 1.0);
     c[k * NC + m] += s;
   }
 }
@@ -499,13 +510,30 @@ void cheb_set_x_tables(const double* T_nx) {
 
 void launch_cheb_nodes_x(const TreeParams& P, int l, double* nx, double* ny, cudaStream_t s) {
   const long long n = (1ll << (2 * (l + 1))) * NXX;
-  k_cheb_nodes_x<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(P, l, nx, ny);
+  k_cheb_nodes_n<0><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(P, l, 0, nx, ny);
 }
 
 void launch_cheb_xring_coef(const int* boxes, int n_boxes, const double* vals, double* coef,
                             cudaStream_t s) {
   if (n_boxes)
-    k_cheb_xring_coef<<<(unsigned)((n_boxes + kXcWarps - 1) / kXcWarps), kXcWarps * 32, 0, s>>>(
+    k_cheb_dct_add<0><<<(unsigned)((n_boxes + kXcWarps - 1) / kXcWarps), kXcWarps * 32, 0, s>>>(
+        boxes, n_boxes, vals, coef);
+}
+
+void cheb_set_inner_tables(const double* T_ni) {
+  cudaMemcpyToSymbol(c_TI, T_ni, (size_t)NI * NI * sizeof(double));
+}
+
+void launch_cheb_nodes_inner(const TreeParams& P, int l, long long node_base, double* nx,
+                             double* ny, cudaStream_t s) {
+  const long long n = (1ll << (2 * (l + 1))) * NI * NI;
+  k_cheb_nodes_n<1><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(P, l, node_base, nx, ny);
+}
+
+void launch_cheb_inner_coef(const int* boxes, int n_boxes, const double* vals, double* coef,
+                            cudaStream_t s) {
+  if (n_boxes)
+    k_cheb_dct_add<1><<<(unsigned)((n_boxes + kXcWarps - 1) / kXcWarps), kXcWarps * 32, 0, s>>>(
         boxes, n_boxes, vals, coef);
 }
 

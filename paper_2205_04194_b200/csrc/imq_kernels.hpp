@@ -118,6 +118,19 @@ constexpr int kRingNr[2] = {kChebNR, kChebNR2};
 #define IMQ_CHEB_NX 12
 #endif
 constexpr int kChebNX = IMQ_CHEB_NX;
+// The own inner lists of the coarse levels with t >= 2.5 h (rings on) through
+// NI x NI nodes, their series added into the level's degree-(NC-1) series.
+#ifndef IMQ_CHEB_NI
+#define IMQ_CHEB_NI 14
+#endif
+constexpr int kChebNI = IMQ_CHEB_NI;
+void cheb_set_inner_tables(const double* T_ni);
+void launch_cheb_nodes_inner(const TreeParams& P, int l, long long node_base, double* nx,
+                             double* ny, cudaStream_t s);
+// coef[X] (NC x NC) += the NI x NI Chebyshev coefficients of the node values
+// of each listed box (values at vals + box * NI^2).
+void launch_cheb_inner_coef(const int* boxes, int n_boxes, const double* vals, double* coef,
+                            cudaStream_t s);
 void cheb_set_x_tables(const double* T_nx);
 void launch_cheb_nodes_x(const TreeParams& P, int l, double* nx, double* ny, cudaStream_t s);
 // coef[X] (NC x NC, x-degree major) += the NX x NX Chebyshev coefficients of

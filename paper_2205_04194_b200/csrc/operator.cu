@@ -602,21 +602,35 @@ void DeviceOperator::build_cheb(int p_lo, int p_hi) {
     for (int l = L_ - 1; l >= 2 && P_.t >= tau * 0.5 * P_.cell[l - 1]; --l) ring_l0_ = l;
     if (ring_l0_ > L_ - 1) ring_ = false;
   }
-  // node geometry (all boxes of levels 1..lc), tables
+  // node geometry (all boxes of levels 1..lc), tables.  The levels whose own
+  // inner lists (rings on) sit where t >= 2.5 h use NI x NI nodes (a suffix
+  // of the levels: h shrinks with the level).
   cheb_base_.assign((size_t)lc + 1, 0);
+  inner_v_.assign((size_t)lc + 1, 0);
+  cnode_base_.assign((size_t)lc + 2, 0);
   long long nb = 0;
-  for (int l = 1; l <= lc; ++l) {
-    cheb_base_[(size_t)l] = nb;
-    nb += 1ll << (2 * (l + 1));
+  {
+    const char* e = getenv("IMQ_INNER_TAU");
+    const double taui = e ? atof(e) : 2.5;
+    for (int l = 1; l <= lc; ++l) {
+      cheb_base_[(size_t)l] = nb;
+      nb += 1ll << (2 * (l + 1));
+      inner_v_[(size_t)l] = ring_ && l >= std::max(2, ring_l0_) && !getenv("IMQ_FAR_NOINNER") &&
+                            P_.t >= taui * 0.5 * P_.cell[l];
+      const long long npl = inner_v_[(size_t)l] ? (long long)imqk::kChebNI * imqk::kChebNI : NN;
+      cnode_base_[(size_t)l + 1] = cnode_base_[(size_t)l] + (1ll << (2 * (l + 1))) * npl;
+    }
   }
-  if (cheb_nodes_ != (size_t)nb * NN) {
+  const size_t want_nodes = (size_t)cnode_base_[(size_t)lc + 1];
+  if (cheb_nodes_ != want_nodes || cheb_coefs_ != (size_t)nb * NN) {
     dfree(d_cnx_); dfree(d_cny_); dfree(d_cnleaf_); dfree(d_cval_); dfree(d_ccoef_);
-    cheb_nodes_ = (size_t)nb * NN;
+    cheb_nodes_ = want_nodes;
+    cheb_coefs_ = (size_t)nb * NN;
     d_cnx_ = dalloc<double>(cheb_nodes_, "cheb nodes");
     d_cny_ = dalloc<double>(cheb_nodes_, "cheb nodes");
     d_cnleaf_ = dalloc<uint32_t>(cheb_nodes_, "cheb node keys");
     d_cval_ = dalloc<double>(cheb_nodes_, "cheb values");
-    d_ccoef_ = dalloc<double>(cheb_nodes_, "cheb coefficients");
+    d_ccoef_ = dalloc<double>(cheb_coefs_, "cheb coefficients");
     cuda_check(cudaMemset(d_cnleaf_, 0, cheb_nodes_ * sizeof(uint32_t)), "cheb keys");
     std::vector<double> T(NN), SL(NN), SR(NN);
     const long double pi = 3.141592653589793238462643383279502884L;
@@ -635,8 +649,19 @@ void DeviceOperator::build_cheb(int p_lo, int p_hi) {
         SR[(size_t)kp * NC + k] = (double)(f * sr);
       }
     imqk::cheb_set_tables(T.data(), SL.data(), SR.data());
-    for (int l = 1; l <= lc; ++l)
-      imqk::launch_cheb_nodes(P_, l, cheb_base_[(size_t)l], d_cnx_, d_cny_, stream_);
+    {
+      constexpr int NI = imqk::kChebNI;
+      std::vector<double> TI((size_t)NI * NI);
+      for (int k = 0; k < NI; ++k)
+        for (int i = 0; i < NI; ++i) TI[(size_t)k * NI + i] = (double)cosl(k * pi * (i + 0.5L) / NI);
+      imqk::cheb_set_inner_tables(TI.data());
+    }
+    for (int l = 1; l <= lc; ++l) {
+      if (inner_v_[(size_t)l])
+        imqk::launch_cheb_nodes_inner(P_, l, cnode_base_[(size_t)l], d_cnx_, d_cny_, stream_);
+      else  // (the NC-node levels come first: their offsets are cheb_base_ * NN)
+        imqk::launch_cheb_nodes(P_, l, cheb_base_[(size_t)l], d_cnx_, d_cny_, stream_);
+    }
     cuda_check(cudaStreamSynchronize(stream_), "cheb nodes");
   }
   Pn_ = P_;
@@ -724,8 +749,12 @@ void DeviceOperator::build_cheb(int p_lo, int p_hi) {
       if (!own(l, q)) continue;
       boxes.push_back((int)q);
       // own list of q at level l (without the ring of its parent when rings are on)
-      chunks(g, (int)(q << (2 * (L_ - 1 - l))), (cheb_base_[(size_t)l] + q) * NN, NN,
-             l | ((ring_ && l >= ring_l0_ ? 1 : 0) << 8));
+      {
+        const long long npl =
+            inner_v_[(size_t)l] ? (long long)imqk::kChebNI * imqk::kChebNI : (long long)NN;
+        chunks(g, (int)(q << (2 * (L_ - 1 - l))), cnode_base_[(size_t)l] + q * npl, (int)npl,
+               l | ((ring_ && l >= ring_l0_ ? 1 : 0) << 8));
+      }
       // the level-(l+1) ring of q at q's ring nodes
       if (ring_ && l + 1 >= ring_l0_)
         chunks(rg, (int)((4 * q) << (2 * (L_ - 2 - l))),
@@ -1220,7 +1249,11 @@ void DeviceOperator::far_near(const double* d_us, double* d_out, const int* perm
           imqk::launch_cheb_ring_coef(ring_v_[(size_t)l - 1], pbx, npb, cheb_base_[(size_t)l - 1],
                                       d_ccoef_, d_rval_ + ring_nbase_[(size_t)l - 1],
                                       d_ccoef_ + cheb_base_[(size_t)l] * NN, s);
-          imqk::launch_cheb_coef(l, bx, nbx, cheb_base_[(size_t)l], -1, d_cval_, d_ccoef_, s);
+          if (inner_v_[(size_t)l])  // own inner lists at NI x NI nodes, added
+            imqk::launch_cheb_inner_coef(bx, nbx, d_cval_ + cnode_base_[(size_t)l],
+                                         d_ccoef_ + cheb_base_[(size_t)l] * NN, s);
+          else
+            imqk::launch_cheb_coef(l, bx, nbx, cheb_base_[(size_t)l], -1, d_cval_, d_ccoef_, s);
         } else {
           imqk::launch_cheb_coef(l, bx, nbx, cheb_base_[(size_t)l],
                                  l > 1 ? cheb_base_[(size_t)l - 1] : 0, d_cval_, d_ccoef_, s);
@@ -1506,9 +1539,12 @@ void DeviceOperator::fill_eval_counts() {
   constexpr double NN = imqk::kChebN * imqk::kChebN, NRR = imqk::kChebNR * imqk::kChebNR;
   double direct = 0, nodes = 0;
   for (int l = 1; l <= L_ && l < (int)far_by_level_.size(); ++l) {
-    if (l <= lc)
+    if (l <= lc) {
+      const double npl = (size_t)l < inner_v_.size() && inner_v_[(size_t)l]
+                             ? (double)imqk::kChebNI * imqk::kChebNI : NN;
       nodes += (lists_by_level_[(size_t)l] -
-                (rings && l >= ring_l0_ ? ring_child_by_level_[(size_t)l] : 0.0)) * NN;
+                (rings && l >= ring_l0_ ? ring_child_by_level_[(size_t)l] : 0.0)) * npl;
+    }
     else
       direct += far_by_level_[(size_t)l];
     if (rings && l >= ring_l0_ && l < L_ && (size_t)l - 1 < ring_v_.size()) {

@@ -224,6 +224,9 @@ class DeviceOperator {
   bool ring_ = false;
   int ring_l0_ = 0;  // rings of levels ring_l0_..L-1
   std::vector<int> ring_v_;            // ring variant per parent level (kRingNr)
+  std::vector<int> inner_v_;           // level's own inner list at NI x NI nodes
+  std::vector<long long> cnode_base_;  // first Chebyshev node of each level
+  size_t cheb_coefs_ = 0;
   std::vector<long long> ring_nbase_;  // first ring node of each parent level
   // the level-L outer ring through NX x NX nodes of the level-(L-1) boxes
   bool xring_ = false;
