@@ -121,7 +121,7 @@ constexpr int kChebNX = IMQ_CHEB_NX;
 // The own inner lists of the coarse levels with t >= 2.5 h (rings on) through
 // NI x NI nodes, their series added into the level's degree-(NC-1) series.
 #ifndef IMQ_CHEB_NI
-#define IMQ_CHEB_NI 14
+#define IMQ_CHEB_NI 16
 #endif
 constexpr int kChebNI = IMQ_CHEB_NI;
 void cheb_set_inner_tables(const double* T_ni);
