@@ -132,6 +132,34 @@ IMQ_API int imq_ext_operator_apply_device(const imq_operator* op, const double* 
 /* Same on vectors already permuted into the operator's Morton order. */
 IMQ_API int imq_ext_operator_apply_sorted_device(const imq_operator* op, const double* d_us,
                                          double* d_bs, void* stream);
+/* Build-time options.  They can only DISABLE an approximation of the default
+ * operator or make an interpolation gate STRICTER (a tau below the default is
+ * raised to it): no option moves a product further from the reference than
+ * the defaults allow.  The library reads no environment variables. */
+#define IMQ_OPT_NO_CHEB 0x1u       /* every far pair evaluated at its target */
+#define IMQ_OPT_NO_RING 0x2u       /* no ring interpolation */
+#define IMQ_OPT_NO_INNER 0x4u      /* coarse inner lists at the full node count */
+#define IMQ_OPT_NO_XRING 0x8u      /* level-L outer rings evaluated at the targets */
+#define IMQ_OPT_NO_LSPLIT 0x10u    /* no per-leaf partial pass */
+#define IMQ_OPT_NO_SPLIT 0x20u     /* one far pass (implies IMQ_OPT_NO_CHEB) */
+#define IMQ_OPT_NEAR_NO_SYM 0x40u  /* per-target near field */
+#define IMQ_OPT_NEAR_NO_PAIR 0x80u /* no chunk-pair near field */
+#define IMQ_OPT_CERT_REPORT 0x100u /* diagnostics: the certificate is estimated but never
+                                      acted on (the swept gates alone, as without it) */
+typedef struct {
+  unsigned flags;        /* IMQ_OPT_* */
+  double ring_tau;       /* gate t/h of the rings (default 1.25; stricter only) */
+  double ring2_tau;      /* rings at fewer nodes (default 2.5) */
+  double inner_tau;      /* inner lists at fewer nodes (default 2.5) */
+  double xring_tau;      /* X-ring gate t/h_X (default 5) */
+  int far_rmax;          /* scheduling only: far targets per lane (0 = auto) */
+  int far_streams;       /* scheduling only: far streams 1..4 (0 = auto) */
+  double cert_budget;    /* certificate budget (default 2e-12; smaller only) */
+} imq_ext_options;
+/* imq_operator_create with options (NULL = the defaults). */
+IMQ_API int imq_ext_operator_create_opts(const double* xy, size_t n, double t, int m, int levels,
+                                         const imq_ext_options* opts, imq_operator** out);
+
 /* Waits for all work queued on the operator's stream. */
 IMQ_API int imq_ext_operator_synchronize(const imq_operator* op);
 /* perm_out[p] = original index of the p-th point in Morton order (length n). */
@@ -153,6 +181,14 @@ typedef struct {
   int cheb_ring;           /* 1: the level-(L-1) ring also goes through the level-(L-2) nodes */
   int kernel_launches;     /* this library's kernel launches per imq_ext_operator_apply_device */
   int cheb_xring;          /* 1: the level-L outer rings go through the level-(L-1) nodes */
+  /* build-time interpolation certificate (DESIGN.md §3 "Safety"): estimated
+   * relative deviation of a product from the all-direct evaluation, the budget
+   * it was held to (0: no interpolation / not run), max|b| of the probe,
+   * the estimate per kind (node levels, inner lists, rings, rings at fewer
+   * nodes, X-ring), interpolations switched off to meet it, probe products */
+  double cert_estimate, cert_budget, cert_scale;
+  double cert_by_kind[5];
+  int cert_fallbacks, cert_rounds;
 } imq_ext_stats;
 IMQ_API int imq_ext_operator_stats(const imq_operator* op, imq_ext_stats* out);
 

@@ -164,12 +164,25 @@ class FastOperator:
     """Device-resident fast IMQ operator (reference fastmv.hpp:19-38).
 
     ``levels <= 0`` selects auto_level(N, M) exactly like the reference.
+    ``options`` (imq_ext_create_opts) may only disable approximations or make
+    their gates stricter: ``flags`` is a list of names from ``capi.OPT``
+    (e.g. ``["no_ring"]``), plus ``ring_tau`` / ``ring2_tau`` / ``inner_tau``
+    / ``xring_tau`` and the scheduling-only ``far_rmax`` / ``far_streams``.
     """
 
-    def __init__(self, xy, t: float, m: int, levels: int = 0):
+    def __init__(self, xy, t: float, m: int, levels: int = 0, **options):
         xy = _f64(xy)
         h = C.c_void_p()
-        check(lib().imq_operator_create(_ptr(xy), xy.size // 2, t, m, levels, C.byref(h)))
+        if options:
+            o = capi.imq_ext_options()
+            for name in options.pop("flags", ()):
+                o.flags |= capi.OPT[name]
+            for k, v in options.items():
+                setattr(o, k, v)
+            check(lib().imq_ext_operator_create_opts(_ptr(xy), xy.size // 2, t, m, levels,
+                                                     C.byref(o), C.byref(h)))
+        else:
+            check(lib().imq_operator_create(_ptr(xy), xy.size // 2, t, m, levels, C.byref(h)))
         self._h = h
         self.t = t
         self.m = m
@@ -249,7 +262,9 @@ class FastOperator:
     def stats(self) -> dict:
         s = capi.imq_ext_stats()
         check(lib().imq_ext_operator_stats(self._h, C.byref(s)))
-        return {k: getattr(s, k) for k, _ in s._fields_}
+        out = {k: getattr(s, k) for k, _ in s._fields_}
+        out["cert_by_kind"] = list(out["cert_by_kind"])
+        return out
 
     def solve(self, f, tol: float = 1e-8, max_iter: int = 500, restart: int = 100) -> SolveReport:
         """imq_iterative_solve (solver.cpp:41-159) with the cycle residual history."""

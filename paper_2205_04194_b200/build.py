@@ -66,7 +66,7 @@ def build(force: bool = False, jobs: int | None = None, verbose: bool = False) -
         objs = list(ex.map(lambda s: compile_one(s, force, verbose), srcs))
     if force or _newer(LIB, objs):
         cmd = [NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", LIB] + objs + [
-            "-lcublas", "-lpthread", "-Xlinker", "-rpath,/usr/local/cuda/lib64"]
+            "-lpthread", "-Xlinker", "-rpath,/usr/local/cuda/lib64"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)

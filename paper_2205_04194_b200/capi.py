@@ -43,8 +43,20 @@ class imq_ext_stats(C.Structure):
                 ("far_items", C.c_longlong), ("near_items", C.c_longlong),
                 ("near_mode", C.c_int), ("far_pairs_direct", C.c_double),
                 ("cheb_node_pairs", C.c_double), ("cheb_levels", C.c_int), ("cheb_ring", C.c_int),
-                ("kernel_launches", C.c_int), ("cheb_xring", C.c_int)]
+                ("kernel_launches", C.c_int), ("cheb_xring", C.c_int),
+                ("cert_estimate", C.c_double), ("cert_budget", C.c_double),
+                ("cert_scale", C.c_double), ("cert_by_kind", C.c_double * 5),
+                ("cert_fallbacks", C.c_int), ("cert_rounds", C.c_int)]
 
+
+class imq_ext_options(C.Structure):
+    _fields_ = [("flags", C.c_uint), ("ring_tau", C.c_double), ("ring2_tau", C.c_double),
+                ("inner_tau", C.c_double), ("xring_tau", C.c_double), ("far_rmax", C.c_int),
+                ("far_streams", C.c_int), ("cert_budget", C.c_double)]
+
+
+OPT = dict(no_cheb=0x1, no_ring=0x2, no_inner=0x4, no_xring=0x8, no_lsplit=0x10, no_split=0x20,
+           near_no_sym=0x40, near_no_pair=0x80, cert_report=0x100)
 
 VERIFY_CB = C.CFUNCTYPE(None, C.c_char_p, C.c_int, C.c_double, C.c_void_p)
 
@@ -74,6 +86,8 @@ _SIGS = {
     "imq_free": (None, [_vp]),
     "imq_set_threads": (C.c_int, [C.c_int]),
     "imq_verify": (C.c_int, [C.POINTER(imq_verify_config), VERIFY_CB, _vp]),
+    "imq_ext_operator_create_opts": (C.c_int, [_dp, C.c_size_t, C.c_double, C.c_int, C.c_int,
+                                               C.POINTER(imq_ext_options), C.POINTER(_vp)]),
     "imq_ext_operator_apply_device": (C.c_int, [_vp, _vp, _vp, _vp]),
     "imq_ext_operator_apply_sorted_device": (C.c_int, [_vp, _vp, _vp, _vp]),
     "imq_ext_operator_synchronize": (C.c_int, [_vp]),

@@ -282,6 +282,22 @@ double measure_dfma_peak(int iters, float* ms_out) {
   return flops / (ms * 1e-3) / 1e12;
 }
 
+// SplitMix64 counter form of random_vector (reference.cpp:94-108): the i-th
+// output uses state seed + (i + 1) * gamma.
+__global__ void k_random_vector(double* __restrict__ out, long long n, unsigned long long seed) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    unsigned long long z = seed + (unsigned long long)(i + 1) * 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    out[i] = 2.0 * ((double)(z >> 11) * 0x1.0p-53) - 1.0;
+  }
+}
+void launch_random_vector(double* out, long long n, unsigned long long seed, cudaStream_t s) {
+  k_random_vector<<<grid_for(n), kThreads, 0, s>>>(out, n, seed);
+}
+
 int mgs_grid(long long n) {
   static int max_blocks = 0;
   if (!max_blocks) {
@@ -291,8 +307,7 @@ int mgs_grid(long long n) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mgs, kMgsThreads, 0);
     max_blocks = sms * (per_sm > 2 ? 2 : per_sm);
   }
-  long long per = 4;
-  if (const char* e = getenv("IMQ_MGS_PER")) per = atoi(e);  // elements per thread (tuning)
+  constexpr long long per = 4;  // elements per thread
   const long long want = (n + kMgsThreads * per - 1) / (kMgsThreads * per);
   return (int)(want < 1 ? 1 : (want > max_blocks ? max_blocks : want));
 }
@@ -301,7 +316,7 @@ cudaError_t launch_mgs(const double* V, double* w, long long n, long long ld, in
                        double* partial, int nparts, double* h, int* flag, double* vnext,
                        cudaStream_t s) {
   constexpr long long T = kClusterCtas * 1024;
-  if (!getenv("IMQ_MGS_COOP") && n <= 16 * T) {
+  if (n <= 16 * T) {
     const int ni = (int)n;
     const dim3 g(kClusterCtas), b(1024);
     if (n <= T) k_mgs_cluster<1><<<g, b, 0, s>>>(V, w, ni, ld, j, h, flag, vnext);

@@ -154,6 +154,34 @@ int imq_operator_create(const double* xy, size_t n, double t, int m, int levels,
   });
 }
 
+int imq_ext_operator_create_opts(const double* xy, size_t n, double t, int m, int levels,
+                                 const imq_ext_options* opts, imq_operator** out) {
+  if (!xy || !out || n == 0)
+    return fail(IMQ_ERR_INVALID_ARG, "imq_ext_operator_create_opts: null argument or empty point set");
+  *out = nullptr;
+  imqh::OperatorOptions o;
+  if (opts) {
+    if (!(opts->ring_tau >= 0) || !(opts->ring2_tau >= 0) || !(opts->inner_tau >= 0) ||
+        !(opts->xring_tau >= 0) || !(opts->cert_budget >= 0) || opts->far_rmax < 0 ||
+        opts->far_streams < 0)
+      return fail(IMQ_ERR_INVALID_ARG, "imq_ext_operator_create_opts: negative or NaN option");
+    o.flags = opts->flags;
+    o.ring_tau = opts->ring_tau;
+    o.ring2_tau = opts->ring2_tau;
+    o.inner_tau = opts->inner_tau;
+    o.xring_tau = opts->xring_tau;
+    o.far_rmax = opts->far_rmax;
+    o.far_streams = opts->far_streams;
+    o.cert_budget = opts->cert_budget;
+  }
+  return guard([&] {
+    auto holder = std::make_unique<imq_operator>();
+    holder->op = std::make_unique<imqh::DeviceOperator>(xy, n, t, m, levels, o);
+    *out = holder.release();
+    return IMQ_OK;
+  });
+}
+
 void imq_operator_destroy(imq_operator* op) { delete op; }
 
 int imq_operator_size(const imq_operator* op, size_t* out) {
@@ -517,6 +545,13 @@ int imq_ext_operator_stats(const imq_operator* op, imq_ext_stats* out) {
     out->cheb_ring = c.cheb_ring;
     out->kernel_launches = c.kernel_launches;
     out->cheb_xring = c.cheb_xring;
+    const imqh::CertReport& r = op->op->certificate();
+    out->cert_estimate = r.estimate;
+    out->cert_budget = r.budget;
+    out->cert_scale = r.scale;
+    for (int k = 0; k < 5; ++k) out->cert_by_kind[k] = r.by_kind[k];
+    out->cert_fallbacks = r.fallbacks;
+    out->cert_rounds = r.rounds;
     return IMQ_OK;
   });
 }

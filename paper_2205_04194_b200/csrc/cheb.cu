@@ -26,6 +26,8 @@
 // index and j the y index; x_i = c_x + (cell/2) cos(pi (i + 1/2) / n).
 #include <algorithm>
 #include <cstdlib>
+#include <stdexcept>
+#include <string>
 
 #include "imq_device.cuh"
 #include "imq_kernels.hpp"
@@ -196,71 +198,6 @@ __global__ void __launch_bounds__(NN) k_cheb_coef(int l, const int* __restrict__
   coef[(base_l + q) * NN + r] = c;
 }
 
-// Warp per item {box q at level lc, first sorted target, count <= 32 R}:
-// out[p] = sum_{k,m} C[k][m] T_k(x^) T_m(y^) at each target.
-constexpr int kEvalWarps = 4, kEvalR = 4;
-__global__ void __launch_bounds__(kEvalWarps * 32) k_cheb_eval(const TreeParams P, int lc,
-                                                               const int4* __restrict__ items,
-                                                               int n_items, long long base_lc,
-                                                               const double* __restrict__ coef,
-                                                               double* __restrict__ out) {
-  __shared__ __align__(16) double cs[kEvalWarps][NN];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int it = blockIdx.x * kEvalWarps + warp;
-  if (it >= n_items) return;
-  const int4 item = items[it];
-  const uint32_t q = (uint32_t)item.x;
-  const int s0 = item.y, cnt = item.z;
-  const double* c = coef + (base_lc + q) * NN;
-  for (int r = lane; r < NN; r += 32) cs[warp][r] = c[r];
-  __syncwarp();
-  int bi, bj;
-  demorton(q, bi, bj);
-  const double cx = block_center(P.ox, bi, P.cell[lc]), cy = block_center(P.oy, bj, P.cell[lc]);
-  const double inv = 2.0 / P.cell[lc];
-  double xh[kEvalR], ty[kEvalR][NC], acc[kEvalR];
-#pragma unroll
-  for (int p = 0; p < kEvalR; ++p) {
-    const int idx = lane + 32 * p < cnt ? s0 + lane + 32 * p : s0;
-    xh[p] = (P.xs[idx] - cx) * inv;
-    const double yh = (P.ys[idx] - cy) * inv;
-    ty[p][0] = 1.0;
-    ty[p][1] = yh;
-#pragma unroll
-    for (int m = 2; m < NC; ++m) ty[p][m] = fma(2.0 * yh, ty[p][m - 1], -ty[p][m - 2]);
-    acc[p] = 0.0;
-  }
-  double tx0[kEvalR], tx1[kEvalR];
-#pragma unroll
-  for (int p = 0; p < kEvalR; ++p) {
-    tx0[p] = 1.0;
-    tx1[p] = xh[p];
-  }
-#pragma unroll 2
-  for (int k = 0; k < NC; ++k) {
-    double s[kEvalR];
-#pragma unroll
-    for (int p = 0; p < kEvalR; ++p) s[p] = 0.0;
-#pragma unroll
-    for (int m = 0; m < NC; m += 2) {
-      const double2 cc = *reinterpret_cast<const double2*>(&cs[warp][k * NC + m]);
-#pragma unroll
-      for (int p = 0; p < kEvalR; ++p) s[p] = fma(cc.y, ty[p][m + 1], fma(cc.x, ty[p][m], s[p]));
-    }
-#pragma unroll
-    for (int p = 0; p < kEvalR; ++p) {
-      const double tk = k == 0 ? 1.0 : (k == 1 ? xh[p] : fma(2.0 * xh[p], tx1[p], -tx0[p]));
-      if (k >= 2) {
-        tx0[p] = tx1[p];
-        tx1[p] = tk;
-      }
-      acc[p] = fma(tk, s[p], acc[p]);
-    }
-  }
-#pragma unroll
-  for (int p = 0; p < kEvalR; ++p)
-    if (lane + 32 * p < cnt) out[s0 + lane + 32 * p] = acc[p];
-}
 
 // Same evaluation on the FP64 tensor cores (mma.sync m8n8k4 f64): per group
 // of 8 targets, Z = Ty C^T ([8 x m] x [m x k], m padded to 4 KS, k to 8 NT)
@@ -482,30 +419,116 @@ __global__ void __launch_bounds__(kRcWarps * 32) k_cheb_ring_coef_mma(
   }
 }
 
-}  // namespace
-
-// IMQ_CHEB_EVAL_FMA=1: the CUDA-core evaluation (comparison / development)
-static bool eval_fma() {
-  static const bool v = getenv("IMQ_CHEB_EVAL_FMA") != nullptr;
-  return v;
+// ------------------------------------------------------- certificate ---
+// Build-time interpolation certificate (operator.cu certify()): for every
+// interpolated box, the tensor Chebyshev coefficients c_{k,m} of its n x n
+// node values (n <= 20) are formed, and the error of the interpolant is
+// estimated from their decay (the chebfun-style tail test on the data
+// itself): with B2 = max |c| over the band max(k, m) in {n-2, n-1} and B4 the
+// same over {n-4, n-3}, the per-degree decay is r = sqrt(B2 / B4) (clamped to
+// <= 0.9: no visible convergence), and for |c_j| ~ A r^j the neglected
+// coefficients of both variables, aliased onto the interpolant, sum to about
+//     est = 4 B2 r^2 / (1 - r).
+// Output per listed box: {est, max |value|}.
+constexpr int kTailMaxN = 20;
+__global__ void __launch_bounds__(128) k_cheb_tail(const int* __restrict__ boxes, int n_boxes,
+                                                   const double* __restrict__ vals, int n,
+                                                   double2* __restrict__ out) {
+  __shared__ double V[kTailMaxN * kTailMaxN], T[kTailMaxN * kTailMaxN],
+      W[kTailMaxN * kTailMaxN];
+  __shared__ double red[3][4];
+  const int nn = n * n;
+  for (int o = threadIdx.x; o < nn; o += blockDim.x) {
+    const int k = o / n, i = o % n;  // T[k][i] = cos(pi k (i + 1/2) / n)
+    T[o] = cospi((double)(k * (2 * i + 1)) / (double)(2 * n));
+  }
+  for (int bx = blockIdx.x; bx < n_boxes; bx += gridDim.x) {
+    const int q = boxes[bx];
+    const double* v = vals + (size_t)q * nn;
+    __syncthreads();
+    double vmax = 0.0;
+    for (int o = threadIdx.x; o < nn; o += blockDim.x) {
+      V[o] = v[o];
+      vmax = fmax(vmax, fabs(V[o]));
+    }
+    __syncthreads();
+    for (int o = threadIdx.x; o < nn; o += blockDim.x) {  // W[i][m] = sum_j V[i][j] T[m][j]
+      const int i = o / n, m = o % n;
+      double acc = 0.0;
+      for (int j = 0; j < n; ++j) acc = fma(V[i * n + j], T[m * n + j], acc);
+      W[o] = acc;
+    }
+    __syncthreads();
+    double b2 = 0.0, b4 = 0.0;
+    for (int o = threadIdx.x; o < nn; o += blockDim.x) {
+      const int k = o / n, m = o % n, d = max(k, m);
+      if (d < n - 4) continue;
+      double acc = 0.0;
+      for (int i = 0; i < n; ++i) acc = fma(T[k * n + i], W[i * n + m], acc);
+      acc = fabs(acc * (2.0 / n) * (2.0 / n) * (k == 0 ? 0.5 : 1.0) * (m == 0 ? 0.5 : 1.0));
+      if (d >= n - 2) b2 = fmax(b2, acc); else b4 = fmax(b4, acc);
+    }
+    for (int d = 16; d; d >>= 1) {
+      b2 = fmax(b2, __shfl_xor_sync(0xffffffffu, b2, d));
+      b4 = fmax(b4, __shfl_xor_sync(0xffffffffu, b4, d));
+      vmax = fmax(vmax, __shfl_xor_sync(0xffffffffu, vmax, d));
+    }
+    if ((threadIdx.x & 31) == 0) {
+      red[0][threadIdx.x >> 5] = b2;
+      red[1][threadIdx.x >> 5] = b4;
+      red[2][threadIdx.x >> 5] = vmax;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double a = 0.0, b = 0.0, c = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+        a = fmax(a, red[0][w]);
+        b = fmax(b, red[1][w]);
+        c = fmax(c, red[2][w]);
+      }
+      const double r = b > 0.0 ? fmin(0.9, sqrt(a / b)) : (a > 0.0 ? 0.9 : 0.0);
+      out[bx] = make_double2(4.0 * a * r * r / (1.0 - r), c);
+    }
+  }
 }
 
+__global__ void k_absmax(const double* __restrict__ x, long long n, double* __restrict__ out) {
+  double m = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    m = fmax(m, fabs(x[i]));
+  for (int d = 16; d; d >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, d));
+  // |x| >= 0: the bit patterns of non-negative doubles order like the values
+  if ((threadIdx.x & 31) == 0)
+    atomicMax(reinterpret_cast<unsigned long long*>(out), (unsigned long long)__double_as_longlong(m));
+}
+
+// Constant-table uploads are checked: a failed upload would leave stale
+// interpolation tables behind every later product.
+void sym_check(cudaError_t e) {
+  if (e != cudaSuccess)
+    throw std::runtime_error(std::string("cudaMemcpyToSymbol (Chebyshev tables): ") +
+                             cudaGetErrorString(e));
+}
+
+}  // namespace
+
 void cheb_set_tables(const double* T, const double* S_left, const double* S_right) {
-  cudaMemcpyToSymbol(c_T, T, NN * sizeof(double));
-  cudaMemcpyToSymbol(c_S, S_left, NN * sizeof(double), 0);
-  cudaMemcpyToSymbol(c_S, S_right, NN * sizeof(double), NN * sizeof(double));
+  sym_check(cudaMemcpyToSymbol(c_T, T, NN * sizeof(double)));
+  sym_check(cudaMemcpyToSymbol(c_S, S_left, NN * sizeof(double), 0));
+  sym_check(cudaMemcpyToSymbol(c_S, S_right, NN * sizeof(double), NN * sizeof(double)));
 }
 
 void cheb_set_ring_tables(int v, const double* T_nr, const double* B_left, const double* B_right) {
   const int nr = kRingNr[v];
-  cudaMemcpyToSymbol(c_TR, T_nr, (size_t)nr * nr * sizeof(double), (size_t)v * NRR * sizeof(double));
+  sym_check(cudaMemcpyToSymbol(c_TR, T_nr, (size_t)nr * nr * sizeof(double), (size_t)v * NRR * sizeof(double)));
   const size_t bsz = (size_t)NC * NR * sizeof(double);
-  cudaMemcpyToSymbol(c_B, B_left, (size_t)NC * nr * sizeof(double), ((size_t)v * 2 + 0) * bsz);
-  cudaMemcpyToSymbol(c_B, B_right, (size_t)NC * nr * sizeof(double), ((size_t)v * 2 + 1) * bsz);
+  sym_check(cudaMemcpyToSymbol(c_B, B_left, (size_t)NC * nr * sizeof(double), ((size_t)v * 2 + 0) * bsz));
+  sym_check(cudaMemcpyToSymbol(c_B, B_right, (size_t)NC * nr * sizeof(double), ((size_t)v * 2 + 1) * bsz));
 }
 
 void cheb_set_x_tables(const double* T_nx) {
-  cudaMemcpyToSymbol(c_TX, T_nx, NXX * sizeof(double));
+  sym_check(cudaMemcpyToSymbol(c_TX, T_nx, NXX * sizeof(double)));
 }
 
 void launch_cheb_nodes_x(const TreeParams& P, int l, double* nx, double* ny, cudaStream_t s) {
@@ -521,7 +544,7 @@ void launch_cheb_xring_coef(const int* boxes, int n_boxes, const double* vals, d
 }
 
 void cheb_set_inner_tables(const double* T_ni) {
-  cudaMemcpyToSymbol(c_TI, T_ni, (size_t)NI * NI * sizeof(double));
+  sym_check(cudaMemcpyToSymbol(c_TI, T_ni, (size_t)NI * NI * sizeof(double)));
 }
 
 void launch_cheb_nodes_inner(const TreeParams& P, int l, long long node_base, double* nx,
@@ -570,14 +593,23 @@ void launch_cheb_coef(int l, const int* boxes, int n_boxes, long long base_l,
 
 void launch_cheb_eval(const TreeParams& P, int lc, const int4* items, int n_items,
                       long long base_lc, const double* coef, double* out, cudaStream_t s) {
-  if (n_items && !eval_fma())
+  if (n_items)
     k_cheb_eval_mma<<<(unsigned)((n_items + kMmaWarps - 1) / kMmaWarps), kMmaWarps * 32, 0, s>>>(
-        P, lc, items, n_items, base_lc, coef, out);
-  else if (n_items)
-    k_cheb_eval<<<(unsigned)((n_items + kEvalWarps - 1) / kEvalWarps), kEvalWarps * 32, 0, s>>>(
         P, lc, items, n_items, base_lc, coef, out);
 }
 
-int cheb_eval_points_per_item() { return eval_fma() ? 32 * kEvalR : 1024; }
+int cheb_eval_points_per_item() { return 1024; }
+
+void launch_cheb_tail(const int* boxes, int n_boxes, const double* vals, int n, double2* out,
+                      cudaStream_t s) {
+  if (n < 3 || n > kTailMaxN) throw std::invalid_argument("cheb tail: node count out of range");
+  if (n_boxes)
+    k_cheb_tail<<<(unsigned)std::min(n_boxes, 148 * 16), 128, 0, s>>>(boxes, n_boxes, vals, n, out);
+}
+
+void launch_absmax(const double* x, long long n, double* out, cudaStream_t s) {
+  cudaMemsetAsync(out, 0, sizeof(double), s);
+  k_absmax<<<(unsigned)std::max(1ll, std::min(148ll * 8, (n + 255) / 256)), 256, 0, s>>>(x, n, out);
+}
 
 }  // namespace imqk

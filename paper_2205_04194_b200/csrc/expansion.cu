@@ -21,7 +21,10 @@
 #include <cstdio>
 #include <algorithm>
 #include <cstdlib>
+#include <map>
 #include <mutex>
+#include <stdexcept>
+#include <string>
 #include <set>
 #include <tuple>
 
@@ -56,16 +59,27 @@ __host__ __device__ constexpr int hz_count(int M) {
   return (M + 1) * (M + 2) / 2 - (M + 1) / 2;
 }
 
-// Opt a kernel into > 48 KB of dynamic shared memory, once per (kernel,
-// device, size); the attribute is per device context.
+// Opt a kernel into large dynamic shared memory.  The attribute is per
+// (kernel, device context) and is an upper bound, so it is raised to the
+// largest size requested so far and never lowered (lowering it after a larger
+// launch of another operator made that operator's next launch fail).
 void ensure_smem_attr(const void* kern, size_t bytes) {
   static std::mutex mtx;
-  static std::set<std::tuple<const void*, int, size_t>> done;
+  static std::map<std::pair<const void*, int>, size_t> done;
   int dev = 0;
   cudaGetDevice(&dev);
   std::lock_guard<std::mutex> lk(mtx);
-  if (done.insert({kern, dev, bytes}).second)
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  size_t& cur = done[{kern, dev}];
+  if (bytes > cur) {
+    const cudaError_t e =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      throw std::runtime_error(std::string("cudaFuncSetAttribute (shared memory): ") +
+                               cudaGetErrorString(e));
+    }
+    cur = bytes;
+  }
 }
 
 __device__ __forceinline__ int block_count(const TreeParams& P, int level, uint32_t q) {
@@ -433,6 +447,365 @@ __global__ void k_transform(const TreeParams P, int level, const double2* __rest
         ci = fma(sval[e], v.y, ci);
       }
       dst[o] = make_double2(cr, ci);
+    }
+  }
+}
+
+// ----------------------------------------------------- M2M + transform ---
+// One warp per parent block q at `level` (kM2tWarps parents per CTA), fused:
+//   1. the four children's moments N^c (level + 1, contiguous in mu) are
+//      staged in shared memory;
+//   2. (coef_child) their far-field coefficients C = T N^c are written -- the
+//      transform of level + 1 happens here, while the moments are on chip;
+//   3. the exact binomial translation (reference moments at the parent centre,
+//      fastmv.cpp:79-100 formed from the children instead of the points):
+//        mu'_{a,b} = sum_c sum_{p<=a} C(a,p) d_c^{a-p} Y^c_{p,b},
+//        Y^c_{p,b} = sum_{r<=b} C(b,r) conj(d_c)^{b-r} N^c_{p,r},
+//      (a, b) = (m + i, i), N_{p,r} = mu_{p-r,r} (p >= r) or conj(mu_{r-p,p}).
+//      Separated into the r-sum and the p-sum this is ~1.3k complex MACs per
+//      child at M = 16 instead of the dense [8 Ke x 2 Ke] product's 26k real
+//      FMA per child; the per-level tables V_c[a][p] = C(a,p) d_c^{a-p} and
+//      W_c[b][r] = C(b,r) conj(d_c)^{b-r} (d_c = +-h +- i h, exact child
+//      offsets) live in shared memory;
+//   4. mu' is written (and, with coef_parent, transformed too: level 1).
+// The children are summed in a fixed order (c = 0..3): deterministic.
+constexpr int kM2tWarps = 8;
+constexpr int kM2tMaxAcc = 8;  // Ke <= 256 outputs per warp (M <= 30)
+struct M2tLayout {             // dynamic shared memory layout (bytes)
+  int M, H, Ke, K, nnz, ny, ysz;
+  size_t v, w, tval, tidx, toff, moff, otab, ytab, yoff, warp0, per_warp, total;
+  // with_v = false: the specialised kernel (no V table in shared memory)
+  __host__ __device__ M2tLayout(int M_, int Ke_, int K_, int nnz_, bool with_v = true)
+      : M(M_), Ke(Ke_), K(K_), nnz(nnz_) {
+    H = M / 2;
+    ny = 0;
+    for (int b = 0; b <= H; ++b) ny += M - b + 1;
+    ysz = ny > (H + 1) * (M + 1) ? ny : (H + 1) * (M + 1);
+    size_t o = 0;
+    auto take = [&](size_t bytes) { const size_t r = o; o += (bytes + 15) & ~(size_t)15; return r; };
+    v = take(with_v ? (size_t)4 * (M + 1) * (M + 1) * 16 : 0);
+    w = take((size_t)4 * (H + 1) * (H + 1) * 16);
+    tval = take((size_t)nnz * 8);
+    tidx = take((size_t)nnz * 4);
+    toff = take((size_t)(K + 1) * 4);
+    moff = take((size_t)(M + 1) * 4);
+    otab = take((size_t)Ke * 4);
+    ytab = take((size_t)ny * 4);
+    yoff = take((size_t)(H + 1) * 4);
+    warp0 = o;
+    const int ytot = ysz > 4 * Ke ? ysz : 4 * Ke;  // generic: Y; specialised: partial parents
+    per_warp = ((size_t)(4 * Ke + ytot + Ke) * 16 + 15) & ~(size_t)15;
+    total = warp0 + kM2tWarps * per_warp;
+  }
+};
+
+__global__ void __launch_bounds__(kM2tWarps * 32) k_m2m_tr(
+    const TreeParams P, int level, const int* __restrict__ plist, long long p0, long long np,
+    const double2* __restrict__ mu_in, double2* __restrict__ mu_out,
+    double2* __restrict__ coef_child, double2* __restrict__ coef_parent,
+    const double2* __restrict__ Vg, const double2* __restrict__ Wg, const TransformTable T) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int M = P.M, Ke = P.Ke, K = P.K;
+  const M2tLayout lay(M, Ke, K, T.nnz);
+  const int H = lay.H, ny = lay.ny, M1 = M + 1, H1 = H + 1;
+  double2* V = reinterpret_cast<double2*>(smem + lay.v);
+  double2* W = reinterpret_cast<double2*>(smem + lay.w);
+  double* tval = reinterpret_cast<double*>(smem + lay.tval);
+  int* tidx = reinterpret_cast<int*>(smem + lay.tidx);
+  int* toff = reinterpret_cast<int*>(smem + lay.toff);
+  int* moff = reinterpret_cast<int*>(smem + lay.moff);
+  int* otab = reinterpret_cast<int*>(smem + lay.otab);  // (a << 8) | b
+  int* ytab = reinterpret_cast<int*>(smem + lay.ytab);  // (p << 8) | b
+  int* yoff = reinterpret_cast<int*>(smem + lay.yoff);  // Y index of (0, b)
+  for (int o = threadIdx.x; o < 4 * M1 * M1; o += blockDim.x) V[o] = Vg[o];
+  for (int o = threadIdx.x; o < 4 * H1 * H1; o += blockDim.x) W[o] = Wg[o];
+  for (int o = threadIdx.x; o < T.nnz; o += blockDim.x) {
+    tval[o] = T.val[o];
+    tidx[o] = T.idx[o];
+  }
+  for (int o = threadIdx.x; o <= K; o += blockDim.x) toff[o] = T.off[o];
+  if (threadIdx.x == 0) {
+    int off = 0, o = 0, e = 0;
+    for (int m = 0; m <= M; ++m) {
+      moff[m] = off;
+      for (int i = 0; m + 2 * i <= M; ++i) otab[o++] = ((m + i) << 8) | i;
+      off += (M - m) / 2 + 1;
+    }
+    for (int b = 0; b <= H; ++b) {
+      yoff[b] = e;
+      for (int p = 0; p + b <= M; ++p) ytab[e++] = (p << 8) | b;
+    }
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double2* N = reinterpret_cast<double2*>(smem + lay.warp0 + (size_t)warp * lay.per_warp);
+  double2* Y = N + 4 * Ke;
+  double2* MU = Y + ny;
+  for (long long it = (long long)blockIdx.x * kM2tWarps + warp; it < np;
+       it += (long long)gridDim.x * kM2tWarps) {
+    const uint32_t q = plist ? (uint32_t)plist[it] : (uint32_t)(p0 + it);
+    int have = 0;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) have |= (block_count(P, level + 1, 4 * q + c) > 0 ? 1 : 0) << c;
+    if (!have) continue;  // the parent's moments stay zero
+    __syncwarp();
+    const double2* src = mu_in + (size_t)(4 * q) * Ke;
+    for (int o = lane; o < 4 * Ke; o += 32)
+      N[o] = ((have >> (o / Ke)) & 1) ? src[o] : make_double2(0.0, 0.0);
+    __syncwarp();
+    if (coef_child) {  // transform of the children (level + 1)
+      for (int e = lane; e < 4 * K; e += 32) {
+        const int c = e / K, o = e - c * K;
+        if (!((have >> c) & 1)) continue;
+        double cr = 0.0, ci = 0.0;
+        for (int t = toff[o]; t < toff[o + 1]; ++t) {
+          const double2 x = N[c * Ke + tidx[t]];
+          cr = fma(tval[t], x.x, cr);
+          ci = fma(tval[t], x.y, ci);
+        }
+        coef_child[(size_t)(4 * q) * K + e] = make_double2(cr, ci);
+      }
+    }
+    double ar[kM2tMaxAcc], ai[kM2tMaxAcc];
+#pragma unroll
+    for (int k = 0; k < kM2tMaxAcc; ++k) ar[k] = ai[k] = 0.0;
+    for (int c = 0; c < 4; ++c) {
+      if (!((have >> c) & 1)) continue;
+      const double2* Nc = N + c * Ke;
+      const double2* Wc = W + c * H1 * H1;
+      const double2* Vc = V + c * M1 * M1;
+      for (int e = lane; e < ny; e += 32) {  // Y[p][b] = sum_r W[b][r] N(p, r)
+        const int p = ytab[e] >> 8, b = ytab[e] & 255;
+        double yr = 0.0, yi = 0.0;
+        for (int r = 0; r <= b; ++r) {
+          double2 x;
+          if (p >= r) {
+            x = Nc[moff[p - r] + r];
+          } else {
+            x = Nc[moff[r - p] + p];
+            x.y = -x.y;
+          }
+          const double2 w = Wc[b * H1 + r];
+          yr = fma(w.x, x.x, fma(-w.y, x.y, yr));
+          yi = fma(w.x, x.y, fma(w.y, x.x, yi));
+        }
+        Y[e] = make_double2(yr, yi);
+      }
+      __syncwarp();
+#pragma unroll
+      for (int k = 0; k < kM2tMaxAcc; ++k) {  // mu'[a][b] += sum_p V[a][p] Y[p][b]
+        const int o = lane + 32 * k;
+        if (o >= Ke) break;
+        const int a = otab[o] >> 8, b = otab[o] & 255;
+        const double2* y = Y + yoff[b];
+        double sr = ar[k], si = ai[k];
+        for (int p = 0; p <= a; ++p) {
+          const double2 v = Vc[a * M1 + p], x = y[p];
+          sr = fma(v.x, x.x, fma(-v.y, x.y, sr));
+          si = fma(v.x, x.y, fma(v.y, x.x, si));
+        }
+        ar[k] = sr;
+        ai[k] = si;
+      }
+      __syncwarp();
+    }
+    double2* dst = mu_out + (size_t)q * Ke;
+#pragma unroll
+    for (int k = 0; k < kM2tMaxAcc; ++k) {
+      const int o = lane + 32 * k;
+      if (o >= Ke) break;
+      // m = 0 moments are real by construction (the reference's v_{n,0} = 0)
+      const double2 r = make_double2(ar[k], (otab[o] >> 8) == (otab[o] & 255) ? 0.0 : ai[k]);
+      dst[o] = r;
+      MU[o] = r;
+    }
+    if (coef_parent) {
+      __syncwarp();
+      for (int o = lane; o < K; o += 32) {
+        double cr = 0.0, ci = 0.0;
+        for (int t = toff[o]; t < toff[o + 1]; ++t) {
+          const double2 x = MU[tidx[t]];
+          cr = fma(tval[t], x.x, cr);
+          ci = fma(tval[t], x.y, ci);
+        }
+        coef_parent[(size_t)q * K + o] = make_double2(cr, ci);
+      }
+    }
+  }
+}
+
+// Specialised orders: eight parents per warp, lane = (parent slot, child c),
+// every lane running the same code on its own child (no divergence, nothing
+// looked up per MAC; the generic kernel above is bound by shared-memory
+// bandwidth, ~3 LDS per complex MAC):
+//   transform: C = T N^c, table entries are warp-wide broadcasts;
+//   translation, column by column (b = 0..M/2, compile-time):
+//     Y[p] = sum_{r <= b} W_c[b][r] N(p, r),  p = 0..M-b  (W row in registers)
+//     then the Taylor shift by d_c in registers (Y[p] += d_c Y[p-1], p
+//     descending, repeated): Y[a] = sum_p C(a,p) d_c^{a-p} Y[p], exactly the
+//     p-sum with no binomials or powers of d_c; a = b..M-b are the column's
+//     outputs;
+//   the four children of a parent are summed by two xor-shuffles, bitwise
+//   identical on the four lanes (commutative pairs): deterministic.
+constexpr int kM2sWarps = 2, kM2sSlots = 8;  // parents per warp
+constexpr bool kM2sStage = true;  // stage the children in shared memory (L1-direct: 0.99 vs 0.78 ms at cfg4 level 7)
+template <int M>
+__host__ __device__ constexpr int mu_off_c(int m) {
+  int o = 0;
+  for (int mm = 0; mm < m; ++mm) o += (M - mm) / 2 + 1;
+  return o;
+}
+
+// (one column per call: inlined, the compiler interleaves the columns and
+// runs out of registers)
+template <int M, int B>
+__device__ __noinline__ void m2m_column(const double2* __restrict__ Nc, const double2* __restrict__ Wc,
+                                        double dre, double dim, double2* __restrict__ dst, int c,
+                                        bool write);
+template <int M, int B>
+__device__ __forceinline__ void m2m_columns(const double2* __restrict__ Nc,
+                                            const double2* __restrict__ Wc, double dre,
+                                            double dim, double2* __restrict__ dst, int c,
+                                            bool write) {
+  if constexpr (B <= M / 2) {
+    m2m_column<M, B>(Nc, Wc, dre, dim, dst, c, write);
+    m2m_columns<M, B + 1>(Nc, Wc, dre, dim, dst, c, write);
+  }
+}
+template <int M, int B>
+__device__ __noinline__ void m2m_column(const double2* __restrict__ Nc,
+                                            const double2* __restrict__ Wc, double dre,
+                                            double dim, double2* __restrict__ dst, int c,
+                                            bool write) {
+  {
+    constexpr int A = M - B, H1 = M / 2 + 1;
+    double yr[A + 1], yi[A + 1];
+    {
+      double wr[B + 1], wi[B + 1];
+#pragma unroll
+      for (int r = 0; r <= B; ++r) {
+        const double2 w = Wc[B * H1 + r];
+        wr[r] = w.x;
+        wi[r] = w.y;
+      }
+#pragma unroll
+      for (int p = 0; p <= A; ++p) {
+        double sr = 0.0, si = 0.0;
+#pragma unroll
+        for (int r = 0; r <= B; ++r) {
+          double2 x;
+          if (p >= r) {
+            x = Nc[mu_off_c<M>(p - r) + r];
+          } else {
+            x = Nc[mu_off_c<M>(r - p) + p];
+            x.y = -x.y;
+          }
+          sr = fma(wr[r], x.x, fma(-wi[r], x.y, sr));
+          si = fma(wr[r], x.y, fma(wi[r], x.x, si));
+        }
+        yr[p] = sr;
+        yi[p] = si;
+      }
+    }
+    // Taylor shift: after pass k, y[p] (p >= k) has absorbed d y[p-1]
+#pragma unroll
+    for (int k = 1; k <= A; ++k)
+#pragma unroll
+      for (int p = A; p >= k; --p) {
+        const double tr = fma(dre, yr[p - 1], fma(-dim, yi[p - 1], yr[p]));
+        const double ti = fma(dre, yi[p - 1], fma(dim, yr[p - 1], yi[p]));
+        yr[p] = tr;
+        yi[p] = ti;
+      }
+    // the parent's column: sum over the four child lanes, a fixed pairing
+#pragma unroll
+    for (int a = B; a <= A; ++a) {
+      double vr = yr[a], vi = yi[a];
+      vr += __shfl_xor_sync(0xffffffffu, vr, 1);
+      vi += __shfl_xor_sync(0xffffffffu, vi, 1);
+      vr += __shfl_xor_sync(0xffffffffu, vr, 2);
+      vi += __shfl_xor_sync(0xffffffffu, vi, 2);
+      // m = a - B = 0 moments are real by construction (reference v_{n,0} = 0)
+      if (write && ((a - B) & 3) == c) dst[mu_off_c<M>(a - B) + B] = make_double2(vr, a == B ? 0.0 : vi);
+    }
+  }
+}
+
+template <int M>
+__global__ void __launch_bounds__(kM2sWarps * 32) k_m2m_tr_s(
+    const TreeParams P, int level, const int* __restrict__ plist, long long p0, long long np,
+    const double2* __restrict__ mu_in, double2* __restrict__ mu_out,
+    double2* __restrict__ coef_child, double2* __restrict__ coef_parent,
+    const double2* __restrict__ Vg, const double2* __restrict__ Wg, const TransformTable T) {
+  constexpr int H1 = M / 2 + 1, M1 = M + 1;
+  constexpr int Ke = mu_off_c<M>(M + 1);
+  constexpr int K = hz_count(M);
+  extern __shared__ __align__(16) unsigned char smem[];
+  double2* W = reinterpret_cast<double2*>(smem);                         // [4][H1][H1]
+  double* tval = reinterpret_cast<double*>(W + 4 * H1 * H1);             // [nnz]
+  int* tidx = reinterpret_cast<int*>(tval + T.nnz);                       // [nnz]
+  int* toff = tidx + T.nnz;                                               // [K + 1]
+  double2* Nall = reinterpret_cast<double2*>(
+      smem + ((((size_t)4 * H1 * H1 * 16 + (size_t)T.nnz * 12 + (size_t)(K + 1) * 4) + 15) & ~(size_t)15));
+  for (int o = threadIdx.x; o < 4 * H1 * H1; o += blockDim.x) W[o] = Wg[o];
+  for (int o = threadIdx.x; o < T.nnz; o += blockDim.x) {
+    tval[o] = T.val[o];
+    tidx[o] = T.idx[o];
+  }
+  for (int o = threadIdx.x; o <= K; o += blockDim.x) toff[o] = T.off[o];
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int slot = lane >> 2, c = lane & 3;
+  double2* N = Nall + (size_t)warp * kM2sSlots * 4 * Ke;   // [slot][child][Ke]
+  const double2* Wc = W + c * H1 * H1;
+  const double2 dc = Vg[c * M1 * M1 + 1 * M1 + 0];  // V_c[1][0] = C(1,0) d_c = d_c
+  for (long long base = ((long long)blockIdx.x * kM2sWarps + warp) * kM2sSlots; base < np;
+       base += (long long)gridDim.x * kM2sWarps * kM2sSlots) {
+    const long long it = base + slot;
+    const bool valid = it < np;
+    const uint32_t q = valid ? (plist ? (uint32_t)plist[it] : (uint32_t)(p0 + it)) : 0u;
+    const bool mine = valid && block_count(P, level + 1, 4 * q + c) > 0;
+    const unsigned ballot = __ballot_sync(0xffffffffu, mine);
+    const bool parent = ((ballot >> (slot * 4)) & 0xfu) != 0;
+    __syncwarp();
+    // stage the eight parents' children (each parent's four are contiguous)
+    const double2* Nc = kM2sStage ? N + (size_t)(slot * 4 + c) * Ke : mu_in + (size_t)(4 * q + c) * Ke;
+    for (int e = lane; kM2sStage && e < kM2sSlots * 4 * Ke; e += 32) {
+      const int sl = e / (4 * Ke), r = e - sl * 4 * Ke;
+      const long long ie = base + sl;
+      double2 v = make_double2(0.0, 0.0);
+      if (((ballot >> (sl * 4 + r / Ke)) & 1u) != 0) {
+        const uint32_t qe = plist ? (uint32_t)plist[ie] : (uint32_t)(p0 + ie);
+        v = mu_in[(size_t)(4 * qe) * Ke + r];
+      }
+      N[e] = v;
+    }
+    __syncwarp();
+    if (coef_child && mine) {  // transform of this lane's child (level + 1)
+      double2* cd = coef_child + (size_t)(4 * q + c) * K;
+      for (int o = 0; o < K; ++o) {
+        double cr = 0.0, ci = 0.0;
+        for (int t = toff[o]; t < toff[o + 1]; ++t) {
+          const double2 x = Nc[tidx[t]];
+          cr = fma(tval[t], x.x, cr);
+          ci = fma(tval[t], x.y, ci);
+        }
+        cd[o] = make_double2(cr, ci);
+      }
+    }
+    double2* dst = mu_out + (size_t)q * Ke;
+    m2m_columns<M, 0>(Nc, Wc, dc.x, dc.y, dst, c, parent);
+    if (coef_parent && parent) {  // level 1: the parents' own coefficients
+      __syncwarp();
+      for (int o = c; o < K; o += 4) {
+        double cr = 0.0, ci = 0.0;
+        for (int t = toff[o]; t < toff[o + 1]; ++t) {
+          const double2 x = dst[tidx[t]];
+          cr = fma(tval[t], x.x, cr);
+          ci = fma(tval[t], x.y, ci);
+        }
+        coef_parent[(size_t)q * K + o] = make_double2(cr, ci);
+      }
     }
   }
 }
@@ -1018,6 +1391,50 @@ void launch_m2m(const TreeParams& P, int level, double2* mu, const double* binom
   k_m2m<<<nb, threads, smem, s>>>(P, level, mu, binom);
 }
 
+size_t m2m_tr_smem(int M, int Ke, int K, int nnz) { return M2tLayout(M, Ke, K, nnz).total; }
+static bool m2m_specialised(int M) {
+  switch (M) {
+#define X(m) case m:
+    IMQ_FOR_SPECIALISED_M(X)
+#undef X
+    return true;
+    default:
+      return false;
+  }
+}
+
+void launch_m2m_tr(const TreeParams& P, int level, const int* plist, long long p0, long long np,
+                   const double2* mu_in, double2* mu_out, double2* coef_child,
+                   double2* coef_parent, const double2* V, const double2* W,
+                   const TransformTable& T, cudaStream_t s) {
+  if (np <= 0) return;
+  if (m2m_specialised(P.M)) {
+    const int H1 = P.M / 2 + 1;
+    const size_t ss = ((((size_t)4 * H1 * H1 * 16 + (size_t)T.nnz * 12 + (size_t)(P.K + 1) * 4) + 15) &
+                       ~(size_t)15) + (kM2sStage ? (size_t)kM2sWarps * kM2sSlots * 4 * P.Ke * 16 : 0);
+    const long long per = (long long)kM2sWarps * kM2sSlots;
+    const unsigned grid = (unsigned)std::min<long long>((np + per - 1) / per, 148ll * 32);
+    switch (P.M) {
+#define X(m)                                                                                    \
+  case m:                                                                                       \
+    ensure_smem_attr((const void*)k_m2m_tr_s<m>, ss);                                           \
+    k_m2m_tr_s<m><<<grid, kM2sWarps * 32, ss, s>>>(P, level, plist, p0, np, mu_in, mu_out,      \
+                                                  coef_child, coef_parent, V, W, T);            \
+    return;
+      IMQ_FOR_SPECIALISED_M(X)
+#undef X
+      default:
+        break;
+    }
+  }
+  const size_t smem = M2tLayout(P.M, P.Ke, P.K, T.nnz).total;
+  const long long want = (np + kM2tWarps - 1) / kM2tWarps;
+  const unsigned grid = (unsigned)std::min<long long>(want, 148ll * 16);
+  ensure_smem_attr((const void*)k_m2m_tr, smem);
+  k_m2m_tr<<<grid, kM2tWarps * 32, smem, s>>>(P, level, plist, p0, np, mu_in, mu_out, coef_child,
+                                             coef_parent, V, W, T);
+}
+
 void launch_transform(const TreeParams& P, const double2* mu, double2* coef,
                       const TransformTable& T, cudaStream_t s, int l_lo, int l_hi,
                       const int* block_list, int n_list) {
@@ -1036,33 +1453,6 @@ void launch_transform(const TreeParams& P, const double2* mu, double2* coef,
   }
 }
 
-// rows[i] <- src[idx[i]] (row = `width` doubles); used to pack / unpack the
-// M2M DGEMM operands of a block subset.
-__global__ void k_gather_rows(const double* __restrict__ src, const int* __restrict__ idx,
-                              int n, int width, double* __restrict__ dst) {
-  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= (long long)n * width) return;
-  const int r = (int)(t / width), c = (int)(t % width);
-  dst[t] = src[(size_t)idx[r] * width + c];
-}
-__global__ void k_scatter_rows(const double* __restrict__ src, const int* __restrict__ idx,
-                               int n, int width, double* __restrict__ dst) {
-  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= (long long)n * width) return;
-  const int r = (int)(t / width), c = (int)(t % width);
-  dst[(size_t)idx[r] * width + c] = src[t];
-}
-
-void launch_gather_rows(const double* src, const int* idx, int n, int width, double* dst,
-                        cudaStream_t s) {
-  const long long t = (long long)n * width;
-  if (t) k_gather_rows<<<(unsigned)((t + 255) / 256), 256, 0, s>>>(src, idx, n, width, dst);
-}
-void launch_scatter_rows(const double* src, const int* idx, int n, int width, double* dst,
-                         cudaStream_t s) {
-  const long long t = (long long)n * width;
-  if (t) k_scatter_rows<<<(unsigned)((t + 255) / 256), 256, 0, s>>>(src, idx, n, width, dst);
-}
 
 void launch_m2p_far(const TreeParams& P, const int4* items, const int* group_off, int begin,
                     int end, const double2* coef, double* far_s_ptr, const cudaStream_t* streams,

@@ -273,47 +273,41 @@ std::vector<double> binomials(int M) {
 // mu'_{a,b} = sum_c sum_{p<=a, r<=b} C(a,p) C(b,r) d_c^{a-p} conj(d_c)^{b-r} N^c_{p,r},
 // N_{p,r} = mu_{p-r,r} (p >= r) or conj(mu_{r-p,p}); a = m+i, b = i.  The m = 0
 // outputs are real in exact arithmetic; their imaginary column is left zero.
-std::vector<double> m2m_matrix(int M, double h) {
-  const int Ke = order_Ke(M);
-  const std::vector<double> bn = binomials(M);
-  std::vector<double> T((size_t)8 * Ke * 2 * Ke, 0.0);
-  std::vector<int> moff((size_t)M + 1);
-  for (int m = 0; m <= M; ++m) moff[(size_t)m] = mu_offset(M, m);
+std::vector<double> m2m_tables(int M, double h) {
+  const int M1 = M + 1, H1 = M / 2 + 1;
+  std::vector<double> out((size_t)2 * 4 * (M1 * M1 + H1 * H1), 0.0);
+  std::vector<long double> bn((size_t)M1 * M1, 0.0L);
+  for (int a = 0; a <= M; ++a) {
+    bn[(size_t)a * M1] = 1.0L;
+    for (int p = 1; p <= a; ++p)
+      bn[(size_t)a * M1 + p] = bn[(size_t)(a - 1) * M1 + p - 1] + (p <= a - 1 ? bn[(size_t)(a - 1) * M1 + p] : 0.0L);
+  }
   for (int c = 0; c < 4; ++c) {
-    const double dx = (c >> 1) ? h : -h, dy = (c & 1) ? h : -h;
-    std::vector<double> pr((size_t)M + 1), pi((size_t)M + 1);  // d^k
-    pr[0] = 1.0;
-    pi[0] = 0.0;
+    const long double dx = (c >> 1) ? h : -h, dy = (c & 1) ? h : -h;
+    std::vector<long double> pr((size_t)M1), pi((size_t)M1);  // d^k
+    pr[0] = 1.0L;
+    pi[0] = 0.0L;
     for (int k = 1; k <= M; ++k) {
       pr[(size_t)k] = pr[(size_t)k - 1] * dx - pi[(size_t)k - 1] * dy;
       pi[(size_t)k] = pr[(size_t)k - 1] * dy + pi[(size_t)k - 1] * dx;
     }
-    for (int m = 0; m <= M; ++m)
-      for (int i = 0; m + 2 * i <= M; ++i) {
-        const int o = moff[(size_t)m] + i, a = m + i, b = i;
-        for (int p = 0; p <= a; ++p)
-          for (int r = 0; r <= b; ++r) {
-            // kappa = C(a,p) C(b,r) d^{a-p} conj(d)^{b-r}
-            const double cr1 = pr[(size_t)(a - p)], ci1 = pi[(size_t)(a - p)];
-            const double cr2 = pr[(size_t)(b - r)], ci2 = -pi[(size_t)(b - r)];
-            const double w = bn[(size_t)a * (M + 1) + p] * bn[(size_t)b * (M + 1) + r];
-            const double kr = w * (cr1 * cr2 - ci1 * ci2), ki = w * (cr1 * ci2 + ci1 * cr2);
-            const bool conj = p < r;
-            const int k = conj ? moff[(size_t)(r - p)] + p : moff[(size_t)(p - r)] + r;
-            const size_t jre = ((size_t)c * Ke + k) * 2, jim = jre + 1;
-            const size_t ore = (size_t)o * 2, oim = ore + 1;
-            const size_t ld = (size_t)2 * Ke;
-            T[jre * ld + ore] += kr;
-            T[jim * ld + ore] += conj ? ki : -ki;
-            if (m != 0) {
-              T[jre * ld + oim] += ki;
-              T[jim * ld + oim] += conj ? -kr : kr;
-            }
-          }
+    for (int a = 0; a <= M; ++a)
+      for (int p = 0; p <= a; ++p) {
+        const size_t o = 2 * ((size_t)c * M1 * M1 + (size_t)a * M1 + p);
+        out[o] = (double)(bn[(size_t)a * M1 + p] * pr[(size_t)(a - p)]);
+        out[o + 1] = (double)(bn[(size_t)a * M1 + p] * pi[(size_t)(a - p)]);
+      }
+    const size_t wbase = (size_t)4 * M1 * M1;
+    for (int b = 0; b < H1; ++b)
+      for (int r = 0; r <= b; ++r) {
+        const size_t o = 2 * (wbase + (size_t)c * H1 * H1 + (size_t)b * H1 + r);
+        out[o] = (double)(bn[(size_t)b * M1 + r] * pr[(size_t)(b - r)]);
+        out[o + 1] = (double)(-bn[(size_t)b * M1 + r] * pi[(size_t)(b - r)]);
       }
   }
-  return T;
+  return out;
 }
+
 
 // ----------------------------------------------------------- dense solve --
 std::vector<double> dense_solve(const double* xy, size_t n, double t, const double* f,

@@ -65,10 +65,12 @@ struct Transform {
 };
 Transform build_transform(int M, double t);
 std::vector<double> binomials(int M);  // [(M+1) x (M+1)], C(a, p)
-// Exact M2M translation of the four children's moments to their parent as a
-// real row-major matrix [8 Ke][2 Ke] (input: children 0..3, Ke complex each;
-// output: Ke complex), for child-centre offsets h (+-1 +- i), h = cell_child/2.
-std::vector<double> m2m_matrix(int M, double h);
+// Per-level tables of the fused M2M (k_m2m_tr), interleaved complex:
+// V[c][a][p] = C(a,p) d_c^{a-p} (a, p <= M) followed by
+// W[c][b][r] = C(b,r) conj(d_c)^{b-r} (b, r <= M/2), d_c = (+-h) + i (+-h)
+// child c at x offset (c >> 1 ? +h : -h), y offset (c & 1 ? +h : -h), the
+// Morton child order.  Evaluated in long double.
+std::vector<double> m2m_tables(int M, double h);
 
 // Dense solve: A = [1/sqrt(t^2+|xi-xj|^2)], n <= 5000 (reference.cpp:30-46),
 // partial-pivot LU + one refinement step, residual guard 1e-10 (48-64).

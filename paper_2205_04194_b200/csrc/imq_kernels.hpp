@@ -71,14 +71,23 @@ void launch_p2m_leaf(const TreeParams& P, const double* u_s, double2* mu, const 
                      int n_list, cudaStream_t s);
 void launch_m2m(const TreeParams& P, int level, double2* mu, const double* binom,
                 cudaStream_t s);
+// Fused M2M + transform (k_m2m_tr): parents plist[0..np) (or p0 .. p0+np-1)
+// at `level` from the children's moments mu_in (level + 1, indexed by child
+// block) into mu_out (level, indexed by parent block); coef_child != nullptr:
+// also the children's far coefficients (level + 1), coef_parent: the
+// parents'.  V, W: the level's translation tables ([4][M+1][M+1] and
+// [4][M/2+1][M/2+1] double2, m2m_tables() in host_math).  Needs
+// m2m_tr_smem() <= the opt-in shared-memory limit (M <= 24 at the B200's
+// 227 KB).
+size_t m2m_tr_smem(int M, int Ke, int K, int nnz);
+void launch_m2m_tr(const TreeParams& P, int level, const int* plist, long long p0, long long np,
+                   const double2* mu_in, double2* mu_out, double2* coef_child,
+                   double2* coef_parent, const double2* V, const double2* W,
+                   const TransformTable& T, cudaStream_t s);
 // Levels [l_lo, l_hi] (<= 0: all); block_list restricts one level's blocks.
 void launch_transform(const TreeParams& P, const double2* mu, double2* coef,
                       const TransformTable& T, cudaStream_t s, int l_lo = 0, int l_hi = 0,
                       const int* block_list = nullptr, int n_list = 0);
-void launch_gather_rows(const double* src, const int* idx, int n, int width, double* dst,
-                        cudaStream_t s);
-void launch_scatter_rows(const double* src, const int* idx, int n, int width, double* dst,
-                         cudaStream_t s);
 // Far work items are grouped by points-per-lane R = ceil(count/32):
 // group R occupies [group_off[R-1], group_off[R]) of `items`.  Launches the
 // items with index in [begin, end).  Group launches are spread round-robin
@@ -158,6 +167,14 @@ void launch_cheb_coef(int l, const int* boxes, int n_boxes, long long base_l,
 void launch_cheb_eval(const TreeParams& P, int lc, const int4* items, int n_items,
                       long long base_lc, const double* coef, double* out, cudaStream_t s);
 int cheb_eval_points_per_item();
+// Certificate (operator.cu certify()): per listed box, {largest Chebyshev
+// coefficient of degree >= n-2 in x or y, max |value|} of its n x n node
+// values at vals + box * n^2; max |x_i| into *out (device).
+void launch_cheb_tail(const int* boxes, int n_boxes, const double* vals, int n, double2* out,
+                      cudaStream_t s);
+void launch_absmax(const double* x, long long n, double* out, cudaStream_t s);
+// u_i = random_vector(n, seed)[i] (reference.cpp:94-108) on the device.
+void launch_random_vector(double* out, long long n, unsigned long long seed, cudaStream_t s);
 int far_max_points_per_lane();
 
 // ---- direct interactions (direct.cu)

@@ -25,7 +25,7 @@
 
 namespace imqh {
 
-constexpr int kGemmM2MMaxKe = 256;  // M <= 30: dense translation matrices stay <= 8 MB/level
+constexpr size_t kM2tMaxSmem = 220 * 1024;  // fused M2M + transform: M <= ~22
 
 void cuda_check(cudaError_t e, const char* what) {
   if (e == cudaSuccess) return;
@@ -66,7 +66,13 @@ struct DeviceGuard {
 
 }  // namespace
 
-DeviceOperator::DeviceOperator(const double* xy_host, size_t n, double t, int M, int levels) {
+DeviceOperator::DeviceOperator(const double* xy_host, size_t n, double t, int M, int levels,
+                               const OperatorOptions& opt)
+    : opt_(opt) {
+  opt_.ring_tau = std::max(opt_.ring_tau, kRingTau);  // stricter only
+  opt_.ring2_tau = std::max(opt_.ring2_tau, kRing2Tau);
+  opt_.inner_tau = std::max(opt_.inner_tau, kInnerTau);
+  opt_.xring_tau = std::max(opt_.xring_tau, kXringTau);
   if (n == 0) throw std::invalid_argument("build_operator: empty point set");
   check_t(t);  // KernelParams(t) precedes build_operator (capi.cpp:110)
   if (n > (size_t)INT_MAX) throw std::invalid_argument("build_operator: too many points");
@@ -92,8 +98,8 @@ DeviceOperator::DeviceOperator(const double* xy_host, size_t n, double t, int M,
   }
   cuda_check(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming), "event create");
   cuda_check(cudaEventCreateWithFlags(&ev_last_, cudaEventDisableTiming), "event create");
-  if (const char* e = getenv("IMQ_FAR_STREAMS"))  // tuning: far groups on 1..4 streams
-    far_streams_ = std::max(1, std::min(1 + kAuxStreams, atoi(e)));
+  if (opt_.far_streams > 0)  // scheduling: far groups on 1..4 streams
+    far_streams_ = std::max(1, std::min(1 + kAuxStreams, opt_.far_streams));
   cuda_check(cudaStreamCreateWithFlags(&near_stream_, cudaStreamNonBlocking), "stream create");
   cuda_check(cudaEventCreateWithFlags(&ev_near_fork_, cudaEventDisableTiming), "event create");
   cuda_check(cudaEventCreateWithFlags(&ev_near_done_, cudaEventDisableTiming), "event create");
@@ -114,12 +120,10 @@ void DeviceOperator::release() {
   if (ev_last_) cudaEventSynchronize(ev_last_);
   dfree(d_xs_); dfree(d_ys_); dfree(d_leaf_); dfree(d_perm_); dfree(d_leaf_start_);
   dfree(d_far_items_); dfree(d_near_items_);
-  dfree(d_tr_off_); dfree(d_tr_idx_); dfree(d_tr_val_); dfree(d_binom_); dfree(d_m2m_);
-  if (blas_) cublasDestroy(blas_);
-  blas_ = nullptr;
+  dfree(d_tr_off_); dfree(d_tr_idx_); dfree(d_tr_val_); dfree(d_binom_); dfree(d_m2t_);
   dfree(d_mu_); dfree(d_coef_); dfree(d_u_); dfree(d_us_); dfree(d_far_); dfree(d_b_);
   dfree(d_part_);
-  dfree(d_need_par_); dfree(d_local_leaves_); dfree(d_pack_a_); dfree(d_pack_c_); dfree(d_own_lvl_);
+  dfree(d_need_par_); dfree(d_local_leaves_); dfree(d_own_lvl_);
   dfree(d_pair_items_); dfree(d_pair_part_); dfree(d_chunks_); dfree(d_contrib_off_);
   dfree(d_contrib_); dfree(d_near_s_); dfree(d_farc_); dfree(d_pull_items_);
   dfree(d_cheb_items_); dfree(d_cboxes_); dfree(d_ceval_items_);
@@ -128,6 +132,8 @@ void DeviceOperator::release() {
   dfree(d_ring_items_); dfree(d_lpart_items_);
   dfree(d_xnx_); dfree(d_xny_); dfree(d_xnleaf_); dfree(d_xval_); dfree(d_xring_items_);
   dfree(d_xboxes_);
+  dfree(solve_ws_);
+  solve_ws_bytes_ = 0;
   if (solve_pin_) cudaFreeHost(solve_pin_);
   solve_pin_ = nullptr;
   solve_pin_bytes_ = 0;
@@ -254,17 +260,18 @@ void DeviceOperator::build(const double* xy_host) {
                                cudaMemcpyHostToDevice, s), "H2D transform");
     cuda_check(cudaMemcpyAsync(d_binom_, bn.data(), bn.size() * sizeof(double),
                                cudaMemcpyHostToDevice, s), "H2D binomials");
-    if (L_ >= 2 && Ke_ <= kGemmM2MMaxKe) {
-      // M2M translation matrices (one per parent level, exact child offsets
-      // +-cell_{l+1}/2), applied as DGEMM [parents x 8Ke] x [8Ke x 2Ke]
-      const size_t msz = (size_t)8 * Ke_ * 2 * Ke_;
-      d_m2m_ = dalloc<double>(msz * (size_t)(L_ - 1), "m2m matrices");
+    if (L_ >= 2 &&
+        imqk::m2m_tr_smem(M_, Ke_, K_, (int)tr.val.size()) <= kM2tMaxSmem) {
+      // fused M2M + transform tables, one set per parent level (exact child
+      // offsets +-cell_{l+1}/2), k_m2m_tr
+      const size_t H1 = (size_t)M_ / 2 + 1, M1 = (size_t)M_ + 1;
+      m2t_stride_ = 4 * (M1 * M1 + H1 * H1);
+      d_m2t_ = dalloc<double2>(m2t_stride_ * (size_t)(L_ - 1), "m2m tables");
       for (int l = 1; l <= L_ - 1; ++l) {
-        const std::vector<double> T = m2m_matrix(M_, 0.5 * P_.cell[l + 1]);
-        cuda_check(cudaMemcpy(d_m2m_ + msz * (size_t)(l - 1), T.data(), msz * sizeof(double),
-                              cudaMemcpyHostToDevice), "H2D m2m");
+        const std::vector<double> T = m2m_tables(M_, 0.5 * P_.cell[l + 1]);
+        cuda_check(cudaMemcpy(d_m2t_ + m2t_stride_ * (size_t)(l - 1), T.data(),
+                              T.size() * sizeof(double), cudaMemcpyHostToDevice), "H2D m2m");
       }
-      if (cublasCreate(&blas_) != CUBLAS_STATUS_SUCCESS) throw cuda_error("cublasCreate failed");
     }
     T_.off = d_tr_off_;
     T_.idx = d_tr_idx_;
@@ -282,6 +289,7 @@ void DeviceOperator::build(const double* xy_host) {
     d_b_ = dalloc<double>((size_t)n, "b");
 
     cuda_check(cudaStreamSynchronize(s), "operator build");
+    certify();
   } catch (...) {
     dfree(d_xy); dfree(d_keys); dfree(d_idx); dfree(d_tmp); dfree(d_part);
     throw;
@@ -314,13 +322,13 @@ void DeviceOperator::build_items(int p_lo, int p_hi) {
   const double nt = (double)(p_hi - p_lo);
   const int rfit = (int)std::max(1.0, std::floor(nt / (32.0 * kWarpsWanted)));
   int rmax = imqk::m2p_specialised(M_) ? std::min(rfit, imqk::far_max_points_per_lane()) : 2;
-  if (const char* e = getenv("IMQ_FAR_RMAX"))  // tuning
-    rmax = std::max(1, std::min(imqk::far_max_points_per_lane(), atoi(e)));
+  if (opt_.far_rmax > 0)  // scheduling only
+    rmax = std::max(1, std::min(imqk::far_max_points_per_lane(), opt_.far_rmax));
   // Level split (L >= 4): the lists of levels 1..L-2 are shared by every
   // target of a level-(L-2) block, so those levels run as a separate "coarse"
   // pass whose items span whole grandparents (fewer idle lanes), and the
   // per-parent "fine" pass covers levels L-1..L and adds the coarse partial.
-  far_split_ = L_ >= 4 && !getenv("IMQ_FAR_NOSPLIT");
+  far_split_ = L_ >= 4 && !opt(kOptNoSplit);
   auto chunked = [&](long long blocks, int span, std::vector<std::vector<int4>>& g) {
     for (long long p = 0; p < blocks; ++p) {
       const int a = std::max(p_lo, ls[(size_t)(span * p)]);
@@ -358,7 +366,7 @@ void DeviceOperator::build_items(int p_lo, int p_hi) {
   dfree(d_lpart_items_);
   n_lpart_items_ = 0;
   lpart_group_off_.assign(16, 0);
-  if (far_split_ && !getenv("IMQ_FAR_NOLSPLIT")) {
+  if (far_split_ && !opt(kOptNoLsplit)) {
     std::vector<std::vector<int4>> pg((size_t)rmax);
     for (long long q = 0; q < n_leaves; ++q) {
       const int a = std::max(p_lo, ls[(size_t)q]), b = std::min(p_hi, ls[(size_t)q + 1]);
@@ -405,8 +413,6 @@ void DeviceOperator::build_items(int p_lo, int p_hi) {
     nrmax = 1;
     nitems = count_items(1);
   }
-  if (const char* e = getenv("IMQ_NEAR_R")) nrmax = std::max(1, std::min(4, atoi(e)));  // tuning
-  if (const char* e = getenv("IMQ_NEAR_SPLIT")) near_split_ = atoi(e) >= 9 ? 9 : (atoi(e) >= 3 ? 3 : 1);
   // symmetric near field: whole point set, every leaf within one item
   int max_leaf = 0;
   for (long long q = 0; q < n_leaves; ++q)
@@ -416,7 +422,7 @@ void DeviceOperator::build_items(int p_lo, int p_hi) {
   // are completed by pull items below)
   const bool full = p_lo == 0 && p_hi == N_;
   near_sym_ = (full ? near_split_ == 1 : true) &&
-              max_leaf <= 32 * imqk::near_max_points_per_lane() && !getenv("IMQ_NEAR_NOSYM");
+              max_leaf <= 32 * imqk::near_max_points_per_lane() && !opt(kOptNearNoSym);
   if (near_sym_) near_split_ = 1;
   if (near_sym_) nrmax = imqk::near_max_points_per_lane();
   std::vector<std::vector<int4>> ngroups((size_t)nrmax);
@@ -484,7 +490,7 @@ void DeviceOperator::build_pair_items(int p_lo, int p_hi) {
   dfree(d_contrib_); dfree(d_near_s_);
   near_pair_ = false;
   n_pair_items_ = n_chunks_ = 0;
-  if (near_sym_ || p_lo != 0 || p_hi != N_ || getenv("IMQ_NEAR_NOPAIR")) return;
+  if (near_sym_ || p_lo != 0 || p_hi != N_ || opt(kOptNearNoPair)) return;
   const std::vector<int>& ls = leaf_start_h_;
   const int g = 1 << (L_ + 1);
   const long long n_leaves = (long long)g * g;
@@ -570,7 +576,7 @@ void DeviceOperator::build_cheb(int p_lo, int p_hi) {
   dfree(d_xring_items_); dfree(d_xboxes_);
   xring_ = false;
   n_cheb_items_ = n_ceval_ = n_ring_items_ = n_xring_items_ = n_xboxes_ = 0;
-  if (!far_split_ || getenv("IMQ_FAR_NOCHEB") || !imqk::m2p_specialised(M_)) return;
+  if (!far_split_ || opt(kOptNoCheb) || !imqk::m2p_specialised(M_)) return;
   const int lc = L_ - 2;
   const std::vector<int>& ls = leaf_start_h_;
   auto own = [&](int l, long long q) {  // targets of block q at level l inside [p_lo, p_hi)
@@ -590,14 +596,13 @@ void DeviceOperator::build_cheb(int p_lo, int p_hi) {
   // average >= 1.25x as many targets as ring nodes (coarser levels always
   // gain: A's four children would evaluate the ring at 4 NC^2 nodes).
   constexpr int NR = imqk::kChebNR, NRR = NR * NR;
-  ring_ = !getenv("IMQ_FAR_NORING") && (double)tot >= 1.25 * NRR * (double)nonempty;
+  ring_ = !opt(kOptNoRing) && (double)tot >= 1.25 * NRR * (double)nonempty;
   // Rings of levels ring_l0_..L-1 only: the level-l ring is interpolated on a
   // level-(l-1) box A of half-width h only where t >= tau h, i.e. where the
   // lifted singularities of the ring's expansions sit >= tau h off the real
   // plane (coarse boxes with t << h need more nodes at high orders).
   {
-    const char* e = getenv("IMQ_RING_TAU");
-    const double tau = e ? atof(e) : 1.25;
+    const double tau = opt_.ring_tau;
     ring_l0_ = L_;
     for (int l = L_ - 1; l >= 2 && P_.t >= tau * 0.5 * P_.cell[l - 1]; --l) ring_l0_ = l;
     if (ring_l0_ > L_ - 1) ring_ = false;
@@ -610,12 +615,11 @@ void DeviceOperator::build_cheb(int p_lo, int p_hi) {
   cnode_base_.assign((size_t)lc + 2, 0);
   long long nb = 0;
   {
-    const char* e = getenv("IMQ_INNER_TAU");
-    const double taui = e ? atof(e) : 2.5;
+    const double taui = opt_.inner_tau;
     for (int l = 1; l <= lc; ++l) {
       cheb_base_[(size_t)l] = nb;
       nb += 1ll << (2 * (l + 1));
-      inner_v_[(size_t)l] = ring_ && l >= std::max(2, ring_l0_) && !getenv("IMQ_FAR_NOINNER") &&
+      inner_v_[(size_t)l] = ring_ && l >= std::max(2, ring_l0_) && !opt(kOptNoInner) &&
                             P_.t >= taui * 0.5 * P_.cell[l];
       const long long npl = inner_v_[(size_t)l] ? (long long)imqk::kChebNI * imqk::kChebNI : NN;
       cnode_base_[(size_t)l + 1] = cnode_base_[(size_t)l] + (1ll << (2 * (l + 1))) * npl;
@@ -672,8 +676,7 @@ void DeviceOperator::build_cheb(int p_lo, int p_hi) {
   if (ring_) {  // ring nodes of every box of levels 1..lc (rings of levels 2..L-1)
     // per parent level a: ring variant (fewer nodes where t >= 2.5 h_a, the
     // singularities sitting further off the real plane) and node offset
-    const char* e2 = getenv("IMQ_RING2_TAU");
-    const double tau2 = e2 ? atof(e2) : 2.5;
+    const double tau2 = opt_.ring2_tau;
     ring_v_.assign((size_t)lc + 1, 0);
     ring_nbase_.assign((size_t)lc + 2, 0);
     for (int a = 1; a <= lc; ++a) {
@@ -800,14 +803,13 @@ void DeviceOperator::build_cheb(int p_lo, int p_hi) {
   // needs t / h_X >= ~5 for ~1e-13) and X holds enough targets.
   if (ring_) {
     constexpr int NX = imqk::kChebNX, NXX = NX * NX;
-    const char* e = getenv("IMQ_XRING_TAU");
-    const double taux = e ? atof(e) : 5.0;
+    const double taux = opt_.xring_tau;
     long long nx_ne = 0, nx_tot = 0;
     for (long long q = 0; q < (1ll << (2 * L_)); ++q) {
       const int c = own(L_ - 1, q);
       if (c > 0) ++nx_ne, nx_tot += c;
     }
-    xring_ = !getenv("IMQ_FAR_NOXRING") && nx_ne > 0 &&
+    xring_ = !opt(kOptNoXring) && nx_ne > 0 &&
              P_.t >= taux * 0.5 * P_.cell[L_ - 1] &&
              (double)nx_tot >= 1.25 * NXX * (double)nx_ne;
     if (xring_) {
@@ -874,11 +876,138 @@ void DeviceOperator::build_cheb(int p_lo, int p_hi) {
   cheb_ = true;
 }
 
+// ------------------------------------------------------------ certificate --
+// Build-time certificate of the interpolated far field (DESIGN.md §3,
+// "Safety").  The gates of build_cheb() (t / h thresholds, node counts) come
+// from sweeps; this check measures, on the operator's own geometry, how well
+// each interpolant resolves its field: one probe product (u = random_vector(N,
+// kProbeSeed), sorted order) fills every node-value array, k_cheb_tail forms
+// each box's tensor Chebyshev coefficients and estimates the interpolation
+// error from their decay (cheb.cu), and the error of a product is estimated as
+//     est = sum over interpolation kinds of max_box estimate  /  max_i |b_i|.
+// While est > budget (kCertBudget = 1e-12, or the stricter option), the kind
+// with the largest contribution is switched off -- a level's inner list back
+// to kChebN nodes, a ring variant back to kChebNR nodes, a ring level (and
+// the coarser ones) back to per-child evaluation, the X-ring off, and as a
+// last resort the whole Chebyshev path (all pairs direct, exact) -- and the
+// work lists are rebuilt.  Sharded ranks inherit the decisions (they are
+// stored in opt_ before restrict_targets rebuilds the lists), so every rank
+// interpolates the same way.
+void DeviceOperator::certify() {
+  cert_ = CertReport{};
+  if (!cheb_) return;
+  constexpr unsigned long long kProbeSeed = 0x1D0C5EEDull;
+  const double budget = opt_.cert_budget > 0 ? std::min(opt_.cert_budget, kCertBudget) : kCertBudget;
+  cert_.budget = budget;
+  double* d_max = dalloc<double>(1, "certificate");
+  double2* d_tail = nullptr;
+  size_t tail_cap = 0;
+  try {
+    for (int round = 0; round < 16 && cheb_; ++round) {
+      cert_.rounds = round + 1;
+      imqk::launch_random_vector(d_us_, N_, kProbeSeed, stream_);
+      apply_sorted_locked(d_us_, d_b_, nullptr, stream_);
+      imqk::launch_absmax(d_b_, N_, d_max, stream_);
+      // kinds: {kind, level, box list offset / count (device), values, n}
+      struct Kind { int kind, level; const int* boxes; int nb; const double* vals; int n; };
+      std::vector<Kind> kinds;
+      const int lc = cheb_lc_;
+      for (int l = 1; l <= lc; ++l) {
+        const int nb = cbox_off_[(size_t)l + 1] - cbox_off_[(size_t)l];
+        if (!nb) continue;
+        const int* bx = d_cboxes_ + cbox_off_[(size_t)l];
+        const int n = inner_v_[(size_t)l] ? imqk::kChebNI : imqk::kChebN;
+        kinds.push_back({inner_v_[(size_t)l] ? 1 : 0, l, bx, nb, d_cval_ + cnode_base_[(size_t)l], n});
+        if (ring_ && l + 1 >= ring_l0_) {
+          const int nr = imqk::kRingNr[ring_v_[(size_t)l]];
+          kinds.push_back({ring_v_[(size_t)l] ? 3 : 2, l, bx, nb, d_rval_ + ring_nbase_[(size_t)l], nr});
+        }
+      }
+      if (xring_ && n_xboxes_) kinds.push_back({4, L_ - 1, d_xboxes_, n_xboxes_, d_xval_, imqk::kChebNX});
+      size_t total = 0;
+      for (const Kind& k : kinds) total += (size_t)k.nb;
+      if (total > tail_cap) {
+        dfree(d_tail);
+        d_tail = dalloc<double2>(total, "certificate tails");
+        tail_cap = total;
+      }
+      size_t off = 0;
+      for (const Kind& k : kinds) {
+        imqk::launch_cheb_tail(k.boxes, k.nb, k.vals, k.n, d_tail + off, stream_);
+        off += (size_t)k.nb;
+      }
+      std::vector<double2> tails(total);
+      double bmax = 0.0;
+      if (total)
+        cuda_check(cudaMemcpyAsync(tails.data(), d_tail, total * sizeof(double2),
+                                   cudaMemcpyDeviceToHost, stream_), "D2H certificate");
+      cuda_check(cudaMemcpyAsync(&bmax, d_max, sizeof(double), cudaMemcpyDeviceToHost, stream_),
+                 "D2H certificate");
+      cuda_check(cudaStreamSynchronize(stream_), "certificate");
+      cuda_check(cudaGetLastError(), "certificate kernels");
+      cert_.scale = bmax;
+      if (!(bmax > 0.0)) break;  // nothing to compare against (all-zero field)
+      std::vector<double> est(kinds.size(), 0.0);
+      double sum = 0.0;
+      off = 0;
+      for (size_t i = 0; i < kinds.size(); ++i) {
+        double m = 0.0;
+        for (int b = 0; b < kinds[i].nb; ++b) m = std::max(m, tails[off + (size_t)b].x);
+        off += (size_t)kinds[i].nb;
+        est[i] = m / bmax;
+        sum += est[i];
+      }
+      for (int k = 0; k < 5; ++k) cert_.by_kind[k] = 0.0;
+      for (size_t i = 0; i < kinds.size(); ++i)
+        cert_.by_kind[kinds[i].kind] = std::max(cert_.by_kind[kinds[i].kind], est[i]);
+      cert_.estimate = sum;
+      if (!(sum > budget) || opt(kOptCertReport)) break;  // certified (NaN fails)
+      // switch off the largest contributor and rebuild
+      size_t w = 0;
+      for (size_t i = 1; i < kinds.size(); ++i)
+        if (!(est[i] <= est[w])) w = i;
+      const Kind& k = kinds[w];
+      const double above = 1.0 + 1e-9;  // just above t / h of that level
+      switch (k.kind) {
+        case 0: opt_.flags |= kOptNoCheb; break;
+        case 1: opt_.inner_tau = std::max(opt_.inner_tau, above * t_ / (0.5 * P_.cell[k.level])); break;
+        case 2: opt_.ring_tau = std::max(opt_.ring_tau, above * t_ / (0.5 * P_.cell[k.level])); break;
+        case 3: opt_.ring2_tau = std::max(opt_.ring2_tau, above * t_ / (0.5 * P_.cell[k.level])); break;
+        case 4: opt_.flags |= kOptNoXring; break;
+      }
+      ++cert_.fallbacks;
+      build_items(0, N_);
+      have_counts_ = false;
+    }
+  } catch (...) {
+    dfree(d_max);
+    dfree(d_tail);
+    throw;
+  }
+  dfree(d_max);
+  dfree(d_tail);
+}
+
 void DeviceOperator::restrict_targets(int p_lo, int p_hi) {
   std::lock_guard<std::mutex> lk(mtx_);
   DeviceGuard g(device_);
   if (p_lo < 0 || p_hi > N_ || p_lo > p_hi)
     throw std::invalid_argument("restrict_targets: bad sorted-position range");
+  // Both ends must be level-(L-1) block boundaries (a value leaf_start[4p]):
+  // setup_sharded_moments() counts a parent as owned only when it lies fully
+  // inside the range, so a parent straddling a cut would add its points to
+  // the coarse moments on no rank.
+  auto boundary = [&](int v) {
+    const long long np = 1ll << (2 * L_);
+    long long lo = 0, hi = np;  // smallest p with leaf_start[4p] >= v
+    while (lo < hi) {
+      const long long mid = (lo + hi) / 2;
+      if (leaf_start_h_[(size_t)(4 * mid)] < v) lo = mid + 1; else hi = mid;
+    }
+    return leaf_start_h_[(size_t)(4 * lo)] == v;
+  };
+  if (!boundary(p_lo) || !boundary(p_hi))
+    throw std::invalid_argument("restrict_targets: range ends must be level-(L-1) block boundaries");
   cuda_check(cudaStreamSynchronize(stream_), "restrict");
   cuda_check(cudaEventSynchronize(ev_last_), "restrict");  // work on other streams
   build_items(p_lo, p_hi);
@@ -1017,23 +1146,18 @@ std::vector<int> shard_bounds_weighted(const std::vector<int>& ls, int L, int wo
 
 void DeviceOperator::moments(const double* d_us, cudaStream_t s) {
   imqk::launch_p2m_leaf(P_, d_us, d_mu_, nullptr, 0, s);
-  if (d_m2m_) {
-    cublasSetStream(blas_, s);
-    const size_t msz = (size_t)8 * Ke_ * 2 * Ke_;
-    const double one = 1.0, zero = 0.0;
-    for (int l = L_ - 1; l >= 1; --l) {
-      const int parents = 1 << (2 * (l + 1));
-      // row-major C[parents x 2Ke] = A[parents x 8Ke] * T[8Ke x 2Ke]
-      const cublasStatus_t st = cublasDgemm(
-          blas_, CUBLAS_OP_N, CUBLAS_OP_N, 2 * Ke_, parents, 8 * Ke_, &one,
-          d_m2m_ + msz * (size_t)(l - 1), 2 * Ke_,
-          reinterpret_cast<const double*>(d_mu_ + P_.mu_off[l + 1]), 8 * Ke_, &zero,
-          reinterpret_cast<double*>(d_mu_ + P_.mu_off[l]), 2 * Ke_);
-      if (st != CUBLAS_STATUS_SUCCESS) throw cuda_error("cublasDgemm (M2M) failed");
-    }
-  } else {
-    for (int l = L_ - 1; l >= 1; --l) imqk::launch_m2m(P_, l, d_mu_, d_binom_, s);
+  if (d_m2t_) {
+    // level l's kernel translates its children (level l + 1) up and writes
+    // their coefficients; level 1 also transforms itself
+    for (int l = L_ - 1; l >= 1; --l)
+      imqk::launch_m2m_tr(P_, l, nullptr, 0, 1ll << (2 * (l + 1)), d_mu_ + P_.mu_off[l + 1],
+                          d_mu_ + P_.mu_off[l], d_coef_ + P_.coef_off[l + 1],
+                          l == 1 ? d_coef_ + P_.coef_off[1] : nullptr, m2t_V(l), m2t_W(l), T_, s);
+    if (L_ == 1) imqk::launch_transform(P_, d_mu_, d_coef_, T_, s);
+    return;
   }
+  // orders beyond the fused kernel's shared memory: separate passes
+  for (int l = L_ - 1; l >= 1; --l) imqk::launch_m2m(P_, l, d_mu_, d_binom_, s);
   imqk::launch_transform(P_, d_mu_, d_coef_, T_, s);
 }
 
@@ -1060,10 +1184,10 @@ void DeviceOperator::gather(const double* d_u, double* d_us, cudaStream_t s) {
 }
 
 void DeviceOperator::setup_sharded_moments(int p_lo, int p_hi) {
-  dfree(d_need_par_); dfree(d_local_leaves_); dfree(d_pack_a_); dfree(d_pack_c_); dfree(d_own_lvl_);
+  dfree(d_need_par_); dfree(d_local_leaves_); dfree(d_own_lvl_);
   need_par_h_.clear();
   local_leaves_h_.clear();
-  if ((p_lo == 0 && p_hi == N_) || L_ < 3 || !d_m2m_) return;
+  if ((p_lo == 0 && p_hi == N_) || L_ < 3 || !d_m2t_) return;
   const std::vector<int>& ls = leaf_start_h_;
   const int G = 1 << L_;  // level L-1 grid
   const long long npar = (long long)G * G;
@@ -1101,8 +1225,6 @@ void DeviceOperator::setup_sharded_moments(int p_lo, int p_hi) {
     cuda_check(cudaMemcpy(d_local_leaves_, local_leaves_h_.data(),
                           local_leaves_h_.size() * sizeof(int), cudaMemcpyHostToDevice),
                "H2D local leaves");
-  d_pack_a_ = dalloc<double>(need_par_h_.size() * (size_t)8 * Ke_, "m2m pack A");
-  d_pack_c_ = dalloc<double>(need_par_h_.size() * (size_t)2 * Ke_, "m2m pack C");
   d_own_lvl_ = dalloc<double2>((size_t)npar * Ke_, "own level moments");
 }
 
@@ -1118,18 +1240,11 @@ void DeviceOperator::moments_local(const double* d_us, cudaStream_t s) {
   const long long npar = (long long)G * G;
   const int nneed = (int)need_par_h_.size();
   imqk::launch_p2m_leaf(P_, d_us, d_mu_, d_local_leaves_, (int)local_leaves_h_.size(), s);
-  cublasSetStream(blas_, s);
-  const size_t msz = (size_t)8 * Ke_ * 2 * Ke_;
-  const double one = 1.0, zero = 0.0;
-  // level L-1 for own + halo blocks: packed DGEMM over the needed parents
-  imqk::launch_gather_rows(reinterpret_cast<const double*>(d_mu_ + P_.mu_off[L_]), d_need_par_,
-                           nneed, 8 * Ke_, d_pack_a_, s);
-  if (cublasDgemm(blas_, CUBLAS_OP_N, CUBLAS_OP_N, 2 * Ke_, nneed, 8 * Ke_, &one,
-                  d_m2m_ + msz * (size_t)(L_ - 2), 2 * Ke_, d_pack_a_, 8 * Ke_, &zero,
-                  d_pack_c_, 2 * Ke_) != CUBLAS_STATUS_SUCCESS)
-    throw cuda_error("cublasDgemm (M2M, level L-1) failed");
-  imqk::launch_scatter_rows(d_pack_c_, d_need_par_, nneed, 2 * Ke_,
-                            reinterpret_cast<double*>(d_mu_ + P_.mu_off[L_ - 1]), s);
+  // level L-1 for own + halo blocks (the needed parents), with the level-L
+  // coefficients of their children (= the local leaves)
+  imqk::launch_m2m_tr(P_, L_ - 1, d_need_par_, 0, nneed, d_mu_ + P_.mu_off[L_],
+                      d_mu_ + P_.mu_off[L_ - 1], d_coef_ + P_.coef_off[L_], nullptr, m2t_V(L_ - 1),
+                      m2t_W(L_ - 1), T_, s);
   // own-only level L-1 -> coarse levels (partial sums, reduced by the caller).
   // The coarse region is zeroed and only the parents above the own range are
   // translated (a contiguous Morton range per level): the all-reduce then
@@ -1150,13 +1265,9 @@ void DeviceOperator::moments_local(const double* d_us, cudaStream_t s) {
                              cudaMemcpyDeviceToDevice, s),
              "own level copy");
   for (int l = L_ - 2; l >= 1; --l) {
-    const double* A = l == L_ - 2 ? reinterpret_cast<const double*>(d_own_lvl_)
-                                  : reinterpret_cast<const double*>(d_mu_ + P_.mu_off[l + 1]);
-    if (cublasDgemm(blas_, CUBLAS_OP_N, CUBLAS_OP_N, 2 * Ke_, (int)(a1 - a0), 8 * Ke_, &one,
-                    d_m2m_ + msz * (size_t)(l - 1), 2 * Ke_, A + (size_t)a0 * 8 * Ke_, 8 * Ke_,
-                    &zero, reinterpret_cast<double*>(d_mu_ + P_.mu_off[l]) + (size_t)a0 * 2 * Ke_,
-                    2 * Ke_) != CUBLAS_STATUS_SUCCESS)
-      throw cuda_error("cublasDgemm (M2M, coarse) failed");
+    const double2* in = l == L_ - 2 ? d_own_lvl_ : d_mu_ + P_.mu_off[l + 1];
+    imqk::launch_m2m_tr(P_, l, nullptr, a0, a1 - a0, in, d_mu_ + P_.mu_off[l], nullptr, nullptr,
+                        m2t_V(l), m2t_W(l), T_, s);
     a0 >>= 2;
     a1 = (a1 + 3) >> 2;
   }
@@ -1175,9 +1286,7 @@ void DeviceOperator::moments_finish(cudaStream_t s) {
   imqk::launch_transform(P_, d_mu_, d_coef_, T_, s, 1, L_ - 2);
   imqk::launch_transform(P_, d_mu_, d_coef_, T_, s, L_ - 1, L_ - 1, d_need_par_,
                          (int)need_par_h_.size());
-  if (!local_leaves_h_.empty())
-    imqk::launch_transform(P_, d_mu_, d_coef_, T_, s, L_, L_, d_local_leaves_,
-                           (int)local_leaves_h_.size());
+  // (the local leaves' level-L coefficients came with moments_local's M2M)
 }
 
 void DeviceOperator::far_near(const double* d_us, double* d_out, const int* perm,
@@ -1507,8 +1616,9 @@ int DeviceOperator::kernel_launches_per_apply() const {
     for (size_t r = 1; r < off.size(); ++r) g += off[r] > off[r - 1];
     return g;
   };
-  int n = 1 + 1 + L_;  // gather, leaf P2M, transform per level
-  if (M_ > 30) n += L_ - 1;  // custom M2M kernel instead of the DGEMMs
+  // gather, leaf P2M, then the fused M2M + transform per parent level (or,
+  // beyond its shared memory, a M2M per parent level and a transform per level)
+  int n = 1 + 1 + (d_m2t_ ? std::max(1, L_ - 1) : (L_ - 1) + L_);
   if (near_sym_) n += groups(near_group_off_) + (n_pull_ > 0);
   else if (near_pair_) n += groups(pair_group_off_) + 1;
   else n += groups(near_group_off_) + (near_split_ > 1);
@@ -1606,8 +1716,7 @@ SolveResult DeviceOperator::solve_host(const double* f, double tol, int max_iter
   cudaEvent_t ev[kRing] = {}, tev[kRing][3] = {};
   const bool trace = getenv("IMQ_TRACE") != nullptr;
   auto cleanup = [&]() {
-    if (ws) cudaFreeAsync(ws, s);
-    ws = nullptr;
+    ws = nullptr;  // solve_ws_ stays cached on the operator
     for (int i = 0; i < kRing; ++i) {
       if (ev[i]) cudaEventDestroy(ev[i]);
       for (auto& e : tev[i])
@@ -1627,22 +1736,22 @@ SolveResult DeviceOperator::solve_host(const double* f, double tol, int max_iter
       const size_t o_V = carve(n * (size_t)(mcap + 1) * 8), o_h = carve(hld * (size_t)(mcap + 1) * 8);
       const size_t o_p = carve((size_t)nparts * 8), o_m = carve(2 * (size_t)mgs_parts * 8);
       const size_t o_fl = carve((size_t)mcap * sizeof(int));
-      cudaMemPool_t pool;
-      if (cudaDeviceGetDefaultMemPool(&pool, device_) == cudaSuccess) {
-        uint64_t thr = 0;
-        cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-        if (thr < off) {
-          thr = off;
-          cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+      // The operator's own cached workspace (grown on demand, freed with the
+      // operator): the process-wide default pool is left untouched.
+      if (solve_ws_bytes_ < off) {
+        cuda_check(cudaStreamSynchronize(s), "gmres workspace");
+        dfree(solve_ws_);
+        solve_ws_bytes_ = 0;
+        const cudaError_t e = cudaMalloc(&solve_ws_, off);
+        if (e == cudaErrorMemoryAllocation) {
+          cudaGetLastError();
+          solve_ws_ = nullptr;
+          throw std::bad_alloc();
         }
+        cuda_check(e, "gmres workspace");
+        solve_ws_bytes_ = off;
       }
-      const cudaError_t e = cudaMallocAsync(&ws, off, s);
-      if (e == cudaErrorMemoryAllocation) {
-        cudaGetLastError();
-        ws = nullptr;
-        throw std::bad_alloc();
-      }
-      cuda_check(e, "gmres workspace");
+      ws = solve_ws_;
       char* b = static_cast<char*>(ws);
       d_f = reinterpret_cast<double*>(b + o_f);
       d_x = reinterpret_cast<double*>(b + o_x);

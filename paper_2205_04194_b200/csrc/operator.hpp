@@ -7,7 +7,6 @@
 // "safe for concurrent application to distinct vectors" contract
 // (fastmv.hpp:17-18) without duplicating the ~GB workspace.
 #pragma once
-#include <cublas_v2.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -43,6 +42,44 @@ struct PairCounts {
   int cheb_xring = 0;           // level-L outer rings through the level-(L-1) nodes
 };
 
+// Build-time options (imq_ext_operator_create_opts).  They can only DISABLE
+// an approximation or make its gate STRICTER: the default operator uses the
+// swept-safe settings, and no option (and no environment variable) can move
+// a product further from the reference than the defaults allow.
+enum : unsigned {
+  kOptNoCheb = 1u << 0,    // no Chebyshev coarse pass (all far pairs direct)
+  kOptNoRing = 1u << 1,    // no ring interpolation
+  kOptNoInner = 1u << 2,   // inner lists at the level's full node count
+  kOptNoXring = 1u << 3,   // no X-ring (level-L outer rings at the targets)
+  kOptNoLsplit = 1u << 4,  // no per-leaf partial pass
+  kOptNoSplit = 1u << 5,   // single far pass (implies no Chebyshev pass)
+  kOptNearNoSym = 1u << 6, // per-target near field (no symmetric evaluation)
+  kOptNearNoPair = 1u << 7,// no chunk-pair near field
+  kOptCertReport = 1u << 8, // diagnostics: certificate estimated, never acted on
+};
+constexpr double kCertBudget = 2e-12;  // estimated relative deviation allowed
+// Build-time interpolation certificate (operator.cu certify()).
+struct CertReport {
+  double estimate = 0;  // estimated rel. deviation of a product from the all-direct one
+  double budget = 0;    // 0: not run (no interpolation)
+  double scale = 0;     // max |b| of the probe product
+  double by_kind[5] = {0, 0, 0, 0, 0};  // node levels, inner (NI), rings (NR), rings (NR2), X-ring
+  int fallbacks = 0;    // interpolations switched off to meet the budget
+  int rounds = 0;       // probe products run
+};
+struct OperatorOptions {
+  unsigned flags = 0;
+  // interpolation gates (t / h thresholds); values below the defaults are
+  // raised to the defaults (stricter only)
+  double ring_tau = 0, ring2_tau = 0, inner_tau = 0, xring_tau = 0;
+  // certificate budget (relative); values above kCertBudget are lowered to it
+  double cert_budget = 0;
+  // scheduling (no effect on any result bit): far items' targets per lane,
+  // far-field streams; 0 = automatic
+  int far_rmax = 0, far_streams = 0;
+};
+constexpr double kRingTau = 1.25, kRing2Tau = 2.5, kInnerTau = 2.5, kXringTau = 5.0;
+
 std::vector<int> shard_bounds(const std::vector<int>& leaf_start, int L, int world);
 std::vector<double> parent_work(const std::vector<int>& leaf_start, int L, int M);
 std::vector<int> shard_bounds_weighted(const std::vector<int>& leaf_start, int L, int world,
@@ -50,7 +87,8 @@ std::vector<int> shard_bounds_weighted(const std::vector<int>& leaf_start, int L
 
 class DeviceOperator {
  public:
-  DeviceOperator(const double* xy_host, size_t n, double t, int M, int levels);
+  DeviceOperator(const double* xy_host, size_t n, double t, int M, int levels,
+                 const OperatorOptions& opt = OperatorOptions());
   ~DeviceOperator();
   DeviceOperator(const DeviceOperator&) = delete;
   DeviceOperator& operator=(const DeviceOperator&) = delete;
@@ -76,6 +114,7 @@ class DeviceOperator {
   void copy_permutation(int* perm_host) const;
   void copy_leaf_start(std::vector<int>& out) const;
   PairCounts pair_counts();
+  const CertReport& certificate() const { return cert_; }
   // Restricts far/near evaluation to targets at sorted positions [lo, hi)
   // (sharded application); b entries of other targets are left untouched.
   void restrict_targets(int p_lo, int p_hi);
@@ -146,6 +185,8 @@ class DeviceOperator {
   void build_items(int p_lo, int p_hi);
   void build_pair_items(int p_lo, int p_hi);
   void build_cheb(int p_lo, int p_hi);
+  void certify();
+  CertReport cert_{};
   int kernel_launches_per_apply() const;
   void fill_eval_counts();
   std::vector<double> far_by_level_, lists_by_level_;
@@ -160,6 +201,8 @@ class DeviceOperator {
                            cudaStream_t s);
 
   int device_ = 0;
+  OperatorOptions opt_{};
+  bool opt(unsigned f) const { return (opt_.flags & f) != 0; }
   cudaStream_t stream_ = nullptr;
   static constexpr int kAuxStreams = 3;  // far-field work groups run concurrently
   cudaStream_t aux_[kAuxStreams] = {};
@@ -194,8 +237,12 @@ class DeviceOperator {
   int* d_tr_idx_ = nullptr;
   double* d_tr_val_ = nullptr;
   double* d_binom_ = nullptr;
-  double* d_m2m_ = nullptr;           // per parent level: [8 Ke][2 Ke] translation
-  cublasHandle_t blas_ = nullptr;     // M2M as one DGEMM per level
+  double2* d_m2t_ = nullptr;  // fused M2M tables per parent level (k_m2m_tr), or none
+  size_t m2t_stride_ = 0;
+  const double2* m2t_V(int l) const { return d_m2t_ + m2t_stride_ * (size_t)(l - 1); }
+  const double2* m2t_W(int l) const {
+    return m2t_V(l) + (size_t)4 * (M_ + 1) * (M_ + 1);
+  }
   double2* d_mu_ = nullptr;
   double2* d_coef_ = nullptr;
   size_t coef_count_ = 0;
@@ -261,6 +308,8 @@ class DeviceOperator {
   int* d_contrib_off_ = nullptr;
   int* d_contrib_ = nullptr;
   double* d_near_s_ = nullptr;
+  void* solve_ws_ = nullptr;  // GMRES device workspace (cached, grown on demand)
+  size_t solve_ws_bytes_ = 0;
   void* solve_pin_ = nullptr;  // pinned GMRES staging (Hessenberg columns, flags)
   size_t solve_pin_bytes_ = 0;
   std::vector<int> leaf_start_h_;
@@ -268,8 +317,6 @@ class DeviceOperator {
   int par_lo_ = 0, par_hi_ = 0;
   int* d_need_par_ = nullptr;
   int* d_local_leaves_ = nullptr;
-  double* d_pack_a_ = nullptr;
-  double* d_pack_c_ = nullptr;
   double2* d_own_lvl_ = nullptr;
   int target_lo_ = 0, target_hi_ = 0;
   bool have_counts_ = false;

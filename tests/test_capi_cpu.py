@@ -102,6 +102,14 @@ def test_argument_validation_codes(imq):
     L.imq_operator_destroy(None)  # NULL is a no-op
     out = C.c_double()
     assert L.imq_dense_matvec(dp, 2, -1.0, dp, C.cast(C.byref(out), C.POINTER(C.c_double))) == 1
+    # options: negative / NaN gates and budgets are rejected before any device work
+    o = capi.imq_ext_options()
+    o.ring_tau = -1.0
+    assert L.imq_ext_operator_create_opts(dp, 2, 1.0, 4, 1, C.byref(o), C.byref(h)) == 1
+    o = capi.imq_ext_options()
+    o.cert_budget = float("nan")
+    assert L.imq_ext_operator_create_opts(dp, 2, 1.0, 4, 1, C.byref(o), C.byref(h)) == 1
+    assert L.imq_ext_operator_create_opts(None, 2, 1.0, 4, 1, None, C.byref(h)) == 1
 
 
 def test_point_file_io(imq, tmp_path):

@@ -242,6 +242,16 @@ def test_operator_errors(imq):
     assert op.size == 10 and op.levels == imq.auto_level(10, 4)
     with pytest.raises(imq.IMQError):
         op.apply(np.ones(9))
+    # restrict: both ends must be level-(L-1) block boundaries
+    xy = imq.halton2d(5000)
+    with imq.FastOperator(xy, 0.1, 8, 4) as op:
+        ls = op.leaf_start()
+        cut = int(ls[4 * 37])
+        assert imq.capi.lib().imq_ext_operator_restrict(op.handle, 0, cut) == 0
+        inner = int(ls[4 * 37 + 1])
+        assert inner != cut
+        assert imq.capi.lib().imq_ext_operator_restrict(op.handle, 0, inner) == 1
+        assert b"boundaries" in imq.capi.lib().imq_last_error()
 
 
 @pytest.mark.parametrize("world", [2, 3, 5])

@@ -45,7 +45,9 @@ for c in range(ncase):
         side = float(max(np.ptp(pts[:, 0]), np.ptp(pts[:, 1])))
         t = float(rng.uniform(5.0, 5.4) * side / 2 ** (L + 1))
     u = inputs.random_vector(n, 100 + c)
-    op = P.FastOperator(xy, t, m, L)
+    # STRESS_REPORT=1: the certificate is estimated but not acted on, to
+    # compare its estimate with the measured deviation of the swept gates
+    op = P.FastOperator(xy, t, m, L, **({"flags": ["cert_report"]} if os.environ.get("STRESS_REPORT") else {}))
     st = op.stats()
     b = op.apply(u)
     rows = np.unique(rng.integers(0, n, 300))
@@ -54,14 +56,14 @@ for c in range(ncase):
     worst = max(worst, err)
     extra = ""
     if st["cheb_ring"] and os.environ.get("STRESS_COMPARE"):
-        os.environ["IMQ_FAR_NORING"] = "1"   # same case without the rings
-        op2 = P.FastOperator(xy, t, m, L)
+        op2 = P.FastOperator(xy, t, m, L, flags=["no_ring"])  # same case without the rings
         b2 = op2.apply(u)
-        del os.environ["IMQ_FAR_NORING"]
         extra = f"  (no rings: {float(np.max(np.abs(b2[rows] - ref)) / np.max(np.abs(ref))):.2e})"
         op2.close()
     print(f"{c:2d} {kind:8s} n={n:8d} L={L} m={m:2d} t={t:.2e}  cheb={st['cheb_levels']} "
-          f"ring={st['cheb_ring']} xring={st['cheb_xring']} near={st['near_mode']}  dev {err:.2e}{extra}",
+          f"ring={st['cheb_ring']} xring={st['cheb_xring']} near={st['near_mode']}  "
+          f"cert {st['cert_estimate']:.1e} [{' '.join(f'{v:.0e}' for v in st['cert_by_kind'])}] "
+          f"fb={st['cert_fallbacks']}  dev {err:.2e}{extra}",
           flush=True)
     op.close()
 print(f"worst {worst:.2e}")
