@@ -20,7 +20,7 @@ value = N points / max-over-ranks time.
 
 --impl reference: the reference's own CPU implementation (oracle/_ref, the
 unmodified /root/reference sources compiled by oracle/Makefile) on the host
-cores, on a bounded sample of the same workload (see cpu_sample()).
+cores, on bounded samples of the same config-4 problem (run_cpu_reference()).
 """
 from __future__ import annotations
 
@@ -112,55 +112,74 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------- CPU side
-def cpu_sample(total_steps: int):
-    """Bounded sample of the config-4 workload for the CPU reference: same
-    point distribution, c, p and leaf occupancy (mean 64 per leaf), smaller N."""
-    if total_steps <= 20:
-        return dict(n=262_144, t=0.01, m=16, levels=5, seed=0)
-    return dict(n=65_536, t=0.01, m=16, levels=4, seed=0)
+def ref_sample_sizes(total_steps: int):
+    """Sample sizes (finest blocks) of one CPU-reference step: moments over
+    n_mom random leaves, far + near over ~n_tgt target leaves in 8x8 tiles."""
+    if total_steps <= 4:
+        return 4096, 4096
+    if total_steps <= 16:
+        return 2048, 2048
+    return 1024, 1024
 
 
 def run_cpu_reference(steps: int, warmup: int):
-    """Times the reference fast matvec on the host cores; returns a dict."""
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    """The reference's own fast-matvec routines (oracle/_ref: the unmodified
+    /root/reference sources, OpenMP on all host cores) on the EXACT config-4
+    problem (N = 16,777,216, L = 8), one bounded sample per step
+    (oracle/ref_sample.cpp): compute_moments over the points of random leaves,
+    apply_far + apply_near onto whole 8x8-leaf tiles of targets, each stage
+    scaled by its exact work ratio to a full product.  Without oracle/_ref
+    (reference not built): the C restatement (port) on a smaller problem."""
+    import ctypes as C
+
+    import numpy as np
+
     from paper_2205_04194_b200 import inputs
-    s = cpu_sample(steps + warmup)
-    xy = inputs.uniform_points(s["n"], s["seed"])
     cores = os.cpu_count() or 1
-    try:
-        from oracle import Reference  # the unmodified reference, compiled (oracle/_ref)
-        R = Reference()
-        R.set_threads(cores)
-        kind = "reference"
-        t0 = time.perf_counter()
-        h = R.create(xy, s["t"], s["m"], s["levels"])
-        setup = time.perf_counter() - t0
-
-        def step(k):
-            R.apply(h, inputs.random_vector(s["n"], 1000 + k))
-    except FileNotFoundError:
-        from oracle import Oracle  # restatement (port) when the reference was not built
-        O = Oracle()
-        kind = "port"
-        setup = 0.0
-        h = None
-
-        def step(k):
-            O.fast_matvec(xy, s["t"], s["m"], s["levels"], inputs.random_vector(s["n"], 1000 + k))
+    lib_path = os.path.join(ROOT, "oracle", "_ref", "libimqfast_ref.so")
+    if os.path.exists(lib_path):
+        n, L = CFG["n"], CFG["levels"]
+        xy = inputs.uniform_points(n, CFG["seed"])
+        u = inputs.random_vector(n, 1000)
+        lib = C.CDLL(lib_path)
+        dp = C.POINTER(C.c_double)
+        f = lib.imqref_sample_time
+        f.argtypes = [dp, C.c_longlong, C.c_double, C.c_int, C.c_int, dp, C.c_int, C.c_int,
+                      C.c_ulonglong, C.c_int, dp]
+        n_mom, n_tgt = ref_sample_sizes(steps + warmup)
+        ests, stages = [], None
+        for k in range(warmup + steps):
+            out = np.zeros(7)
+            rc = f(xy.ctypes.data_as(dp), n, CFG["t"], CFG["m"], L, u.ctypes.data_as(dp), n_mom,
+                   n_tgt, 7 + k, cores, out.ctypes.data_as(dp))
+            if rc != 0:
+                raise RuntimeError("imqref_sample_time failed")
+            if k >= warmup:
+                ests.append(out[6])
+                stages = out
+        sec = sum(ests) / len(ests)
+        sample = (f"cfg4 exactly (N={n}, L={L}, c={CFG['t']}, p={CFG['m']}, u=random_vector(N,1000)): "
+                  f"the reference's compute_moments over {int(stages[3])} points of {n_mom} random "
+                  f"leaves, apply_far + apply_near onto {int(stages[4])} targets in 8x8-leaf tiles "
+                  f"({stages[5]:.3g} far pairs), each stage scaled by its exact work ratio; "
+                  f"{len(ests)} sample(s) after {warmup} warm-up; build excluded "
+                  f"(full-product record: profiles/r02_cfg4_reference_full.json)")
+        return dict(value=n / sec, unit=UNIT, cores=cores, kind="reference", sample=sample,
+                    sec_per_step=sec)
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from oracle import Oracle  # restatement (port) when the reference was not built
+    s = dict(n=262_144, t=0.01, m=16, levels=5, seed=0)
+    xy = inputs.uniform_points(s["n"], s["seed"])
+    O = Oracle()
     times = []
     for k in range(warmup + steps):
         t0 = time.perf_counter()
-        step(k)
-        dt = time.perf_counter() - t0
+        O.fast_matvec(xy, s["t"], s["m"], s["levels"], inputs.random_vector(s["n"], 1000 + k))
         if k >= warmup:
-            times.append(dt)
-    if h is not None:
-        R.destroy(h)
+            times.append(time.perf_counter() - t0)
     mean = sum(times) / len(times)
-    sample = (f"N={s['n']} uniform seed 0, c={s['t']}, p={s['m']}, L={s['levels']} "
-              f"(mean 64 pts/leaf like cfg 4), {len(times)} matvec(s) after {warmup} warm-up; "
-              f"operator build {setup:.2f}s excluded")
-    return dict(value=s["n"] / mean, unit=UNIT, cores=cores, kind=kind, sample=sample,
+    return dict(value=s["n"] / mean, unit=UNIT, cores=cores, kind="port",
+                sample=f"port (oracle/liboracle.so), N={s['n']}, L={s['levels']}, full products",
                 sec_per_step=mean)
 
 
@@ -174,7 +193,7 @@ def reference_arm(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": r["sec_per_step"] * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "cfg4-shaped CPU sample: " + r["sample"]},
+        "config": {"workload": "cfg4 CPU reference: " + r["sample"]},
         "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")},
         "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
@@ -292,6 +311,22 @@ def b200_arm(args):
     if world > 1:
         dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
     e2e_value = n / float(e2e_s.item())
+    # the same call with pageable host buffers (what a reference caller passes:
+    # std::vector memory, reference capi.cpp:130-138)
+    e2e_pageable = None
+    if world == 1:
+        page_u = [host_u[i].numpy() for i in range(2)]
+        page_b = np.empty(n)
+
+        def page_step(k):
+            P.capi.check(P.capi.lib().imq_operator_apply(
+                op.handle, page_u[k % 2].ctypes.data_as(P.api._dp),
+                page_b.ctypes.data_as(P.api._dp)))
+        page_step(0)
+        t0 = time.perf_counter()
+        for k in range(e2e_steps):
+            page_step(k)
+        e2e_pageable = n / ((time.perf_counter() - t0) / e2e_steps)
 
     # ---- roofline of the dominant kernel (M2P far field), timed live
     torch.index_select(dev_u[0], 0, perm, out=d_us)
@@ -346,12 +381,23 @@ def b200_arm(args):
             t0 = time.perf_counter()
             r = op2.solve(f2, 1e-8, args.gmres_iters, 50)
             gs = time.perf_counter() - t0
+            # SURVEY 8(d) protocol: iterations and time to each tolerance
+            # (separate solves with the reference's stopping rule)
+            to_tol = []
+            for tol in (1e-3, 5e-4, 2e-4):
+                t1 = time.perf_counter()
+                rt = op2.solve(f2, tol, args.gmres_iters, 50)
+                to_tol.append({"tol": tol, "iterations": rt.iterations,
+                               "time_s": time.perf_counter() - t1,
+                               "final_relative_residual": rt.final_relative_residual,
+                               "converged": rt.converged})
         cr = r.cycle_residuals
         gm = {"config": "cfg2: N=65536 uniform, c=0.05, p=12, L=auto(2), GMRES(50), x0=0",
               "tol": 1e-8, "max_iter": args.gmres_iters, "iterations": r.iterations,
               "time_s": gs, "ms_per_iteration": gs * 1e3 / max(1, r.iterations),
               "final_relative_residual": r.final_relative_residual,
-              "converged": r.converged,
+              "converged": r.converged, "to_tolerance": to_tol,
+              "reference_record": "profiles/r02_gmres_protocol.json",
               "cycle_residuals_head": cr[:6], "cycle_residuals_tail": cr[-3:]}
 
     if world > 1 and not args.no_gmres:
@@ -379,7 +425,7 @@ def b200_arm(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = run_cpu_reference(1, 0)
+        cpu = run_cpu_reference(1, 1)
         cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
 
     if rank == 0:
@@ -402,7 +448,8 @@ def b200_arm(args):
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * n * world,
                     "d2h_bytes_per_step": 8 * n,
                     "path": "imq_operator_apply (C ABI, pinned host u/b)" if world == 1 else
-                            "sharded ext API, pinned host buffers"},
+                            "sharded ext API, pinned host buffers",
+                    "pageable": e2e_pageable},
             "roofline": {"bound": "fp64",
                          "kernel": "k_m2p_far (M2P far field: direct for the fine levels, at "
                                    "Chebyshev nodes for levels 1..%d%s) + k_cheb_*"
