@@ -136,3 +136,20 @@ def test_config2_gmres_iteration_matched(imq, oracle):
     cr, rr = np.array(r.cycle_residuals), ref["cycle_residuals"]
     assert cr.size == rr.size
     assert np.max(np.abs(cr - rr) / rr) <= 1e-6
+    # the coefficient vector against the REFERENCE's own c at matched caps
+    # (tests/golden/cfg2_ref_it*.npz, make_golden_big.py; BASELINE config 2):
+    # measured 4.9e-10 (100 iterations) and 7.6e-8 (2,000), where GMRES has
+    # amplified the last-bit differences of the products for 40 cycles
+    import os
+    from conftest import GOLDEN
+    for cap, bound in ((100, 1e-8), (2000, 1e-6)):
+        g = np.load(os.path.join(GOLDEN, f"cfg2_ref_it{cap}.npz"))
+        rc = r if cap == 100 else op.solve(f, 1e-8, cap, 50)
+        assert rc.iterations == int(g["iterations"]) == cap
+        assert abs(rc.final_relative_residual - float(g["res"])) <= 1e-6 * float(g["res"])
+        assert float(np.max(np.abs(rc.c - g["c"])) / np.max(np.abs(g["c"]))) <= bound, cap
+    # iterations to each tolerance of the protocol equal the reference's (87,
+    # 182, 691: profiles/r02_gmres_protocol.json)
+    for tol, its in ((1e-3, 87), (5e-4, 182), (2e-4, 691)):
+        rt = op.solve(f, tol, 2000, 50)
+        assert rt.converged and rt.iterations == its, (tol, rt.iterations)
