@@ -313,8 +313,25 @@ def b200_arm(args):
     e2e_value = n / float(e2e_s.item())
     # the same call with pageable host buffers (what a reference caller passes:
     # std::vector memory, reference capi.cpp:130-138)
-    e2e_pageable = None
+    e2e_pageable = e2e_batch = None
     if world == 1:
+        # the repeated-product workload through imq_ext_operator_apply_batch:
+        # all nb host vectors in one call, copies pipelined with the products
+        nb = max(3, min(args.steps, 8))
+        bat_u = torch.empty((nb, n), dtype=torch.float64, pin_memory=True)
+        bat_b = torch.empty((nb, n), dtype=torch.float64, pin_memory=True)
+        for k in range(nb):
+            bat_u[k].copy_(host_u[k % nvec])
+
+        def batch_call():
+            P.capi.check(P.capi.lib().imq_ext_operator_apply_batch(
+                op.handle, nb, P.api.C.cast(bat_u.data_ptr(), P.api._dp),
+                P.api.C.cast(bat_b.data_ptr(), P.api._dp)))
+        batch_call()
+        t0 = time.perf_counter()
+        batch_call()
+        e2e_batch = nb * n / (time.perf_counter() - t0)
+        del bat_u, bat_b
         page_u = [host_u[i].numpy() for i in range(2)]
         page_b = np.empty(n)
 
@@ -449,7 +466,10 @@ def b200_arm(args):
                     "d2h_bytes_per_step": 8 * n,
                     "path": "imq_operator_apply (C ABI, pinned host u/b)" if world == 1 else
                             "sharded ext API, pinned host buffers",
-                    "pageable": e2e_pageable},
+                    "pageable": e2e_pageable,
+                    "batch": e2e_batch,
+                    "batch_path": "imq_ext_operator_apply_batch, pinned host U/B, copies "
+                                  "pipelined with the products (same bytes per product)"},
             "roofline": {"bound": "fp64",
                          "kernel": "k_m2p_far (M2P far field: direct for the fine levels, at "
                                    "Chebyshev nodes for levels 1..%d%s) + k_cheb_*"

@@ -129,6 +129,13 @@ IMQ_API int imq_verify(const imq_verify_config* cfg, imq_verify_callback cb, voi
  * workspace: issue them on one stream (or synchronise between streams). */
 IMQ_API int imq_ext_operator_apply_device(const imq_operator* op, const double* d_u, double* d_b,
                                   void* stream);
+/* Multi-RHS product: b_k = A u_k for k < nrhs, host vectors
+ * in original point order, U and B row-major nrhs x n (pinned or pageable).
+ * The products run in a pipeline: the copy-in of u_{k+1} and the copy-out
+ * of b_{k-1} overlap the product of u_k; results equal imq_operator_apply's
+ * bit for bit. */
+IMQ_API int imq_ext_operator_apply_batch(const imq_operator* op, int nrhs, const double* U,
+                                         double* B);
 /* Same on vectors already permuted into the operator's Morton order. */
 IMQ_API int imq_ext_operator_apply_sorted_device(const imq_operator* op, const double* d_us,
                                          double* d_bs, void* stream);

@@ -236,6 +236,16 @@ class FastOperator:
 
     __call__ = apply
 
+    def apply_batch(self, U) -> np.ndarray:
+        """imq_ext_operator_apply_batch: rows of U (nrhs x N, host) -> rows of B,
+        products pipelined with their host copies."""
+        U = np.ascontiguousarray(np.atleast_2d(U), dtype=np.float64)
+        if U.shape[1] != self.size:
+            raise IMQError(capi.IMQ_ERR_INVALID_ARG, "apply_batch: length mismatch")
+        B = np.empty_like(U)
+        check(lib().imq_ext_operator_apply_batch(self._h, U.shape[0], _ptr(U), _ptr(B)))
+        return B
+
     def apply_device(self, d_u, d_b, stream=None) -> None:
         """Device pointers (ints or torch CUDA tensors), original point order."""
         check(lib().imq_ext_operator_apply_device(self._h, _addr(d_u), _addr(d_b),

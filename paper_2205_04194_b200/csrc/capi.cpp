@@ -204,6 +204,15 @@ int imq_operator_apply(const imq_operator* op, const double* u, double* b_out) {
   });
 }
 
+int imq_ext_operator_apply_batch(const imq_operator* op, int nrhs, const double* U, double* B) {
+  if (!op || !U || !B) return fail(IMQ_ERR_INVALID_ARG, "imq_ext_operator_apply_batch: null argument");
+  if (nrhs < 1) return fail(IMQ_ERR_INVALID_ARG, "imq_ext_operator_apply_batch: nrhs must be >= 1");
+  return guard([&] {
+    op->op->apply_batch(nrhs, U, B);
+    return IMQ_OK;
+  });
+}
+
 int imq_dense_matvec(const double* xy, size_t n, double t, const double* u, double* b_out) {
   if (!xy || !u || !b_out || n == 0)
     return fail(IMQ_ERR_INVALID_ARG, "imq_dense_matvec: null argument or empty point set");

@@ -18,6 +18,7 @@
 #include <cstring>
 #include <new>
 #include <stdexcept>
+#include <thread>
 
 #include "host_math.hpp"
 #include "imq_device.cuh"
@@ -134,6 +135,26 @@ void DeviceOperator::release() {
   dfree(d_xboxes_);
   dfree(solve_ws_);
   solve_ws_bytes_ = 0;
+  dfree(d_u2_);
+  dfree(d_b2_);
+  for (int sl = 0; sl < 2; ++sl) {
+    if (pin_in_[sl]) cudaFreeHost(pin_in_[sl]);
+    if (pin_out_[sl]) cudaFreeHost(pin_out_[sl]);
+    pin_in_[sl] = pin_out_[sl] = nullptr;
+    for (cudaEvent_t e : ev_chunk_[sl]) cudaEventDestroy(e);
+    ev_chunk_[sl].clear();
+  }
+  pool_.reset();
+  if (cin_) {
+    cudaStreamSynchronize(cin_);
+    cudaStreamSynchronize(cout_);
+    cudaStreamDestroy(cin_);
+    cudaStreamDestroy(cout_);
+    for (cudaEvent_t e : {ev_io_start_, ev_in_[0], ev_in_[1], ev_gath_[0], ev_gath_[1], ev_done_[0],
+                          ev_done_[1], ev_out_[0], ev_out_[1]})
+      if (e) cudaEventDestroy(e);
+    cin_ = cout_ = nullptr;
+  }
   if (solve_pin_) cudaFreeHost(solve_pin_);
   solve_pin_ = nullptr;
   solve_pin_bytes_ = 0;
@@ -1487,17 +1508,133 @@ void DeviceOperator::apply_device(const double* d_u, double* d_b, cudaStream_t s
   cuda_check(cudaGetLastError(), "apply_device launch");
 }
 
-void DeviceOperator::apply_host(const double* u, double* b) {
+void DeviceOperator::apply_host(const double* u, double* b) { apply_batch(1, u, b); }
+
+// Host vectors (imq_operator_apply semantics), nrhs products in a pipeline:
+// the copy-in of u_{k+1} (copy engine 1) and the copy-out of b_{k-1} (copy
+// engine 2) overlap the product of u_k (SMs).  Device input / output
+// buffers are double-buffered.  Pageable host buffers (what a reference
+// caller passes: std::vector memory, capi.cpp:130-138) are staged through
+// pinned buffers in kIoChunk pieces by a thread pool, each piece's DMA
+// overlapping the CPU copy of the next.  Results are identical to
+// apply_device's (the same kernels on the same data).
+void DeviceOperator::io_setup(bool pin_in, bool pin_out, bool two_slots) {
+  if (!cin_) {
+    cuda_check(cudaStreamCreateWithFlags(&cin_, cudaStreamNonBlocking), "stream create");
+    cuda_check(cudaStreamCreateWithFlags(&cout_, cudaStreamNonBlocking), "stream create");
+    for (cudaEvent_t* e : {&ev_io_start_, &ev_in_[0], &ev_in_[1], &ev_gath_[0], &ev_gath_[1],
+                           &ev_done_[0], &ev_done_[1], &ev_out_[0], &ev_out_[1]})
+      cuda_check(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "event create");
+  }
+  const size_t bytes = (size_t)N_ * sizeof(double);
+  const int slots = two_slots ? 2 : 1;
+  if (two_slots && !d_u2_) {
+    d_u2_ = dalloc<double>((size_t)N_, "u (second slot)");
+    d_b2_ = dalloc<double>((size_t)N_, "b (second slot)");
+  }
+  auto pinned = [&](double*& p) {
+    if (!p) {
+      void* q = nullptr;
+      cuda_check(cudaHostAlloc(&q, bytes, cudaHostAllocDefault), "pinned staging");
+      p = static_cast<double*>(q);
+    }
+  };
+  for (int sl = 0; sl < slots; ++sl) {
+    if (pin_in) pinned(pin_in_[sl]);
+    if (pin_out) {
+      pinned(pin_out_[sl]);
+      const size_t nch = (bytes + kIoChunk - 1) / kIoChunk;
+      while (ev_chunk_[sl].size() < nch) {
+        cudaEvent_t e;
+        cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event create");
+        ev_chunk_[sl].push_back(e);
+      }
+    }
+  }
+  if ((pin_in || pin_out) && !pool_) {
+    const unsigned hw = std::thread::hardware_concurrency();
+    pool_ = std::make_unique<CopyPool>((int)std::max(1u, std::min(8u, hw ? hw : 1u)));
+  }
+}
+
+void DeviceOperator::apply_batch(int nrhs, const double* U, double* B) {
+  if (nrhs < 1) throw std::invalid_argument("apply_batch: nrhs must be >= 1");
   std::lock_guard<std::mutex> lk(mtx_);
   DeviceGuard g(device_);
   cudaStream_t s = stream_;
   Ordered o(*this, s);
-  cuda_check(cudaMemcpyAsync(d_u_, u, (size_t)N_ * sizeof(double), cudaMemcpyHostToDevice, s),
-             "H2D u");
-  imqk::launch_gather(d_u_, d_perm_, N_, d_us_, s);
-  apply_sorted_locked(d_us_, d_b_, d_perm_, s);
-  cuda_check(cudaMemcpyAsync(b, d_b_, (size_t)N_ * sizeof(double), cudaMemcpyDeviceToHost, s),
-             "D2H b");
+  const size_t n = (size_t)N_, bytes = n * sizeof(double);
+  const bool pu = host_pinned(U), pb = host_pinned(B);
+  io_setup(!pu, !pb, nrhs > 1);
+  double* du[2] = {d_u_, nrhs > 1 ? d_u2_ : d_u_};
+  double* db[2] = {d_b_, nrhs > 1 ? d_b2_ : d_b_};
+  const size_t nch = (bytes + kIoChunk - 1) / kIoChunk;
+  auto piece = [&](size_t c, size_t& off, size_t& len) {
+    off = c * kIoChunk;
+    len = std::min(kIoChunk, bytes - off);
+  };
+  // everything queued on s before this call precedes the copies
+  cuda_check(cudaEventRecord(ev_io_start_, s), "io start");
+  cuda_check(cudaStreamWaitEvent(cin_, ev_io_start_, 0), "io wait");
+  cuda_check(cudaStreamWaitEvent(cout_, ev_io_start_, 0), "io wait");
+  auto drain = [&](int j) {  // pageable output of product j
+    const int sj = j & 1;
+    char* dst = reinterpret_cast<char*>(B + (size_t)j * n);
+    const char* src = reinterpret_cast<const char*>(pin_out_[sj]);
+    for (size_t c = 0; c < nch; ++c) {
+      size_t off, len;
+      piece(c, off, len);
+      cuda_check(cudaEventSynchronize(ev_chunk_[sj][c]), "D2H chunk");
+      pool_->copy(dst + off, src + off, len);
+    }
+  };
+  for (int k = 0; k < nrhs; ++k) {
+    const int sl = k & 1;
+    const double* src = U + (size_t)k * n;
+    // d_u[sl] was last read by the gather of product k - 2
+    cuda_check(cudaStreamWaitEvent(cin_, ev_gath_[sl], 0), "slot wait");
+    if (pu) {
+      cuda_check(cudaMemcpyAsync(du[sl], src, bytes, cudaMemcpyHostToDevice, cin_), "H2D u");
+    } else {
+      cuda_check(cudaEventSynchronize(ev_in_[sl]), "staging wait");  // pin_in[sl] free
+      const char* hs = reinterpret_cast<const char*>(src);
+      char* ps = reinterpret_cast<char*>(pin_in_[sl]);
+      char* ds = reinterpret_cast<char*>(du[sl]);
+      for (size_t c = 0; c < nch; ++c) {
+        size_t off, len;
+        piece(c, off, len);
+        pool_->copy(ps + off, hs + off, len);
+        cuda_check(cudaMemcpyAsync(ds + off, ps + off, len, cudaMemcpyHostToDevice, cin_), "H2D u");
+      }
+    }
+    cuda_check(cudaEventRecord(ev_in_[sl], cin_), "event");
+    cuda_check(cudaStreamWaitEvent(s, ev_in_[sl], 0), "event");
+    imqk::launch_gather(du[sl], d_perm_, N_, d_us_, s);
+    cuda_check(cudaEventRecord(ev_gath_[sl], s), "event");
+    cuda_check(cudaStreamWaitEvent(s, ev_out_[sl], 0), "event");  // d_b[sl] copied out
+    apply_sorted_locked(d_us_, db[sl], d_perm_, s);
+    cuda_check(cudaEventRecord(ev_done_[sl], s), "event");
+    cuda_check(cudaStreamWaitEvent(cout_, ev_done_[sl], 0), "event");
+    if (pb) {
+      cuda_check(cudaMemcpyAsync(B + (size_t)k * n, db[sl], bytes, cudaMemcpyDeviceToHost, cout_),
+                 "D2H b");
+    } else {
+      char* ps = reinterpret_cast<char*>(pin_out_[sl]);
+      const char* ds = reinterpret_cast<const char*>(db[sl]);
+      for (size_t c = 0; c < nch; ++c) {
+        size_t off, len;
+        piece(c, off, len);
+        cuda_check(cudaMemcpyAsync(ps + off, ds + off, len, cudaMemcpyDeviceToHost, cout_), "D2H b");
+        cuda_check(cudaEventRecord(ev_chunk_[sl][c], cout_), "event");
+      }
+    }
+    cuda_check(cudaEventRecord(ev_out_[sl], cout_), "event");
+    cuda_check(cudaGetLastError(), "apply kernels");
+    if (!pb && k >= 1) drain(k - 1);
+  }
+  if (!pb) drain(nrhs - 1);
+  cuda_check(cudaStreamSynchronize(cout_), "apply");
+  cuda_check(cudaStreamSynchronize(cin_), "apply");
   cuda_check(cudaStreamSynchronize(s), "apply");
   cuda_check(cudaGetLastError(), "apply kernels");
 }

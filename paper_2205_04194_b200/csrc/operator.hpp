@@ -14,6 +14,9 @@
 #include <string>
 #include <vector>
 
+#include <memory>
+
+#include "hostio.hpp"
 #include "imq_kernels.hpp"
 
 namespace imqh {
@@ -100,8 +103,12 @@ class DeviceOperator {
   int device() const { return device_; }
   const double* square() const { return sq_; }
 
-  // Host vectors in original point order (imq_operator_apply semantics).
+  // Host vectors in original point order (imq_operator_apply semantics);
+  // pinned or pageable.
   void apply_host(const double* u, double* b);
+  // nrhs host vectors (U: nrhs x N, B: nrhs x N, original order) in a
+  // copy / compute pipeline (imq_ext_operator_apply_batch).
+  void apply_batch(int nrhs, const double* U, double* B);
   // Device vectors in original order; enqueued on `stream` (0 = the legacy
   // default stream, as everywhere in CUDA), no host synchronisation.
   void apply_device(const double* d_u, double* d_b, cudaStream_t stream);
@@ -308,6 +315,18 @@ class DeviceOperator {
   int* d_contrib_off_ = nullptr;
   int* d_contrib_ = nullptr;
   double* d_near_s_ = nullptr;
+  // host I/O (apply_batch): copy streams, second device slot, pinned staging
+  static constexpr size_t kIoChunk = (size_t)8 << 20;
+  void io_setup(bool pin_in, bool pin_out, bool two_slots);
+  cudaStream_t cin_ = nullptr, cout_ = nullptr;
+  cudaEvent_t ev_io_start_ = nullptr, ev_in_[2] = {}, ev_gath_[2] = {}, ev_done_[2] = {},
+              ev_out_[2] = {};
+  std::vector<cudaEvent_t> ev_chunk_[2];
+  double* d_u2_ = nullptr;
+  double* d_b2_ = nullptr;
+  double* pin_in_[2] = {nullptr, nullptr};
+  double* pin_out_[2] = {nullptr, nullptr};
+  std::unique_ptr<CopyPool> pool_;
   void* solve_ws_ = nullptr;  // GMRES device workspace (cached, grown on demand)
   size_t solve_ws_bytes_ = 0;
   void* solve_pin_ = nullptr;  // pinned GMRES staging (Hessenberg columns, flags)

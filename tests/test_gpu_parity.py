@@ -418,3 +418,34 @@ def test_device_applies_on_different_streams_do_not_race(imq, kind):
     torch.cuda.synchronize()
     for k in range(2):
         assert torch.equal(outs[k], want[k])
+
+
+def test_batch_and_pageable_host_paths_bitwise(imq):
+    """imq_ext_operator_apply_batch (copy / compute pipeline, f4) and the
+    pageable-buffer staging of imq_operator_apply give the same bits as the
+    pinned single product, at a size with several staging chunks."""
+    torch = pytest.importorskip("torch")
+    from paper_2205_04194_b200 import inputs
+    n = 1 << 21
+    xy = inputs.uniform_points(n, 0)
+    U = np.stack([inputs.random_vector(n, 100 + k) for k in range(3)])
+    with imq.FastOperator(xy, 0.02, 12, 6) as op:
+        ref = []
+        pin_u = torch.empty(n, dtype=torch.float64).pin_memory()
+        pin_b = torch.empty(n, dtype=torch.float64).pin_memory()
+        for k in range(3):
+            pin_u.copy_(torch.from_numpy(U[k]))
+            imq.capi.check(imq.capi.lib().imq_operator_apply(
+                op.handle, imq.api.C.cast(pin_u.data_ptr(), imq.api._dp),
+                imq.api.C.cast(pin_b.data_ptr(), imq.api._dp)))
+            ref.append(pin_b.numpy().copy())
+        ref = np.stack(ref)
+        assert np.array_equal(op.apply(U[1]), ref[1])          # pageable single
+        assert np.array_equal(op.apply_batch(U), ref)          # pageable batch
+        PU = torch.from_numpy(U).pin_memory()
+        PB = torch.empty_like(PU).pin_memory()
+        imq.capi.check(imq.capi.lib().imq_ext_operator_apply_batch(
+            op.handle, 3, imq.api.C.cast(PU.data_ptr(), imq.api._dp),
+            imq.api.C.cast(PB.data_ptr(), imq.api._dp)))
+        assert np.array_equal(PB.numpy(), ref)                 # pinned batch
+        assert np.array_equal(op.apply_batch(U[:1]), ref[:1])  # one row
