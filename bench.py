@@ -239,7 +239,7 @@ def b200_arm(args):
     if world > 1:
         from paper_2205_04194_b200.parallel import ShardedOperator
         sh = ShardedOperator(op, rank, world)   # far/near restricted to own targets
-        owned = torch.from_numpy(sh.owned_original_indices().astype(np.int64)).cuda()
+        halo = sh.enable_halo()                 # collective: the halo all-to-all plan
         share = (sh.hi - sh.lo) / n
     far_items, near_items = len(op.items("far")), len(op.items("near"))
 
@@ -251,11 +251,18 @@ def b200_arm(args):
     d_us = torch.empty_like(d_b)
     perm = torch.from_numpy(op.permutation().astype(np.int64)).cuda()
 
+    if world > 1:
+        # each rank holds only its Morton segment of every vector (the
+        # distributed layout of the sharded GMRES); a product exchanges the
+        # halo (all-to-all) and all-reduces the coarse moments
+        seg_u = [dev_u[k][perm[sh.lo:sh.hi]].contiguous() for k in range(nvec)]
+        seg_b = torch.empty(sh.hi - sh.lo, dtype=torch.float64, device="cuda")
+
     def step(k):
         if world == 1:
             op.apply_device(dev_u[k % nvec], d_b, stream)
         else:
-            sh.apply_device(dev_u[k % nvec], d_b, stream)
+            sh.apply_segment(seg_u[k % nvec], seg_b, stream)
 
     def barrier():
         if world > 1:
@@ -292,12 +299,10 @@ def b200_arm(args):
             P.capi.check(P.capi.lib().imq_operator_apply(
                 op.handle, P.api.C.cast(pin_u[k % 2].data_ptr(), P.api._dp),
                 P.api.C.cast(pin_b.data_ptr(), P.api._dp)))
-        else:
-            d_u = dev_u[0]
-            d_u.copy_(pin_u[k % 2], non_blocking=True)
-            sh.apply_device(d_u, d_b, stream)
-            mine = torch.index_select(d_b, 0, owned)
-            pin_b[:mine.numel()].copy_(mine, non_blocking=True)
+        else:  # this rank's segment in and out (host, pinned)
+            seg_u[0].copy_(pin_u[k % 2][:sh.hi - sh.lo], non_blocking=True)
+            sh.apply_segment(seg_u[0], seg_b, stream)
+            pin_b[:sh.hi - sh.lo].copy_(seg_b, non_blocking=True)
             torch.cuda.synchronize()
 
     e2e_step(0)
@@ -462,10 +467,13 @@ def b200_arm(args):
                        "far_pairs": st["far_pairs"], "near_pairs": st["near_pairs"],
                        "setup_s": setup_s, "l2": "inputs larger than L2 (no flush)",
                        "parallelism": f"points sharded {world}-way (Morton ranges)"},
-            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * n * world,
+            "e2e": {"value": e2e_value, "unit": UNIT,
+                    "h2d_bytes_per_step": 8 * n,
                     "d2h_bytes_per_step": 8 * n,
                     "path": "imq_operator_apply (C ABI, pinned host u/b)" if world == 1 else
-                            "sharded ext API, pinned host buffers",
+                            "sharded segments (each rank its Morton range of u and b), pinned "
+                            "host buffers",
+                    "halo_bytes_received_rank0": halo.bytes_received if world > 1 else 0,
                     "pageable": e2e_pageable,
                     "batch": e2e_batch,
                     "batch_path": "imq_ext_operator_apply_batch, pinned host U/B, copies "

@@ -250,6 +250,11 @@ IMQ_API int imq_ext_shard_bounds(const int* leaf_start, int levels, int world, i
 IMQ_API int imq_ext_shard_bounds_work(const int* leaf_start, int levels, int m, int world,
                                       int* bounds_out);
 IMQ_API int imq_ext_operator_restrict(const imq_operator* op, int sorted_lo, int sorted_hi);
+/* After imq_ext_operator_restrict: the non-empty finest leaves (Morton keys,
+ * ascending) whose source values the rank's moments and near field read --
+ * its own leaves and its halo.  out may be NULL (count only). */
+IMQ_API int imq_ext_operator_local_leaves(const imq_operator* op, int* out, size_t capacity,
+                                          size_t* count);
 
 /* Measured FP64 FMA-pipe throughput (TFLOP/s) of the current device: the
  * roofline denominator of the FP64-bound far-field kernel. */

@@ -665,6 +665,18 @@ int imq_ext_operator_items(const imq_operator* op, int which, int* items_xyzw, s
   return IMQ_OK;
 }
 
+int imq_ext_operator_local_leaves(const imq_operator* op, int* out, size_t capacity,
+                                  size_t* count) {
+  if (!op || !count) return fail(IMQ_ERR_INVALID_ARG, "imq_ext_operator_local_leaves: null argument");
+  const std::vector<int>& v = op->op->local_leaves_host();
+  *count = v.size();
+  if (out) {
+    if (capacity < v.size()) return fail(IMQ_ERR_INVALID_ARG, "imq_ext_operator_local_leaves: capacity too small");
+    std::memcpy(out, v.data(), v.size() * sizeof(int));
+  }
+  return IMQ_OK;
+}
+
 int imq_ext_operator_far_near(const imq_operator* op, const double* d_us, double* d_bs,
                               int far_begin, int far_end, int near_begin, int near_end,
                               int scatter, void* stream) {

@@ -174,6 +174,9 @@ class DeviceOperator {
   cudaStream_t stream() const { return stream_; }
   const std::vector<int4>& far_items_host() const { return far_items_h_; }
   const std::vector<int4>& near_items_host() const { return near_items_h_; }
+  // restricted operators: the non-empty leaves whose u the rank reads (own +
+  // halo), Morton order; empty when unrestricted
+  const std::vector<int>& local_leaves_host() const { return local_leaves_h_; }
 
  private:
   // Device-side ordering of every entry point that touches the operator's
