@@ -256,6 +256,13 @@ IMQ_API int imq_ext_operator_restrict(const imq_operator* op, int sorted_lo, int
 IMQ_API int imq_ext_operator_local_leaves(const imq_operator* op, int* out, size_t capacity,
                                           size_t* count);
 
+/* Self-check of the device enumeration (imq_verify "exact_cover"): every far
+ * pass of the operator (single pass, coarse / fine / per-leaf partial, or
+ * Chebyshev node / ring / X-ring items) replayed for up to max_targets
+ * targets against the reference interaction lists (partition.cpp:56-72).
+ * out5 = {targets, missing, duplicated, extra, max entries per target}. */
+IMQ_API int imq_ext_operator_check_lists(const imq_operator* op, int max_targets, long long* out5);
+
 /* Measured FP64 FMA-pipe throughput (TFLOP/s) of the current device: the
  * roofline denominator of the FP64-bound far-field kernel. */
 IMQ_API int imq_ext_fp64_peak(int iters, double* tflops, double* ms);

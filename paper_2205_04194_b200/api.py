@@ -276,6 +276,13 @@ class FastOperator:
         out["cert_by_kind"] = list(out["cert_by_kind"])
         return out
 
+    def check_lists(self, max_targets: int = 4096) -> dict:
+        """imq_ext_operator_check_lists: the device far-list enumeration of every
+        pass vs the reference interaction lists."""
+        o = (C.c_longlong * 5)()
+        check(lib().imq_ext_operator_check_lists(self._h, max_targets, o))
+        return dict(zip(("targets", "missing", "duplicated", "extra", "max_entries"), list(o)))
+
     def solve(self, f, tol: float = 1e-8, max_iter: int = 500, restart: int = 100) -> SolveReport:
         """imq_iterative_solve (solver.cpp:41-159) with the cycle residual history."""
         f = _f64(f)

@@ -112,6 +112,7 @@ _SIGS = {
     "imq_ext_shard_bounds": (C.c_int, [_ip, C.c_int, C.c_int, _ip]),
     "imq_ext_shard_bounds_work": (C.c_int, [_ip, C.c_int, C.c_int, C.c_int, _ip]),
     "imq_ext_operator_restrict": (C.c_int, [_vp, C.c_int, C.c_int]),
+    "imq_ext_operator_check_lists": (C.c_int, [_vp, C.c_int, C.POINTER(C.c_longlong)]),
     "imq_ext_operator_local_leaves": (C.c_int, [_vp, _ip, C.c_size_t, C.POINTER(C.c_size_t)]),
     "imq_ext_fp64_peak": (C.c_int, [C.c_int, _dp, _dp]),
     "imq_ext_device_count": (C.c_int, [_ip]),

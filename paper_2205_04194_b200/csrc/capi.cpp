@@ -376,32 +376,42 @@ int imq_verify(const imq_verify_config* cfg, imq_verify_callback cb, void* user_
     const imqh::Separation sep0 = imqh::verify_separation(op.square(), op.levels(), 0.0);
     report("separation_ratio_planar", sep0.valid, sep0.max_ratio);
     {
-      // list sizes of the uniform grid: <= 12 at level 1, <= 27 below, near <= 9
+      // list sizes of every block of every level (partition.cpp:56-83: the
+      // reference counts its built slist / near_lists, empty blocks included):
+      // the 6 x 6 candidate window of the parent's neighbourhood (level 1: the
+      // whole 4 x 4 grid) minus the Chebyshev-distance < 2 part; near lists are
+      // the clipped 3 x 3 neighbourhoods of the finest level
       int max_far = 0, max_near = 0;
       bool within = true;
       for (int l = 1; l <= op.levels(); ++l) {
         const int grid = 1 << (l + 1), cap = l == 1 ? 12 : 27;
-        for (int i = 0; i < std::min(grid, 8); ++i)
-          for (int j = 0; j < std::min(grid, 8); ++j) {
-            int c = 0;
-            for (int qi = 0; qi < grid; ++qi)
-              for (int qj = 0; qj < grid; ++qj) {
-                if (std::max(std::abs(qi - i), std::abs(qj - j)) < 2) continue;
-                if (l >= 2 && std::max(std::abs(qi / 2 - i / 2), std::abs(qj / 2 - j / 2)) > 1)
-                  continue;
-                ++c;
-              }
+        for (int i = 0; i < grid; ++i)
+          for (int j = 0; j < grid; ++j) {
+            const int li = l == 1 ? 0 : std::max(0, 2 * (i / 2) - 2);
+            const int hi = l == 1 ? grid - 1 : std::min(grid - 1, 2 * (i / 2) + 3);
+            const int lj = l == 1 ? 0 : std::max(0, 2 * (j / 2) - 2);
+            const int hj = l == 1 ? grid - 1 : std::min(grid - 1, 2 * (j / 2) + 3);
+            const int win = (hi - li + 1) * (hj - lj + 1);
+            const int ni = std::min(grid - 1, i + 1) - std::max(0, i - 1) + 1;
+            const int nj = std::min(grid - 1, j + 1) - std::max(0, j - 1) + 1;
+            const int c = win - ni * nj;  // the 3 x 3 neighbourhood lies inside the window
             max_far = std::max(max_far, c);
             if (c > cap) within = false;
+            if (l == op.levels()) max_near = std::max(max_near, ni * nj);
           }
       }
-      max_near = op.levels() >= 1 ? 9 : 0;
+      if (max_near > 9) within = false;
       report("interaction_counts", within, (double)std::max(max_far, max_near));
     }
     {
       const size_t nsub = std::min<size_t>(cfg->n, 200);
       int dev = 0;
       for (int L = 1; L <= 3; ++L) dev = std::max(dev, exact_cover_deviation(cfg->xy, nsub, L));
+      // the device enumeration: every far pass of this operator replayed per
+      // target (k_far_cover) must produce each reference list entry exactly
+      // once (all targets up to 4096, else 4096 spread over the set)
+      const imqh::ListCheck lc = op.far_list_check(4096);
+      dev = std::max(dev, lc.max_deviation);
       report("exact_cover", dev == 0, (double)dev);
     }
     {
@@ -663,6 +673,20 @@ int imq_ext_operator_items(const imq_operator* op, int which, int* items_xyzw, s
     std::memcpy(items_xyzw, v.data(), v.size() * sizeof(int4));
   }
   return IMQ_OK;
+}
+
+int imq_ext_operator_check_lists(const imq_operator* op, int max_targets, long long* out5) {
+  if (!op || !out5 || max_targets < 1)
+    return fail(IMQ_ERR_INVALID_ARG, "imq_ext_operator_check_lists: bad argument");
+  return guard([&] {
+    const imqh::ListCheck r = op->op->far_list_check(max_targets);
+    out5[0] = r.targets;
+    out5[1] = r.missing;
+    out5[2] = r.duplicated;
+    out5[3] = r.extra;
+    out5[4] = r.max_entries;
+    return IMQ_OK;
+  });
 }
 
 int imq_ext_operator_local_leaves(const imq_operator* op, int* out, size_t capacity,

@@ -900,6 +900,88 @@ __device__ int build_far_list(const TreeParams& P, uint32_t par, int s, int cnt,
   return n;
 }
 
+// -------------------------------------------------------- list cover check --
+// imq_verify / tests: for each listed target, replays every far pass of the
+// product (modes from the operator: single pass, coarse + fine + per-leaf
+// partial, or Chebyshev node / ring / X-ring items) through build_far_list
+// exactly as the kernels call it, with the target as a one-point item, and
+// compares the (level, block) entries collected over all passes with the
+// reference's interaction lists (partition.cpp:56-72; non-empty source
+// blocks, fastmv.cpp:207): out = {missing, duplicated, extra, entries}.
+constexpr int kCoverWarps = 4, kCoverCap = 1024;
+__global__ void __launch_bounds__(kCoverWarps * 32) k_far_cover(const TreeParams P,
+                                                               const int* __restrict__ targets,
+                                                               int n_t, const CoverModes Mo,
+                                                               int4* __restrict__ out) {
+  __shared__ uint32_t lists[kCoverWarps][kMaxList];
+  __shared__ uint32_t got[kCoverWarps][kCoverCap];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int it = blockIdx.x * kCoverWarps + warp;
+  if (it >= n_t) return;
+  const int t = targets[it], L = P.L;
+  const uint32_t T = P.leaf[t], X = T >> 2;
+  int ng = 0, overflow = 0;
+  auto add = [&](uint32_t par, int lmin, int lmax, int ring, int lsplit) {
+    const int n = build_far_list(P, par, t, 1, lists[warp], lane, lmin, lmax, ring, lsplit);
+    for (int e = lane; e < n; e += 32)
+      if (ng + e < kCoverCap) got[warp][ng + e] = lists[warp][e];
+    if (ng + n > kCoverCap) overflow = 1;
+    ng = min(kCoverCap, ng + n);
+    __syncwarp();
+  };
+  if (!Mo.split) {
+    add(X, 1, L, 0, 0);
+  } else if (!Mo.cheb) {
+    add((X >> 2) << 2, 1, L - 2, 0, 0);
+    add(X, L - 1, L, 0, Mo.lsplit ? 1 : 0);
+    if (Mo.lsplit) add(X, L, L, 0, 2);
+  } else {
+    for (int l = 1; l <= Mo.lc; ++l) {
+      const uint32_t q = T >> (2 * (L - l));
+      add(q << (2 * (L - 1 - l)), l, l, (Mo.ring && l >= Mo.ring_l0) ? 1 : 0, 0);
+      if (Mo.ring && l + 1 >= Mo.ring_l0) add((4 * q) << (2 * (L - 2 - l)), l + 1, l + 1, 2, 0);
+    }
+    if (Mo.xring) {
+      add(X, L - 1, L, 1, 4);
+      add(X, L, L, 0, 2);
+    } else {
+      if (Mo.lsplit) add(X, L, L, 0, 2);
+      add(X, L - 1, L, Mo.ring ? 1 : 0, Mo.lsplit ? 1 : 0);
+    }
+  }
+  int missing = 0, dup = 0, matched = 0;
+  for (int l = 1; l <= L; ++l) {
+    int bi, bj;
+    demorton(T >> (2 * (L - l)), bi, bj);
+    const int grid = 1 << (l + 1);
+    int lo_i = 0, lo_j = 0, wi = grid, wj = grid;
+    if (l >= 2) {
+      lo_i = max(0, 2 * (bi >> 1) - 2);
+      lo_j = max(0, 2 * (bj >> 1) - 2);
+      wi = min(grid - 1, 2 * (bi >> 1) + 3) - lo_i + 1;
+      wj = min(grid - 1, 2 * (bj >> 1) + 3) - lo_j + 1;
+    }
+    for (int c = lane; c < wi * wj; c += 32) {
+      const int qi = lo_i + c / wj, qj = lo_j + c % wj;
+      if (max(abs(qi - bi), abs(qj - bj)) < 2) continue;
+      const uint32_t q = morton(qi, qj);
+      if (block_count(P, l, q) == 0) continue;
+      const uint32_t key = ((uint32_t)l << 28) | q;
+      int cnt = 0;
+      for (int e = 0; e < ng; ++e) cnt += got[warp][e] == key;
+      missing += cnt == 0;
+      dup += cnt > 1;
+      matched += cnt;
+    }
+  }
+  for (int d = 16; d; d >>= 1) {
+    missing += __shfl_xor_sync(0xffffffffu, missing, d);
+    dup += __shfl_xor_sync(0xffffffffu, dup, d);
+    matched += __shfl_xor_sync(0xffffffffu, matched, d);
+  }
+  if (lane == 0) out[it] = make_int4(missing, dup + overflow, ng - matched, ng);
+}
+
 // Complex Horner evaluation of one source block's expansion at R targets of
 // the lane.  c: K coefficients (double2) in Horner order.  Every coefficient
 // read from shared memory feeds 2R DFMAs; shared-memory -> register delivery
@@ -1487,6 +1569,13 @@ void launch_m2p_far(const TreeParams& P, const int4* items, const int* group_off
         break;
     }
   }
+}
+
+void launch_far_cover(const TreeParams& P, const int* targets, int n_t, const CoverModes& Mo,
+                      int4* out, cudaStream_t s) {
+  if (n_t > 0)
+    k_far_cover<<<(unsigned)((n_t + kCoverWarps - 1) / kCoverWarps), kCoverWarps * 32, 0, s>>>(
+        P, targets, n_t, Mo, out);
 }
 
 }  // namespace imqk

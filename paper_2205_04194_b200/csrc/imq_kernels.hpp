@@ -102,6 +102,19 @@ void launch_m2p_far(const TreeParams& P, const int4* items, const int* group_off
                     const double* far_add = nullptr, int lmin = 1, int lmax = 0,
                     int ring = 0, int lsplit = 0);
 bool m2p_specialised(int M);
+// The far passes' enumeration modes of an operator (k_far_cover replays them).
+struct CoverModes {
+  int split;    // coarse / fine passes (else one pass over levels 1..L)
+  int cheb;     // levels 1..lc through Chebyshev node items
+  int lc;       // last node-pass level (L - 2)
+  int ring;     // ring items on
+  int ring_l0;  // rings of levels ring_l0..L-1
+  int xring;    // X-ring items (level-(L-1) inner + level-L outer ring at X's nodes)
+  int lsplit;   // per-leaf partial pass
+};
+// out[i] = {missing, duplicated, extra, entries} of targets[i]'s far lists
+void launch_far_cover(const TreeParams& P, const int* targets, int n_t, const CoverModes& Mo,
+                      int4* out, cudaStream_t s);
 
 // ---- coarse far field by Chebyshev interpolation (cheb.cu)
 #ifndef IMQ_CHEB_N

@@ -1009,6 +1009,54 @@ void DeviceOperator::certify() {
   dfree(d_tail);
 }
 
+// Device list check (imq_verify "exact_cover", tests): the far passes'
+// enumeration replayed per target (k_far_cover) against the reference lists.
+ListCheck DeviceOperator::far_list_check(int max_targets) {
+  std::lock_guard<std::mutex> lk(mtx_);
+  DeviceGuard g(device_);
+  cuda_check(cudaStreamSynchronize(stream_), "list check");
+  cuda_check(cudaEventSynchronize(ev_last_), "list check");
+  ListCheck r;
+  const int lo = target_lo_, hi = target_hi_, n = hi - lo;
+  if (n <= 0) return r;
+  const int nt = std::max(1, std::min(n, max_targets));
+  std::vector<int> tg((size_t)nt);
+  for (int i = 0; i < nt; ++i) tg[(size_t)i] = lo + (int)(((long long)i * n) / nt);
+  imqk::CoverModes Mo{};
+  Mo.split = far_split_ ? 1 : 0;
+  Mo.cheb = cheb_ ? 1 : 0;
+  Mo.lc = cheb_lc_;
+  Mo.ring = cheb_ && ring_ ? 1 : 0;
+  Mo.ring_l0 = ring_l0_;
+  Mo.lsplit = n_lpart_items_ > 0 ? 1 : 0;
+  Mo.xring = cheb_ && ring_ && xring_ && n_lpart_items_ > 0 ? 1 : 0;
+  int* d_t = dalloc<int>((size_t)nt, "list check");
+  int4* d_o = dalloc<int4>((size_t)nt, "list check");
+  std::vector<int4> o((size_t)nt);
+  try {
+    cuda_check(cudaMemcpy(d_t, tg.data(), tg.size() * sizeof(int), cudaMemcpyHostToDevice), "H2D");
+    imqk::launch_far_cover(P_, d_t, nt, Mo, d_o, stream_);
+    cuda_check(cudaStreamSynchronize(stream_), "list check");
+    cuda_check(cudaGetLastError(), "list check kernel");
+    cuda_check(cudaMemcpy(o.data(), d_o, o.size() * sizeof(int4), cudaMemcpyDeviceToHost), "D2H");
+  } catch (...) {
+    dfree(d_t);
+    dfree(d_o);
+    throw;
+  }
+  dfree(d_t);
+  dfree(d_o);
+  r.targets = nt;
+  for (const int4& v : o) {
+    r.missing += v.x;
+    r.duplicated += v.y;
+    r.extra += v.z;
+    r.max_deviation = std::max(r.max_deviation, v.x + v.y + v.z);
+    r.max_entries = std::max(r.max_entries, v.w);
+  }
+  return r;
+}
+
 void DeviceOperator::restrict_targets(int p_lo, int p_hi) {
   std::lock_guard<std::mutex> lk(mtx_);
   DeviceGuard g(device_);

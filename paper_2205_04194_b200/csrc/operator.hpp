@@ -88,6 +88,13 @@ std::vector<double> parent_work(const std::vector<int>& leaf_start, int L, int M
 std::vector<int> shard_bounds_weighted(const std::vector<int>& leaf_start, int L, int world,
                                        const std::vector<double>& w);
 
+// Device far-list enumeration vs the reference lists (far_list_check).
+struct ListCheck {
+  long long targets = 0, missing = 0, duplicated = 0, extra = 0;
+  int max_deviation = 0;  // per target: missing + duplicated + extra
+  int max_entries = 0;    // (level, block) entries one target's far passes evaluate
+};
+
 class DeviceOperator {
  public:
   DeviceOperator(const double* xy_host, size_t n, double t, int M, int levels,
@@ -122,6 +129,9 @@ class DeviceOperator {
   void copy_leaf_start(std::vector<int>& out) const;
   PairCounts pair_counts();
   const CertReport& certificate() const { return cert_; }
+  // Replays every far pass's list enumeration for <= max_targets targets
+  // (all when N is smaller, else evenly spread) against the reference lists.
+  ListCheck far_list_check(int max_targets);
   // Restricts far/near evaluation to targets at sorted positions [lo, hi)
   // (sharded application); b entries of other targets are left untouched.
   void restrict_targets(int p_lo, int p_hi);

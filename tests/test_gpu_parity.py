@@ -449,3 +449,50 @@ def test_batch_and_pageable_host_paths_bitwise(imq):
             imq.api.C.cast(PB.data_ptr(), imq.api._dp)))
         assert np.array_equal(PB.numpy(), ref)                 # pinned batch
         assert np.array_equal(op.apply_batch(U[:1]), ref[:1])  # one row
+
+
+@pytest.mark.parametrize("case", ["single_pass", "split_no_cheb", "cheb_nodes", "cheb_rings",
+                                  "cheb_rings_xring", "clustered", "strip"])
+def test_device_list_enumeration_matches_reference_lists(imq, case):
+    """imq_verify's device check: every far pass of the operator (as built for
+    the case) replayed per target through build_far_list gives each reference
+    interaction-list entry (partition.cpp:56-72, non-empty blocks) exactly once
+    -- in every enumeration mode (single pass; coarse + fine + per-leaf
+    partial; Chebyshev node items; ring items; X-ring items)."""
+    from paper_2205_04194_b200 import inputs
+    rng = np.random.default_rng(17)
+    n1 = 1 << 20
+    cfg = {"single_pass": (inputs.uniform_points(4096, 0), 0.1, 10, 2, {}),
+           "split_no_cheb": (inputs.uniform_points(20000, 1), 0.05, 8, 4, {}),
+           "cheb_nodes": (inputs.uniform_points(n1, 0), 0.001, 16, 6, {"cheb_levels": 4, "cheb_ring": 0}),
+           "cheb_rings": (inputs.uniform_points(n1, 0), 0.02, 16, 6, {"cheb_ring": 1, "cheb_xring": 0}),
+           "cheb_rings_xring": (inputs.uniform_points(n1, 0), 0.04, 16, 6, {"cheb_ring": 1, "cheb_xring": 1}),
+           "clustered": (inputs.gaussian_mixture(n1, 1), 0.02, 14, 6, {"cheb_ring": 1}),
+           "strip": (np.stack([rng.random(n1), 0.3 + 0.01 * rng.random(n1)], 1).reshape(-1),
+                     0.05, 12, 6, {})}[case]
+    xy, t, m, L, want = cfg
+    with imq.FastOperator(xy, t, m, L) as op:
+        st = op.stats()
+        for k, v in want.items():
+            assert st[k] == v, (case, k, st[k])
+        r = op.check_lists(4096)
+    assert r["targets"] == min(4096, xy.size // 2)
+    assert r["missing"] == 0 and r["duplicated"] == 0 and r["extra"] == 0, (case, r)
+    assert r["max_entries"] > 0
+
+
+def test_square_bits_match_oracle(imq, oracle):
+    """The GPU bounding square (min/max reduction + host arithmetic,
+    partition.cpp:9-23) equals the oracle's bit for bit."""
+    from paper_2205_04194_b200 import inputs
+    rng = np.random.default_rng(4)
+    sets = [inputs.uniform_points(4096, 0), inputs.gaussian_mixture(50000, 1),
+            1000.0 * rng.random(6000) - 12345.0,
+            np.stack([rng.random(3000), 0.3 + 1e-7 * rng.random(3000)], 1).reshape(-1),
+            np.tile([0.3, 0.4], 12)]
+    for xy in sets:
+        with imq.FastOperator(xy, 0.1, 6, 2) as op:
+            st = op.stats()
+        o = oracle.bounding_square(xy)
+        got = (st["origin_x"], st["origin_y"], st["side"])
+        assert all(np.float64(a).tobytes() == np.float64(b).tobytes() for a, b in zip(got, o)), (got, o)
