@@ -1,0 +1,9 @@
+# Round-2 record: full GPU suite, bench (both arms), launch list, full ncu captures
+set -x
+python -m pytest tests -m gpu -q > gpurun_out/r02_pytest.log 2>&1
+python bench.py > gpurun_out/r02_bench.json 2> gpurun_out/r02_bench.err
+python bench.py --impl reference > gpurun_out/r02_bench_ref.json 2> gpurun_out/r02_bench_ref.err
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r02_launches.csv python tools/profile_step.py 4 > /dev/null 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"k_m2p_far|k_m2m_tr_s|k_p2p_near_sym|k_p2m_leaf|k_cheb_eval_mma" --launch-skip 0 --launch-count 40 -o gpurun_out/r02_full python tools/profile_step.py 4 > gpurun_out/r02_ncu_full.log 2>&1
+ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active --clock-control none --csv --log-file gpurun_out/r02_far_metrics.csv python tools/profile_step.py 4 > /dev/null 2>&1
+tail -3 gpurun_out/r02_pytest.log
