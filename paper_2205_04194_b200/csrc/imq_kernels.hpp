@@ -190,6 +190,30 @@ void launch_absmax(const double* x, long long n, double* out, cudaStream_t s);
 void launch_random_vector(double* out, long long n, unsigned long long seed, cudaStream_t s);
 int far_max_points_per_lane();
 
+// ---- far field at Chebyshev nodes as tensor-core GEMMs (nodegemm.cu)
+// One source offset of a box class: the source block at level `level` is the
+// box's cell (shifted to that level) + (dx, dy); A = the basis at every node
+// for that offset, k-major [k2pad][8 * ceil(n_nodes / 8)] (rows 2j, 2j+1 =
+// Re, -Im of the basis of Horner coefficient j).
+struct GemmDelta {
+  int level, dx, dy, pad;
+  const double* A;
+};
+// Box classes of one launch (boxes of class c: boxes[box_off[c] .. box_off[c+1]),
+// offsets deltas[c * n_deltas ..], CTAs [tile_off[c], tile_off[c+1]) of
+// node_gemm_tile() boxes each).
+struct GemmClasses {
+  int n;
+  int box_off[5];
+  int tile_off[5];
+};
+// out[box * n_nodes + n] = sum_delta Re sum_j Phi_delta[n][j] C_j(src(box, delta))
+void launch_node_gemm(const TreeParams& P, int box_level, const int* boxes,
+                      const GemmClasses& G, const GemmDelta* deltas, int n_deltas, int k2pad,
+                      const double2* coef, double* out, int n_nodes, cudaStream_t s);
+int node_gemm_k2pad(int K);
+int node_gemm_tile();
+
 // ---- direct interactions (direct.cu)
 // Near work items (one leaf each) grouped by points-per-lane like the far ones.
 void launch_p2p_near(const TreeParams& P, const int4* items, const int* group_off, int begin,

@@ -1,0 +1,235 @@
+// nodegemm.cu -- far field at Chebyshev nodes as GEMMs on the FP64 tensor
+// cores (mma.sync m8n8k4 f64).
+//
+// The nodes of every box of a level sit at the same positions relative to
+// the box, and a box's interaction list is a fixed set of offsets (clipped at
+// the domain edge, empty blocks contributing nothing).  So the field of the
+// source block at offset delta, evaluated at node n of ANY box, is
+//     V[n] = Re sum_j Phi_delta[n][j] C_j(src)
+// with the SAME basis Phi_delta[n][j] = rho^-1 conj(xi)^m q^(k-m) (the
+// reference's truncated expansion, fastmv.cpp:104-138, in the monomial form
+// of DESIGN.md §3; j over the Horner-ordered coefficients (m, k)).  The node
+// pass of a box class is then one GEMM per offset,
+//     V[n][box] += sum_k A_delta[k][n] B_delta[k][box],
+// A_delta = the basis (real form: rows 2j, 2j+1 = Re, -Im), B_delta = the
+// source coefficients of each box's delta-neighbour (Re, Im interleaved,
+// exactly the coefficient array).  This replaces the per-(node, source)
+// complex Horner of k_m2p_far (LDS-fed, ~76 % of the FP64 pipe) by dense
+// tensor-core tiles with no idle target slots; in real arithmetic it is the
+// same sum.
+//
+// CTA: 32 boxes x all nodes (MT m-tiles of 8), 4 warps as 2 box pairs x 2
+// node halves (each A fragment feeds two tensor-core ops); k in chunks of 16
+// (4 mma k-steps), A and B chunks in a 2-stage cp.async pipeline.  Measured
+// at config 4 (X-node pass, 65,536 boxes x 144 nodes x 27 offsets; ncu,
+// tensor pipe active): 32 boxes / k16 / 2 stages 5.33 ms (76.8 %), 64 / 16 /
+// 2 5.35 ms, 64 / 16 / 3 5.46 ms, 32 / 8 / 2 5.65 ms, 64 / 32 / 3 6.00 ms
+// (68 %), 32 / 16 / 3 6.59 ms, 16 / 16 / 2 7.34 ms (55 %); the Horner pass
+// it replaces took 6.96 ms.
+#include <algorithm>
+#include <stdexcept>
+
+#include "imq_device.cuh"
+#include "imq_kernels.hpp"
+
+#ifndef IMQ_GEMM_NB
+#define IMQ_GEMM_NB 32
+#endif
+#ifndef IMQ_GEMM_KC
+#define IMQ_GEMM_KC 16
+#endif
+#ifndef IMQ_GEMM_ST
+#define IMQ_GEMM_ST 2
+#endif
+
+namespace imqk {
+
+namespace {
+
+using namespace imqdev;
+
+// boxes per CTA (warps = kGtN / 8: box pairs x 2 node halves), k chunk, stages
+constexpr int kGtN = IMQ_GEMM_NB, kGtKC = IMQ_GEMM_KC, kGtWarps = kGtN / 8, kGtStages = IMQ_GEMM_ST;
+constexpr int kGtMaxDelta = 32;
+constexpr int kGtSBn = kGtKC + 4;  // B rows [box][k]: stride = 4 (mod 16)
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
+}
+// 16-byte async copy global -> shared; src_bytes = 0 zero-fills
+__device__ __forceinline__ void cp16(void* dst, const void* src, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src),
+               "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+__host__ __device__ constexpr int gemm_sa(int MT) {  // A rows [k][node]: stride = 4 (mod 16)
+  return 8 * MT + ((4 - (8 * MT) % 16) + 16) % 16;
+}
+constexpr size_t gemm_smem(int MT) {
+  return (size_t)kGtStages * kGtKC * gemm_sa(MT) * sizeof(double) +
+         (size_t)kGtStages * kGtN * kGtSBn * sizeof(double) +
+         (size_t)kGtMaxDelta * kGtN * sizeof(const double*);
+}
+
+__device__ __forceinline__ int gemm_block_count(const TreeParams& P, int level, uint32_t q) {
+  const int sh = 2 * (P.L - level);
+  return P.leaf_start[(size_t)(q + 1) << sh] - P.leaf_start[(size_t)q << sh];
+}
+
+// MT: m-tiles (nodes padded to 8 MT).  The (offset, k-chunk) steps run as one
+// flattened cp.async pipeline of kGtStages stages: no bubble at offset
+// boundaries, no register staging.  Source pointers of every (offset, box)
+// are resolved once at the start (null: outside the grid or empty block ->
+// zero-filled B rows).
+template <int MT>
+__global__ void __launch_bounds__(kGtWarps * 32) k_node_gemm(
+    const TreeParams P, int box_level, const int* __restrict__ boxes_all, const GemmClasses G,
+    const GemmDelta* __restrict__ deltas_all, int n_deltas, int k2pad,
+    const double2* __restrict__ coef, double* __restrict__ out, int n_nodes) {
+  constexpr int MP = 8 * MT;
+  constexpr int SA = gemm_sa(MT);
+  extern __shared__ __align__(16) double gsm[];
+  double* As = gsm;                                   // [stage][KC][SA]
+  double* Bs = gsm + (size_t)kGtStages * kGtKC * SA;  // [stage][N][SBn]
+  const double** srcs = reinterpret_cast<const double**>(Bs + (size_t)kGtStages * kGtN * kGtSBn);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int r = lane >> 2, c = lane & 3;
+  // this CTA's box class: its boxes and its offsets (tiles never straddle classes)
+  int cls = 0;
+  while (cls + 1 < G.n && (int)blockIdx.x >= G.tile_off[cls + 1]) ++cls;
+  const int* boxes = boxes_all + G.box_off[cls];
+  const int n_boxes = G.box_off[cls + 1] - G.box_off[cls];
+  const GemmDelta* deltas = deltas_all + (size_t)cls * n_deltas;
+  const int b0 = ((int)blockIdx.x - G.tile_off[cls]) * kGtN;
+  for (int e = tid; e < n_deltas * kGtN; e += blockDim.x) {
+    const int di = e / kGtN, n = e % kGtN;
+    const GemmDelta D = deltas[di];
+    const double* p = nullptr;
+    if (b0 + n < n_boxes) {
+      int bi, bj;
+      demorton((uint32_t)boxes[b0 + n], bi, bj);
+      const int sh = D.level - box_level;
+      const int si = (bi << sh) + D.dx, sj = (bj << sh) + D.dy, g = 1 << (D.level + 1);
+      if (si >= 0 && sj >= 0 && si < g && sj < g) {
+        const uint32_t q = morton((uint32_t)si, (uint32_t)sj);
+        if (gemm_block_count(P, D.level, q) > 0)
+          p = reinterpret_cast<const double*>(coef + P.coef_off[D.level] + (size_t)q * P.K);
+      }
+    }
+    srcs[e] = p;
+  }
+  __syncthreads();
+  // warp w: boxes of n-tiles 2 np, +1 and m-tiles [mh MH, +MH), np = w % (N / 16),
+  // mh = w / (N / 16): every A fragment feeds two tensor-core ops
+  static_assert(MT % 2 == 0 && kGtN % 16 == 0, "m-tiles over two warp rows, box pairs");
+  constexpr int MH = MT / 2, NP = kGtN / 16;
+  const int np = warp % NP, mh = warp / NP;
+  double acc[MH][2][2];
+#pragma unroll
+  for (int mt = 0; mt < MH; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+  const int k2 = 2 * P.K, nchunk = k2pad / kGtKC, nsteps = n_deltas * nchunk;
+  auto issue = [&](int step) {
+    if (step < nsteps) {
+      const int di = step / nchunk, k0 = (step % nchunk) * kGtKC, st = step % kGtStages;
+      const double* A = deltas[di].A + (size_t)k0 * MP;
+      double* as = As + (size_t)st * kGtKC * SA;
+      for (int e = tid; e < kGtKC * MP / 2; e += blockDim.x) {  // 16-byte pieces
+        const int k = (2 * e) / MP, m = (2 * e) % MP;
+        cp16(as + k * SA + m, A + (size_t)k * MP + m, 16);
+      }
+      double* bs = Bs + (size_t)st * kGtN * kGtSBn;
+      const double* const* sp = srcs + di * kGtN;
+      for (int e = tid; e < kGtN * kGtKC / 2; e += blockDim.x) {
+        const int n = e / (kGtKC / 2), kk = 2 * (e % (kGtKC / 2));
+        const double* p = sp[n];
+        const bool ok = p && k0 + kk < k2;  // zero-fill padding rows and absent sources
+        cp16(bs + n * kGtSBn + kk, ok ? (const void*)(p + k0 + kk) : (const void*)coef, ok ? 16 : 0);
+      }
+    }
+    cp_commit();
+  };
+#pragma unroll
+  for (int i = 0; i < kGtStages - 1; ++i) issue(i);
+  for (int step = 0; step < nsteps; ++step) {
+    cp_wait<kGtStages - 2>();
+    __syncthreads();  // stage `step` visible; stage step-1 free for reuse
+    issue(step + kGtStages - 1);
+    const int st = step % kGtStages;
+    const int kleft = k2 - (step % nchunk) * kGtKC;  // the last chunk's k-steps past 2K are all zero
+    const double* as = As + (size_t)st * kGtKC * SA + mh * MH * 8 + r;
+    const double* bs = Bs + (size_t)st * kGtN * kGtSBn + (size_t)(np * 16 + r) * kGtSBn;
+#pragma unroll
+    for (int ks = 0; ks < kGtKC / 4; ++ks) {
+      if (4 * ks >= kleft) break;
+      const double b0 = bs[ks * 4 + c], b1 = bs[8 * kGtSBn + ks * 4 + c];
+      const double* ar = as + (ks * 4 + c) * SA;
+#pragma unroll
+      for (int mt = 0; mt < MH; ++mt) {
+        const double a = ar[mt * 8];
+        dmma(acc[mt][0][0], acc[mt][0][1], a, b0);
+        dmma(acc[mt][1][0], acc[mt][1][1], a, b1);
+      }
+    }
+  }
+  cp_wait<0>();
+  // C fragment: rows (mh MH + mt) 8 + r (nodes), columns (2 np + nt) 8 + 2c, +1 (boxes)
+#pragma unroll
+  for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int bx = b0 + (2 * np + nt) * 8 + 2 * c + h;
+      if (bx >= n_boxes) continue;
+      double* o = out + (size_t)boxes[bx] * n_nodes;
+#pragma unroll
+      for (int mt = 0; mt < MH; ++mt) {
+        const int n = (mh * MH + mt) * 8 + r;
+        if (n < n_nodes) o[n] = acc[mt][nt][h];
+      }
+    }
+}
+
+}  // namespace
+
+void launch_node_gemm(const TreeParams& P, int box_level, const int* boxes,
+                      const GemmClasses& G, const GemmDelta* deltas, int n_deltas, int k2pad,
+                      const double2* coef, double* out, int n_nodes, cudaStream_t s) {
+  if (G.n < 1 || G.tile_off[G.n] <= 0) return;
+  if (k2pad % kGtKC) throw std::invalid_argument("node gemm: k2pad must be a multiple of the k chunk");
+  if (n_deltas > kGtMaxDelta) throw std::invalid_argument("node gemm: too many offsets");
+  const unsigned grid = (unsigned)G.tile_off[G.n];
+  const int mt = (n_nodes + 7) / 8;
+  auto run = [&](auto kern, size_t smem) {
+    static unsigned done = 0;  // devices whose attribute is set (the size is fixed per MT)
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!((done >> (dev & 31)) & 1u)) {
+      if (cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem) != cudaSuccess) {
+        cudaGetLastError();
+        throw std::runtime_error("node gemm: shared-memory attribute");
+      }
+      done |= 1u << (dev & 31);
+    }
+    kern<<<grid, kGtWarps * 32, smem, s>>>(P, box_level, boxes, G, deltas, n_deltas, k2pad, coef,
+                                           out, n_nodes);
+  };
+  switch (mt) {
+    case 18: run(k_node_gemm<18>, gemm_smem(18)); break;
+    default: throw std::invalid_argument("node gemm: unsupported node count");
+  }
+}
+
+int node_gemm_k2pad(int K) { return ((2 * K + kGtKC - 1) / kGtKC) * kGtKC; }
+int node_gemm_tile() { return kGtN; }
+
+}  // namespace imqk

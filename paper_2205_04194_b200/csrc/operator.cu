@@ -132,6 +132,7 @@ void DeviceOperator::release() {
   dfree(d_rnx_); dfree(d_rny_); dfree(d_rnleaf_); dfree(d_rval_); dfree(d_rcoef_);
   dfree(d_ring_items_); dfree(d_lpart_items_);
   dfree(d_xnx_); dfree(d_xny_); dfree(d_xnleaf_); dfree(d_xval_); dfree(d_xring_items_);
+  dfree(d_gA_); dfree(d_gD_); dfree(d_gboxes_);
   dfree(d_xboxes_);
   dfree(solve_ws_);
   solve_ws_bytes_ = 0;
@@ -596,6 +597,7 @@ void DeviceOperator::build_cheb(int p_lo, int p_hi) {
   dfree(d_ring_items_);
   dfree(d_xring_items_); dfree(d_xboxes_);
   xring_ = false;
+  xgemm_ = false;
   n_cheb_items_ = n_ceval_ = n_ring_items_ = n_xring_items_ = n_xboxes_ = 0;
   if (!far_split_ || opt(kOptNoCheb) || !imqk::m2p_specialised(M_)) return;
   const int lc = L_ - 2;
@@ -880,6 +882,7 @@ void DeviceOperator::build_cheb(int p_lo, int p_hi) {
       if (n_xboxes_)
         cuda_check(cudaMemcpy(d_xboxes_, xboxes.data(), xboxes.size() * sizeof(int),
                               cudaMemcpyHostToDevice), "H2D x-ring boxes");
+      setup_xring_gemm(xboxes);
     }
   }
   n_cheb_items_ = (int)citems.size();
@@ -1055,6 +1058,102 @@ ListCheck DeviceOperator::far_list_check(int max_targets) {
     r.max_entries = std::max(r.max_entries, v.w);
   }
   return r;
+}
+
+// The X-node pass as tensor-core GEMMs (nodegemm.cu): the basis of every
+// (node, source offset) pair of a level-(L-1) box is the same for all boxes,
+// so A_delta[k][n] is formed once here (long double, the reference's
+// truncated expansion in the monomial form) for the 20
+// level-L outer-ring offsets and, per box class (the box's position in its
+// parent: its level-(L-1) inner list depends on it), the 7 level-(L-1) inner
+// offsets, exactly the lists build_far_list enumerates (ring mode 1 at level
+// L-1, lsplit 4 at level L).  Boxes are grouped by class.
+void DeviceOperator::setup_xring_gemm(const std::vector<int>& xboxes) {
+  dfree(d_gA_);
+  dfree(d_gD_);
+  dfree(d_gboxes_);
+  xgemm_ = false;
+  constexpr int NX = imqk::kChebNX, NXX = NX * NX;
+  if (!imqk::m2p_specialised(M_) || NXX % 8 || xboxes.empty()) return;
+  const int Lx = L_ - 1, k2pad = imqk::node_gemm_k2pad(K_);
+  const long double pi = 3.141592653589793238462643383279502884L;
+  const long double hx = 0.5L * (long double)P_.cell[Lx], cL = (long double)P_.cell[L_];
+  const long double cX = (long double)P_.cell[Lx], t2 = (long double)P_.t2;
+  // Horner order of the stored coefficients: m = M..0, k = top(m)..m
+  std::vector<std::pair<int, int>> jm;
+  for (int m = M_; m >= 0; --m)
+    for (int k = horner_top(M_, m); k >= m; --k) jm.push_back({m, k});
+  struct Off { int level, dx, dy; long double sx, sy; };
+  std::vector<Off> offs;  // per class: 7 inner (level L-1), then the 20 outer (level L)
+  for (int cls = 0; cls < 4; ++cls) {
+    const int cx = cls >> 1, cy = cls & 1;
+    for (int ri = -1; ri <= 2; ++ri)
+      for (int rj = -1; rj <= 2; ++rj) {
+        const int dx = ri - cx, dy = rj - cy;
+        if (std::max(std::abs(dx), std::abs(dy)) < 2) continue;
+        offs.push_back({Lx, dx, dy, dx * cX, dy * cX});
+      }
+    for (int ri = -2; ri <= 3; ++ri)
+      for (int rj = -2; rj <= 3; ++rj) {
+        if (!(ri == -2 || ri == 3 || rj == -2 || rj == 3)) continue;
+        offs.push_back({L_, ri, rj, (ri - 0.5L) * cL, (rj - 0.5L) * cL});
+      }
+  }
+  const int nd = (int)offs.size() / 4;  // 27
+  std::vector<double> A((size_t)offs.size() * k2pad * NXX, 0.0);
+  std::vector<long double> tc((size_t)NX);
+  for (int i = 0; i < NX; ++i) tc[(size_t)i] = hx * cosl(pi * (i + 0.5L) / NX);
+  for (size_t d = 0; d < offs.size(); ++d) {
+    double* Ad = A.data() + d * (size_t)k2pad * NXX;
+    for (int n = 0; n < NXX; ++n) {
+      const long double dx = tc[(size_t)(n / NX)] - offs[d].sx, dy = tc[(size_t)(n % NX)] - offs[d].sy;
+      const long double r = 1.0L / sqrtl(dx * dx + dy * dy + t2), q = r * r;
+      const long double xr = dx * q, xi = -dy * q;  // conj(xi)
+      // powers conj(xi)^m and q^p
+      std::vector<long double> pr((size_t)M_ + 1), pim((size_t)M_ + 1), qp((size_t)M_ + 1);
+      pr[0] = 1.0L;
+      pim[0] = 0.0L;
+      qp[0] = 1.0L;
+      for (int m = 1; m <= M_; ++m) {
+        pr[(size_t)m] = pr[(size_t)m - 1] * xr - pim[(size_t)m - 1] * xi;
+        pim[(size_t)m] = pr[(size_t)m - 1] * xi + pim[(size_t)m - 1] * xr;
+        qp[(size_t)m] = qp[(size_t)m - 1] * q;
+      }
+      for (size_t j = 0; j < jm.size(); ++j) {
+        const int m = jm[j].first, k = jm[j].second;
+        const long double f = r * qp[(size_t)(k - m)];
+        Ad[(2 * j) * (size_t)NXX + (size_t)n] = (double)(f * pr[(size_t)m]);
+        Ad[(2 * j + 1) * (size_t)NXX + (size_t)n] = (double)(-f * pim[(size_t)m]);
+      }
+    }
+  }
+  d_gA_ = dalloc<double>(A.size(), "x-ring gemm basis");
+  cuda_check(cudaMemcpy(d_gA_, A.data(), A.size() * sizeof(double), cudaMemcpyHostToDevice),
+             "H2D basis");
+  std::vector<imqk::GemmDelta> D(offs.size());
+  for (size_t d = 0; d < offs.size(); ++d)
+    D[d] = {offs[d].level, offs[d].dx, offs[d].dy, 0, d_gA_ + d * (size_t)k2pad * NXX};
+  d_gD_ = dalloc<imqk::GemmDelta>(D.size(), "x-ring gemm offsets");
+  cuda_check(cudaMemcpy(d_gD_, D.data(), D.size() * sizeof(imqk::GemmDelta),
+                        cudaMemcpyHostToDevice), "H2D offsets");
+  std::vector<int> bx;
+  gcls_.n = 4;
+  const int tile = imqk::node_gemm_tile();
+  gcls_.box_off[0] = 0;
+  gcls_.tile_off[0] = 0;
+  for (int cls = 0; cls < 4; ++cls) {
+    for (int q : xboxes)
+      if ((q & 3) == cls) bx.push_back(q);
+    gcls_.box_off[cls + 1] = (int)bx.size();
+    const int nb = gcls_.box_off[cls + 1] - gcls_.box_off[cls];
+    gcls_.tile_off[cls + 1] = gcls_.tile_off[cls] + (nb + tile - 1) / tile;
+  }
+  d_gboxes_ = dalloc<int>(bx.size(), "x-ring gemm boxes");
+  cuda_check(cudaMemcpy(d_gboxes_, bx.data(), bx.size() * sizeof(int), cudaMemcpyHostToDevice),
+             "H2D boxes");
+  gemm_nd_ = nd;
+  gemm_k2pad_ = k2pad;
+  xgemm_ = true;
 }
 
 void DeviceOperator::restrict_targets(int p_lo, int p_hi) {
@@ -1412,8 +1511,11 @@ void DeviceOperator::far_near(const double* d_us, double* d_out, const int* perm
       if (ring_)  // the level-(l+1) rings at the NR x NR nodes of the level-l boxes
         far_pass(0, n_ring_items_, ring_group_off_.data(), nullptr, 0, nullptr, nullptr, d_rval_,
                  nullptr, 2, L_ - 1, &Pr_, d_ring_items_);
-      if (xr)  // at the NX x NX nodes of each level-(L-1) box X: its level-(L-1)
-               // inner blocks (ring mode 1) and its level-L outer ring (lsplit 4)
+      if (xr && xgemm_)  // at the NX x NX nodes of each level-(L-1) box X: its level-(L-1)
+                         // inner blocks and its level-L outer ring, as GEMMs
+        imqk::launch_node_gemm(P_, L_ - 1, d_gboxes_, gcls_, d_gD_, gemm_nd_, gemm_k2pad_, d_coef_,
+                               d_xval_, imqk::kChebNX * imqk::kChebNX, s);
+      else if (xr)  // the same through k_m2p_far (ring mode 1 at level L-1, lsplit 4 at L)
         far_pass(0, n_xring_items_, xring_group_off_.data(), nullptr, 0, nullptr, nullptr,
                  d_xval_, nullptr, L_ - 1, L_, &Px_, d_xring_items_, 1, 4);
       constexpr long long NN = imqk::kChebN * imqk::kChebN, NRR = imqk::kChebNR * imqk::kChebNR;
@@ -1816,7 +1918,7 @@ int DeviceOperator::kernel_launches_per_apply() const {
       n += groups(cheb_group_off_) + cheb_lc_ + 1;  // node groups, coefficients, evaluation
       if (ring_) {
         n += groups(ring_group_off_) + 1;  // ring node groups, level-(L-1) ring coefficients
-        if (xring_) n += groups(xring_group_off_) + 1;  // X-ring node groups, coefficients
+        if (xring_) n += (xgemm_ ? 1 : groups(xring_group_off_)) + 1;  // X-node pass, coefficients
         for (int l = std::max(2, ring_l0_); l <= cheb_lc_; ++l) ++n;  // coarse ring coefficients
       }
     } else {

@@ -304,6 +304,14 @@ class DeviceOperator {
   double *d_xnx_ = nullptr, *d_xny_ = nullptr, *d_xval_ = nullptr;
   uint32_t* d_xnleaf_ = nullptr;
   int4* d_xring_items_ = nullptr;
+  // X-node pass as tensor-core GEMMs (setup_xring_gemm, nodegemm.cu)
+  void setup_xring_gemm(const std::vector<int>& xboxes);
+  bool xgemm_ = false;
+  double* d_gA_ = nullptr;
+  imqk::GemmDelta* d_gD_ = nullptr;
+  int* d_gboxes_ = nullptr;
+  imqk::GemmClasses gcls_{};
+  int gemm_nd_ = 0, gemm_k2pad_ = 0;
   int* d_xboxes_ = nullptr;
   int n_ring_items_ = 0;
   size_t ring_nodes_ = 0;
