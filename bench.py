@@ -382,8 +382,12 @@ def b200_arm(args):
     peak_tf, _ = P.api.fp64_peak(8192)
     far_flops = st["far_pairs"] * f_pair(M) * share  # this rank's targets
     survey_achieved = far_flops / (far_ms * 1e-3) / 1e12
-    exec_flops = ((st["far_pairs_direct"] + st["cheb_node_pairs"]) * share
-                  * 2 * (M * M + 4 * M + 12))
+    # executed flops of the algorithm: complex Horner 2(M^2+4M+12) per (target
+    # or node, block) pair; the GEMM node pairs 2 x 2K (K = stored coefficients)
+    K_h = (M + 1) * (M + 2) // 2 - (M + 1) // 2
+    gemm_pairs = st.get("gemm_node_pairs", 0.0)
+    exec_flops = ((st["far_pairs_direct"] + st["cheb_node_pairs"] - gemm_pairs) * 2 * (M * M + 4 * M + 12)
+                  + gemm_pairs * 4 * K_h) * share
     achieved = exec_flops / (far_ms * 1e-3) / 1e12
     traffic = None
     prof = os.path.join(ROOT, "profiles", "far_kernel_ncu.json")
@@ -480,7 +484,8 @@ def b200_arm(args):
                                   "pipelined with the products (same bytes per product)"},
             "roofline": {"bound": "fp64",
                          "kernel": "k_m2p_far (M2P far field: direct for the fine levels, at "
-                                   "Chebyshev nodes for levels 1..%d%s) + k_cheb_*"
+                                   "Chebyshev nodes for levels 1..%d%s) + k_node_gemm (X nodes, "
+                                   "DMMA) + k_cheb_*"
                                    % (st["cheb_levels"], " and the level-%d ring" % (L - 1)
                                       if st["cheb_ring"] else ""),
                          "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
@@ -491,10 +496,12 @@ def b200_arm(args):
                                         "MEASURED_PEAKS.json has no FP64 entry",
                          "flops_per_launch": exec_flops,
                          "flop_model": "evaluated (target or Chebyshev node, source block) pairs "
-                                       "x 2(M^2+4M+12) flop (complex-Horner M2P, DESIGN.md s4)"
+                                       "x 2(M^2+4M+12) flop (complex-Horner M2P, DESIGN.md s4); "
+                                       "pairs evaluated by the node GEMMs x 4K flop"
                                        + ("" if world == 1 else " x rank-0 target share"),
                          "evaluated_pairs": {"direct": st["far_pairs_direct"] * share,
                                              "cheb_nodes": st["cheb_node_pairs"] * share,
+                                             "gemm_nodes": gemm_pairs * share,
                                              "algorithmic_P_far": st["far_pairs"] * share},
                          "survey_model": {"achieved": survey_achieved,
                                           "frac": survey_achieved / peak_tf,

@@ -196,6 +196,7 @@ typedef struct {
   double cert_estimate, cert_budget, cert_scale;
   double cert_by_kind[5];
   int cert_fallbacks, cert_rounds;
+  double gemm_node_pairs;  /* of cheb_node_pairs: evaluated as tensor-core GEMMs (2 x 2K flop each) */
 } imq_ext_stats;
 IMQ_API int imq_ext_operator_stats(const imq_operator* op, imq_ext_stats* out);
 

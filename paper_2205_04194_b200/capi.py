@@ -46,7 +46,8 @@ class imq_ext_stats(C.Structure):
                 ("kernel_launches", C.c_int), ("cheb_xring", C.c_int),
                 ("cert_estimate", C.c_double), ("cert_budget", C.c_double),
                 ("cert_scale", C.c_double), ("cert_by_kind", C.c_double * 5),
-                ("cert_fallbacks", C.c_int), ("cert_rounds", C.c_int)]
+                ("cert_fallbacks", C.c_int), ("cert_rounds", C.c_int),
+                ("gemm_node_pairs", C.c_double)]
 
 
 class imq_ext_options(C.Structure):

@@ -571,6 +571,7 @@ int imq_ext_operator_stats(const imq_operator* op, imq_ext_stats* out) {
     for (int k = 0; k < 5; ++k) out->cert_by_kind[k] = r.by_kind[k];
     out->cert_fallbacks = r.fallbacks;
     out->cert_rounds = r.rounds;
+    out->gemm_node_pairs = c.gemm_node_pairs;
     return IMQ_OK;
   });
 }

@@ -1955,6 +1955,9 @@ void DeviceOperator::fill_eval_counts() {
     const double inner_lm1 = lists_by_level_[(size_t)L_ - 1] - ring_child_by_level_[(size_t)L_ - 1];
     direct -= xring_direct_ + (far_by_level_[(size_t)L_ - 1] - ring_direct_);
     nodes += (xring_lists_ + inner_lm1) * imqk::kChebNX * imqk::kChebNX;
+    counts_.gemm_node_pairs = xgemm_ ? (xring_lists_ + inner_lm1) * imqk::kChebNX * imqk::kChebNX : 0.0;
+  } else {
+    counts_.gemm_node_pairs = 0.0;
   }
   counts_.far_pairs_direct = direct;
   counts_.cheb_node_pairs = nodes;

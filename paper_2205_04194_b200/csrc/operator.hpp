@@ -43,6 +43,7 @@ struct PairCounts {
   int cheb_ring = 0;            // level-(L-1) ring through the level-(L-2) nodes
   int kernel_launches = 0;      // this library's kernels per apply_device
   int cheb_xring = 0;           // level-L outer rings through the level-(L-1) nodes
+  double gemm_node_pairs = 0;   // of cheb_node_pairs: evaluated by tensor-core GEMMs (nodegemm.cu)
 };
 
 // Build-time options (imq_ext_operator_create_opts).  They can only DISABLE
