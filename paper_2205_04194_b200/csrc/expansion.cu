@@ -912,6 +912,7 @@ constexpr int kCoverWarps = 4, kCoverCap = 1024;
 __global__ void __launch_bounds__(kCoverWarps * 32) k_far_cover(const TreeParams P,
                                                                const int* __restrict__ targets,
                                                                int n_t, const CoverModes Mo,
+                                                               const CoverGemm Gm,
                                                                int4* __restrict__ out) {
   __shared__ uint32_t lists[kCoverWarps][kMaxList];
   __shared__ uint32_t got[kCoverWarps][kCoverCap];
@@ -929,6 +930,31 @@ __global__ void __launch_bounds__(kCoverWarps * 32) k_far_cover(const TreeParams
     ng = min(kCoverCap, ng + n);
     __syncwarp();
   };
+  // a pass run as a tensor-core GEMM: its offset table for the box's class
+  auto add_gemm = [&](uint32_t box, int box_level, const GemmDelta* D, int nd, int nc) {
+    int bi, bj;
+    demorton(box, bi, bj);
+    const GemmDelta* Dc = D + (size_t)(nc == 4 ? (int)(box & 3u) : 0) * nd;
+    for (int d = lane; d < nd; d += 32) {
+      const GemmDelta e = Dc[d];
+      const int sh = e.level - box_level, g = 1 << (e.level + 1);
+      const long long si = ((long long)bi << sh) + e.dx, sj = ((long long)bj << sh) + e.dy;
+      bool keep = si >= 0 && sj >= 0 && si < g && sj < g;
+      uint32_t q = 0;
+      if (keep) {
+        q = morton((uint32_t)si, (uint32_t)sj);
+        keep = block_count(P, e.level, q) > 0;
+      }
+      const uint32_t bal = __ballot_sync(__activemask(), keep);
+      if (keep) {
+        const int pos = ng + __popc(bal & ((1u << lane) - 1u));
+        if (pos < kCoverCap) got[warp][pos] = ((uint32_t)e.level << 28) | q;
+      }
+      ng = min(kCoverCap, ng + __popc(bal));
+    }
+    ng = __shfl_sync(0xffffffffu, ng, 0);
+    __syncwarp();
+  };
   if (!Mo.split) {
     add(X, 1, L, 0, 0);
   } else if (!Mo.cheb) {
@@ -938,11 +964,22 @@ __global__ void __launch_bounds__(kCoverWarps * 32) k_far_cover(const TreeParams
   } else {
     for (int l = 1; l <= Mo.lc; ++l) {
       const uint32_t q = T >> (2 * (L - l));
-      add(q << (2 * (L - 1 - l)), l, l, (Mo.ring && l >= Mo.ring_l0) ? 1 : 0, 0);
-      if (Mo.ring && l + 1 >= Mo.ring_l0) add((4 * q) << (2 * (L - 2 - l)), l + 1, l + 1, 2, 0);
+      if (Gm.node[l])
+        add_gemm(q, l, Gm.node[l], Gm.node_nd[l], 4);
+      else
+        add(q << (2 * (L - 1 - l)), l, l, (Mo.ring && l >= Mo.ring_l0) ? 1 : 0, 0);
+      if (Mo.ring && l + 1 >= Mo.ring_l0) {
+        if (Gm.ring[l])
+          add_gemm(q, l, Gm.ring[l], Gm.ring_nd[l], 1);
+        else
+          add((4 * q) << (2 * (L - 2 - l)), l + 1, l + 1, 2, 0);
+      }
     }
     if (Mo.xring) {
-      add(X, L - 1, L, 1, 4);
+      if (Gm.x)
+        add_gemm(X, L - 1, Gm.x, Gm.x_nd, 4);
+      else
+        add(X, L - 1, L, 1, 4);
       add(X, L, L, 0, 2);
     } else {
       if (Mo.lsplit) add(X, L, L, 0, 2);
@@ -1572,10 +1609,10 @@ void launch_m2p_far(const TreeParams& P, const int4* items, const int* group_off
 }
 
 void launch_far_cover(const TreeParams& P, const int* targets, int n_t, const CoverModes& Mo,
-                      int4* out, cudaStream_t s) {
+                      const CoverGemm& Gm, int4* out, cudaStream_t s) {
   if (n_t > 0)
     k_far_cover<<<(unsigned)((n_t + kCoverWarps - 1) / kCoverWarps), kCoverWarps * 32, 0, s>>>(
-        P, targets, n_t, Mo, out);
+        P, targets, n_t, Mo, Gm, out);
 }
 
 }  // namespace imqk

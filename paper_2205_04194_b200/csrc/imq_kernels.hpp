@@ -113,8 +113,20 @@ struct CoverModes {
   int lsplit;   // per-leaf partial pass
 };
 // out[i] = {missing, duplicated, extra, entries} of targets[i]'s far lists
+struct GemmDelta;
+// passes run as tensor-core GEMMs (nullptr: through build_far_list): node pass
+// of level l (4 box classes), ring of level l + 1 at level-l boxes (1 class),
+// X-node pass (4 classes); offsets per class
+struct CoverGemm {
+  const GemmDelta* node[kMaxLevels + 1];
+  int node_nd[kMaxLevels + 1];
+  const GemmDelta* ring[kMaxLevels + 1];
+  int ring_nd[kMaxLevels + 1];
+  const GemmDelta* x;
+  int x_nd;
+};
 void launch_far_cover(const TreeParams& P, const int* targets, int n_t, const CoverModes& Mo,
-                      int4* out, cudaStream_t s);
+                      const CoverGemm& Gm, int4* out, cudaStream_t s);
 
 // ---- coarse far field by Chebyshev interpolation (cheb.cu)
 #ifndef IMQ_CHEB_N
@@ -213,6 +225,13 @@ void launch_node_gemm(const TreeParams& P, int box_level, const int* boxes,
                       const double2* coef, double* out, int n_nodes, cudaStream_t s);
 int node_gemm_k2pad(int K);
 int node_gemm_tile();
+// padded m-tiles of a node count (0: no GEMM kernel for it)
+int node_gemm_mt(int n_nodes);
+// A[d][k][n] for offsets d (source centre sx, sy relative to the box centre)
+// at nodes (nx, ny) relative to the box centre; mp = 8 node_gemm_mt(n_nodes)
+void launch_gemm_basis(double* A, const double* sx, const double* sy, int n_off, const double* nx,
+                       const double* ny, int n_nodes, int mp, int k2pad, int M, double t2,
+                       cudaStream_t s);
 
 // ---- direct interactions (direct.cu)
 // Near work items (one leaf each) grouped by points-per-lane like the far ones.

@@ -27,7 +27,11 @@
 // (68 %), 32 / 16 / 3 6.59 ms, 16 / 16 / 2 7.34 ms (55 %); the Horner pass
 // it replaces took 6.96 ms.
 #include <algorithm>
+#include <mutex>
+#include <set>
 #include <stdexcept>
+#include <string>
+#include <utility>
 
 #include "imq_device.cuh"
 #include "imq_kernels.hpp"
@@ -49,7 +53,7 @@ namespace {
 using namespace imqdev;
 
 // boxes per CTA (warps = kGtN / 8: box pairs x 2 node halves), k chunk, stages
-constexpr int kGtN = IMQ_GEMM_NB, kGtKC = IMQ_GEMM_KC, kGtWarps = kGtN / 8, kGtStages = IMQ_GEMM_ST;
+constexpr int kGtN = IMQ_GEMM_NB, kGtKC = IMQ_GEMM_KC, kGtStages = IMQ_GEMM_ST;
 constexpr int kGtMaxDelta = 32;
 constexpr int kGtSBn = kGtKC + 4;  // B rows [box][k]: stride = 4 (mod 16)
 
@@ -89,8 +93,9 @@ __device__ __forceinline__ int gemm_block_count(const TreeParams& P, int level, 
 // boundaries, no register staging.  Source pointers of every (offset, box)
 // are resolved once at the start (null: outside the grid or empty block ->
 // zero-filled B rows).
-template <int MT>
-__global__ void __launch_bounds__(kGtWarps * 32) k_node_gemm(
+// MG: node-tile groups (warps = kGtN / 16 box pairs x MG, MT / MG m-tiles each)
+template <int MT, int MG>
+__global__ void __launch_bounds__(kGtN / 16 * MG * 32) k_node_gemm(
     const TreeParams P, int box_level, const int* __restrict__ boxes_all, const GemmClasses G,
     const GemmDelta* __restrict__ deltas_all, int n_deltas, int k2pad,
     const double2* __restrict__ coef, double* __restrict__ out, int n_nodes) {
@@ -129,8 +134,8 @@ __global__ void __launch_bounds__(kGtWarps * 32) k_node_gemm(
   __syncthreads();
   // warp w: boxes of n-tiles 2 np, +1 and m-tiles [mh MH, +MH), np = w % (N / 16),
   // mh = w / (N / 16): every A fragment feeds two tensor-core ops
-  static_assert(MT % 2 == 0 && kGtN % 16 == 0, "m-tiles over two warp rows, box pairs");
-  constexpr int MH = MT / 2, NP = kGtN / 16;
+  static_assert(MT % MG == 0 && kGtN % 16 == 0, "m-tiles over MG warp rows, box pairs");
+  constexpr int MH = MT / MG, NP = kGtN / 16;
   const int np = warp % NP, mh = warp / NP;
   double acc[MH][2][2];
 #pragma unroll
@@ -200,6 +205,17 @@ __global__ void __launch_bounds__(kGtWarps * 32) k_node_gemm(
 
 }  // namespace
 
+// nodes -> (MT, MG): MT m-tiles of 8 (padded), MG warp rows of <= 10 m-tiles
+int node_gemm_mt(int n_nodes) {
+  switch ((n_nodes + 7) / 8) {
+    case 18: return 18;                    // 12 x 12 (X-ring)
+    case 32: return 32;                    // 16 x 16
+    case 41: case 42: return 42;           // 18 x 18
+    case 50: return 50;                    // 20 x 20
+    default: return 0;
+  }
+}
+
 void launch_node_gemm(const TreeParams& P, int box_level, const int* boxes,
                       const GemmClasses& G, const GemmDelta* deltas, int n_deltas, int k2pad,
                       const double2* coef, double* out, int n_nodes, cudaStream_t s) {
@@ -207,26 +223,88 @@ void launch_node_gemm(const TreeParams& P, int box_level, const int* boxes,
   if (k2pad % kGtKC) throw std::invalid_argument("node gemm: k2pad must be a multiple of the k chunk");
   if (n_deltas > kGtMaxDelta) throw std::invalid_argument("node gemm: too many offsets");
   const unsigned grid = (unsigned)G.tile_off[G.n];
-  const int mt = (n_nodes + 7) / 8;
-  auto run = [&](auto kern, size_t smem) {
-    static unsigned done = 0;  // devices whose attribute is set (the size is fixed per MT)
+  auto run = [&](auto kern, size_t smem, int warps) {
+    // the attribute is per (kernel, device); every instantiation has the same
+    // function-pointer type, so key by the pointer
+    static std::mutex mtx;
+    static std::set<std::pair<const void*, int>> done;
     int dev = 0;
     cudaGetDevice(&dev);
-    if (!((done >> (dev & 31)) & 1u)) {
-      if (cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    {
+      std::lock_guard<std::mutex> lk(mtx);
+      if (done.insert({(const void*)kern, dev}).second &&
+          cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)smem) != cudaSuccess) {
         cudaGetLastError();
+        done.erase({(const void*)kern, dev});
         throw std::runtime_error("node gemm: shared-memory attribute");
       }
-      done |= 1u << (dev & 31);
     }
-    kern<<<grid, kGtWarps * 32, smem, s>>>(P, box_level, boxes, G, deltas, n_deltas, k2pad, coef,
-                                           out, n_nodes);
+    kern<<<grid, warps * 32, smem, s>>>(P, box_level, boxes, G, deltas, n_deltas, k2pad, coef, out,
+                                        n_nodes);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess)
+      throw std::runtime_error(std::string("node gemm launch (") + std::to_string(n_nodes) +
+                               " nodes, " + std::to_string(smem) + " B shared): " +
+                               cudaGetErrorString(e));
   };
-  switch (mt) {
-    case 18: run(k_node_gemm<18>, gemm_smem(18)); break;
+  constexpr int NP = kGtN / 16;
+  switch (node_gemm_mt(n_nodes)) {
+    case 18: run(k_node_gemm<18, 2>, gemm_smem(18), NP * 2); break;
+    case 32: run(k_node_gemm<32, 4>, gemm_smem(32), NP * 4); break;
+    case 42: run(k_node_gemm<42, 6>, gemm_smem(42), NP * 6); break;
+    case 50: run(k_node_gemm<50, 5>, gemm_smem(50), NP * 5); break;
     default: throw std::invalid_argument("node gemm: unsupported node count");
   }
+}
+
+// A[d][k][n] (k-major, n padded to 8 MT): the basis of Horner coefficient j =
+// k / 2 at node n for source offset d: rho^-1 conj(xi)^m q^(k-m) (rows 2j, 2j+1
+// = Re, -Im), from the node position relative to its box centre (nx, ny)
+// minus the source centre relative to it (sx[d], sy[d]).
+__global__ void k_gemm_basis(double* __restrict__ A, const double* __restrict__ sx,
+                             const double* __restrict__ sy, int n_off, const double* __restrict__ nx,
+                             const double* __restrict__ ny, int n_nodes, int mp, int k2pad, int M,
+                             double t2) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long long)n_off * mp) return;
+  const int d = (int)(t / mp), n = (int)(t % mp);
+  double* Ad = A + (size_t)d * k2pad * mp;
+  if (n >= n_nodes) {
+    for (int k = 0; k < k2pad; ++k) Ad[(size_t)k * mp + n] = 0.0;
+    return;
+  }
+  const double dx = nx[n] - sx[d], dy = ny[n] - sy[d];
+  const double r = 1.0 / sqrt(fma(dx, dx, fma(dy, dy, t2))), q = r * r;
+  const double xr = dx * q, xi = -dy * q;
+  int jb = 0;  // first Horner slot of group m (groups m = M..0, k = top(m)..m)
+  for (int m = M; m >= 0; --m) {
+    double mr = 1.0, mi = 0.0;  // conj(xi)^m
+    for (int e = 0; e < m; ++e) {
+      const double tr = mr * xr - mi * xi;
+      mi = mr * xi + mi * xr;
+      mr = tr;
+    }
+    const int top = M - ((M - m) & 1);
+    double f = r;  // r q^(k - m)
+    for (int k = m; k <= top; ++k) {
+      const int j = jb + (top - k);
+      Ad[(size_t)(2 * j) * mp + n] = f * mr;
+      Ad[(size_t)(2 * j + 1) * mp + n] = -f * mi;
+      f *= q;
+    }
+    jb += top - m + 1;
+  }
+  for (int k = 2 * jb; k < k2pad; ++k) Ad[(size_t)k * mp + n] = 0.0;
+}
+
+void launch_gemm_basis(double* A, const double* sx, const double* sy, int n_off, const double* nx,
+                       const double* ny, int n_nodes, int mp, int k2pad, int M, double t2,
+                       cudaStream_t s) {
+  const long long n = (long long)n_off * mp;
+  if (n > 0)
+    k_gemm_basis<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(A, sx, sy, n_off, nx, ny, n_nodes, mp,
+                                                            k2pad, M, t2);
 }
 
 int node_gemm_k2pad(int K) { return ((2 * K + kGtKC - 1) / kGtKC) * kGtKC; }

@@ -132,7 +132,9 @@ void DeviceOperator::release() {
   dfree(d_rnx_); dfree(d_rny_); dfree(d_rnleaf_); dfree(d_rval_); dfree(d_rcoef_);
   dfree(d_ring_items_); dfree(d_lpart_items_);
   dfree(d_xnx_); dfree(d_xny_); dfree(d_xnleaf_); dfree(d_xval_); dfree(d_xring_items_);
-  dfree(d_gA_); dfree(d_gD_); dfree(d_gboxes_);
+  free_gemm_pass(gx_);
+  for (GemmPass& g : gnode_) free_gemm_pass(g);
+  for (GemmPass& g : gring_) free_gemm_pass(g);
   dfree(d_xboxes_);
   dfree(solve_ws_);
   solve_ws_bytes_ = 0;
@@ -598,6 +600,7 @@ void DeviceOperator::build_cheb(int p_lo, int p_hi) {
   dfree(d_xring_items_); dfree(d_xboxes_);
   xring_ = false;
   xgemm_ = false;
+  free_gemm_pass(gx_);
   n_cheb_items_ = n_ceval_ = n_ring_items_ = n_xring_items_ = n_xboxes_ = 0;
   if (!far_split_ || opt(kOptNoCheb) || !imqk::m2p_specialised(M_)) return;
   const int lc = L_ - 2;
@@ -769,20 +772,41 @@ void DeviceOperator::build_cheb(int p_lo, int p_hi) {
       grp[(size_t)((cnt + 31) / 32 - 1)].push_back(make_int4(par, (int)(start + c), cnt, w));
     }
   };
+  // node / ring passes of the levels with enough boxes run as tensor-core
+  // GEMMs (make_gemm_pass below): no work items for them
+  const int gtile = imqk::node_gemm_tile();
+  std::vector<char> gn((size_t)lc + 1, 0), gr((size_t)lc + 1, 0);
+  for (int l = 2; l <= lc; ++l) {
+    long long nb_own = 0;
+    for (long long q = 0; q < (1ll << (2 * (l + 1))); ++q) nb_own += own(l, q) > 0;
+    // where the GEMM wins (measured at config 4, k_node_gemm vs k_m2p_far): node
+    // counts that leave idle target slots in the Horner kernel's 32-lane x R
+    // items (not a multiple of 256), and levels with enough boxes to fill the
+    // GPU (>= 256 tiles); the 16 x 16 passes run at 77 % of the pipe as Horner
+    // items of R = 8 and at 63 % as GEMMs
+    const int npd = inner_v_[(size_t)l] ? imqk::kChebNI : imqk::kChebN;
+    const bool big = imqk::m2p_specialised(M_) && nb_own >= 256 * (long long)gtile;
+    auto wins = [&](int nn) { return nn % 256 != 0 && imqk::node_gemm_mt(nn) > 0; };
+    gn[(size_t)l] = big && wins(npd * npd);
+    if (ring_ && l + 1 >= ring_l0_) {
+      const int nr = imqk::kRingNr[ring_v_[(size_t)l]];
+      gr[(size_t)l] = big && wins(nr * nr);
+    }
+  }
   for (int l = 1; l <= lc; ++l) {
     cbox_off_[(size_t)l] = (int)boxes.size();
     for (long long q = 0; q < (1ll << (2 * (l + 1))); ++q) {
       if (!own(l, q)) continue;
       boxes.push_back((int)q);
       // own list of q at level l (without the ring of its parent when rings are on)
-      {
+      if (!gn[(size_t)l]) {
         const long long npl =
             inner_v_[(size_t)l] ? (long long)imqk::kChebNI * imqk::kChebNI : (long long)NN;
         chunks(g, (int)(q << (2 * (L_ - 1 - l))), cnode_base_[(size_t)l] + q * npl, (int)npl,
                l | ((ring_ && l >= ring_l0_ ? 1 : 0) << 8));
       }
       // the level-(l+1) ring of q at q's ring nodes
-      if (ring_ && l + 1 >= ring_l0_)
+      if (ring_ && l + 1 >= ring_l0_ && !gr[(size_t)l])
         chunks(rg, (int)((4 * q) << (2 * (L_ - 2 - l))),
                ring_nbase_[(size_t)l] + q * imqk::kRingNr[ring_v_[(size_t)l]] *
                                             imqk::kRingNr[ring_v_[(size_t)l]],
@@ -791,6 +815,47 @@ void DeviceOperator::build_cheb(int p_lo, int p_hi) {
     }
   }
   cbox_off_[(size_t)lc + 1] = (int)boxes.size();
+  {
+    const long double pi = 3.141592653589793238462643383279502884L;
+    auto rel = [&](int l, int n) {  // node offsets h cos(pi (i + 1/2) / n), as the node kernels
+      std::vector<double> r((size_t)n);
+      for (int i = 0; i < n; ++i) r[(size_t)i] = 0.5 * P_.cell[l] * (double)cosl(pi * (i + 0.5L) / n);
+      return r;
+    };
+    for (GemmPass& g : gnode_) free_gemm_pass(g);
+    for (GemmPass& g : gring_) free_gemm_pass(g);
+    gnode_.resize((size_t)lc + 1);
+    gring_.resize((size_t)lc + 1);
+    for (int l = 2; l <= lc; ++l) {
+      const std::vector<int> bl(boxes.begin() + cbox_off_[(size_t)l], boxes.begin() + cbox_off_[(size_t)l + 1]);
+      if (gn[(size_t)l]) {
+        const bool inner = ring_ && l >= ring_l0_;
+        const int npd = inner_v_[(size_t)l] ? imqk::kChebNI : imqk::kChebN;
+        const long long npl = (long long)npd * npd;
+        make_gemm_pass(gnode_[(size_t)l], l, npd, rel(l, npd), bl, true,
+                       [&](int c, std::vector<GemmOff>& o) {
+                         const int cx = c >> 1, cy = c & 1, lo = inner ? -1 : -2, hi = inner ? 2 : 3;
+                         for (int ri = lo; ri <= hi; ++ri)
+                           for (int rj = lo; rj <= hi; ++rj) {
+                             const int dx = ri - cx, dy = rj - cy;
+                             if (std::max(std::abs(dx), std::abs(dy)) >= 2) o.push_back({l, dx, dy});
+                           }
+                       },
+                       d_cval_ + cnode_base_[(size_t)l]);
+        (void)npl;
+      }
+      if (gr[(size_t)l]) {
+        const int nr = imqk::kRingNr[ring_v_[(size_t)l]];
+        make_gemm_pass(gring_[(size_t)l], l, nr, rel(l, nr), bl, false,
+                       [&](int, std::vector<GemmOff>& o) {
+                         for (int ri = -2; ri <= 3; ++ri)
+                           for (int rj = -2; rj <= 3; ++rj)
+                             if (ri == -2 || ri == 3 || rj == -2 || rj == 3) o.push_back({l + 1, ri, rj});
+                       },
+                       d_rval_ + ring_nbase_[(size_t)l]);
+      }
+    }
+  }
   std::vector<int4> citems, ritems;
   cheb_group_off_.assign(16, 0);
   ring_group_off_.assign(16, 0);
@@ -882,7 +947,28 @@ void DeviceOperator::build_cheb(int p_lo, int p_hi) {
       if (n_xboxes_)
         cuda_check(cudaMemcpy(d_xboxes_, xboxes.data(), xboxes.size() * sizeof(int),
                               cudaMemcpyHostToDevice), "H2D x-ring boxes");
-      setup_xring_gemm(xboxes);
+      {  // the X-node pass as a GEMM: per class the 7 level-(L-1) inner blocks
+         // (ring mode 1), then the 20 level-L outer-ring leaves (lsplit 4)
+        const long double pi = 3.141592653589793238462643383279502884L;
+        std::vector<double> rx((size_t)NX);
+        for (int i = 0; i < NX; ++i)
+          rx[(size_t)i] = 0.5 * P_.cell[L_ - 1] * (double)cosl(pi * (i + 0.5L) / NX);
+        const int Lx = L_ - 1;
+        make_gemm_pass(gx_, Lx, NX, rx, xboxes, true,
+                       [&](int c, std::vector<GemmOff>& o) {
+                         const int cx = c >> 1, cy = c & 1;
+                         for (int ri = -1; ri <= 2; ++ri)
+                           for (int rj = -1; rj <= 2; ++rj) {
+                             const int dx = ri - cx, dy = rj - cy;
+                             if (std::max(std::abs(dx), std::abs(dy)) >= 2) o.push_back({Lx, dx, dy});
+                           }
+                         for (int ri = -2; ri <= 3; ++ri)
+                           for (int rj = -2; rj <= 3; ++rj)
+                             if (ri == -2 || ri == 3 || rj == -2 || rj == 3) o.push_back({L_, ri, rj});
+                       },
+                       d_xval_);
+        xgemm_ = gx_.on;
+      }
     }
   }
   n_cheb_items_ = (int)citems.size();
@@ -1038,7 +1124,22 @@ ListCheck DeviceOperator::far_list_check(int max_targets) {
   std::vector<int4> o((size_t)nt);
   try {
     cuda_check(cudaMemcpy(d_t, tg.data(), tg.size() * sizeof(int), cudaMemcpyHostToDevice), "H2D");
-    imqk::launch_far_cover(P_, d_t, nt, Mo, d_o, stream_);
+    imqk::CoverGemm Gm{};
+    for (size_t l = 0; l < gnode_.size() && l <= (size_t)imqk::kMaxLevels; ++l)
+      if (gnode_[l].on) {
+        Gm.node[l] = gnode_[l].d_D;
+        Gm.node_nd[l] = gnode_[l].n_deltas;
+      }
+    for (size_t l = 0; l < gring_.size() && l <= (size_t)imqk::kMaxLevels; ++l)
+      if (gring_[l].on) {
+        Gm.ring[l] = gring_[l].d_D;
+        Gm.ring_nd[l] = gring_[l].n_deltas;
+      }
+    if (xgemm_ && gx_.on) {
+      Gm.x = gx_.d_D;
+      Gm.x_nd = gx_.n_deltas;
+    }
+    imqk::launch_far_cover(P_, d_t, nt, Mo, Gm, d_o, stream_);
     cuda_check(cudaStreamSynchronize(stream_), "list check");
     cuda_check(cudaGetLastError(), "list check kernel");
     cuda_check(cudaMemcpy(o.data(), d_o, o.size() * sizeof(int4), cudaMemcpyDeviceToHost), "D2H");
@@ -1060,100 +1161,121 @@ ListCheck DeviceOperator::far_list_check(int max_targets) {
   return r;
 }
 
-// The X-node pass as tensor-core GEMMs (nodegemm.cu): the basis of every
-// (node, source offset) pair of a level-(L-1) box is the same for all boxes,
-// so A_delta[k][n] is formed once here (long double, the reference's
-// truncated expansion in the monomial form) for the 20
-// level-L outer-ring offsets and, per box class (the box's position in its
-// parent: its level-(L-1) inner list depends on it), the 7 level-(L-1) inner
-// offsets, exactly the lists build_far_list enumerates (ring mode 1 at level
-// L-1, lsplit 4 at level L).  Boxes are grouped by class.
-void DeviceOperator::setup_xring_gemm(const std::vector<int>& xboxes) {
-  dfree(d_gA_);
-  dfree(d_gD_);
-  dfree(d_gboxes_);
-  xgemm_ = false;
-  constexpr int NX = imqk::kChebNX, NXX = NX * NX;
-  if (!imqk::m2p_specialised(M_) || NXX % 8 || xboxes.empty()) return;
-  const int Lx = L_ - 1, k2pad = imqk::node_gemm_k2pad(K_);
-  const long double pi = 3.141592653589793238462643383279502884L;
-  const long double hx = 0.5L * (long double)P_.cell[Lx], cL = (long double)P_.cell[L_];
-  const long double cX = (long double)P_.cell[Lx], t2 = (long double)P_.t2;
-  // Horner order of the stored coefficients: m = M..0, k = top(m)..m
-  std::vector<std::pair<int, int>> jm;
-  for (int m = M_; m >= 0; --m)
-    for (int k = horner_top(M_, m); k >= m; --k) jm.push_back({m, k});
-  struct Off { int level, dx, dy; long double sx, sy; };
-  std::vector<Off> offs;  // per class: 7 inner (level L-1), then the 20 outer (level L)
-  for (int cls = 0; cls < 4; ++cls) {
-    const int cx = cls >> 1, cy = cls & 1;
-    for (int ri = -1; ri <= 2; ++ri)
-      for (int rj = -1; rj <= 2; ++rj) {
-        const int dx = ri - cx, dy = rj - cy;
-        if (std::max(std::abs(dx), std::abs(dy)) < 2) continue;
-        offs.push_back({Lx, dx, dy, dx * cX, dy * cX});
-      }
-    for (int ri = -2; ri <= 3; ++ri)
-      for (int rj = -2; rj <= 3; ++rj) {
-        if (!(ri == -2 || ri == 3 || rj == -2 || rj == 3)) continue;
-        offs.push_back({L_, ri, rj, (ri - 0.5L) * cL, (rj - 0.5L) * cL});
-      }
-  }
-  const int nd = (int)offs.size() / 4;  // 27
-  std::vector<double> A((size_t)offs.size() * k2pad * NXX, 0.0);
-  std::vector<long double> tc((size_t)NX);
-  for (int i = 0; i < NX; ++i) tc[(size_t)i] = hx * cosl(pi * (i + 0.5L) / NX);
-  for (size_t d = 0; d < offs.size(); ++d) {
-    double* Ad = A.data() + d * (size_t)k2pad * NXX;
-    for (int n = 0; n < NXX; ++n) {
-      const long double dx = tc[(size_t)(n / NX)] - offs[d].sx, dy = tc[(size_t)(n % NX)] - offs[d].sy;
-      const long double r = 1.0L / sqrtl(dx * dx + dy * dy + t2), q = r * r;
-      const long double xr = dx * q, xi = -dy * q;  // conj(xi)
-      // powers conj(xi)^m and q^p
-      std::vector<long double> pr((size_t)M_ + 1), pim((size_t)M_ + 1), qp((size_t)M_ + 1);
-      pr[0] = 1.0L;
-      pim[0] = 0.0L;
-      qp[0] = 1.0L;
-      for (int m = 1; m <= M_; ++m) {
-        pr[(size_t)m] = pr[(size_t)m - 1] * xr - pim[(size_t)m - 1] * xi;
-        pim[(size_t)m] = pr[(size_t)m - 1] * xi + pim[(size_t)m - 1] * xr;
-        qp[(size_t)m] = qp[(size_t)m - 1] * q;
-      }
-      for (size_t j = 0; j < jm.size(); ++j) {
-        const int m = jm[j].first, k = jm[j].second;
-        const long double f = r * qp[(size_t)(k - m)];
-        Ad[(2 * j) * (size_t)NXX + (size_t)n] = (double)(f * pr[(size_t)m]);
-        Ad[(2 * j + 1) * (size_t)NXX + (size_t)n] = (double)(-f * pim[(size_t)m]);
-      }
+// Node passes as tensor-core GEMMs (nodegemm.cu).  The nodes of every box of
+// a level sit at the same positions relative to the box, and a box's list is
+// a fixed set of source offsets (per class = the box's position in its parent
+// where the list depends on it), so the basis A_delta[k][n] of every (node,
+// offset) pair is formed once here (k_gemm_basis: the reference's truncated
+// expansion in the monomial form) and each pass is one GEMM
+// launch.  The offsets are exactly those build_far_list enumerates for the
+// pass (the device list check replays both, k_far_cover).
+void DeviceOperator::free_gemm_pass(GemmPass& g) {
+  dfree(g.d_A);
+  dfree(g.d_D);
+  dfree(g.d_boxes);
+  g = GemmPass{};
+}
+
+void DeviceOperator::make_gemm_pass(GemmPass& g, int box_level, int n_per_dim,
+                                    const std::vector<double>& rel, const std::vector<int>& boxes,
+                                    bool by_class,
+                                    const std::function<void(int, std::vector<GemmOff>&)>& offsets,
+                                    double* out) {
+  free_gemm_pass(g);
+  const int n_nodes = n_per_dim * n_per_dim, mt = imqk::node_gemm_mt(n_nodes);
+  if (!imqk::m2p_specialised(M_) || mt == 0 || boxes.empty()) return;
+  const int mp = 8 * mt, k2pad = imqk::node_gemm_k2pad(K_), ncls = by_class ? 4 : 1;
+  // offsets per class; unique (level, dx, dy) -> one basis matrix
+  std::vector<std::vector<GemmOff>> per((size_t)ncls);
+  std::vector<GemmOff> uniq;
+  std::vector<std::vector<int>> idx((size_t)ncls);
+  int nd = 0;
+  for (int c = 0; c < ncls; ++c) {
+    offsets(c, per[(size_t)c]);
+    nd = std::max(nd, (int)per[(size_t)c].size());
+    for (const GemmOff& o : per[(size_t)c]) {
+      int u = 0;
+      while (u < (int)uniq.size() &&
+             !(uniq[(size_t)u].level == o.level && uniq[(size_t)u].dx == o.dx && uniq[(size_t)u].dy == o.dy))
+        ++u;
+      if (u == (int)uniq.size()) uniq.push_back(o);
+      idx[(size_t)c].push_back(u);
     }
   }
-  d_gA_ = dalloc<double>(A.size(), "x-ring gemm basis");
-  cuda_check(cudaMemcpy(d_gA_, A.data(), A.size() * sizeof(double), cudaMemcpyHostToDevice),
-             "H2D basis");
-  std::vector<imqk::GemmDelta> D(offs.size());
-  for (size_t d = 0; d < offs.size(); ++d)
-    D[d] = {offs[d].level, offs[d].dx, offs[d].dy, 0, d_gA_ + d * (size_t)k2pad * NXX};
-  d_gD_ = dalloc<imqk::GemmDelta>(D.size(), "x-ring gemm offsets");
-  cuda_check(cudaMemcpy(d_gD_, D.data(), D.size() * sizeof(imqk::GemmDelta),
-                        cudaMemcpyHostToDevice), "H2D offsets");
-  std::vector<int> bx;
-  gcls_.n = 4;
-  const int tile = imqk::node_gemm_tile();
-  gcls_.box_off[0] = 0;
-  gcls_.tile_off[0] = 0;
-  for (int cls = 0; cls < 4; ++cls) {
-    for (int q : xboxes)
-      if ((q & 3) == cls) bx.push_back(q);
-    gcls_.box_off[cls + 1] = (int)bx.size();
-    const int nb = gcls_.box_off[cls + 1] - gcls_.box_off[cls];
-    gcls_.tile_off[cls + 1] = gcls_.tile_off[cls] + (nb + tile - 1) / tile;
+  if (nd == 0) return;
+  // source centres relative to the box centre: level box_level + sh, cell index
+  // (b << sh) + d -> (d + 0.5 - 2^sh / 2) cell_src
+  std::vector<double> sx(uniq.size()), sy(uniq.size()), nx((size_t)n_nodes), ny((size_t)n_nodes);
+  for (size_t u = 0; u < uniq.size(); ++u) {
+    const int sh = uniq[u].level - box_level;
+    const double cs = P_.cell[uniq[u].level], base = 0.5 - 0.5 * (double)(1 << sh);
+    sx[u] = (uniq[u].dx + base) * cs;
+    sy[u] = (uniq[u].dy + base) * cs;
   }
-  d_gboxes_ = dalloc<int>(bx.size(), "x-ring gemm boxes");
-  cuda_check(cudaMemcpy(d_gboxes_, bx.data(), bx.size() * sizeof(int), cudaMemcpyHostToDevice),
+  for (int n = 0; n < n_nodes; ++n) {
+    nx[(size_t)n] = rel[(size_t)(n / n_per_dim)];
+    ny[(size_t)n] = rel[(size_t)(n % n_per_dim)];
+  }
+  double* d_tmp = dalloc<double>(2 * uniq.size() + 2 * (size_t)n_nodes, "gemm geometry");
+  try {
+    cuda_check(cudaMemcpy(d_tmp, sx.data(), sx.size() * sizeof(double), cudaMemcpyHostToDevice), "H2D");
+    cuda_check(cudaMemcpy(d_tmp + uniq.size(), sy.data(), sy.size() * sizeof(double),
+                          cudaMemcpyHostToDevice), "H2D");
+    cuda_check(cudaMemcpy(d_tmp + 2 * uniq.size(), nx.data(), nx.size() * sizeof(double),
+                          cudaMemcpyHostToDevice), "H2D");
+    cuda_check(cudaMemcpy(d_tmp + 2 * uniq.size() + n_nodes, ny.data(), ny.size() * sizeof(double),
+                          cudaMemcpyHostToDevice), "H2D");
+    g.d_A = dalloc<double>(uniq.size() * (size_t)k2pad * mp, "gemm basis");
+    imqk::launch_gemm_basis(g.d_A, d_tmp, d_tmp + uniq.size(), (int)uniq.size(),
+                            d_tmp + 2 * uniq.size(), d_tmp + 2 * uniq.size() + n_nodes, n_nodes, mp,
+                            k2pad, M_, P_.t2, stream_);
+    cuda_check(cudaStreamSynchronize(stream_), "gemm basis");
+    cuda_check(cudaGetLastError(), "gemm basis");
+  } catch (...) {
+    dfree(d_tmp);
+    throw;
+  }
+  dfree(d_tmp);
+  std::vector<imqk::GemmDelta> D((size_t)ncls * nd);
+  for (int c = 0; c < ncls; ++c)
+    for (int d = 0; d < nd; ++d) {
+      if (d < (int)idx[(size_t)c].size()) {
+        const GemmOff& o = uniq[(size_t)idx[(size_t)c][(size_t)d]];
+        D[(size_t)c * nd + d] = {o.level, o.dx, o.dy, 0,
+                                 g.d_A + (size_t)idx[(size_t)c][(size_t)d] * k2pad * mp};
+      } else {  // padding: a source outside every grid (no contribution)
+        D[(size_t)c * nd + d] = {box_level, 1 << 28, 0, 0, g.d_A};
+      }
+    }
+  g.d_D = dalloc<imqk::GemmDelta>(D.size(), "gemm offsets");
+  cuda_check(cudaMemcpy(g.d_D, D.data(), D.size() * sizeof(imqk::GemmDelta), cudaMemcpyHostToDevice),
+             "H2D offsets");
+  std::vector<int> bx;
+  const int tile = imqk::node_gemm_tile();
+  g.cls.n = ncls;
+  g.cls.box_off[0] = 0;
+  g.cls.tile_off[0] = 0;
+  for (int c = 0; c < ncls; ++c) {
+    for (int q : boxes)
+      if (!by_class || (q & 3) == c) bx.push_back(q);
+    g.cls.box_off[c + 1] = (int)bx.size();
+    g.cls.tile_off[c + 1] = g.cls.tile_off[c] + (g.cls.box_off[c + 1] - g.cls.box_off[c] + tile - 1) / tile;
+  }
+  g.d_boxes = dalloc<int>(bx.size(), "gemm boxes");
+  cuda_check(cudaMemcpy(g.d_boxes, bx.data(), bx.size() * sizeof(int), cudaMemcpyHostToDevice),
              "H2D boxes");
-  gemm_nd_ = nd;
-  gemm_k2pad_ = k2pad;
-  xgemm_ = true;
+  g.box_level = box_level;
+  g.n_nodes = n_nodes;
+  g.n_deltas = nd;
+  g.k2pad = k2pad;
+  g.out = out;
+  g.on = true;
+}
+
+void DeviceOperator::launch_gemm_pass(const GemmPass& g, cudaStream_t s) {
+  if (g.on)
+    imqk::launch_node_gemm(P_, g.box_level, g.d_boxes, g.cls, g.d_D, g.n_deltas, g.k2pad, d_coef_,
+                           g.out, g.n_nodes, s);
 }
 
 void DeviceOperator::restrict_targets(int p_lo, int p_hi) {
@@ -1508,13 +1630,15 @@ void DeviceOperator::far_near(const double* d_us, double* d_out, const int* perm
       // (parent restricted + own), summed at the targets of the level-lc boxes
       far_pass(0, n_cheb_items_, cheb_group_off_.data(), nullptr, 0, nullptr, nullptr, d_cval_,
                nullptr, 1, cheb_lc_, &Pn_, d_cheb_items_);
+      for (const GemmPass& g : gnode_) launch_gemm_pass(g, s);  // the GEMM levels
       if (ring_)  // the level-(l+1) rings at the NR x NR nodes of the level-l boxes
         far_pass(0, n_ring_items_, ring_group_off_.data(), nullptr, 0, nullptr, nullptr, d_rval_,
                  nullptr, 2, L_ - 1, &Pr_, d_ring_items_);
+      if (ring_)
+        for (const GemmPass& g : gring_) launch_gemm_pass(g, s);
       if (xr && xgemm_)  // at the NX x NX nodes of each level-(L-1) box X: its level-(L-1)
                          // inner blocks and its level-L outer ring, as GEMMs
-        imqk::launch_node_gemm(P_, L_ - 1, d_gboxes_, gcls_, d_gD_, gemm_nd_, gemm_k2pad_, d_coef_,
-                               d_xval_, imqk::kChebNX * imqk::kChebNX, s);
+        launch_gemm_pass(gx_, s);
       else if (xr)  // the same through k_m2p_far (ring mode 1 at level L-1, lsplit 4 at L)
         far_pass(0, n_xring_items_, xring_group_off_.data(), nullptr, 0, nullptr, nullptr,
                  d_xval_, nullptr, L_ - 1, L_, &Px_, d_xring_items_, 1, 4);
@@ -1916,9 +2040,11 @@ int DeviceOperator::kernel_launches_per_apply() const {
          groups(lpart_group_off_);
     if (cheb_) {
       n += groups(cheb_group_off_) + cheb_lc_ + 1;  // node groups, coefficients, evaluation
+      for (const GemmPass& g : gnode_) n += g.on ? 1 : 0;
       if (ring_) {
         n += groups(ring_group_off_) + 1;  // ring node groups, level-(L-1) ring coefficients
         if (xring_) n += (xgemm_ ? 1 : groups(xring_group_off_)) + 1;  // X-node pass, coefficients
+        for (const GemmPass& g : gring_) n += g.on ? 1 : 0;
         for (int l = std::max(2, ring_l0_); l <= cheb_lc_; ++l) ++n;  // coarse ring coefficients
       }
     } else {
@@ -1934,19 +2060,23 @@ void DeviceOperator::fill_eval_counts() {
   const int lc = cheb_ ? cheb_lc_ : 0;
   const bool rings = cheb_ && ring_ && ring_par_by_level_.size() == far_by_level_.size();
   constexpr double NN = imqk::kChebN * imqk::kChebN, NRR = imqk::kChebNR * imqk::kChebNR;
-  double direct = 0, nodes = 0;
+  double direct = 0, nodes = 0, gemm = 0;
   for (int l = 1; l <= L_ && l < (int)far_by_level_.size(); ++l) {
     if (l <= lc) {
       const double npl = (size_t)l < inner_v_.size() && inner_v_[(size_t)l]
                              ? (double)imqk::kChebNI * imqk::kChebNI : NN;
-      nodes += (lists_by_level_[(size_t)l] -
-                (rings && l >= ring_l0_ ? ring_child_by_level_[(size_t)l] : 0.0)) * npl;
+      const double p = (lists_by_level_[(size_t)l] -
+                        (rings && l >= ring_l0_ ? ring_child_by_level_[(size_t)l] : 0.0)) * npl;
+      nodes += p;
+      if ((size_t)l < gnode_.size() && gnode_[(size_t)l].on) gemm += p;
     }
     else
       direct += far_by_level_[(size_t)l];
     if (rings && l >= ring_l0_ && l < L_ && (size_t)l - 1 < ring_v_.size()) {
       const double nr = imqk::kRingNr[ring_v_[(size_t)l - 1]];
-      nodes += ring_par_by_level_[(size_t)l] * nr * nr;
+      const double p = ring_par_by_level_[(size_t)l] * nr * nr;
+      nodes += p;
+      if ((size_t)l - 1 < gring_.size() && gring_[(size_t)l - 1].on) gemm += p;
     }
   }
   if (rings) direct -= ring_direct_;
@@ -1955,10 +2085,9 @@ void DeviceOperator::fill_eval_counts() {
     const double inner_lm1 = lists_by_level_[(size_t)L_ - 1] - ring_child_by_level_[(size_t)L_ - 1];
     direct -= xring_direct_ + (far_by_level_[(size_t)L_ - 1] - ring_direct_);
     nodes += (xring_lists_ + inner_lm1) * imqk::kChebNX * imqk::kChebNX;
-    counts_.gemm_node_pairs = xgemm_ ? (xring_lists_ + inner_lm1) * imqk::kChebNX * imqk::kChebNX : 0.0;
-  } else {
-    counts_.gemm_node_pairs = 0.0;
+    if (xgemm_) gemm += (xring_lists_ + inner_lm1) * imqk::kChebNX * imqk::kChebNX;
   }
+  counts_.gemm_node_pairs = gemm;
   counts_.far_pairs_direct = direct;
   counts_.cheb_node_pairs = nodes;
   counts_.cheb_levels = lc;

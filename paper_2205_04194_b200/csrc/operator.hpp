@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <functional>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -305,14 +306,30 @@ class DeviceOperator {
   double *d_xnx_ = nullptr, *d_xny_ = nullptr, *d_xval_ = nullptr;
   uint32_t* d_xnleaf_ = nullptr;
   int4* d_xring_items_ = nullptr;
-  // X-node pass as tensor-core GEMMs (setup_xring_gemm, nodegemm.cu)
-  void setup_xring_gemm(const std::vector<int>& xboxes);
+  // node passes as tensor-core GEMMs (nodegemm.cu): the X-node pass, the
+  // node pass of levels 2..lc, the rings (make_gemm_pass)
+  struct GemmPass {
+    bool on = false;
+    int box_level = 0, n_nodes = 0, n_deltas = 0, k2pad = 0;
+    imqk::GemmClasses cls{};
+    double* d_A = nullptr;
+    imqk::GemmDelta* d_D = nullptr;
+    int* d_boxes = nullptr;
+    double* out = nullptr;  // node values of box q at out + q * n_nodes
+  };
+  struct GemmOff {
+    int level, dx, dy;
+  };
+  void make_gemm_pass(GemmPass& g, int box_level, int n_per_dim, const std::vector<double>& rel,
+                      const std::vector<int>& boxes, bool by_class,
+                      const std::function<void(int, std::vector<GemmOff>&)>& offsets,
+                      double* out);
+  void free_gemm_pass(GemmPass& g);
+  void launch_gemm_pass(const GemmPass& g, cudaStream_t s);
+  GemmPass gx_;                          // X-node pass (level L-1 boxes)
+  std::vector<GemmPass> gnode_, gring_;  // per level l: node pass of level l / ring of level l+1
   bool xgemm_ = false;
-  double* d_gA_ = nullptr;
-  imqk::GemmDelta* d_gD_ = nullptr;
-  int* d_gboxes_ = nullptr;
-  imqk::GemmClasses gcls_{};
-  int gemm_nd_ = 0, gemm_k2pad_ = 0;
+
   int* d_xboxes_ = nullptr;
   int n_ring_items_ = 0;
   size_t ring_nodes_ = 0;
