@@ -31,6 +31,10 @@
 #include "imq_device.cuh"
 #include "imq_kernels.hpp"
 
+#ifndef IMQ_M2T_SMALL
+#define IMQ_M2T_SMALL 1024  // parents up to which a level uses the warp-per-parent kernel (0 / 1024 / 4096 / 16384: moments 2.23 / 2.18 / 2.28 / 2.61 ms at config 4)
+#endif
+
 namespace imqk {
 using namespace imqdev;
 
@@ -470,6 +474,7 @@ __global__ void k_transform(const TreeParams P, int level, const double2* __rest
 //   4. mu' is written (and, with coef_parent, transformed too: level 1).
 // The children are summed in a fixed order (c = 0..3): deterministic.
 constexpr int kM2tWarps = 8;
+constexpr long long kM2tSmallLevel = IMQ_M2T_SMALL;
 constexpr int kM2tMaxAcc = 8;  // Ke <= 256 outputs per warp (M <= 30)
 struct M2tLayout {             // dynamic shared memory layout (bytes)
   int M, H, Ke, K, nnz, ny, ysz;
@@ -1527,7 +1532,10 @@ void launch_m2m_tr(const TreeParams& P, int level, const int* plist, long long p
                    double2* coef_parent, const double2* V, const double2* W,
                    const TransformTable& T, cudaStream_t s) {
   if (np <= 0) return;
-  if (m2m_specialised(P.M)) {
+  // few parents (coarse levels): the warp-per-parent kernel spreads one
+  // parent over 32 lanes (lower latency); the specialised kernel's eight
+  // parents per warp pay ~70 us of per-warp latency whatever the level size
+  if (m2m_specialised(P.M) && np > kM2tSmallLevel) {
     const int H1 = P.M / 2 + 1;
     const size_t ss = ((((size_t)4 * H1 * H1 * 16 + (size_t)T.nnz * 12 + (size_t)(P.K + 1) * 4) + 15) &
                        ~(size_t)15) + (kM2sStage ? (size_t)kM2sWarps * kM2sSlots * 4 * P.Ke * 16 : 0);
