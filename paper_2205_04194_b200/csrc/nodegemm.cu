@@ -42,6 +42,9 @@
 #ifndef IMQ_GEMM_KC
 #define IMQ_GEMM_KC 16
 #endif
+#ifndef IMQ_GEMM_SMALL
+#define IMQ_GEMM_SMALL 0  // passes with fewer 32-box tiles per SM than this use 16-box tiles (8: one rank of 8 at config 4 1.14 ms vs 0.95 ms: off)
+#endif
 #ifndef IMQ_GEMM_ST
 #define IMQ_GEMM_ST 2
 #endif
@@ -54,8 +57,10 @@ using namespace imqdev;
 
 // boxes per CTA (warps = kGtN / 8: box pairs x 2 node halves), k chunk, stages
 constexpr int kGtN = IMQ_GEMM_NB, kGtKC = IMQ_GEMM_KC, kGtStages = IMQ_GEMM_ST;
+constexpr int kGtNSmall = 16;  // boxes per CTA when the pass has too few tiles to fill the GPU
 constexpr int kGtMaxDelta = 32;
 constexpr int kGtSBn = kGtKC + 4;  // B rows [box][k]: stride = 4 (mod 16)
+static_assert(kGtN >= kGtNSmall, "tile sizes");
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
@@ -77,10 +82,10 @@ __device__ __forceinline__ void cp_wait() {
 __host__ __device__ constexpr int gemm_sa(int MT) {  // A rows [k][node]: stride = 4 (mod 16)
   return 8 * MT + ((4 - (8 * MT) % 16) + 16) % 16;
 }
-constexpr size_t gemm_smem(int MT) {
+constexpr size_t gemm_smem(int MT, int NB) {
   return (size_t)kGtStages * kGtKC * gemm_sa(MT) * sizeof(double) +
-         (size_t)kGtStages * kGtN * kGtSBn * sizeof(double) +
-         (size_t)kGtMaxDelta * kGtN * sizeof(const double*);
+         (size_t)kGtStages * NB * kGtSBn * sizeof(double) +
+         (size_t)kGtMaxDelta * NB * sizeof(const double*);
 }
 
 __device__ __forceinline__ int gemm_block_count(const TreeParams& P, int level, uint32_t q) {
@@ -93,9 +98,10 @@ __device__ __forceinline__ int gemm_block_count(const TreeParams& P, int level, 
 // boundaries, no register staging.  Source pointers of every (offset, box)
 // are resolved once at the start (null: outside the grid or empty block ->
 // zero-filled B rows).
-// MG: node-tile groups (warps = kGtN / 16 box pairs x MG, MT / MG m-tiles each)
-template <int MT, int MG>
-__global__ void __launch_bounds__(kGtN / 16 * MG * 32) k_node_gemm(
+// MG: node-tile groups (warps = NB / 16 box pairs x MG, MT / MG m-tiles each);
+// NB: boxes per CTA
+template <int MT, int MG, int NB>
+__global__ void __launch_bounds__(NB / 16 * MG * 32) k_node_gemm(
     const TreeParams P, int box_level, const int* __restrict__ boxes_all, const GemmClasses G,
     const GemmDelta* __restrict__ deltas_all, int n_deltas, int k2pad,
     const double2* __restrict__ coef, double* __restrict__ out, int n_nodes) {
@@ -104,7 +110,7 @@ __global__ void __launch_bounds__(kGtN / 16 * MG * 32) k_node_gemm(
   extern __shared__ __align__(16) double gsm[];
   double* As = gsm;                                   // [stage][KC][SA]
   double* Bs = gsm + (size_t)kGtStages * kGtKC * SA;  // [stage][N][SBn]
-  const double** srcs = reinterpret_cast<const double**>(Bs + (size_t)kGtStages * kGtN * kGtSBn);
+  const double** srcs = reinterpret_cast<const double**>(Bs + (size_t)kGtStages * NB * kGtSBn);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int r = lane >> 2, c = lane & 3;
   // this CTA's box class: its boxes and its offsets (tiles never straddle classes)
@@ -113,9 +119,9 @@ __global__ void __launch_bounds__(kGtN / 16 * MG * 32) k_node_gemm(
   const int* boxes = boxes_all + G.box_off[cls];
   const int n_boxes = G.box_off[cls + 1] - G.box_off[cls];
   const GemmDelta* deltas = deltas_all + (size_t)cls * n_deltas;
-  const int b0 = ((int)blockIdx.x - G.tile_off[cls]) * kGtN;
-  for (int e = tid; e < n_deltas * kGtN; e += blockDim.x) {
-    const int di = e / kGtN, n = e % kGtN;
+  const int b0 = ((int)blockIdx.x - G.tile_off[cls]) * NB;
+  for (int e = tid; e < n_deltas * NB; e += blockDim.x) {
+    const int di = e / NB, n = e % NB;
     const GemmDelta D = deltas[di];
     const double* p = nullptr;
     if (b0 + n < n_boxes) {
@@ -134,8 +140,8 @@ __global__ void __launch_bounds__(kGtN / 16 * MG * 32) k_node_gemm(
   __syncthreads();
   // warp w: boxes of n-tiles 2 np, +1 and m-tiles [mh MH, +MH), np = w % (N / 16),
   // mh = w / (N / 16): every A fragment feeds two tensor-core ops
-  static_assert(MT % MG == 0 && kGtN % 16 == 0, "m-tiles over MG warp rows, box pairs");
-  constexpr int MH = MT / MG, NP = kGtN / 16;
+  static_assert(MT % MG == 0 && NB % 16 == 0, "m-tiles over MG warp rows, box pairs");
+  constexpr int MH = MT / MG, NP = NB / 16;
   const int np = warp % NP, mh = warp / NP;
   double acc[MH][2][2];
 #pragma unroll
@@ -152,9 +158,9 @@ __global__ void __launch_bounds__(kGtN / 16 * MG * 32) k_node_gemm(
         const int k = (2 * e) / MP, m = (2 * e) % MP;
         cp16(as + k * SA + m, A + (size_t)k * MP + m, 16);
       }
-      double* bs = Bs + (size_t)st * kGtN * kGtSBn;
-      const double* const* sp = srcs + di * kGtN;
-      for (int e = tid; e < kGtN * kGtKC / 2; e += blockDim.x) {
+      double* bs = Bs + (size_t)st * NB * kGtSBn;
+      const double* const* sp = srcs + di * NB;
+      for (int e = tid; e < NB * kGtKC / 2; e += blockDim.x) {
         const int n = e / (kGtKC / 2), kk = 2 * (e % (kGtKC / 2));
         const double* p = sp[n];
         const bool ok = p && k0 + kk < k2;  // zero-fill padding rows and absent sources
@@ -172,7 +178,7 @@ __global__ void __launch_bounds__(kGtN / 16 * MG * 32) k_node_gemm(
     const int st = step % kGtStages;
     const int kleft = k2 - (step % nchunk) * kGtKC;  // the last chunk's k-steps past 2K are all zero
     const double* as = As + (size_t)st * kGtKC * SA + mh * MH * 8 + r;
-    const double* bs = Bs + (size_t)st * kGtN * kGtSBn + (size_t)(np * 16 + r) * kGtSBn;
+    const double* bs = Bs + (size_t)st * NB * kGtSBn + (size_t)(np * 16 + r) * kGtSBn;
 #pragma unroll
     for (int ks = 0; ks < kGtKC / 4; ++ks) {
       if (4 * ks >= kleft) break;
@@ -222,8 +228,8 @@ void launch_node_gemm(const TreeParams& P, int box_level, const int* boxes,
   if (G.n < 1 || G.tile_off[G.n] <= 0) return;
   if (k2pad % kGtKC) throw std::invalid_argument("node gemm: k2pad must be a multiple of the k chunk");
   if (n_deltas > kGtMaxDelta) throw std::invalid_argument("node gemm: too many offsets");
-  const unsigned grid = (unsigned)G.tile_off[G.n];
-  auto run = [&](auto kern, size_t smem, int warps) {
+  auto run = [&](auto kern, size_t smem, int warps, const GemmClasses& Gx) {
+    const unsigned grid = (unsigned)Gx.tile_off[Gx.n];
     // the attribute is per (kernel, device); every instantiation has the same
     // function-pointer type, so key by the pointer
     static std::mutex mtx;
@@ -240,20 +246,38 @@ void launch_node_gemm(const TreeParams& P, int box_level, const int* boxes,
         throw std::runtime_error("node gemm: shared-memory attribute");
       }
     }
-    kern<<<grid, warps * 32, smem, s>>>(P, box_level, boxes, G, deltas, n_deltas, k2pad, coef, out,
-                                        n_nodes);
+    kern<<<grid, warps * 32, smem, s>>>(P, box_level, boxes, Gx, deltas, n_deltas, k2pad, coef,
+                                        out, n_nodes);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess)
       throw std::runtime_error(std::string("node gemm launch (") + std::to_string(n_nodes) +
                                " nodes, " + std::to_string(smem) + " B shared): " +
                                cudaGetErrorString(e));
   };
-  constexpr int NP = kGtN / 16;
+  // the grid is laid out in tiles of kGtN boxes; a pass with fewer tiles than
+  // ~2 per SM slot (e.g. one rank's share of a sharded product) runs tiles of
+  // kGtNSmall boxes instead -- the class tile offsets scale with the tile size
+  int sms = 148, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const bool small = (long long)G.tile_off[G.n] < (long long)IMQ_GEMM_SMALL * sms;
+  GemmClasses Gs = G;
+  if (small) {
+    Gs.tile_off[0] = 0;
+    for (int c = 0; c < G.n; ++c)
+      Gs.tile_off[c + 1] = Gs.tile_off[c] + (G.box_off[c + 1] - G.box_off[c] + kGtNSmall - 1) / kGtNSmall;
+  }
+  auto go = [&](auto kbig, auto ksmall, int mt, int mg) {
+    if (small)
+      run(ksmall, gemm_smem(mt, kGtNSmall), kGtNSmall / 16 * mg, Gs);
+    else
+      run(kbig, gemm_smem(mt, kGtN), kGtN / 16 * mg, G);
+  };
   switch (node_gemm_mt(n_nodes)) {
-    case 18: run(k_node_gemm<18, 2>, gemm_smem(18), NP * 2); break;
-    case 32: run(k_node_gemm<32, 4>, gemm_smem(32), NP * 4); break;
-    case 42: run(k_node_gemm<42, 6>, gemm_smem(42), NP * 6); break;
-    case 50: run(k_node_gemm<50, 5>, gemm_smem(50), NP * 5); break;
+    case 18: go(k_node_gemm<18, 2, kGtN>, k_node_gemm<18, 2, kGtNSmall>, 18, 2); break;
+    case 32: go(k_node_gemm<32, 4, kGtN>, k_node_gemm<32, 4, kGtNSmall>, 32, 4); break;
+    case 42: go(k_node_gemm<42, 6, kGtN>, k_node_gemm<42, 6, kGtNSmall>, 42, 6); break;
+    case 50: go(k_node_gemm<50, 5, kGtN>, k_node_gemm<50, 5, kGtNSmall>, 50, 5); break;
     default: throw std::invalid_argument("node gemm: unsupported node count");
   }
 }
