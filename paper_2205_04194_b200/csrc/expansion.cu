@@ -905,6 +905,30 @@ __device__ int build_far_list(const TreeParams& P, uint32_t par, int s, int cnt,
   return n;
 }
 
+// The partial pass's per-leaf list, one leaf per half-warp (all 32 lanes
+// call; lane l evaluates candidate l & 15 of its half's leaf): the level-L
+// leaves of the 4x4 inner square of the leaf's level-(L-1) block at Chebyshev
+// distance >= 2 from the leaf, non-empty, in the reference's row-major list
+// order -- exactly build_far_list(lsplit = 2) for a one-leaf item.
+__device__ int leaf_inner_list(const TreeParams& P, uint32_t leaf, bool active, int lane,
+                               uint32_t* list) {
+  const int L = P.L, g = 1 << (L + 1), c = lane & 15;
+  int ci, cj;
+  demorton(leaf, ci, cj);
+  const int qi = (ci & ~1) - 1 + (c >> 2), qj = (cj & ~1) - 1 + (c & 3);
+  bool keep = active && qi >= 0 && qj >= 0 && qi < g && qj < g &&
+              max(abs(qi - ci), abs(qj - cj)) >= 2;
+  uint32_t q = 0;
+  if (keep) {
+    q = morton((uint32_t)qi, (uint32_t)qj);
+    keep = block_count(P, L, q) > 0;
+  }
+  const uint32_t bal = (__ballot_sync(0xffffffffu, keep) >> (lane & 16)) & 0xffffu;
+  if (keep) list[__popc(bal & ((1u << c) - 1u))] = ((uint32_t)L << 28) | q;
+  __syncwarp();
+  return __popc(bal);
+}
+
 // -------------------------------------------------------- list cover check --
 // imq_verify / tests: for each listed target, replays every far pass of the
 // product (modes from the operator: single pass, coarse + fine + per-leaf
@@ -960,12 +984,23 @@ __global__ void __launch_bounds__(kCoverWarps * 32) k_far_cover(const TreeParams
     ng = __shfl_sync(0xffffffffu, ng, 0);
     __syncwarp();
   };
+  // the per-leaf partial pass: its own list builder when it runs two leaves
+  // per warp (both halves enumerate this target's leaf; same entries)
+  auto add_part = [&]() {
+    if (!Mo.leaf2) return add(X, L, L, 0, 2);
+    const int n = leaf_inner_list(P, T, true, lane, lists[warp]);
+    for (int e = lane; e < n; e += 32)
+      if (ng + e < kCoverCap) got[warp][ng + e] = lists[warp][e];
+    if (ng + n > kCoverCap) overflow = 1;
+    ng = min(kCoverCap, ng + n);
+    __syncwarp();
+  };
   if (!Mo.split) {
     add(X, 1, L, 0, 0);
   } else if (!Mo.cheb) {
     add((X >> 2) << 2, 1, L - 2, 0, 0);
     add(X, L - 1, L, 0, Mo.lsplit ? 1 : 0);
-    if (Mo.lsplit) add(X, L, L, 0, 2);
+    if (Mo.lsplit) add_part();
   } else {
     for (int l = 1; l <= Mo.lc; ++l) {
       const uint32_t q = T >> (2 * (L - l));
@@ -985,9 +1020,9 @@ __global__ void __launch_bounds__(kCoverWarps * 32) k_far_cover(const TreeParams
         add_gemm(X, L - 1, Gm.x, Gm.x_nd, 4);
       else
         add(X, L - 1, L, 1, 4);
-      add(X, L, L, 0, 2);
+      add_part();
     } else {
-      if (Mo.lsplit) add(X, L, L, 0, 2);
+      if (Mo.lsplit) add_part();
       add(X, L - 1, L, Mo.ring ? 1 : 0, Mo.lsplit ? 1 : 0);
     }
   }
@@ -1369,6 +1404,102 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_m2p_far(const TreeParams P
     if ((T.valid >> p) & 1u) far_store(P, O, s0 + lane + 32 * p, acc[p]);
 }
 
+// Per-leaf partial pass, two leaves per warp: half-warp h (16 lanes) takes
+// item 2w + h -- <= 16 R targets of ONE leaf, R per lane -- against that
+// leaf's own inner-ring leaves (leaf_inner_list: the 7 of the level-(L-1)
+// block's 12 inner-ring leaves at Chebyshev distance >= 2, the reference's
+// level-L list minus the outer ring that the X-node pass covers).  A 64-point
+// leaf runs R = 4 (8 DFMA per shared load, against 4 with 32 lanes x R = 2),
+// and a 65..80-point leaf fills 80 target slots instead of 96.  Each half has
+// its own TMA staging ring and producer lane (hl == 0); the two halves' lists
+// may differ in length (domain edge, empty leaves): a half past its list
+// waits on nothing and its (stale) evaluations are discarded.  Per target the
+// sources are summed in list order with the same evaluation as k_m2p_far, so
+// the result is bitwise that of the one-leaf-per-warp pass.
+template <int M, int R, int WARPS, int STAGES, int MINB>
+__global__ void __launch_bounds__(WARPS * 32, MINB) k_m2p_leaf2(const TreeParams P,
+                                                               const int4* __restrict__ items,
+                                                               int n_items,
+                                                               const double2* __restrict__ coef,
+                                                               const FarOut O) {
+  constexpr int K = hz_count(M);
+  constexpr uint32_t kBytes = K * 16;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, hl = lane & 15;
+  const int hw = warp * 2 + (lane >> 4);  // half-warp index in the CTA
+  double2* stage = reinterpret_cast<double2*>(smem_raw) + (size_t)hw * STAGES * K;
+  uint64_t* bars =
+      reinterpret_cast<uint64_t*>(reinterpret_cast<double2*>(smem_raw) + 2 * WARPS * STAGES * K) +
+      hw * STAGES;
+  uint32_t* list = reinterpret_cast<uint32_t*>(
+                       reinterpret_cast<uint64_t*>(reinterpret_cast<double2*>(smem_raw) +
+                                                   2 * WARPS * STAGES * K) +
+                       2 * WARPS * STAGES) +
+                   hw * 16;
+  const int it0 = (blockIdx.x * WARPS + warp) * 2;
+  if (it0 >= n_items) return;
+  const int it = it0 + (lane >> 4);
+  if (hl == 0) {
+#pragma unroll
+    for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  const int4 item = it < n_items ? items[it] : make_int4(0, 0, 0, 0);
+  const uint32_t leaf = (uint32_t)item.x;
+  const int s0 = item.y, cnt = item.z;
+  const int n = leaf_inner_list(P, leaf, cnt > 0, lane, list);
+  const int nmax = max(n, __shfl_xor_sync(0xffffffffu, n, 16));
+  double tx[R], ty[R];
+  uint32_t valid = 0;
+#pragma unroll
+  for (int p = 0; p < R; ++p) {
+    const bool v = hl + 16 * p < cnt;
+    const int a = v ? s0 + hl + 16 * p : s0;
+    tx[p] = P.xs[a];
+    ty[p] = P.ys[a];
+    valid |= (v ? 1u : 0u) << p;
+  }
+  const int L = P.L;
+  auto issue = [&](int e, int slot) {
+    const uint32_t q = list[e] & 0x0fffffffu;
+    mbar_arrive_expect_tx(&bars[slot], kBytes);
+    tma_load_1d(stage + (size_t)slot * K, coef + P.coef_off[L] + (size_t)q * K, kBytes,
+                &bars[slot]);
+  };
+  if (hl == 0)
+    for (int e = 0; e < STAGES && e < n; ++e) issue(e, e);
+  double acc[R];
+#pragma unroll
+  for (int p = 0; p < R; ++p) acc[p] = 0.0;
+  for (int e = 0; e < nmax; ++e) {
+    const int slot = e % STAGES;
+    const bool live = e < n;
+    int qi = 0, qj = 0;
+    if (live) demorton(list[e] & 0x0fffffffu, qi, qj);
+    const double zx = block_center(P.ox, qi, P.cell[L]);
+    const double zy = block_center(P.oy, qj, P.cell[L]);
+    double dx[R], dy[R], v[R];
+#pragma unroll
+    for (int p = 0; p < R; ++p) {
+      dx[p] = tx[p] - zx;
+      dy[p] = ty[p] - zy;
+    }
+    if (live) mbar_wait(&bars[slot], (uint32_t)((e / STAGES) & 1));
+    far_evalT<M, R>(stage + (size_t)slot * K, dx, dy, P.t2, v);
+#pragma unroll
+    for (int p = 0; p < R; ++p) acc[p] += (live && ((valid >> p) & 1u)) ? v[p] : 0.0;
+    __syncwarp();
+    if (hl == 0 && e + STAGES < n) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(e + STAGES, slot);
+    }
+  }
+#pragma unroll
+  for (int p = 0; p < R; ++p)
+    if ((valid >> p) & 1u) far_store(P, O, s0 + hl + 16 * p, acc[p]);
+}
+
 template <int WARPS>
 __global__ void __launch_bounds__(WARPS * 32) k_m2p_far_generic(const TreeParams P,
                                                                const int4* __restrict__ items,
@@ -1424,6 +1555,18 @@ void run_far_cfg(const TreeParams& P, const int4* items, int n_items, const doub
   kern<<<grid, W * 32, smem, s>>>(P, items, n_items, coef, far_s);
 }
 
+// Two leaves per warp (k_m2p_leaf2): items of <= 16 R targets, paired.
+template <int M, int R, int W, int S, int MINB>
+void run_leaf2_cfg(const TreeParams& P, const int4* items, int n_items, const double2* coef,
+                   const FarOut& far_s, cudaStream_t s) {
+  constexpr int K = hz_count(M);
+  auto kern = k_m2p_leaf2<M, R, W, S, MINB>;
+  const size_t smem = (size_t)2 * W * S * K * 16 + 2 * W * S * 8 + 2 * W * 16 * 4;
+  if (smem > 48 * 1024) ensure_smem_attr((const void*)kern, smem);
+  const unsigned grid = (unsigned)((n_items + 2 * W - 1) / (2 * W));
+  kern<<<grid, W * 32, smem, s>>>(P, items, n_items, coef, far_s);
+}
+
 }  // namespace
 
 int far_max_points_per_lane() { return kFarMaxR; }
@@ -1442,6 +1585,21 @@ void run_far(const TreeParams& P, int R, const int4* items, int n_items, const d
     case 6: return run_far_cfg<M, 6, 4, 3, 1>(P, items, n_items, coef, far_s, s);
     case 7: return run_far_cfg<M, 7, 4, 3, 1>(P, items, n_items, coef, far_s, s);
     default: return run_far_cfg<M, 8, 4, 3, 1>(P, items, n_items, coef, far_s, s);
+  }
+}
+
+template <int M>
+void run_leaf2(const TreeParams& P, int R, const int4* items, int n_items, const double2* coef,
+               const FarOut& far_s, cudaStream_t s) {
+  switch (R) {
+    case 1: return run_leaf2_cfg<M, 1, 4, 3, 1>(P, items, n_items, coef, far_s, s);
+    case 2: return run_leaf2_cfg<M, 2, 4, 3, 1>(P, items, n_items, coef, far_s, s);
+    case 3: return run_leaf2_cfg<M, 3, 4, 3, 1>(P, items, n_items, coef, far_s, s);
+    case 4: return run_leaf2_cfg<M, 4, 4, 3, 1>(P, items, n_items, coef, far_s, s);
+    case 5: return run_leaf2_cfg<M, 5, 4, 3, 1>(P, items, n_items, coef, far_s, s);
+    case 6: return run_leaf2_cfg<M, 6, 4, 3, 1>(P, items, n_items, coef, far_s, s);
+    case 7: return run_leaf2_cfg<M, 7, 4, 3, 1>(P, items, n_items, coef, far_s, s);
+    default: return run_leaf2_cfg<M, 8, 4, 3, 1>(P, items, n_items, coef, far_s, s);
   }
 }
 
@@ -1585,7 +1743,7 @@ void launch_m2p_far(const TreeParams& P, const int4* items, const int* group_off
                     int end, const double2* coef, double* far_s_ptr, const cudaStream_t* streams,
                     int nstreams, const double* near_part, int nslots, double* out,
                     const int* perm, const double* far_add, int lmin, int lmax, int ring,
-                    int lsplit) {
+                    int lsplit, bool leaf2) {
   if (end <= begin) return;
   if (lmin < 1) lmin = 1;
   if (lmax < 1 || lmax > P.L) lmax = P.L;
@@ -1605,8 +1763,12 @@ void launch_m2p_far(const TreeParams& P, const int4* items, const int* group_off
     switch (P.M) {
 #define X(m)                                                   \
   case m:                                                      \
-    run_far<m>(P, R, items + lo, hi - lo, coef, far_s,          \
-               streams[launched++ % nstreams]);               \
+    if (leaf2)                                                 \
+      run_leaf2<m>(P, R, items + lo, hi - lo, coef, far_s,      \
+                   streams[launched++ % nstreams]);           \
+    else                                                       \
+      run_far<m>(P, R, items + lo, hi - lo, coef, far_s,        \
+                 streams[launched++ % nstreams]);             \
     break;
       IMQ_FOR_SPECIALISED_M(X)
 #undef X

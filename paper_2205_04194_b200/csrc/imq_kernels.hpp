@@ -100,7 +100,7 @@ void launch_m2p_far(const TreeParams& P, const int4* items, const int* group_off
                     int nstreams, const double* near_part = nullptr, int nslots = 0,
                     double* out = nullptr, const int* perm = nullptr,
                     const double* far_add = nullptr, int lmin = 1, int lmax = 0,
-                    int ring = 0, int lsplit = 0);
+                    int ring = 0, int lsplit = 0, bool leaf2 = false);
 bool m2p_specialised(int M);
 // The far passes' enumeration modes of an operator (k_far_cover replays them).
 struct CoverModes {
@@ -111,6 +111,7 @@ struct CoverModes {
   int ring_l0;  // rings of levels ring_l0..L-1
   int xring;    // X-ring items (level-(L-1) inner + level-L outer ring at X's nodes)
   int lsplit;   // per-leaf partial pass
+  int leaf2;    // ... run two leaves per warp (k_m2p_leaf2, leaf_inner_list)
 };
 // out[i] = {missing, duplicated, extra, entries} of targets[i]'s far lists
 struct GemmDelta;

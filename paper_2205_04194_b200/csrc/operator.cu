@@ -390,18 +390,30 @@ void DeviceOperator::build_items(int p_lo, int p_hi) {
   dfree(d_lpart_items_);
   n_lpart_items_ = 0;
   lpart_group_off_.assign(16, 0);
+  lpart_leaf2_ = imqk::m2p_specialised(M_);
   if (far_split_ && !opt(kOptNoLsplit)) {
-    std::vector<std::vector<int4>> pg((size_t)rmax);
+    // specialised orders: two leaves per warp (k_m2p_leaf2), items of
+    // <= 16 R2 targets grouped by R = ceil(count / 16) and paired inside a
+    // group (an odd group gets an empty partner); else one leaf chunk of
+    // <= 32 rmax targets per warp (k_m2p_far_generic, lsplit 2)
+    const int gran = lpart_leaf2_ ? 16 : 32;
+    const int rm = lpart_leaf2_ ? std::min(imqk::far_max_points_per_lane(), 2 * rmax) : rmax;
+    std::vector<std::vector<int4>> pg((size_t)rm);
     for (long long q = 0; q < n_leaves; ++q) {
       const int a = std::max(p_lo, ls[(size_t)q]), b = std::min(p_hi, ls[(size_t)q + 1]);
       if (b <= a) continue;
-      const int nchunk = (b - a + 32 * rmax - 1) / (32 * rmax);
-      const int size = 32 * ((b - a + 32 * nchunk - 1) / (32 * nchunk));
+      const int nchunk = (b - a + gran * rm - 1) / (gran * rm);
+      const int size = gran * ((b - a + gran * nchunk - 1) / (gran * nchunk));
       for (int c = a; c < b; c += size) {
         const int cnt = std::min(size, b - c);
-        pg[(size_t)((cnt + 31) / 32 - 1)].push_back(make_int4((int)(q >> 2), c, cnt, L_ | (2 << 12)));
+        pg[(size_t)((cnt + gran - 1) / gran - 1)].push_back(
+            lpart_leaf2_ ? make_int4((int)q, c, cnt, 0)
+                         : make_int4((int)(q >> 2), c, cnt, L_ | (2 << 12)));
       }
     }
+    if (lpart_leaf2_)
+      for (auto& g : pg)
+        if (g.size() & 1) g.push_back(make_int4(0, 0, 0, 0));
     std::vector<int4> pitems;
     grouped(pg, pitems, lpart_group_off_);
     n_lpart_items_ = (int)pitems.size();
@@ -1118,6 +1130,7 @@ ListCheck DeviceOperator::far_list_check(int max_targets) {
   Mo.ring = cheb_ && ring_ ? 1 : 0;
   Mo.ring_l0 = ring_l0_;
   Mo.lsplit = n_lpart_items_ > 0 ? 1 : 0;
+  Mo.leaf2 = lpart_leaf2_ ? 1 : 0;
   Mo.xring = cheb_ && ring_ && xring_ && n_lpart_items_ > 0 ? 1 : 0;
   int* d_t = dalloc<int>((size_t)nt, "list check");
   int4* d_o = dalloc<int4>((size_t)nt, "list check");
@@ -1601,7 +1614,8 @@ void DeviceOperator::far_near(const double* d_us, double* d_out, const int* perm
   auto far_pass = [&](int b, int e, const int* goff, const double* near_part, int nslots,
                       double* out, const int* pm, double* far_s, const double* far_add, int lmin,
                       int lmax, const imqk::TreeParams* Pp = nullptr,
-                      const int4* its = nullptr, int ring = 0, int lsplit = 0) {
+                      const int4* its = nullptr, int ring = 0, int lsplit = 0,
+                      bool leaf2 = false) {
     if (e <= b) return;
     cudaStream_t ss[1 + kAuxStreams] = {s};
     cuda_check(cudaEventRecord(ev_fork_, s), "fork");
@@ -1611,7 +1625,7 @@ void DeviceOperator::far_near(const double* d_us, double* d_out, const int* perm
     }
     imqk::launch_m2p_far(Pp ? *Pp : P_, its ? its : d_far_items_, goff, b, e, d_coef_, far_s, ss,
                          far_streams_, near_part, nslots, out, pm, far_add, lmin, lmax, ring,
-                         lsplit);
+                         lsplit, leaf2);
     for (int k = 0; k < kAuxStreams; ++k) {
       cuda_check(cudaEventRecord(ev_join_[k], aux_[k]), "join");
       cuda_check(cudaStreamWaitEvent(s, ev_join_[k], 0), "join wait");
@@ -1684,13 +1698,13 @@ void DeviceOperator::far_near(const double* d_us, double* d_out, const int* perm
       // per-leaf partial pass is the last far pass and combines far + near
       if (near_launched && sym) cuda_check(cudaStreamWaitEvent(s, ev_near_done_, 0), "near join");
       far_pass(0, n_lpart_items_, lpart_group_off_.data(), near_part, nslots, d_out, perm, d_far_,
-               d_farc_, L_, L_, nullptr, d_lpart_items_);
+               d_farc_, L_, L_, nullptr, d_lpart_items_, 0, 0, lpart_leaf2_);
     } else {
       // the partial pass: inner-ring leaves of level L per leaf, accumulated
       // into the coarse partial
       if (lsplit)
         far_pass(0, n_lpart_items_, lpart_group_off_.data(), nullptr, 0, nullptr, nullptr, d_farc_,
-                 d_farc_, L_, L_, nullptr, d_lpart_items_);
+                 d_farc_, L_, L_, nullptr, d_lpart_items_, 0, 0, lpart_leaf2_);
       if (near_launched && sym) cuda_check(cudaStreamWaitEvent(s, ev_near_done_, 0), "near join");
       far_pass(far_begin, std::min(far_end, n_far_fine_), far_group_off_.data(), near_part, nslots,
                d_out, perm, d_far_, d_farc_, L_ - 1, L_, nullptr, nullptr,

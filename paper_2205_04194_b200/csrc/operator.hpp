@@ -343,6 +343,7 @@ class DeviceOperator {
   int n_far_fine_ = 0;     // far items [0, n_far_fine_) fine, the rest coarse
   // partial pass (far_split_): per-leaf items for the inner ring of level L
   int n_lpart_items_ = 0;
+  bool lpart_leaf2_ = false;  // partial pass: two leaves per warp (k_m2p_leaf2)
   std::vector<int> lpart_group_off_;
   int4* d_lpart_items_ = nullptr;
   std::vector<int> far_cgroup_off_;
