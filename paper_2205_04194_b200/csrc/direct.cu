@@ -19,6 +19,7 @@ namespace {
 
 constexpr int kNearWarps = 4;
 constexpr int kNearMaxR = 4;  // a near work item holds <= 32 * kNearMaxR targets of one leaf
+constexpr int kNearSymMaxR = 8;  // symmetric items: <= 16 * kNearSymMaxR points of one leaf (half-warp)
 
 // Warp per near work item: <= 32 R targets of one leaf, R per lane.  Every
 // source point staged in the warp's shared-memory tile is read back once per
@@ -128,22 +129,30 @@ __global__ void __launch_bounds__(kNearWarps * 32) k_p2p_near(
   }
 }
 
-// Symmetric near field (every leaf <= 32 R points, unsharded): the item of
-// leaf C evaluates its self tile and each unordered pair {C, B} with B one of
-// its four "forward" neighbours (0,+1), (+1,-1), (+1,0), (+1,+1) once:
-// forward sums sum_j u_j phi_ij accumulate in registers (slot 0), and the
-// reverse sums sum_i u_i phi_ij for B's points are formed by a register that
-// rotates through the lanes with one shuffle per step (lane l evaluates source
-// (l + k) mod 32 at step k), ending in lane j for source j; they go to B's
-// slot 1 + dir.  Slots are combined with the far field in a fixed order.
+// Symmetric near field (every leaf <= 128 points), two leaves per warp: the
+// half-warp h (16 lanes, shuffles and syncs on its own 16-lane mask) takes
+// item 2w + h, the <= 16 R points of one leaf C, R per lane (R = ceil(count /
+// 16): a 65..80-point leaf fills 80 slots instead of 96, and every staged
+// source feeds 2R pair evaluations).  The item evaluates C's self tile and
+// each unordered pair {C, B} with B one of its four "forward" neighbours
+// (0,+1), (+1,-1), (+1,0), (+1,+1) once: forward sums sum_j u_j phi_ij
+// accumulate in registers (slot 0), and the reverse sums sum_i u_i phi_ij for
+// B's points are formed by a register that rotates through the half's lanes
+// with one shuffle per step (lane l evaluates source (l + k) mod 16 at step
+// k), ending in lane j for source j; they go to B's slot 1 + dir.  Slots are
+// combined with the far field in a fixed order.  Items of one R group are
+// sorted by their forward-source count, so the two halves of a warp run
+// loops of (nearly) the same length.
 template <int R>
 __global__ void __launch_bounds__(kNearWarps * 32) k_p2p_near_sym(
     const TreeParams P, const int4* __restrict__ items, int n_items,
     const double* __restrict__ u_s, double* __restrict__ part) {
-  __shared__ double2 sxy[kNearWarps][32];
-  __shared__ double su[kNearWarps][32];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int it = blockIdx.x * kNearWarps + warp;
+  __shared__ double2 sxy[2 * kNearWarps][16];
+  __shared__ double su[2 * kNearWarps][16];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, hl = lane & 15;
+  const int hw = 2 * warp + (lane >> 4);
+  const unsigned hm = 0xffffu << (lane & 16);
+  const int it = (blockIdx.x * kNearWarps + warp) * 2 + (lane >> 4);
   if (it >= n_items) return;
   const int4 item = items[it];
   const uint32_t leaf = (uint32_t)item.x;
@@ -152,8 +161,8 @@ __global__ void __launch_bounds__(kNearWarps * 32) k_p2p_near_sym(
   double xi[R], yi[R], ui[R], acc[R];
 #pragma unroll
   for (int p = 0; p < R; ++p) {
-    const bool v = lane + 32 * p < cnt;
-    const int q = v ? s0 + lane + 32 * p : s0;
+    const bool v = hl + 16 * p < cnt;
+    const int q = v ? s0 + hl + 16 * p : s0;
     xi[p] = P.xs[q];
     yi[p] = P.ys[q];
     ui[p] = v ? u_s[q] : 0.0;  // padded targets must not feed reverse sums
@@ -163,27 +172,27 @@ __global__ void __launch_bounds__(kNearWarps * 32) k_p2p_near_sym(
   const int g = 1 << (P.L + 1);
   int li, lj;
   demorton(leaf, li, lj);
-  // self block (cnt <= 32 R: the whole leaf is in this item's registers), each
-  // unordered pair once: source tile pt = the targets of slot pt.  Slots
-  // p < pt take a full rotation against the tile (forward into acc[p], the
-  // reverse sums rotate into lane j = target j of slot pt); slot pt itself
-  // takes a half rotation (k = 0: the pair (i, i), forward only; k = 1..15;
-  // k = 16 by lanes 0..15 only), its reverse sums realigned by 17 lanes.
-  const int ntile = (cnt + 31) / 32;
+  // self block (the whole leaf is in this half's registers), each unordered
+  // pair once: source tile pt = the targets of slot pt.  Slots p < pt take a
+  // full rotation against the tile (forward into acc[p], the reverse sums
+  // rotate into lane j = target j of slot pt); slot pt itself takes a half
+  // rotation (k = 0: the pair (i, i), forward only; k = 1..7; k = 8 by lanes
+  // 0..7 only), its reverse sums realigned by 9 lanes.
+  const int ntile = (cnt + 15) / 16;
 #pragma unroll
   for (int pt = 0; pt < R; ++pt) {
     if (pt >= ntile) break;
-    __syncwarp();
-    sxy[warp][lane] = make_double2(xi[pt], yi[pt]);  // padding: a valid point, u = 0
-    su[warp][lane] = ui[pt];
-    __syncwarp();
+    __syncwarp(hm);
+    sxy[hw][hl] = make_double2(xi[pt], yi[pt]);  // padding: a valid point, u = 0
+    su[hw][hl] = ui[pt];
+    __syncwarp(hm);
     if (pt > 0) {
       double racc = 0.0;
 #pragma unroll 8
-      for (int k = 0; k < 32; ++k) {
-        const int jj = (lane + k) & 31;
-        const double2 sp = sxy[warp][jj];
-        const double uk = su[warp][jj];
+      for (int k = 0; k < 16; ++k) {
+        const int jj = (hl + k) & 15;
+        const double2 sp = sxy[hw][jj];
+        const double uk = su[hw][jj];
         double r = 0.0;
 #pragma unroll
         for (int p = 0; p < R; ++p) {
@@ -195,7 +204,7 @@ __global__ void __launch_bounds__(kNearWarps * 32) k_p2p_near_sym(
           }
         }
         racc += r;
-        racc = __shfl_sync(0xffffffffu, racc, (lane + 1) & 31);
+        racc = __shfl_sync(hm, racc, (hl + 1) & 15, 16);
       }
       acc[pt] += racc;
     }
@@ -203,23 +212,23 @@ __global__ void __launch_bounds__(kNearWarps * 32) k_p2p_near_sym(
       const double dx0 = xi[pt] - xi[pt], dy0 = yi[pt] - yi[pt];
       acc[pt] = fma(ui[pt], rsqrt_pos(fma(dx0, dx0, fma(dy0, dy0, t2))), acc[pt]);  // k = 0
       double racc = 0.0;
-#pragma unroll 4
-      for (int k = 1; k <= 16; ++k) {
-        const int jj = (lane + k) & 31;
-        const double2 sp = sxy[warp][jj];
-        const double uk = (k < 16 || lane < 16) ? su[warp][jj] : 0.0;
-        const double ul = (k < 16 || lane < 16) ? ui[pt] : 0.0;
+#pragma unroll
+      for (int k = 1; k <= 8; ++k) {
+        const int jj = (hl + k) & 15;
+        const double2 sp = sxy[hw][jj];
+        const double uk = (k < 8 || hl < 8) ? su[hw][jj] : 0.0;
+        const double ul = (k < 8 || hl < 8) ? ui[pt] : 0.0;
         const double dx = xi[pt] - sp.x, dy = yi[pt] - sp.y;
         const double phi = rsqrt_pos(fma(dx, dx, fma(dy, dy, t2)));
         acc[pt] = fma(uk, phi, acc[pt]);
         racc = fma(ul, phi, racc);
-        racc = __shfl_sync(0xffffffffu, racc, (lane + 1) & 31);
+        racc = __shfl_sync(hm, racc, (hl + 1) & 15, 16);
       }
-      acc[pt] += __shfl_sync(0xffffffffu, racc, (lane + 15) & 31);
+      acc[pt] += __shfl_sync(hm, racc, (hl + 7) & 15, 16);
     }
   }
   // forward neighbours: forward + reverse sums over the concatenation of the
-  // four neighbour ranges (tiles of 32 sources cross leaf boundaries)
+  // four neighbour ranges (tiles of 16 sources cross leaf boundaries)
   int na[4], nb[4];
 #pragma unroll
   for (int dir = 0; dir < 4; ++dir) {
@@ -233,25 +242,25 @@ __global__ void __launch_bounds__(kNearWarps * 32) k_p2p_near_sym(
   }
   const int e1 = nb[0] - na[0], e2 = e1 + nb[1] - na[1], e3 = e2 + nb[2] - na[2];
   const int total = e3 + nb[3] - na[3];
-  for (int base = 0; base < total; base += 32) {
-    const int v = base + lane;
+  for (int base = 0; base < total; base += 16) {
+    const int v = base + hl;
     const int dir = v < e1 ? 0 : (v < e2 ? 1 : (v < e3 ? 2 : 3));
     const int j = na[dir] + v - (dir == 0 ? 0 : (dir == 1 ? e1 : (dir == 2 ? e2 : e3)));
-    __syncwarp();
+    __syncwarp(hm);
     if (v < total) {
-      sxy[warp][lane] = make_double2(P.xs[j], P.ys[j]);
-      su[warp][lane] = u_s[j];
+      sxy[hw][hl] = make_double2(P.xs[j], P.ys[j]);
+      su[hw][hl] = u_s[j];
     } else {
-      sxy[warp][lane] = make_double2(xi[0], yi[0]);
-      su[warp][lane] = 0.0;
+      sxy[hw][hl] = make_double2(xi[0], yi[0]);
+      su[hw][hl] = 0.0;
     }
-    __syncwarp();
+    __syncwarp(hm);
     double racc = 0.0;
 #pragma unroll 8
-    for (int k = 0; k < 32; ++k) {
-      const int jj = (lane + k) & 31;
-      const double2 sp = sxy[warp][jj];
-      const double uk = su[warp][jj];
+    for (int k = 0; k < 16; ++k) {
+      const int jj = (hl + k) & 15;
+      const double2 sp = sxy[hw][jj];
+      const double uk = su[hw][jj];
       double r = 0.0;
 #pragma unroll
       for (int p = 0; p < R; ++p) {
@@ -261,13 +270,13 @@ __global__ void __launch_bounds__(kNearWarps * 32) k_p2p_near_sym(
         r = fma(ui[p], phi, r);
       }
       racc += r;
-      racc = __shfl_sync(0xffffffffu, racc, (lane + 1) & 31);
+      racc = __shfl_sync(hm, racc, (hl + 1) & 15, 16);
     }
     if (v < total) part[(size_t)(1 + dir) * N + j] = racc;  // lane holds its source's reverse sum
   }
 #pragma unroll
   for (int p = 0; p < R; ++p)
-    if (lane + 32 * p < cnt) part[s0 + lane + 32 * p] = acc[p];
+    if (hl + 16 * p < cnt) part[s0 + hl + 16 * p] = acc[p];
   // reverse slots nobody writes (no / empty backward neighbour): zero them here
 #pragma unroll 1
   for (int dir = 0; dir < 4; ++dir) {
@@ -279,7 +288,7 @@ __global__ void __launch_bounds__(kNearWarps * 32) k_p2p_near_sym(
       has = P.leaf_start[q + 1] > P.leaf_start[q];
     }
     if (!has)
-      for (int p = lane; p < cnt; p += 32) part[(size_t)(1 + dir) * N + s0 + p] = 0.0;
+      for (int p = hl; p < cnt; p += 16) part[(size_t)(1 + dir) * N + s0 + p] = 0.0;
   }
 }
 
@@ -506,16 +515,18 @@ int near_max_points_per_lane() { return kNearMaxR; }
 
 void launch_p2p_near_sym(const TreeParams& P, const int4* items, const int* group_off, int begin,
                          int end, const double* u_s, double* part, cudaStream_t s) {
-  for (int R = 1; R <= kNearMaxR; ++R) {
+  for (int R = kNearSymMaxR; R >= 1; --R) {  // longest items first
     const int lo = max(begin, group_off[R - 1]), hi = min(end, group_off[R]);
     if (hi <= lo) continue;
-    const unsigned grid = (unsigned)((hi - lo + kNearWarps - 1) / kNearWarps);
+    const unsigned grid = (unsigned)((hi - lo + 2 * kNearWarps - 1) / (2 * kNearWarps));
+#define NEAR_SYM_CASE(r) \
+  case r: k_p2p_near_sym<r><<<grid, kNearWarps * 32, 0, s>>>(P, items + lo, hi - lo, u_s, part); break;
     switch (R) {
-      case 1: k_p2p_near_sym<1><<<grid, kNearWarps * 32, 0, s>>>(P, items + lo, hi - lo, u_s, part); break;
-      case 2: k_p2p_near_sym<2><<<grid, kNearWarps * 32, 0, s>>>(P, items + lo, hi - lo, u_s, part); break;
-      case 3: k_p2p_near_sym<3><<<grid, kNearWarps * 32, 0, s>>>(P, items + lo, hi - lo, u_s, part); break;
-      default: k_p2p_near_sym<4><<<grid, kNearWarps * 32, 0, s>>>(P, items + lo, hi - lo, u_s, part); break;
+      NEAR_SYM_CASE(1) NEAR_SYM_CASE(2) NEAR_SYM_CASE(3) NEAR_SYM_CASE(4)
+      NEAR_SYM_CASE(5) NEAR_SYM_CASE(6) NEAR_SYM_CASE(7)
+      default: k_p2p_near_sym<8><<<grid, kNearWarps * 32, 0, s>>>(P, items + lo, hi - lo, u_s, part); break;
     }
+#undef NEAR_SYM_CASE
   }
 }
 

@@ -460,15 +460,42 @@ void DeviceOperator::build_items(int p_lo, int p_hi) {
   near_sym_ = (full ? near_split_ == 1 : true) &&
               max_leaf <= 32 * imqk::near_max_points_per_lane() && !opt(kOptNearNoSym);
   if (near_sym_) near_split_ = 1;
-  if (near_sym_) nrmax = imqk::near_max_points_per_lane();
-  std::vector<std::vector<int4>> ngroups((size_t)nrmax);
-  for (long long q = 0; q < n_leaves; ++q) {
-    const int a = std::max(p_lo, ls[(size_t)q]), b = std::min(p_hi, ls[(size_t)q + 1]);
-    for (int c = a; c < b; c += 32 * nrmax) {
-      const int cnt = std::min(32 * nrmax, b - c);
-      for (int r = 0; r < near_split_; ++r)
-        ngroups[(size_t)((cnt + 31) / 32 - 1)].push_back(make_int4(
-            (int)q, c, cnt, near_split_ == 1 ? 15 : (near_split_ == 3 ? 16 + r : 32 + r)));
+  std::vector<std::vector<int4>> ngroups((size_t)(near_sym_ ? 8 : nrmax));
+  if (near_sym_) {
+    // symmetric: one leaf per half-warp item, grouped by R = ceil(count / 16)
+    // and sorted inside a group by the forward neighbours' point count (the
+    // two halves of a warp then stream (nearly) equally long source ranges)
+    const int g = 1 << (L_ + 1);
+    std::vector<std::vector<std::pair<int, int4>>> keyed(8);
+    for (long long q = 0; q < n_leaves; ++q) {
+      const int a = std::max(p_lo, ls[(size_t)q]), b = std::min(p_hi, ls[(size_t)q + 1]);
+      if (b <= a) continue;
+      int li, lj, fwd = 0;
+      imqdev::demorton((uint32_t)q, li, lj);
+      for (int dir = 0; dir < 4; ++dir) {
+        const int bi = li + (dir == 0 ? 0 : 1), bj = lj + (dir == 0 ? 1 : dir - 2);
+        if (bi > g - 1 || bj < 0 || bj > g - 1) continue;
+        const uint32_t qb = imqdev::morton((uint32_t)bi, (uint32_t)bj);
+        fwd += ls[(size_t)qb + 1] - ls[qb];
+      }
+      keyed[(size_t)((b - a + 15) / 16 - 1)].push_back({fwd, make_int4((int)q, a, b - a, 15)});
+    }
+    for (size_t r = 0; r < keyed.size(); ++r) {
+      std::stable_sort(keyed[r].begin(), keyed[r].end(),
+                       [](const std::pair<int, int4>& x, const std::pair<int, int4>& y) {
+                         return x.first < y.first;
+                       });
+      for (const auto& e : keyed[r]) ngroups[r].push_back(e.second);
+    }
+  } else {
+    for (long long q = 0; q < n_leaves; ++q) {
+      const int a = std::max(p_lo, ls[(size_t)q]), b = std::min(p_hi, ls[(size_t)q + 1]);
+      for (int c = a; c < b; c += 32 * nrmax) {
+        const int cnt = std::min(32 * nrmax, b - c);
+        for (int r = 0; r < near_split_; ++r)
+          ngroups[(size_t)((cnt + 31) / 32 - 1)].push_back(make_int4(
+              (int)q, c, cnt, near_split_ == 1 ? 15 : (near_split_ == 3 ? 16 + r : 32 + r)));
+      }
     }
   }
   // pull items (sharded symmetric mode): own leaf B, direction d, backward
