@@ -64,13 +64,20 @@ class ClockSampler:
     def __init__(self, gpu_index: int):
         self.idx = gpu_index
         self.proc = None
-        self.lines: list[str] = []
+        self.lines: list[tuple[float, str]] = []
+        self.t0 = self.t1 = None
+
+    def mark_start(self):
+        self.t0 = time.perf_counter()
+
+    def mark_end(self):
+        self.t1 = time.perf_counter()
 
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.th = threading.Thread(target=self._read, daemon=True)
             self.th.start()
@@ -80,7 +87,7 @@ class ClockSampler:
 
     def _read(self):
         for ln in self.proc.stdout:
-            self.lines.append(ln.strip())
+            self.lines.append((time.perf_counter(), ln.strip()))
 
     def __exit__(self, *a):
         if self.proc:
@@ -93,7 +100,13 @@ class ClockSampler:
     def summary(self):
         sm, mx, reasons = [], 0.0, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        # samples received inside the timed region (the sampler starts before
+        # the warm-up so nvidia-smi is already streaming)
+        lines = [ln for ts, ln in self.lines
+                 if self.t0 is None or (self.t0 <= ts <= (self.t1 or ts) + 0.05)]
+        if not lines:  # a timed region shorter than one sampling period
+            lines = [ln for _, ln in self.lines]
+        for ln in lines:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 9:
                 continue
@@ -269,17 +282,19 @@ def b200_arm(args):
             dist.barrier()
         torch.cuda.synchronize()
 
-    for k in range(args.warmup):
-        step(k)
-    barrier()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     with ClockSampler(dev) as clk:
+        for k in range(args.warmup):
+            step(k)
+        barrier()
+        clk.mark_start()
         e0.record(stream)
         for k in range(args.steps):
             step(args.warmup + k)
         e1.record(stream)
         barrier()
+        clk.mark_end()
     ms = e0.elapsed_time(e1) / args.steps
     ms_t = torch.tensor([ms], device="cuda", dtype=torch.float64)
     if world > 1:
@@ -318,7 +333,7 @@ def b200_arm(args):
     e2e_value = n / float(e2e_s.item())
     # the same call with pageable host buffers (what a reference caller passes:
     # std::vector memory, reference capi.cpp:130-138)
-    e2e_pageable = e2e_batch = None
+    e2e_pageable = e2e_batch = e2e_block = block_ms_per_vector = None
     if world == 1:
         # the repeated-product workload through imq_ext_operator_apply_batch:
         # all nb host vectors in one call, copies pipelined with the products
@@ -336,7 +351,31 @@ def b200_arm(args):
         t0 = time.perf_counter()
         batch_call()
         e2e_batch = nb * n / (time.perf_counter() - t0)
-        del bat_u, bat_b
+
+        # block product (f4): the same nb vectors through
+        # imq_ext_operator_apply_block -- groups of 4 share the near field's
+        # kernel evaluations; host matrices (copies inside) and device-resident
+        def block_call():
+            P.capi.check(P.capi.lib().imq_ext_operator_apply_block(
+                op.handle, nb, P.api.C.cast(bat_u.data_ptr(), P.api._dp),
+                P.api.C.cast(bat_b.data_ptr(), P.api._dp)))
+        block_call()
+        t0 = time.perf_counter()
+        block_call()
+        e2e_block = nb * n / (time.perf_counter() - t0)
+        blk_u = bat_u[:4].cuda()
+        blk_b = torch.empty_like(blk_u)
+        op.apply_block_device(blk_u, blk_b, 4, stream)
+        torch.cuda.synchronize()
+        eb0 = torch.cuda.Event(enable_timing=True)
+        eb1 = torch.cuda.Event(enable_timing=True)
+        eb0.record(stream)
+        for _ in range(2):
+            op.apply_block_device(blk_u, blk_b, 4, stream)
+        eb1.record(stream)
+        torch.cuda.synchronize()
+        block_ms_per_vector = eb0.elapsed_time(eb1) / 8
+        del bat_u, bat_b, blk_u, blk_b
         page_u = [host_u[i].numpy() for i in range(2)]
         page_b = np.empty(n)
 
@@ -481,7 +520,12 @@ def b200_arm(args):
                     "pageable": e2e_pageable,
                     "batch": e2e_batch,
                     "batch_path": "imq_ext_operator_apply_batch, pinned host U/B, copies "
-                                  "pipelined with the products (same bytes per product)"},
+                                  "pipelined with the products (same bytes per product)",
+                    "block": e2e_block,
+                    "block_path": "imq_ext_operator_apply_block, pinned host U/B: groups of 4 "
+                                  "vectors share the near field's kernel evaluations "
+                                  "(bitwise the single products)",
+                    "block_device_ms_per_vector": block_ms_per_vector},
             "roofline": {"bound": "fp64",
                          "kernel": "k_m2p_far (M2P far field: direct for the fine levels, at "
                                    "Chebyshev nodes for levels 1..%d%s) + k_node_gemm (X nodes, "

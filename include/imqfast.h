@@ -136,6 +136,17 @@ IMQ_API int imq_ext_operator_apply_device(const imq_operator* op, const double* 
  * bit for bit. */
 IMQ_API int imq_ext_operator_apply_batch(const imq_operator* op, int nrhs, const double* U,
                                          double* B);
+/* Block product (the reference evaluates one vector per
+ * accumulate_far_block / near loop, fastmv.cpp:104-182): B = A U for nrhs
+ * vectors at once, rows of U and B (row-major nrhs x n, original point
+ * order).  Groups of up to 4 vectors share every near-field kernel
+ * evaluation; each row of B equals imq_operator_apply's result bit for bit.
+ * Host matrices (copies pipelined with the block products) or device
+ * matrices enqueued on `stream` without host synchronisation. */
+IMQ_API int imq_ext_operator_apply_block(const imq_operator* op, int nrhs, const double* U,
+                                         double* B);
+IMQ_API int imq_ext_operator_apply_block_device(const imq_operator* op, int nrhs,
+                                                const double* d_U, double* d_B, void* stream);
 /* Same on vectors already permuted into the operator's Morton order. */
 IMQ_API int imq_ext_operator_apply_sorted_device(const imq_operator* op, const double* d_us,
                                          double* d_bs, void* stream);

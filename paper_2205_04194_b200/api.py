@@ -246,6 +246,21 @@ class FastOperator:
         check(lib().imq_ext_operator_apply_batch(self._h, U.shape[0], _ptr(U), _ptr(B)))
         return B
 
+    def apply_block(self, U) -> np.ndarray:
+        """imq_ext_operator_apply_block: rows of U (nrhs x N, host) -> rows of B;
+        groups of 4 vectors share the near field's kernel evaluations."""
+        U = np.ascontiguousarray(np.atleast_2d(U), dtype=np.float64)
+        if U.shape[1] != self.size:
+            raise IMQError(capi.IMQ_ERR_INVALID_ARG, "apply_block: length mismatch")
+        B = np.empty_like(U)
+        check(lib().imq_ext_operator_apply_block(self._h, U.shape[0], _ptr(U), _ptr(B)))
+        return B
+
+    def apply_block_device(self, d_U, d_B, nrhs, stream=None) -> None:
+        """Device matrices (nrhs x N row-major, original point order)."""
+        check(lib().imq_ext_operator_apply_block_device(self._h, int(nrhs), _addr(d_U),
+                                                        _addr(d_B), _stream(stream)))
+
     def apply_device(self, d_u, d_b, stream=None) -> None:
         """Device pointers (ints or torch CUDA tensors), original point order."""
         check(lib().imq_ext_operator_apply_device(self._h, _addr(d_u), _addr(d_b),

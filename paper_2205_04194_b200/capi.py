@@ -90,6 +90,8 @@ _SIGS = {
     "imq_ext_operator_create_opts": (C.c_int, [_dp, C.c_size_t, C.c_double, C.c_int, C.c_int,
                                                C.POINTER(imq_ext_options), C.POINTER(_vp)]),
     "imq_ext_operator_apply_batch": (C.c_int, [_vp, C.c_int, _dp, _dp]),
+    "imq_ext_operator_apply_block": (C.c_int, [_vp, C.c_int, _dp, _dp]),
+    "imq_ext_operator_apply_block_device": (C.c_int, [_vp, C.c_int, _vp, _vp, _vp]),
     "imq_ext_operator_apply_device": (C.c_int, [_vp, _vp, _vp, _vp]),
     "imq_ext_operator_apply_sorted_device": (C.c_int, [_vp, _vp, _vp, _vp]),
     "imq_ext_operator_synchronize": (C.c_int, [_vp]),

@@ -213,6 +213,27 @@ int imq_ext_operator_apply_batch(const imq_operator* op, int nrhs, const double*
   });
 }
 
+int imq_ext_operator_apply_block(const imq_operator* op, int nrhs, const double* U, double* B) {
+  if (!op || !U || !B) return fail(IMQ_ERR_INVALID_ARG, "imq_ext_operator_apply_block: null argument");
+  if (nrhs < 1) return fail(IMQ_ERR_INVALID_ARG, "imq_ext_operator_apply_block: nrhs must be >= 1");
+  return guard([&] {
+    op->op->apply_block_host(nrhs, U, B);
+    return IMQ_OK;
+  });
+}
+
+int imq_ext_operator_apply_block_device(const imq_operator* op, int nrhs, const double* d_U,
+                                        double* d_B, void* stream) {
+  if (!op || !d_U || !d_B)
+    return fail(IMQ_ERR_INVALID_ARG, "imq_ext_operator_apply_block_device: null argument");
+  if (nrhs < 1)
+    return fail(IMQ_ERR_INVALID_ARG, "imq_ext_operator_apply_block_device: nrhs must be >= 1");
+  return guard([&] {
+    op->op->apply_block_device(nrhs, d_U, d_B, static_cast<cudaStream_t>(stream));
+    return IMQ_OK;
+  });
+}
+
 int imq_dense_matvec(const double* xy, size_t n, double t, const double* u, double* b_out) {
   if (!xy || !u || !b_out || n == 0)
     return fail(IMQ_ERR_INVALID_ARG, "imq_dense_matvec: null argument or empty point set");

@@ -9,6 +9,8 @@
 //   Dense product / interpolant evaluation (reference.cpp:11-28,
 //   solver.cpp:161-172): tiled all-pairs kernel, one target per thread, source
 //   tiles staged in shared memory; every thread sums its row in ascending j.
+#include <stdexcept>
+
 #include "imq_device.cuh"
 #include "imq_kernels.hpp"
 
@@ -19,7 +21,8 @@ namespace {
 
 constexpr int kNearWarps = 4;
 constexpr int kNearMaxR = 4;  // a near work item holds <= 32 * kNearMaxR targets of one leaf
-constexpr int kNearSymMaxR = 8;  // symmetric items: <= 16 * kNearSymMaxR points of one leaf (half-warp)
+constexpr int kNearSymMaxR = 8;
+constexpr int kNearBlockV = 4;   // right-hand sides per block near-field launch  // symmetric items: <= 16 * kNearSymMaxR points of one leaf (half-warp)
 
 // Warp per near work item: <= 32 R targets of one leaf, R per lane.  Every
 // source point staged in the warp's shared-memory tile is read back once per
@@ -143,12 +146,17 @@ __global__ void __launch_bounds__(kNearWarps * 32) k_p2p_near(
 // combined with the far field in a fixed order.  Items of one R group are
 // sorted by their forward-source count, so the two halves of a warp run
 // loops of (nearly) the same length.
-template <int R>
+// V right-hand sides at once (block product, V > 1): the kernel values phi
+// are evaluated once and feed V forward and V reverse sums; vector v of the
+// block lives at u_s + v * ustride, its partial slots at part + v * pstride.
+// Every sum has the single-vector order, so a block equals V single products
+// bit for bit.
+template <int R, int V>
 __global__ void __launch_bounds__(kNearWarps * 32) k_p2p_near_sym(
     const TreeParams P, const int4* __restrict__ items, int n_items,
-    const double* __restrict__ u_s, double* __restrict__ part) {
+    const double* __restrict__ u_s, size_t ustride, double* __restrict__ part, size_t pstride) {
   __shared__ double2 sxy[2 * kNearWarps][16];
-  __shared__ double su[2 * kNearWarps][16];
+  __shared__ double su[2 * kNearWarps][16][V];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, hl = lane & 15;
   const int hw = 2 * warp + (lane >> 4);
   const unsigned hm = 0xffffu << (lane & 16);
@@ -158,15 +166,18 @@ __global__ void __launch_bounds__(kNearWarps * 32) k_p2p_near_sym(
   const uint32_t leaf = (uint32_t)item.x;
   const int s0 = item.y, cnt = item.z;
   const size_t N = (size_t)P.N;
-  double xi[R], yi[R], ui[R], acc[R];
+  double xi[R], yi[R], ui[R][V], acc[R][V];
 #pragma unroll
   for (int p = 0; p < R; ++p) {
     const bool v = hl + 16 * p < cnt;
     const int q = v ? s0 + hl + 16 * p : s0;
     xi[p] = P.xs[q];
     yi[p] = P.ys[q];
-    ui[p] = v ? u_s[q] : 0.0;  // padded targets must not feed reverse sums
-    acc[p] = 0.0;
+#pragma unroll
+    for (int w = 0; w < V; ++w) {
+      ui[p][w] = v ? u_s[q + w * ustride] : 0.0;  // padded targets must not feed reverse sums
+      acc[p][w] = 0.0;
+    }
   }
   const double t2 = P.t2;
   const int g = 1 << (P.L + 1);
@@ -184,47 +195,71 @@ __global__ void __launch_bounds__(kNearWarps * 32) k_p2p_near_sym(
     if (pt >= ntile) break;
     __syncwarp(hm);
     sxy[hw][hl] = make_double2(xi[pt], yi[pt]);  // padding: a valid point, u = 0
-    su[hw][hl] = ui[pt];
+#pragma unroll
+    for (int w = 0; w < V; ++w) su[hw][hl][w] = ui[pt][w];
     __syncwarp(hm);
     if (pt > 0) {
-      double racc = 0.0;
+      double racc[V];
+#pragma unroll
+      for (int w = 0; w < V; ++w) racc[w] = 0.0;
 #pragma unroll 8
       for (int k = 0; k < 16; ++k) {
         const int jj = (hl + k) & 15;
         const double2 sp = sxy[hw][jj];
-        const double uk = su[hw][jj];
-        double r = 0.0;
+        double uk[V], r[V];
+#pragma unroll
+        for (int w = 0; w < V; ++w) {
+          uk[w] = su[hw][jj][w];
+          r[w] = 0.0;
+        }
 #pragma unroll
         for (int p = 0; p < R; ++p) {
           if (p < pt) {
             const double dx = xi[p] - sp.x, dy = yi[p] - sp.y;
             const double phi = rsqrt_pos(fma(dx, dx, fma(dy, dy, t2)));
-            acc[p] = fma(uk, phi, acc[p]);
-            r = fma(ui[p], phi, r);
+#pragma unroll
+            for (int w = 0; w < V; ++w) {
+              acc[p][w] = fma(uk[w], phi, acc[p][w]);
+              r[w] = fma(ui[p][w], phi, r[w]);
+            }
           }
         }
-        racc += r;
-        racc = __shfl_sync(hm, racc, (hl + 1) & 15, 16);
+#pragma unroll
+        for (int w = 0; w < V; ++w) {
+          racc[w] += r[w];
+          racc[w] = __shfl_sync(hm, racc[w], (hl + 1) & 15, 16);
+        }
       }
-      acc[pt] += racc;
+#pragma unroll
+      for (int w = 0; w < V; ++w) acc[pt][w] += racc[w];
     }
     {
       const double dx0 = xi[pt] - xi[pt], dy0 = yi[pt] - yi[pt];
-      acc[pt] = fma(ui[pt], rsqrt_pos(fma(dx0, dx0, fma(dy0, dy0, t2))), acc[pt]);  // k = 0
-      double racc = 0.0;
+      const double phi0 = rsqrt_pos(fma(dx0, dx0, fma(dy0, dy0, t2)));
+      double racc[V];
+#pragma unroll
+      for (int w = 0; w < V; ++w) {
+        acc[pt][w] = fma(ui[pt][w], phi0, acc[pt][w]);  // k = 0
+        racc[w] = 0.0;
+      }
 #pragma unroll
       for (int k = 1; k <= 8; ++k) {
         const int jj = (hl + k) & 15;
         const double2 sp = sxy[hw][jj];
-        const double uk = (k < 8 || hl < 8) ? su[hw][jj] : 0.0;
-        const double ul = (k < 8 || hl < 8) ? ui[pt] : 0.0;
+        const bool on = k < 8 || hl < 8;
         const double dx = xi[pt] - sp.x, dy = yi[pt] - sp.y;
         const double phi = rsqrt_pos(fma(dx, dx, fma(dy, dy, t2)));
-        acc[pt] = fma(uk, phi, acc[pt]);
-        racc = fma(ul, phi, racc);
-        racc = __shfl_sync(hm, racc, (hl + 1) & 15, 16);
+#pragma unroll
+        for (int w = 0; w < V; ++w) {
+          const double uk = on ? su[hw][jj][w] : 0.0;
+          const double ul = on ? ui[pt][w] : 0.0;
+          acc[pt][w] = fma(uk, phi, acc[pt][w]);
+          racc[w] = fma(ul, phi, racc[w]);
+          racc[w] = __shfl_sync(hm, racc[w], (hl + 1) & 15, 16);
+        }
       }
-      acc[pt] += __shfl_sync(hm, racc, (hl + 7) & 15, 16);
+#pragma unroll
+      for (int w = 0; w < V; ++w) acc[pt][w] += __shfl_sync(hm, racc[w], (hl + 7) & 15, 16);
     }
   }
   // forward neighbours: forward + reverse sums over the concatenation of the
@@ -249,34 +284,54 @@ __global__ void __launch_bounds__(kNearWarps * 32) k_p2p_near_sym(
     __syncwarp(hm);
     if (v < total) {
       sxy[hw][hl] = make_double2(P.xs[j], P.ys[j]);
-      su[hw][hl] = u_s[j];
+#pragma unroll
+      for (int w = 0; w < V; ++w) su[hw][hl][w] = u_s[j + w * ustride];
     } else {
       sxy[hw][hl] = make_double2(xi[0], yi[0]);
-      su[hw][hl] = 0.0;
+#pragma unroll
+      for (int w = 0; w < V; ++w) su[hw][hl][w] = 0.0;
     }
     __syncwarp(hm);
-    double racc = 0.0;
+    double racc[V];
+#pragma unroll
+    for (int w = 0; w < V; ++w) racc[w] = 0.0;
 #pragma unroll 8
     for (int k = 0; k < 16; ++k) {
       const int jj = (hl + k) & 15;
       const double2 sp = sxy[hw][jj];
-      const double uk = su[hw][jj];
-      double r = 0.0;
+      double uk[V], r[V];
+#pragma unroll
+      for (int w = 0; w < V; ++w) {
+        uk[w] = su[hw][jj][w];
+        r[w] = 0.0;
+      }
 #pragma unroll
       for (int p = 0; p < R; ++p) {
         const double dx = xi[p] - sp.x, dy = yi[p] - sp.y;
         const double phi = rsqrt_pos(fma(dx, dx, fma(dy, dy, t2)));
-        acc[p] = fma(uk, phi, acc[p]);
-        r = fma(ui[p], phi, r);
+#pragma unroll
+        for (int w = 0; w < V; ++w) {
+          acc[p][w] = fma(uk[w], phi, acc[p][w]);
+          r[w] = fma(ui[p][w], phi, r[w]);
+        }
       }
-      racc += r;
-      racc = __shfl_sync(hm, racc, (hl + 1) & 15, 16);
+#pragma unroll
+      for (int w = 0; w < V; ++w) {
+        racc[w] += r[w];
+        racc[w] = __shfl_sync(hm, racc[w], (hl + 1) & 15, 16);
+      }
     }
-    if (v < total) part[(size_t)(1 + dir) * N + j] = racc;  // lane holds its source's reverse sum
+    if (v < total) {  // lane holds its source's reverse sums
+#pragma unroll
+      for (int w = 0; w < V; ++w) part[w * pstride + (size_t)(1 + dir) * N + j] = racc[w];
+    }
   }
 #pragma unroll
   for (int p = 0; p < R; ++p)
-    if (hl + 16 * p < cnt) part[s0 + hl + 16 * p] = acc[p];
+    if (hl + 16 * p < cnt) {
+#pragma unroll
+      for (int w = 0; w < V; ++w) part[w * pstride + s0 + hl + 16 * p] = acc[p][w];
+    }
   // reverse slots nobody writes (no / empty backward neighbour): zero them here
 #pragma unroll 1
   for (int dir = 0; dir < 4; ++dir) {
@@ -288,7 +343,10 @@ __global__ void __launch_bounds__(kNearWarps * 32) k_p2p_near_sym(
       has = P.leaf_start[q + 1] > P.leaf_start[q];
     }
     if (!has)
-      for (int p = hl; p < cnt; p += 16) part[(size_t)(1 + dir) * N + s0 + p] = 0.0;
+      for (int p = hl; p < cnt; p += 16) {
+#pragma unroll
+        for (int w = 0; w < V; ++w) part[w * pstride + (size_t)(1 + dir) * N + s0 + p] = 0.0;
+      }
   }
 }
 
@@ -513,20 +571,47 @@ __global__ void __launch_bounds__(kDirThreads) k_direct(const double* __restrict
 
 int near_max_points_per_lane() { return kNearMaxR; }
 
-void launch_p2p_near_sym(const TreeParams& P, const int4* items, const int* group_off, int begin,
-                         int end, const double* u_s, double* part, cudaStream_t s) {
+template <int V>
+static void launch_near_sym_v(const TreeParams& P, const int4* items, const int* group_off,
+                              int begin, int end, const double* u_s, size_t ustride, double* part,
+                              size_t pstride, cudaStream_t s) {
   for (int R = kNearSymMaxR; R >= 1; --R) {  // longest items first
     const int lo = max(begin, group_off[R - 1]), hi = min(end, group_off[R]);
     if (hi <= lo) continue;
     const unsigned grid = (unsigned)((hi - lo + 2 * kNearWarps - 1) / (2 * kNearWarps));
-#define NEAR_SYM_CASE(r) \
-  case r: k_p2p_near_sym<r><<<grid, kNearWarps * 32, 0, s>>>(P, items + lo, hi - lo, u_s, part); break;
+#define NEAR_SYM_CASE(r)                                                                        \
+  case r:                                                                                       \
+    k_p2p_near_sym<r, V><<<grid, kNearWarps * 32, 0, s>>>(P, items + lo, hi - lo, u_s, ustride, \
+                                                          part, pstride);                       \
+    break;
     switch (R) {
       NEAR_SYM_CASE(1) NEAR_SYM_CASE(2) NEAR_SYM_CASE(3) NEAR_SYM_CASE(4)
       NEAR_SYM_CASE(5) NEAR_SYM_CASE(6) NEAR_SYM_CASE(7)
-      default: k_p2p_near_sym<8><<<grid, kNearWarps * 32, 0, s>>>(P, items + lo, hi - lo, u_s, part); break;
+      default:
+        k_p2p_near_sym<8, V><<<grid, kNearWarps * 32, 0, s>>>(P, items + lo, hi - lo, u_s, ustride,
+                                                              part, pstride);
+        break;
     }
 #undef NEAR_SYM_CASE
+  }
+}
+
+void launch_p2p_near_sym(const TreeParams& P, const int4* items, const int* group_off, int begin,
+                         int end, const double* u_s, double* part, cudaStream_t s) {
+  launch_near_sym_v<1>(P, items, group_off, begin, end, u_s, 0, part, 0, s);
+}
+
+// Block near field: nv (2..kNearBlockV) vectors share every kernel evaluation.
+int near_block_max() { return kNearBlockV; }
+void launch_p2p_near_sym_block(const TreeParams& P, const int4* items, const int* group_off,
+                               int begin, int end, int nv, const double* u_s, size_t ustride,
+                               double* part, size_t pstride, cudaStream_t s) {
+  switch (nv) {
+    case 1: launch_near_sym_v<1>(P, items, group_off, begin, end, u_s, ustride, part, pstride, s); break;
+    case 2: launch_near_sym_v<2>(P, items, group_off, begin, end, u_s, ustride, part, pstride, s); break;
+    case 3: launch_near_sym_v<3>(P, items, group_off, begin, end, u_s, ustride, part, pstride, s); break;
+    case 4: launch_near_sym_v<4>(P, items, group_off, begin, end, u_s, ustride, part, pstride, s); break;
+    default: throw std::invalid_argument("near block: 1..4 vectors per launch");
   }
 }
 

@@ -247,6 +247,13 @@ int near_max_points_per_lane();
 // slots 1..4 zeroed by the caller; combine with launch_near_combine(..., 5).
 void launch_p2p_near_sym(const TreeParams& P, const int4* items, const int* group_off, int begin,
                          int end, const double* u_s, double* part, cudaStream_t s);
+// Block product: nv <= near_block_max() vectors (vector v at u_s + v ustride,
+// its 5 slots at part + v pstride) share every kernel evaluation; each
+// vector's sums equal the single-vector launch bit for bit.
+int near_block_max();
+void launch_p2p_near_sym_block(const TreeParams& P, const int4* items, const int* group_off,
+                               int begin, int end, int nv, const double* u_s, size_t ustride,
+                               double* part, size_t pstride, cudaStream_t s);
 // Chunk-pair symmetric near field (large leaves): items {a_start, a_cnt,
 // b_start, b_cnt} (chunks <= 128 points), part = n_items x 256 doubles; the
 // reduction adds each chunk's rows (contrib CSR over chunks): out[q] = near

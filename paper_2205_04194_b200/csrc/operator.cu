@@ -140,6 +140,14 @@ void DeviceOperator::release() {
   solve_ws_bytes_ = 0;
   dfree(d_u2_);
   dfree(d_b2_);
+  dfree(d_blk_us_);
+  dfree(d_blk_part_);
+  blk_cap_ = 0;
+  for (int sl = 0; sl < 2; ++sl) {
+    dfree(d_blk_u_[sl]);
+    dfree(d_blk_b_[sl]);
+  }
+  blk_io_cap_ = 0;
   for (int sl = 0; sl < 2; ++sl) {
     if (pin_in_[sl]) cudaFreeHost(pin_in_[sl]);
     if (pin_out_[sl]) cudaFreeHost(pin_out_[sl]);
@@ -1952,6 +1960,129 @@ void DeviceOperator::apply_batch(int nrhs, const double* U, double* B) {
   cuda_check(cudaStreamSynchronize(cin_), "apply");
   cuda_check(cudaStreamSynchronize(s), "apply");
   cuda_check(cudaGetLastError(), "apply kernels");
+}
+
+// ------------------------------------------------------ block product (f4) --
+// The per-leaf symmetric near field is the one stage where several
+// right-hand sides share arithmetic: a pair's kernel value costs ~10 FP64
+// instructions and each vector only adds two DFMAs to it.  (The far field in
+// its GEMM form -- basis x coefficient matrix, fastmv.cpp:125-135 -- needs as
+// many DFMA-pipe slots per vector as the Horner form, and the FP64 tensor
+// cores share that pipe on B200, so the far passes run per vector.)
+bool DeviceOperator::block_near_ok() const {
+  return near_sym_ && !near_pair_ && n_near_ > 0 && n_far_ > 0 && !sharded() && n_pull_ == 0;
+}
+
+void DeviceOperator::apply_block_locked(int nv, const double* d_U, size_t ldu, double* d_B,
+                                        size_t ldb, cudaStream_t s) {
+  const size_t n = (size_t)N_;
+  if (nv < 2 || !block_near_ok()) {  // other near-field modes: vector by vector
+    for (int v = 0; v < nv; ++v) {
+      imqk::launch_gather(d_U + v * ldu, d_perm_, N_, d_us_, s);
+      apply_sorted_locked(d_us_, d_B + v * ldb, d_perm_, s);
+    }
+    return;
+  }
+  if (nv > imqk::near_block_max()) throw std::invalid_argument("apply_block: group too large");
+  if (blk_cap_ < nv) {
+    cuda_check(cudaStreamSynchronize(s), "block workspace");
+    cuda_check(cudaEventSynchronize(ev_last_), "block workspace");
+    dfree(d_blk_us_);
+    dfree(d_blk_part_);
+    blk_cap_ = 0;
+    d_blk_us_ = dalloc<double>((size_t)nv * n, "block vectors");
+    d_blk_part_ = dalloc<double>((size_t)nv * 5 * n, "block near partials");
+    blk_cap_ = nv;
+  }
+  for (int v = 0; v < nv; ++v)
+    imqk::launch_gather(d_U + v * ldu, d_perm_, N_, d_blk_us_ + v * n, s);
+  // one near-field launch sequence for the whole group, on the near stream
+  cuda_check(cudaEventRecord(ev_near_fork_, s), "near fork");
+  cuda_check(cudaStreamWaitEvent(near_stream_, ev_near_fork_, 0), "near fork wait");
+  imqk::launch_p2p_near_sym_block(P_, d_near_items_, near_group_off_.data(), 0, n_near_, nv,
+                                  d_blk_us_, n, d_blk_part_, 5 * n, near_stream_);
+  cuda_check(cudaEventRecord(ev_near_done_, near_stream_), "near done");
+  // moments + far field per vector on the high-priority stream; each final
+  // pass adds its vector's near slots
+  cuda_check(cudaStreamWaitEvent(hp_stream_, ev_near_fork_, 0), "hp fork wait");
+  double* const part_single = d_part_;
+  try {
+    for (int v = 0; v < nv; ++v) {
+      d_part_ = d_blk_part_ + (size_t)v * 5 * n;
+      moments(d_blk_us_ + v * n, hp_stream_);
+      far_near(d_blk_us_ + v * n, d_B + v * ldb, d_perm_, hp_stream_, 0, n_far_, 0, n_near_, true);
+    }
+  } catch (...) {
+    d_part_ = part_single;
+    throw;
+  }
+  d_part_ = part_single;
+  cuda_check(cudaEventRecord(ev_hp_done_, hp_stream_), "hp done");
+  cuda_check(cudaStreamWaitEvent(s, ev_hp_done_, 0), "hp join");
+}
+
+void DeviceOperator::apply_block_device(int nrhs, const double* d_U, double* d_B,
+                                        cudaStream_t stream) {
+  if (nrhs < 1) throw std::invalid_argument("apply_block: nrhs must be >= 1");
+  std::lock_guard<std::mutex> lk(mtx_);
+  DeviceGuard g(device_);
+  Ordered o(*this, stream);
+  const size_t n = (size_t)N_;
+  const int G = imqk::near_block_max();
+  for (int k = 0; k < nrhs; k += G)
+    apply_block_locked(std::min(G, nrhs - k), d_U + (size_t)k * n, n, d_B + (size_t)k * n, n,
+                       stream);
+  cuda_check(cudaGetLastError(), "apply_block launch");
+}
+
+void DeviceOperator::apply_block_host(int nrhs, const double* U, double* B) {
+  if (nrhs < 1) throw std::invalid_argument("apply_block: nrhs must be >= 1");
+  std::lock_guard<std::mutex> lk(mtx_);
+  DeviceGuard g(device_);
+  cudaStream_t s = stream_;
+  Ordered o(*this, s);
+  const size_t n = (size_t)N_, bytes = n * sizeof(double);
+  const int G = std::min(nrhs, imqk::near_block_max());
+  io_setup(false, false, false);  // copy streams and events
+  const int slots = nrhs > G ? 2 : 1;
+  if (blk_io_cap_ < G || (slots == 2 && !d_blk_u_[1])) {
+    cuda_check(cudaStreamSynchronize(s), "block slots");
+    for (int sl = 0; sl < 2; ++sl) {
+      dfree(d_blk_u_[sl]);
+      dfree(d_blk_b_[sl]);
+    }
+    blk_io_cap_ = 0;
+    for (int sl = 0; sl < slots; ++sl) {
+      d_blk_u_[sl] = dalloc<double>((size_t)G * n, "block input slot");
+      d_blk_b_[sl] = dalloc<double>((size_t)G * n, "block output slot");
+    }
+    blk_io_cap_ = G;
+  }
+  cuda_check(cudaEventRecord(ev_io_start_, s), "io start");
+  cuda_check(cudaStreamWaitEvent(cin_, ev_io_start_, 0), "io wait");
+  cuda_check(cudaStreamWaitEvent(cout_, ev_io_start_, 0), "io wait");
+  for (int k = 0, gi = 0; k < nrhs; k += G, ++gi) {
+    const int sl = slots == 2 ? (gi & 1) : 0, nv = std::min(G, nrhs - k);
+    // the slot's previous group (gi - 2) has been gathered / copied out
+    if (gi >= slots) cuda_check(cudaStreamWaitEvent(cin_, ev_gath_[sl], 0), "slot wait");
+    cuda_check(cudaMemcpyAsync(d_blk_u_[sl], U + (size_t)k * n, (size_t)nv * bytes,
+                               cudaMemcpyHostToDevice, cin_), "H2D U");
+    cuda_check(cudaEventRecord(ev_in_[sl], cin_), "event");
+    cuda_check(cudaStreamWaitEvent(s, ev_in_[sl], 0), "event");
+    if (gi >= slots) cuda_check(cudaStreamWaitEvent(s, ev_out_[sl], 0), "event");
+    apply_block_locked(nv, d_blk_u_[sl], n, d_blk_b_[sl], n, s);
+    cuda_check(cudaEventRecord(ev_gath_[sl], s), "event");
+    cuda_check(cudaEventRecord(ev_done_[sl], s), "event");
+    cuda_check(cudaStreamWaitEvent(cout_, ev_done_[sl], 0), "event");
+    cuda_check(cudaMemcpyAsync(B + (size_t)k * n, d_blk_b_[sl], (size_t)nv * bytes,
+                               cudaMemcpyDeviceToHost, cout_), "D2H B");
+    cuda_check(cudaEventRecord(ev_out_[sl], cout_), "event");
+    cuda_check(cudaGetLastError(), "apply_block kernels");
+  }
+  cuda_check(cudaStreamSynchronize(cout_), "apply_block");
+  cuda_check(cudaStreamSynchronize(cin_), "apply_block");
+  cuda_check(cudaStreamSynchronize(s), "apply_block");
+  cuda_check(cudaGetLastError(), "apply_block kernels");
 }
 
 void DeviceOperator::copy_permutation(int* perm_host) const {

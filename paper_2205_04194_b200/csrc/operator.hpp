@@ -121,6 +121,17 @@ class DeviceOperator {
   // Device vectors in original order; enqueued on `stream` (0 = the legacy
   // default stream, as everywhere in CUDA), no host synchronisation.
   void apply_device(const double* d_u, double* d_b, cudaStream_t stream);
+  // Block product: rows of d_U / d_B (nrhs x N, original
+  // order, device).  Groups of up to imqk::near_block_max() vectors go through
+  // ONE near-field launch sequence in which every kernel value 1/sqrt(r^2+t^2)
+  // is evaluated once and feeds all vectors of the group (the far field is
+  // per vector: its GEMM form has no FP64 saving on B200); each
+  // b_k equals the single product bit for bit.  Enqueued on `stream`.
+  void apply_block_device(int nrhs, const double* d_U, double* d_B, cudaStream_t stream);
+  // The same with host matrices; group k+1's copy-in and group k-1's copy-out
+  // overlap group k's block product (pinned buffers; pageable ones are
+  // copied by the driver's staging and serialise).
+  void apply_block_host(int nrhs, const double* U, double* B);
   // Device vectors already in Morton order (no gather/scatter).
   void apply_sorted(const double* d_us, double* d_bs, cudaStream_t stream);
 
@@ -221,6 +232,17 @@ class DeviceOperator {
   void release();
   void apply_sorted_locked(const double* d_us, double* d_bs, const int* perm,
                            cudaStream_t s);
+  // nv <= near_block_max() vectors (original order, strides ldu / ldb); the
+  // caller holds the lock and the Ordered guard
+  void apply_block_locked(int nv, const double* d_U, size_t ldu, double* d_B, size_t ldb,
+                          cudaStream_t s);
+  bool block_near_ok() const;
+  double* d_blk_us_ = nullptr;    // [blk_cap_][N] Morton-ordered block vectors
+  double* d_blk_part_ = nullptr;  // [blk_cap_][5][N] near-field slots per vector
+  int blk_cap_ = 0;
+  double* d_blk_u_[2] = {nullptr, nullptr};  // host path: group slots [blk_io_cap_][N]
+  double* d_blk_b_[2] = {nullptr, nullptr};
+  int blk_io_cap_ = 0;
 
   int device_ = 0;
   OperatorOptions opt_{};

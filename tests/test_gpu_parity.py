@@ -450,6 +450,48 @@ def test_batch_and_pageable_host_paths_bitwise(imq):
         assert np.array_equal(PB.numpy(), ref)                 # pinned batch
         assert np.array_equal(op.apply_batch(U[:1]), ref[:1])  # one row
 
+@pytest.mark.parametrize("nrhs", [2, 3, 4, 7])
+def test_block_product_bitwise_equals_single_products(imq, nrhs):
+    """imq_ext_operator_apply_block (f4): groups of <= 4 vectors share the
+    near field's kernel evaluations; every row equals the single product bit
+    for bit (host matrices and device matrices), and the oracle rows to 1e-10."""
+    torch = pytest.importorskip("torch")
+    from paper_2205_04194_b200 import inputs
+    n = 1 << 19
+    xy = inputs.uniform_points(n, 3)
+    U = np.stack([inputs.random_vector(n, 300 + k) for k in range(nrhs)])
+    with imq.FastOperator(xy, 0.03, 12, 6) as op:
+        ref = np.stack([op.apply(U[k]) for k in range(nrhs)])
+        assert np.array_equal(op.apply_block(U), ref)            # pageable host matrices
+        PU = torch.from_numpy(U).pin_memory()
+        PB = torch.empty_like(PU).pin_memory()
+        imq.capi.check(imq.capi.lib().imq_ext_operator_apply_block(
+            op.handle, nrhs, imq.api.C.cast(PU.data_ptr(), imq.api._dp),
+            imq.api.C.cast(PB.data_ptr(), imq.api._dp)))
+        assert np.array_equal(PB.numpy(), ref)                   # pinned host matrices
+        dU = torch.from_numpy(U).cuda()
+        dB = torch.zeros_like(dU)
+        op.apply_block_device(dU, dB, nrhs, torch.cuda.current_stream())
+        torch.cuda.synchronize()
+        assert np.array_equal(dB.cpu().numpy(), ref)             # device matrices
+        assert np.array_equal(op.apply(U[0]), ref[0])            # single path intact afterwards
+
+
+def test_block_product_other_near_modes(imq, oracle):
+    """Operators whose near field is not the per-leaf symmetric kernel (large
+    leaves: chunk pairs; tiny trees) take the block entry point vector by
+    vector; rows equal the single products and the oracle."""
+    from paper_2205_04194_b200 import inputs
+    for n, levels in ((20000, 2), (3000, 1)):
+        xy = inputs.uniform_points(n, 5)
+        U = np.stack([inputs.random_vector(n, 40 + k) for k in range(3)])
+        with imq.FastOperator(xy, 0.05, 10, levels) as op:
+            B = op.apply_block(U)
+            for k in range(3):
+                assert np.array_equal(B[k], op.apply(U[k]))
+        want = oracle.fast_matvec(xy, 0.05, 10, levels, U[2])
+        assert np.max(np.abs(B[2] - want)) / np.max(np.abs(want)) <= 1e-10
+
 
 @pytest.mark.parametrize("case", ["single_pass", "split_no_cheb", "cheb_nodes", "cheb_rings",
                                   "cheb_rings_xring", "clustered", "strip"])

@@ -6,7 +6,7 @@ python bench.py > gpurun_out/r02_bench.json 2> gpurun_out/r02_bench.err
 python bench.py --impl reference > gpurun_out/r02_bench_ref.json 2> gpurun_out/r02_bench_ref.err
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r02_launches.csv python tools/profile_step.py 4 > /dev/null 2>&1
 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active,sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active --clock-control none --csv --log-file gpurun_out/r02_far_metrics.csv python tools/profile_step.py 4 > /dev/null 2>&1
-ncu --set full --clock-control none -k regex:"k_node_gemm|k_m2p_far|k_m2m_tr_s|k_p2p_near_sym|k_p2m_leaf" --launch-skip 30 --launch-count 10 -o /tmp/r02_full python tools/profile_step.py 4 > gpurun_out/r02_ncu_full.log 2>&1
+ncu --set full --clock-control none --import-source on --profile-from-start off -o /tmp/r02_full python tools/profile_step.py 4 > gpurun_out/r02_ncu_full.log 2>&1
 ncu -i /tmp/r02_full.ncu-rep --page details --csv > gpurun_out/r02_ncu_full_details.csv 2>&1
 ncu -i /tmp/r02_full.ncu-rep --page raw --csv > gpurun_out/r02_ncu_full_raw.csv 2>&1
 ls -la gpurun_out

@@ -32,7 +32,7 @@ def main(src, dst):
     seq = list(launches.values())
     starts = [i for i, d in enumerate(seq) if re.search(r"k_gather\b", d["name"]) and "rows" not in d["name"]]
     last = seq[starts[-1]:] if starts else seq
-    far = [d for d in last if "k_m2p_far" in d["name"]]
+    far = [d for d in last if re.search(r"k_m2p_far|k_m2p_leaf2|k_node_gemm", d["name"])]
     cheb = [d for d in last if "k_cheb" in d["name"]]
     ms = lambda d: d.get("gpu__time_duration.sum", 0.0) / 1e6
     dram = lambda d: d.get("dram__bytes_read.sum", 0.0) + d.get("dram__bytes_write.sum", 0.0)
@@ -40,7 +40,8 @@ def main(src, dst):
         "source": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,"
                   "sm__pipe_fp64_cycles_active... --clock-control none, tools/profile_step.py (cfg4), "
                   "last of 3 products; summarised by tools/far_ncu_summary.py",
-        "kernel": "k_m2p_far (node, ring and fine passes of one fast product) and the k_cheb_* kernels",
+        "kernel": "k_m2p_far / k_m2p_leaf2 / k_node_gemm (node, ring, X-node and partial passes of "
+                  "one fast product) and the k_cheb_* kernels",
         "dram_bytes_per_launch": sum(dram(d) for d in far),
         "ncu_ms": sum(ms(d) for d in far),
         "launches": len(far),
@@ -48,6 +49,7 @@ def main(src, dst):
                               "ms": sum(ms(d) for d in far + cheb)},
         "per_launch": [{"name": re.sub(r"\(.*", "", d["name"]), "grid": d["grid"], "ms": ms(d),
                         "fp64_pipe_pct": d.get("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
+                        "tensor_pipe_pct": d.get("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active"),
                         "dram_read": d.get("dram__bytes_read.sum"),
                         "dram_write": d.get("dram__bytes_write.sum"),
                         "regs": d.get("launch__registers_per_thread")} for d in far + cheb],

@@ -16,7 +16,12 @@ xy = inputs.config_points(cfg)
 op = P.FastOperator(xy, c["t"], c["m"], c["levels"])
 u = torch.tensor(inputs.random_vector(c["n"], 1000), device="cuda")
 b = torch.empty_like(u)
-for _ in range(3):
+for _ in range(2):
     op.apply_device(u, b, torch.cuda.current_stream())
 torch.cuda.synchronize()
+# `ncu --profile-from-start off` captures only the measured (third) product
+torch.cuda.profiler.start()
+op.apply_device(u, b, torch.cuda.current_stream())
+torch.cuda.synchronize()
+torch.cuda.profiler.stop()
 print("ok", float(b.abs().max()))
