@@ -219,6 +219,10 @@ struct GemmClasses {
   int n;
   int box_off[5];
   int tile_off[5];
+  // CTA -> (class, tile of the class), classes interleaved so the tiles that
+  // cover the same parents run together (their sources overlap: L2 reuse);
+  // null: CTAs in class order
+  const int2* order;
 };
 // out[box * n_nodes + n] = sum_delta Re sum_j Phi_delta[n][j] C_j(src(box, delta))
 void launch_node_gemm(const TreeParams& P, int box_level, const int* boxes,

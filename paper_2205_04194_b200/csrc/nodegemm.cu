@@ -114,12 +114,19 @@ __global__ void __launch_bounds__(NB / 16 * MG * 32) k_node_gemm(
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int r = lane >> 2, c = lane & 3;
   // this CTA's box class: its boxes and its offsets (tiles never straddle classes)
-  int cls = 0;
-  while (cls + 1 < G.n && (int)blockIdx.x >= G.tile_off[cls + 1]) ++cls;
+  int cls = 0, tile;
+  if (G.order) {
+    const int2 o = G.order[blockIdx.x];
+    cls = o.x;
+    tile = o.y;
+  } else {
+    while (cls + 1 < G.n && (int)blockIdx.x >= G.tile_off[cls + 1]) ++cls;
+    tile = (int)blockIdx.x - G.tile_off[cls];
+  }
   const int* boxes = boxes_all + G.box_off[cls];
   const int n_boxes = G.box_off[cls + 1] - G.box_off[cls];
   const GemmDelta* deltas = deltas_all + (size_t)cls * n_deltas;
-  const int b0 = ((int)blockIdx.x - G.tile_off[cls]) * NB;
+  const int b0 = tile * NB;
   for (int e = tid; e < n_deltas * NB; e += blockDim.x) {
     const int di = e / NB, n = e % NB;
     const GemmDelta D = deltas[di];
@@ -263,6 +270,7 @@ void launch_node_gemm(const TreeParams& P, int box_level, const int* boxes,
   const bool small = (long long)G.tile_off[G.n] < (long long)IMQ_GEMM_SMALL * sms;
   GemmClasses Gs = G;
   if (small) {
+    Gs.order = nullptr;  // the interleaved order is laid out for kGtN-box tiles
     Gs.tile_off[0] = 0;
     for (int c = 0; c < G.n; ++c)
       Gs.tile_off[c + 1] = Gs.tile_off[c] + (G.box_off[c + 1] - G.box_off[c] + kGtNSmall - 1) / kGtNSmall;

@@ -1221,6 +1221,7 @@ void DeviceOperator::free_gemm_pass(GemmPass& g) {
   dfree(g.d_A);
   dfree(g.d_D);
   dfree(g.d_boxes);
+  dfree(g.d_order);
   g = GemmPass{};
 }
 
@@ -1240,6 +1241,20 @@ void DeviceOperator::make_gemm_pass(GemmPass& g, int box_level, int n_per_dim,
   int nd = 0;
   for (int c = 0; c < ncls; ++c) {
     offsets(c, per[(size_t)c]);
+    // Phase order: offsets sorted by the residue of the source's cell index
+    // modulo 2^(sh+1) per dimension (sh = source level - box level; a box of
+    // class c has index = (c >> 1, c & 1) mod 2).  CTAs working on
+    // neighbouring boxes (and the other classes of the same parents, which
+    // run beside them) then read the same source coefficients at the same
+    // time, so those re-reads hit L2 instead of DRAM (config 4 X-node pass:
+    // 4.0 GB -> see profiles/README.md).  Any fixed order is a valid sum.
+    const int cx = by_class ? (c >> 1) : 0, cy = by_class ? (c & 1) : 0;
+    auto key = [&](const GemmOff& o) {
+      const int sh = o.level - box_level, md = (2 << sh) - 1;
+      return ((sh & 7) << 16) | ((((cx << sh) + o.dx) & md) << 8) | (((cy << sh) + o.dy) & md);
+    };
+    std::stable_sort(per[(size_t)c].begin(), per[(size_t)c].end(),
+                     [&](const GemmOff& a, const GemmOff& b) { return key(a) > key(b); });
     nd = std::max(nd, (int)per[(size_t)c].size());
     for (const GemmOff& o : per[(size_t)c]) {
       int u = 0;
@@ -1312,6 +1327,19 @@ void DeviceOperator::make_gemm_pass(GemmPass& g, int box_level, int n_per_dim,
   g.d_boxes = dalloc<int>(bx.size(), "gemm boxes");
   cuda_check(cudaMemcpy(g.d_boxes, bx.data(), bx.size() * sizeof(int), cudaMemcpyHostToDevice),
              "H2D boxes");
+  g.cls.order = nullptr;
+  if (ncls > 1) {  // tile j of every class before tile j + 1 of any
+    std::vector<int2> ord;
+    int most = 0;
+    for (int c = 0; c < ncls; ++c) most = std::max(most, g.cls.tile_off[c + 1] - g.cls.tile_off[c]);
+    for (int j = 0; j < most; ++j)
+      for (int c = 0; c < ncls; ++c)
+        if (j < g.cls.tile_off[c + 1] - g.cls.tile_off[c]) ord.push_back(make_int2(c, j));
+    g.d_order = dalloc<int2>(ord.size(), "gemm tile order");
+    cuda_check(cudaMemcpy(g.d_order, ord.data(), ord.size() * sizeof(int2), cudaMemcpyHostToDevice),
+               "H2D tile order");
+    g.cls.order = g.d_order;
+  }
   g.box_level = box_level;
   g.n_nodes = n_nodes;
   g.n_deltas = nd;

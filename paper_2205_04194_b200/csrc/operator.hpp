@@ -337,6 +337,7 @@ class DeviceOperator {
     double* d_A = nullptr;
     imqk::GemmDelta* d_D = nullptr;
     int* d_boxes = nullptr;
+    int2* d_order = nullptr;  // CTA -> (class, tile), classes interleaved
     double* out = nullptr;  // node values of box q at out + q * n_nodes
   };
   struct GemmOff {
