@@ -164,6 +164,7 @@ IMQ_API int imq_ext_operator_apply_sorted_device(const imq_operator* op, const d
 #define IMQ_OPT_NEAR_NO_PAIR 0x80u /* no chunk-pair near field */
 #define IMQ_OPT_CERT_REPORT 0x100u /* diagnostics: the certificate is estimated but never
                                       acted on (the swept gates alone, as without it) */
+#define IMQ_OPT_TRACE 0x200u       /* diagnostics: GMRES stage timings on stderr */
 typedef struct {
   unsigned flags;        /* IMQ_OPT_* */
   double ring_tau;       /* gate t/h of the rings (default 1.25; stricter only) */

@@ -57,7 +57,7 @@ class imq_ext_options(C.Structure):
 
 
 OPT = dict(no_cheb=0x1, no_ring=0x2, no_inner=0x4, no_xring=0x8, no_lsplit=0x10, no_split=0x20,
-           near_no_sym=0x40, near_no_pair=0x80, cert_report=0x100)
+           near_no_sym=0x40, near_no_pair=0x80, cert_report=0x100, trace=0x200)
 
 VERIFY_CB = C.CFUNCTYPE(None, C.c_char_p, C.c_int, C.c_double, C.c_void_p)
 

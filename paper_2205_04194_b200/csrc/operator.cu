@@ -2220,7 +2220,7 @@ PairCounts DeviceOperator::pair_counts() {
 
 // Pairs the kernels actually evaluate: direct (target, block) pairs of the
 // levels not covered by the Chebyshev pass, and (node, block) pairs.
-// This library's kernel launches in one apply_device (cuBLAS M2M excluded).
+// This library's kernel launches in one apply_device (every kernel of a product is its own).
 int DeviceOperator::kernel_launches_per_apply() const {
   auto groups = [](const std::vector<int>& off) {
     int g = 0;
@@ -2333,7 +2333,7 @@ SolveResult DeviceOperator::solve_host(const double* f, double tol, int max_iter
   int *d_flag = nullptr, *flag_pin = nullptr;
   void* ws = nullptr;
   cudaEvent_t ev[kRing] = {}, tev[kRing][3] = {};
-  const bool trace = getenv("IMQ_TRACE") != nullptr;
+  const bool trace = opt(kOptTrace);
   auto cleanup = [&]() {
     ws = nullptr;  // solve_ws_ stays cached on the operator
     for (int i = 0; i < kRing; ++i) {
@@ -2528,7 +2528,7 @@ SolveResult DeviceOperator::solve_host(const double* f, double tol, int max_iter
     throw;
   }
   cleanup();
-  if (getenv("IMQ_TRACE"))
+  if (trace)
     fprintf(stderr, "[imq trace] gmres total %.1f ms\n",
             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_enter)
                 .count());

@@ -61,6 +61,7 @@ enum : unsigned {
   kOptNearNoSym = 1u << 6, // per-target near field (no symmetric evaluation)
   kOptNearNoPair = 1u << 7,// no chunk-pair near field
   kOptCertReport = 1u << 8, // diagnostics: certificate estimated, never acted on
+  kOptTrace = 1u << 9,      // diagnostics: GMRES stage timings on stderr
 };
 constexpr double kCertBudget = 2e-12;  // estimated relative deviation allowed
 // Build-time interpolation certificate (operator.cu certify()).

@@ -29,6 +29,17 @@ def test_every_declared_symbol_is_exported(imq):
     assert set(ref22) <= exported
 
 
+def test_library_sources_read_no_environment_variable():
+    # include/imqfast.h: "The library reads no environment variables" -- a
+    # caller's environment cannot change a product (options go through
+    # imq_ext_operator_create_opts); no library (CUB / cuBLAS) in the sources
+    csrc = os.path.join(ROOT, "paper_2205_04194_b200", "csrc")
+    for f in sorted(os.listdir(csrc)):
+        text = open(os.path.join(csrc, f)).read()
+        assert "getenv" not in text, f
+        assert "#include <cub" not in text and "cublas" not in text.lower(), f
+
+
 def test_library_is_sm100a(imq):
     from paper_2205_04194_b200 import capi
     out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", capi.LIB_PATH],
