@@ -20,7 +20,9 @@
 //
 // CTA: 32 boxes x all nodes (MT m-tiles of 8), 4 warps as 2 box pairs x 2
 // node halves (each A fragment feeds two tensor-core ops); k in chunks of 16
-// (4 mma k-steps), A and B chunks in a 2-stage cp.async pipeline.  Measured
+// (4 mma k-steps), A and B chunks staged by TMA bulk copies (one per A row
+// and per box row, issued by the lanes of one warp per step, completion on
+// the stage's mbarrier) in a 2-stage ring.  Measured (cp.async staging)
 // at config 4 (X-node pass, 65,536 boxes x 144 nodes x 27 offsets; ncu,
 // tensor pipe active): 32 boxes / k16 / 2 stages 5.33 ms (76.8 %), 64 / 16 /
 // 2 5.35 ms, 64 / 16 / 3 5.46 ms, 32 / 8 / 2 5.65 ms, 64 / 32 / 3 6.00 ms
@@ -67,16 +69,8 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
       : "+d"(d0), "+d"(d1)
       : "d"(a), "d"(b));
 }
-// 16-byte async copy global -> shared; src_bytes = 0 zero-fills
-__device__ __forceinline__ void cp16(void* dst, const void* src, int src_bytes) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src),
-               "r"(src_bytes)
-               : "memory");
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
 __host__ __device__ constexpr int gemm_sa(int MT) {  // A rows [k][node]: stride = 4 (mod 16)
@@ -85,8 +79,12 @@ __host__ __device__ constexpr int gemm_sa(int MT) {  // A rows [k][node]: stride
 constexpr size_t gemm_smem(int MT, int NB) {
   return (size_t)kGtStages * kGtKC * gemm_sa(MT) * sizeof(double) +
          (size_t)kGtStages * NB * kGtSBn * sizeof(double) +
-         (size_t)kGtMaxDelta * NB * sizeof(const double*);
+         (size_t)kGtMaxDelta * NB * sizeof(const double*) + (size_t)2 * kGtStages * sizeof(uint64_t);
 }
+
+// rows of absent sources (outside the grid, empty blocks) are copied from here
+constexpr int kGtZeros = 512;
+__device__ __align__(16) double g_gemm_zeros[kGtZeros];
 
 __device__ __forceinline__ int gemm_block_count(const TreeParams& P, int level, uint32_t q) {
   const int sh = 2 * (P.L - level);
@@ -101,7 +99,7 @@ __device__ __forceinline__ int gemm_block_count(const TreeParams& P, int level, 
 // MG: node-tile groups (warps = NB / 16 box pairs x MG, MT / MG m-tiles each);
 // NB: boxes per CTA
 template <int MT, int MG, int NB>
-__global__ void __launch_bounds__(NB / 16 * MG * 32) k_node_gemm(
+__global__ void __launch_bounds__((NB / 16 * MG + 1) * 32) k_node_gemm(
     const TreeParams P, int box_level, const int* __restrict__ boxes_all, const GemmClasses G,
     const GemmDelta* __restrict__ deltas_all, int n_deltas, int k2pad,
     const double2* __restrict__ coef, double* __restrict__ out, int n_nodes) {
@@ -142,47 +140,64 @@ __global__ void __launch_bounds__(NB / 16 * MG * 32) k_node_gemm(
           p = reinterpret_cast<const double*>(coef + P.coef_off[D.level] + (size_t)q * P.K);
       }
     }
-    srcs[e] = p;
+    srcs[e] = p ? p : g_gemm_zeros;
+  }
+  // B stages start as zeros: a chunk shorter than the k chunk leaves the rest
+  // of its rows as they were, and those meet zero rows of A (0 x finite)
+  for (int e = tid; e < kGtStages * NB * kGtSBn; e += blockDim.x) Bs[e] = 0.0;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  uint64_t* bars = reinterpret_cast<uint64_t*>(srcs + (size_t)kGtMaxDelta * NB);
+  // full[stage]: the producer's expect_tx arrival + the copies' bytes;
+  // empty[stage]: one arrival per consumer warp when it is done reading
+  static_assert(MT % MG == 0 && NB % 16 == 0, "m-tiles over MG warp rows, box pairs");
+  constexpr int MH = MT / MG, NP = NB / 16, NW = NP * MG;
+  uint64_t* full = bars;
+  uint64_t* empty = bars + kGtStages;
+  if (tid == 0) {
+#pragma unroll
+    for (int i = 0; i < kGtStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], NW);
+    }
+    fence_mbar_init();
   }
   __syncthreads();
-  // warp w: boxes of n-tiles 2 np, +1 and m-tiles [mh MH, +MH), np = w % (N / 16),
-  // mh = w / (N / 16): every A fragment feeds two tensor-core ops
-  static_assert(MT % MG == 0 && NB % 16 == 0, "m-tiles over MG warp rows, box pairs");
-  constexpr int MH = MT / MG, NP = NB / 16;
+  const int k2 = 2 * P.K, nchunk = k2pad / kGtKC, nsteps = n_deltas * nchunk;
+  if (warp == NW) {
+    // producer warp: stages step after step as the consumers free the ring.
+    // Lane k copies the A row k0 + k (all nodes), lane n the coefficients
+    // k0.. of box n's source (only the part below 2K: the rest of the row
+    // keeps finite values of an earlier chunk, times zero rows of A).
+    for (int step = 0; step < nsteps; ++step) {
+      const int di = step / nchunk, k0 = (step % nchunk) * kGtKC, st = step % kGtStages;
+      if (step >= kGtStages) mbar_wait(&empty[st], (uint32_t)((step / kGtStages - 1) & 1));
+      const int kb = min(kGtKC, k2 - k0);
+      uint64_t* bar = &full[st];
+      if (lane == 0)
+        mbar_arrive_expect_tx(bar, (uint32_t)((kGtKC * MP + NB * kb) * sizeof(double)));
+      __syncwarp();
+      const double* A = deltas[di].A + (size_t)k0 * MP;
+      double* as = As + (size_t)st * kGtKC * SA;
+      for (int k = lane; k < kGtKC; k += 32)
+        tma_load_1d(as + k * SA, A + (size_t)k * MP, MP * sizeof(double), bar);
+      double* bs = Bs + (size_t)st * NB * kGtSBn;
+      const double* const* sp = srcs + di * NB;
+      for (int n = lane; n < NB; n += 32)
+        tma_load_1d(bs + n * kGtSBn, sp[n] + k0, kb * sizeof(double), bar);
+    }
+    return;
+  }
+  // consumer warp w: boxes of n-tiles 2 np, +1 and m-tiles [mh MH, +MH), np =
+  // w % (N / 16), mh = w / (N / 16): every A fragment feeds two tensor-core ops
   const int np = warp % NP, mh = warp / NP;
   double acc[MH][2][2];
 #pragma unroll
   for (int mt = 0; mt < MH; ++mt)
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
-  const int k2 = 2 * P.K, nchunk = k2pad / kGtKC, nsteps = n_deltas * nchunk;
-  auto issue = [&](int step) {
-    if (step < nsteps) {
-      const int di = step / nchunk, k0 = (step % nchunk) * kGtKC, st = step % kGtStages;
-      const double* A = deltas[di].A + (size_t)k0 * MP;
-      double* as = As + (size_t)st * kGtKC * SA;
-      for (int e = tid; e < kGtKC * MP / 2; e += blockDim.x) {  // 16-byte pieces
-        const int k = (2 * e) / MP, m = (2 * e) % MP;
-        cp16(as + k * SA + m, A + (size_t)k * MP + m, 16);
-      }
-      double* bs = Bs + (size_t)st * NB * kGtSBn;
-      const double* const* sp = srcs + di * NB;
-      for (int e = tid; e < NB * kGtKC / 2; e += blockDim.x) {
-        const int n = e / (kGtKC / 2), kk = 2 * (e % (kGtKC / 2));
-        const double* p = sp[n];
-        const bool ok = p && k0 + kk < k2;  // zero-fill padding rows and absent sources
-        cp16(bs + n * kGtSBn + kk, ok ? (const void*)(p + k0 + kk) : (const void*)coef, ok ? 16 : 0);
-      }
-    }
-    cp_commit();
-  };
-#pragma unroll
-  for (int i = 0; i < kGtStages - 1; ++i) issue(i);
   for (int step = 0; step < nsteps; ++step) {
-    cp_wait<kGtStages - 2>();
-    __syncthreads();  // stage `step` visible; stage step-1 free for reuse
-    issue(step + kGtStages - 1);
     const int st = step % kGtStages;
+    mbar_wait(&full[st], (uint32_t)((step / kGtStages) & 1));
     const int kleft = k2 - (step % nchunk) * kGtKC;  // the last chunk's k-steps past 2K are all zero
     const double* as = As + (size_t)st * kGtKC * SA + mh * MH * 8 + r;
     const double* bs = Bs + (size_t)st * NB * kGtSBn + (size_t)(np * 16 + r) * kGtSBn;
@@ -198,8 +213,9 @@ __global__ void __launch_bounds__(NB / 16 * MG * 32) k_node_gemm(
         dmma(acc[mt][1][0], acc[mt][1][1], a, b1);
       }
     }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);  // this warp is done with stage st
   }
-  cp_wait<0>();
   // C fragment: rows (mh MH + mt) 8 + r (nodes), columns (2 np + nt) 8 + 2c, +1 (boxes)
 #pragma unroll
   for (int nt = 0; nt < 2; ++nt)
@@ -235,6 +251,7 @@ void launch_node_gemm(const TreeParams& P, int box_level, const int* boxes,
   if (G.n < 1 || G.tile_off[G.n] <= 0) return;
   if (k2pad % kGtKC) throw std::invalid_argument("node gemm: k2pad must be a multiple of the k chunk");
   if (n_deltas > kGtMaxDelta) throw std::invalid_argument("node gemm: too many offsets");
+  if (k2pad > kGtZeros) throw std::invalid_argument("node gemm: order too large for the zero block");
   auto run = [&](auto kern, size_t smem, int warps, const GemmClasses& Gx) {
     const unsigned grid = (unsigned)Gx.tile_off[Gx.n];
     // the attribute is per (kernel, device); every instantiation has the same
@@ -253,7 +270,8 @@ void launch_node_gemm(const TreeParams& P, int box_level, const int* boxes,
         throw std::runtime_error("node gemm: shared-memory attribute");
       }
     }
-    kern<<<grid, warps * 32, smem, s>>>(P, box_level, boxes, Gx, deltas, n_deltas, k2pad, coef,
+    kern<<<grid, (warps + 1) * 32, smem, s>>>(P,  // + the producer warp
+        box_level, boxes, Gx, deltas, n_deltas, k2pad, coef,
                                         out, n_nodes);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess)
