@@ -833,7 +833,7 @@ void DeviceOperator::build_cheb(int p_lo, int p_hi) {
     // items of R = 8 and at 63 % as GEMMs
     const int npd = inner_v_[(size_t)l] ? imqk::kChebNI : imqk::kChebN;
     const bool big = imqk::m2p_specialised(M_) && nb_own >= 256 * (long long)gtile;
-    auto wins = [&](int nn) { return nn % 256 != 0 && imqk::node_gemm_mt(nn) > 0; };
+    auto wins = [&](int nn) { return imqk::node_gemm_mt(nn) > 0; };
     gn[(size_t)l] = big && wins(npd * npd);
     if (ring_ && l + 1 >= ring_l0_) {
       const int nr = imqk::kRingNr[ring_v_[(size_t)l]];
