@@ -24,6 +24,10 @@
 #include "imq_device.cuh"
 #include "operator.hpp"
 
+#ifndef IMQ_GEMM_MIN_TILES
+#define IMQ_GEMM_MIN_TILES 256  // node / ring passes with fewer 32-box tiles stay Horner items
+#endif
+
 namespace imqh {
 
 constexpr size_t kM2tMaxSmem = 220 * 1024;  // fused M2M + transform: M <= ~22
@@ -832,7 +836,7 @@ void DeviceOperator::build_cheb(int p_lo, int p_hi) {
     // GPU (>= 256 tiles); the 16 x 16 passes run at 77 % of the pipe as Horner
     // items of R = 8 and at 63 % as GEMMs
     const int npd = inner_v_[(size_t)l] ? imqk::kChebNI : imqk::kChebN;
-    const bool big = imqk::m2p_specialised(M_) && nb_own >= 256 * (long long)gtile;
+    const bool big = imqk::m2p_specialised(M_) && nb_own >= IMQ_GEMM_MIN_TILES * (long long)gtile;
     auto wins = [&](int nn) { return imqk::node_gemm_mt(nn) > 0; };
     gn[(size_t)l] = big && wins(npd * npd);
     if (ring_ && l + 1 >= ring_l0_) {
