@@ -180,10 +180,11 @@ __global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(1024)
                   double* __restrict__ h, int* flag, double* __restrict__ vnext) {
   cg::cluster_group cl = cg::this_cluster();
   __shared__ double red[32];
-  __shared__ double slot[2];
+  __shared__ double slots[2][kClusterCtas];  // [buffer][source CTA]: pushed by the peers
   __shared__ double bcast;
   constexpr int T = kClusterCtas * 1024;
-  const int tid = (int)cl.block_rank() * 1024 + threadIdx.x;
+  const unsigned rank = cl.block_rank();
+  const int tid = (int)rank * 1024 + threadIdx.x;
   double wr[E];
   bool bad = false;
 #pragma unroll
@@ -193,28 +194,35 @@ __global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(1024)
     bad |= k < n && !isfinite(wr[e]);
   }
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+  cl.sync();  // every CTA of the cluster is running before the first remote store
   for (int i = 0; i <= j + 1; ++i) {
     const double* Vi = V + (size_t)i * ld;
+    constexpr bool kKeep = E <= 8;  // V_i's slice stays in registers for the update (E = 16: reloaded)
+    double vi[kKeep ? E : 1];
     double acc = 0.0;
 #pragma unroll
     for (int e = 0; e < E; ++e) {
       const int k = tid + e * T;
-      if (k < n) acc = fma(wr[e], i <= j ? Vi[k] : wr[e], acc);
+      const double v = (k < n && i <= j) ? Vi[k] : 0.0;
+      if (kKeep) vi[e] = v;
+      if (k < n) acc = fma(wr[e], i <= j ? v : wr[e], acc);
     }
     // fixed-order tree reductions (warp, CTA, cluster): every CTA forms the
-    // same total; the serial per-thread sums they replace cost ~1 us per
-    // projection
+    // same total.  The CTA's sum is PUSHED into every peer's slots (remote
+    // stores ahead of the cluster barrier), so after the barrier each CTA
+    // reads its own shared memory only.
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
     __syncthreads();
     if (threadIdx.x < 32) {
       double t = red[threadIdx.x];
       for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-      if (threadIdx.x == 0) slot[i & 1] = t;
+      if (threadIdx.x < kClusterCtas)
+        *cl.map_shared_rank(&slots[i & 1][rank], threadIdx.x) = t;
     }
     cl.sync();
     if (threadIdx.x < 32) {
-      double t = threadIdx.x < kClusterCtas ? *cl.map_shared_rank(&slot[i & 1], threadIdx.x) : 0.0;
+      double t = threadIdx.x < kClusterCtas ? slots[i & 1][threadIdx.x] : 0.0;
       for (int o = kClusterCtas / 2; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
       if (threadIdx.x == 0) bcast = t;
     }
@@ -225,7 +233,7 @@ __global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(1024)
 #pragma unroll
       for (int e = 0; e < E; ++e) {
         const int k = tid + e * T;
-        if (k < n) wr[e] = fma(-tot, Vi[k], wr[e]);
+        if (k < n) wr[e] = fma(-tot, kKeep ? vi[e] : Vi[k], wr[e]);
       }
     } else {
       const double hn = sqrt(tot);
@@ -245,7 +253,7 @@ __global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(1024)
     const int k = tid + e * T;
     if (k < n) out[k] = wr[e];
   }
-  cl.sync();  // keep every CTA's shared memory alive until all remote reads are done
+  cl.sync();  // keep every CTA's shared memory alive until all remote stores have landed
 }
 
 inline unsigned grid_for(long long n) {
