@@ -1709,20 +1709,48 @@ void DeviceOperator::far_near(const double* d_us, double* d_out, const int* perm
     if (cheb_run) {
       // list fields at the Chebyshev nodes of every box, series per level
       // (parent restricted + own), summed at the targets of the level-lc boxes
-      far_pass(0, n_cheb_items_, cheb_group_off_.data(), nullptr, 0, nullptr, nullptr, d_cval_,
-               nullptr, 1, cheb_lc_, &Pn_, d_cheb_items_);
-      for (const GemmPass& g : gnode_) launch_gemm_pass(g, s);  // the GEMM levels
-      if (ring_)  // the level-(l+1) rings at the NR x NR nodes of the level-l boxes
-        far_pass(0, n_ring_items_, ring_group_off_.data(), nullptr, 0, nullptr, nullptr, d_rval_,
-                 nullptr, 2, L_ - 1, &Pr_, d_ring_items_);
-      if (ring_)
-        for (const GemmPass& g : gring_) launch_gemm_pass(g, s);
-      if (xr && xgemm_)  // at the NX x NX nodes of each level-(L-1) box X: its level-(L-1)
-                         // inner blocks and its level-L outer ring, as GEMMs
-        launch_gemm_pass(gx_, s);
-      else if (xr)  // the same through k_m2p_far (ring mode 1 at level L-1, lsplit 4 at L)
-        far_pass(0, n_xring_items_, xring_group_off_.data(), nullptr, 0, nullptr, nullptr,
-                 d_xval_, nullptr, L_ - 1, L_, &Px_, d_xring_items_, 1, 4);
+      // The node, ring and X-node passes are independent of one another
+      // (each reads the coefficients and writes its own node values): ONE
+      // fork over s + the aux streams, the GEMMs first (one stream each), the
+      // Horner item groups round-robin behind them, one join -- every
+      // kernel's tail is filled by whatever is ready on another stream.
+      {
+        cudaStream_t ss[1 + kAuxStreams] = {s};
+        cuda_check(cudaEventRecord(ev_fork_, s), "fork");
+        for (int k = 0; k < kAuxStreams; ++k) {
+          ss[k + 1] = aux_[k];
+          cuda_check(cudaStreamWaitEvent(aux_[k], ev_fork_, 0), "fork wait");
+        }
+        int gi = 0;
+        auto gstream = [&]() { return ss[1 + (gi++ % kAuxStreams)]; };
+        if (xr && xgemm_)  // at the NX x NX nodes of each level-(L-1) box X: its level-(L-1)
+                           // inner blocks and its level-L outer ring, as GEMMs
+          launch_gemm_pass(gx_, gstream());
+        if (ring_)
+          for (const GemmPass& g : gring_)
+            if (g.on) launch_gemm_pass(g, gstream());
+        for (const GemmPass& g : gnode_)  // the GEMM levels
+          if (g.on) launch_gemm_pass(g, gstream());
+        auto items_pass = [&](int n_it, const int* goff, double* far_s, int lmin, int lmax,
+                              const imqk::TreeParams& Pp, const int4* its, int ring, int lsp) {
+          if (n_it > 0)
+            imqk::launch_m2p_far(Pp, its, goff, 0, n_it, d_coef_, far_s, ss, far_streams_, nullptr,
+                                 0, nullptr, nullptr, nullptr, lmin, lmax, ring, lsp, false);
+        };
+        // list fields at the Chebyshev nodes of every box
+        items_pass(n_cheb_items_, cheb_group_off_.data(), d_cval_, 1, cheb_lc_, Pn_, d_cheb_items_,
+                   0, 0);
+        if (ring_)  // the level-(l+1) rings at the NR x NR nodes of the level-l boxes
+          items_pass(n_ring_items_, ring_group_off_.data(), d_rval_, 2, L_ - 1, Pr_,
+                     d_ring_items_, 0, 0);
+        if (xr && !xgemm_)  // X nodes through k_m2p_far (ring mode 1 at level L-1, lsplit 4 at L)
+          items_pass(n_xring_items_, xring_group_off_.data(), d_xval_, L_ - 1, L_, Px_,
+                     d_xring_items_, 1, 4);
+        for (int k = 0; k < kAuxStreams; ++k) {
+          cuda_check(cudaEventRecord(ev_join_[k], aux_[k]), "join");
+          cuda_check(cudaStreamWaitEvent(s, ev_join_[k], 0), "join wait");
+        }
+      }
       constexpr long long NN = imqk::kChebN * imqk::kChebN, NRR = imqk::kChebNR * imqk::kChebNR;
       for (int l = 1; l <= cheb_lc_; ++l) {
         const int* bx = d_cboxes_ + cbox_off_[(size_t)l];
