@@ -1936,7 +1936,7 @@ void DeviceOperator::io_setup(bool pin_in, bool pin_out, bool two_slots) {
   }
   if ((pin_in || pin_out) && !pool_) {
     const unsigned hw = std::thread::hardware_concurrency();
-    pool_ = std::make_unique<CopyPool>((int)std::max(1u, std::min(8u, hw ? hw : 1u)));
+    pool_ = std::make_unique<CopyPool>((int)std::max(1u, std::min(16u, hw ? hw : 1u)));
   }
 }
 
@@ -1964,12 +1964,24 @@ void DeviceOperator::apply_batch(int nrhs, const double* U, double* B) {
     const int sj = j & 1;
     char* dst = reinterpret_cast<char*>(B + (size_t)j * n);
     const char* src = reinterpret_cast<const char*>(pin_out_[sj]);
-    for (size_t c = 0; c < nch; ++c) {
-      size_t off, len;
-      piece(c, off, len);
-      cuda_check(cudaEventSynchronize(ev_chunk_[sj][c]), "D2H chunk");
-      pool_->copy(dst + off, src + off, len);
+    if (pool_->threads() < 2) {
+      for (size_t c = 0; c < nch; ++c) {
+        size_t off, len;
+        piece(c, off, len);
+        cuda_check(cudaEventSynchronize(ev_chunk_[sj][c]), "D2H chunk");
+        std::memcpy(dst + off, src + off, len);
+      }
+      return;
     }
+    // the workers copy piece c as soon as its DMA has landed
+    pool_->stream_begin(dst, src, bytes, kIoChunk, false);
+    cudaError_t err = cudaSuccess;
+    for (size_t c = 0; c < nch; ++c) {
+      if (err == cudaSuccess) err = cudaEventSynchronize(ev_chunk_[sj][c]);
+      pool_->stream_release(c + 1);  // (on an error too: the workers must finish the job)
+    }
+    pool_->stream_end();
+    cuda_check(err, "D2H chunk");
   };
   for (int k = 0; k < nrhs; ++k) {
     const int sl = k & 1;
@@ -1983,11 +1995,27 @@ void DeviceOperator::apply_batch(int nrhs, const double* U, double* B) {
       const char* hs = reinterpret_cast<const char*>(src);
       char* ps = reinterpret_cast<char*>(pin_in_[sl]);
       char* ds = reinterpret_cast<char*>(du[sl]);
-      for (size_t c = 0; c < nch; ++c) {
-        size_t off, len;
-        piece(c, off, len);
-        pool_->copy(ps + off, hs + off, len);
-        cuda_check(cudaMemcpyAsync(ds + off, ps + off, len, cudaMemcpyHostToDevice, cin_), "H2D u");
+      if (pool_->threads() < 2) {
+        for (size_t c = 0; c < nch; ++c) {
+          size_t off, len;
+          piece(c, off, len);
+          std::memcpy(ps + off, hs + off, len);
+          cuda_check(cudaMemcpyAsync(ds + off, ps + off, len, cudaMemcpyHostToDevice, cin_), "H2D u");
+        }
+      } else {
+        // the workers stage piece after piece; each piece's DMA is queued as
+        // soon as it is staged
+        pool_->stream_begin(ps, hs, bytes, kIoChunk, true);
+        cudaError_t err = cudaSuccess;
+        for (size_t c = 0; c < nch; ++c) {
+          size_t off, len;
+          piece(c, off, len);
+          pool_->stream_wait(c);
+          if (err == cudaSuccess)
+            err = cudaMemcpyAsync(ds + off, ps + off, len, cudaMemcpyHostToDevice, cin_);
+        }
+        pool_->stream_end();
+        cuda_check(err, "H2D u");
       }
     }
     cuda_check(cudaEventRecord(ev_in_[sl], cin_), "event");
