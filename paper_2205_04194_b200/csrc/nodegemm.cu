@@ -51,6 +51,9 @@
 #ifndef IMQ_GEMM_ST
 #define IMQ_GEMM_ST 2
 #endif
+#ifndef IMQ_GEMM_PRODUCERS
+#define IMQ_GEMM_PRODUCERS 2
+#endif
 
 namespace imqk {
 
@@ -62,7 +65,8 @@ using namespace imqdev;
 constexpr int kGtN = IMQ_GEMM_NB, kGtKC = IMQ_GEMM_KC, kGtStages = IMQ_GEMM_ST;
 constexpr int kGtNSmall = 16;  // boxes per CTA when the pass has too few tiles to fill the GPU
 constexpr int kGtMaxDelta = 32;
-constexpr int kGtSBn = kGtKC + 4;  // B rows [box][k]: stride = 4 (mod 16)
+constexpr int kGtProducers = IMQ_GEMM_PRODUCERS;  // staging warps per CTA
+constexpr int kGtSBn = kGtKC % 16 == 0 ? kGtKC + 4 : kGtKC + 12;  // B rows [box][k]: stride = 4 (mod 16)
 static_assert(kGtN >= kGtNSmall, "tile sizes");
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
@@ -100,7 +104,7 @@ __device__ __forceinline__ int gemm_block_count(const TreeParams& P, int level, 
 // MG: node-tile groups (warps = NB / 16 box pairs x MG, MT / MG m-tiles each);
 // NB: boxes per CTA
 template <int MT, int MG, int NB>
-__global__ void __launch_bounds__((NB / 16 * MG + 1) * 32) k_node_gemm(
+__global__ void __launch_bounds__((NB / 16 * MG + kGtProducers) * 32) k_node_gemm(
     const TreeParams P, int box_level, const int* __restrict__ boxes_all, const GemmClasses G,
     const GemmDelta* __restrict__ deltas_all, int n_deltas, int k2pad,
     const double2* __restrict__ coef, double* __restrict__ out, int n_nodes) {
@@ -157,34 +161,43 @@ __global__ void __launch_bounds__((NB / 16 * MG + 1) * 32) k_node_gemm(
   if (tid == 0) {
 #pragma unroll
     for (int i = 0; i < kGtStages; ++i) {
-      mbar_init(&full[i], 1);
+      mbar_init(&full[i], kGtProducers);
       mbar_init(&empty[i], NW);
     }
     fence_mbar_init();
   }
   __syncthreads();
   const int k2 = 2 * P.K, nchunk = k2pad / kGtKC, nsteps = n_deltas * nchunk;
-  if (warp == NW) {
-    // producer warp: stages step after step as the consumers free the ring.
-    // Lane k copies the A row k0 + k (all nodes), lane n the coefficients
-    // k0.. of box n's source (only the part below 2K: the rest of the row
-    // keeps finite values of an earlier chunk, times zero rows of A).
+  if (warp >= NW) {
+    // producer warps: stage step after step as the consumers free the ring.
+    // The kGtKC A rows (row k0 + k, all nodes) and the NB box rows (the
+    // coefficients k0.. of each box's source, only the part below 2K: the
+    // rest of the row keeps finite values of an earlier chunk, times zero
+    // rows of A) are dealt round-robin to the producers' lanes: a bulk copy
+    // issues lane by lane (UBLKCP), ~48 of them per step are more than one
+    // warp can issue in the time the consumers need for the step's DMMAs.
+    const int pw = warp - NW;
     for (int step = 0; step < nsteps; ++step) {
       const int di = step / nchunk, k0 = (step % nchunk) * kGtKC, st = step % kGtStages;
       if (step >= kGtStages) mbar_wait(&empty[st], (uint32_t)((step / kGtStages - 1) & 1));
       const int kb = min(kGtKC, k2 - k0);
       uint64_t* bar = &full[st];
-      if (lane == 0)
-        mbar_arrive_expect_tx(bar, (uint32_t)((kGtKC * MP + NB * kb) * sizeof(double)));
+      if (lane == 0) {  // this producer's share of the step's bytes
+        int na = 0, nb = 0;
+        for (int i = pw; i < kGtKC + NB; i += kGtProducers) (i < kGtKC ? na : nb) += 1;
+        mbar_arrive_expect_tx(bar, (uint32_t)((na * MP + nb * kb) * sizeof(double)));
+      }
       __syncwarp();
       const double* A = deltas[di].A + (size_t)k0 * MP;
       double* as = As + (size_t)st * kGtKC * SA;
-      for (int k = lane; k < kGtKC; k += 32)
-        tma_load_1d(as + k * SA, A + (size_t)k * MP, MP * sizeof(double), bar);
       double* bs = Bs + (size_t)st * NB * kGtSBn;
       const double* const* sp = srcs + di * NB;
-      for (int n = lane; n < NB; n += 32)
-        tma_load_1d(bs + n * kGtSBn, sp[n] + k0, kb * sizeof(double), bar);
+      for (int i = pw + kGtProducers * lane; i < kGtKC + NB; i += kGtProducers * 32) {
+        if (i < kGtKC)
+          tma_load_1d(as + i * SA, A + (size_t)i * MP, MP * sizeof(double), bar);
+        else
+          tma_load_1d(bs + (i - kGtKC) * kGtSBn, sp[i - kGtKC] + k0, kb * sizeof(double), bar);
+      }
     }
     return;
   }
@@ -271,7 +284,7 @@ void launch_node_gemm(const TreeParams& P, int box_level, const int* boxes,
         throw std::runtime_error("node gemm: shared-memory attribute");
       }
     }
-    kern<<<grid, (warps + 1) * 32, smem, s>>>(P,  // + the producer warp
+    kern<<<grid, (warps + kGtProducers) * 32, smem, s>>>(P,  // + the producer warps
         box_level, boxes, Gx, deltas, n_deltas, k2pad, coef,
                                         out, n_nodes);
     const cudaError_t e = cudaGetLastError();
