@@ -19,16 +19,18 @@
 // same sum.
 //
 // CTA: 32 boxes x all nodes (MT m-tiles of 8), 4 consumer warps as 2 box
-// pairs x 2 node halves + a producer warp (each A fragment feeds two tensor-core ops); k in chunks of 16
-// (4 mma k-steps), A and B chunks staged by TMA bulk copies (one per A row
-// and per box row, issued by the lanes of one warp per step, completion on
-// the stage's mbarrier) in a 2-stage ring.  Measured at config 4 (X-node
-// pass, 65,536 boxes x 144 nodes x 27 offsets; ncu, tensor pipe active), TMA
-// staging with a producer warp: 32 boxes / k16 / 2 stages 4.73 ms (86.3 %),
+// pairs x 2 node halves (each A fragment feeds two tensor-core ops) + two
+// producer warps; k in chunks of 16 (4 mma k-steps), A and B chunks staged by
+// TMA bulk copies (one per A row and per box row, dealt to the producers'
+// lanes, completion on the stage's `full` mbarrier; the consumers hand a
+// stage back through its `empty` mbarrier) in a 2-stage ring.  Measured at
+// config 4 (X-node pass, 65,536 boxes x 144 nodes x 27 offsets; ncu, tensor
+// pipe active), TMA staging: 32 boxes / k16 / 2 stages 4.73 ms (86.3 %),
 // 32 / 32 / 2 4.82 ms (84.2 %), 64 / 16 / 2 5.26 ms (78.2 %), 64 / 16 / 3
-// 5.29 ms, 32 / 16 / 3 5.63 ms (71.6 %: 2 CTAs per SM).  With per-thread
-// cp.async staging the same tile took 5.33 ms (76.8 %); the Horner pass it
-// replaces 6.96 ms.
+// 5.29 ms, 32 / 16 / 3 5.63 ms (71.6 %: 2 CTAs per SM), 32 / 8 / 3 6.72 ms
+// (60.8 %: one producer warp cannot issue 40 copies per half-size step).
+// With per-thread cp.async staging the same tile took 5.33 ms (76.8 %); the
+// Horner pass it replaces 6.96 ms.
 #include <algorithm>
 #include <mutex>
 #include <set>
