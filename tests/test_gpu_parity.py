@@ -450,6 +450,42 @@ def test_batch_and_pageable_host_paths_bitwise(imq):
         assert np.array_equal(PB.numpy(), ref)                 # pinned batch
         assert np.array_equal(op.apply_batch(U[:1]), ref[:1])  # one row
 
+def test_pageable_staging_odd_sizes_and_alignment(imq):
+    """The streamed staging of pageable buffers (worker pool, non-temporal
+    copies in 8 MB pieces): a length that leaves a partial last piece and
+    parts that are not multiples of 64 bytes, and host pointers that are only
+    8-byte aligned (the copy falls back to memcpy) -- same bits as the pinned
+    product."""
+    torch = pytest.importorskip("torch")
+    from paper_2205_04194_b200 import inputs
+    n = 1_300_003
+    xy = inputs.uniform_points(n, 3)
+    u = inputs.random_vector(n, 77)
+    with imq.FastOperator(xy, 0.03, 8, 5) as op:
+        pin_u = torch.from_numpy(u).pin_memory()
+        pin_b = torch.empty(n, dtype=torch.float64).pin_memory()
+        imq.capi.check(imq.capi.lib().imq_operator_apply(
+            op.handle, imq.api.C.cast(pin_u.data_ptr(), imq.api._dp),
+            imq.api.C.cast(pin_b.data_ptr(), imq.api._dp)))
+        ref = pin_b.numpy().copy()
+        assert np.array_equal(op.apply(u), ref)
+        # 8-byte aligned but not 16-byte aligned views of pageable arrays
+        base_u = np.empty(n + 3)
+        off_u = 1 if base_u.ctypes.data % 16 == 0 else 0
+        mu = base_u[off_u:off_u + n]
+        mu[:] = u
+        base_b = np.full(n + 3, np.nan)
+        off_b = 1 if base_b.ctypes.data % 16 == 0 else 0
+        mb = base_b[off_b:off_b + n]
+        assert mu.ctypes.data % 16 == 8 and mb.ctypes.data % 16 == 8
+        for _ in range(2):
+            imq.capi.check(imq.capi.lib().imq_operator_apply(
+                op.handle, mu.ctypes.data_as(imq.api._dp), mb.ctypes.data_as(imq.api._dp)))
+            assert np.array_equal(mb, ref)
+        # the guard elements around the output view are untouched
+        assert np.isnan(base_b[:off_b]).all() and np.isnan(base_b[off_b + n:]).all()
+
+
 @pytest.mark.parametrize("nrhs", [2, 3, 4, 7])
 def test_block_product_bitwise_equals_single_products(imq, nrhs):
     """imq_ext_operator_apply_block (f4): groups of <= 4 vectors share the
