@@ -1,5 +1,5 @@
 """Fixed launch sequence for ncu: build the cfg-4 operator, run 2 warm-up
-fast products and 1 measured one (19 kernel launches per product at L=8)."""
+fast products and 1 measured one (38 kernel launches per product at config 4)."""
 import os
 import sys
 
