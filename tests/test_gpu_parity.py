@@ -62,6 +62,11 @@ def test_binning_bit_exact(imq, oracle, golden):
     check_binning(imq, oracle, np.tile([0.3, 0.4], 50), 0.7, 4, 2)
     strip = np.stack([np.linspace(-3, 5, 400), np.full(400, 2.0)], 1).ravel()
     check_binning(imq, oracle, strip, 0.1, 6, 3)
+    # the radix sort over many 4,096-key tiles with a partial last one, three
+    # 8-bit passes (18-bit keys at L = 8) and two (14-bit keys at L = 6)
+    rng = np.random.default_rng(5)
+    check_binning(imq, oracle, rng.random(2 * 300_001), 0.05, 4, 8)
+    check_binning(imq, oracle, rng.normal(0.5, 0.1, 2 * 123_457), 0.05, 4, 6)
 
 
 def test_config1_fast_matches_reference(imq, golden):
