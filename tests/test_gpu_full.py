@@ -138,7 +138,7 @@ def test_config2_gmres_iteration_matched(imq, oracle):
     assert np.max(np.abs(cr - rr) / rr) <= 1e-6
     # the coefficient vector against the REFERENCE's own c at matched caps
     # (tests/golden/cfg2_ref_it*.npz, make_golden_big.py; BASELINE config 2):
-    # measured 4.9e-10 (100 iterations) and 7.6e-8 (2,000), where GMRES has
+    # measured 3.3e-11 (100 iterations) and 6.2e-8 (2,000), where GMRES has
     # amplified the last-bit differences of the products for 40 cycles
     import os
     from conftest import GOLDEN
