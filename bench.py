@@ -363,18 +363,19 @@ def b200_arm(args):
         t0 = time.perf_counter()
         block_call()
         e2e_block = nb * n / (time.perf_counter() - t0)
-        blk_u = bat_u[:4].cuda()
+        nblk = min(4, nb)  # (nb is 3 for --steps < 3)
+        blk_u = bat_u[:nblk].cuda()
         blk_b = torch.empty_like(blk_u)
-        op.apply_block_device(blk_u, blk_b, 4, stream)
+        op.apply_block_device(blk_u, blk_b, nblk, stream)
         torch.cuda.synchronize()
         eb0 = torch.cuda.Event(enable_timing=True)
         eb1 = torch.cuda.Event(enable_timing=True)
         eb0.record(stream)
         for _ in range(2):
-            op.apply_block_device(blk_u, blk_b, 4, stream)
+            op.apply_block_device(blk_u, blk_b, nblk, stream)
         eb1.record(stream)
         torch.cuda.synchronize()
-        block_ms_per_vector = eb0.elapsed_time(eb1) / 8
+        block_ms_per_vector = eb0.elapsed_time(eb1) / (2 * nblk)
         del bat_u, bat_b, blk_u, blk_b
         page_u = [host_u[i].numpy() for i in range(2)]
         page_b = np.empty(n)
